@@ -1,0 +1,159 @@
+/*
+ * lance_b200.h -- C ABI of the B200-native LANCE int8 Winograd-domain
+ * convolution (the reference's `lance_gemm` path).
+ *
+ * Reference: /root/reference/proj/include/lance/ (header-only C++20, no FFI).
+ * Each entry point cites the reference interface it replaces.  The reference
+ * has no C ABI; a C++ host above this ABI (include/lance/b200.hpp) keeps the
+ * reference's operator API (ConvSpec / LanceConfig / QuantParams / Tensor4 /
+ * FilterBank -> Tensor4) and its exception behaviour.
+ *
+ * Conventions: plain pointers and sizes; no exceptions cross the ABI; every
+ * function returns a lance_status.  Device entry points are stream-ordered on
+ * the caller's cudaStream_t (passed as void*).  x is NHWC fp32, w is KRSC fp32,
+ * y is NHWC fp32 -- the reference layouts (tensor.hpp:24-86).
+ */
+#ifndef LANCE_B200_H
+#define LANCE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LANCE_B200_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define LANCE_API __attribute__((visibility("default")))
+#else
+#define LANCE_API
+#endif
+
+/* lance::Granularity (quant.hpp:44), enum order kept. */
+typedef enum {
+  LANCE_GRAN_PER_TILE = 0,
+  LANCE_GRAN_PER_POSITION = 1,
+  LANCE_GRAN_PER_TENSOR = 2
+} lance_granularity;
+
+/* lance::LanceMode (engines.hpp:56). */
+typedef enum { LANCE_MODE_FAITHFUL = 0, LANCE_MODE_GEMM = 1 } lance_mode;
+
+/* lance::ConvSpec (engines.hpp:33-54).  r = s = 3 and stride = 1 are fixed. */
+typedef struct {
+  int n, c, h, w, k;
+  int pad; /* 0 or 1 */
+} lance_conv_spec;
+
+/* lance::LanceConfig (engines.hpp:60-80). */
+typedef struct {
+  int bits_w;      /* 2..8 (32 = unquantized, rejected by the Gemm path) */
+  int bits_i;      /* 2..8 */
+  int granularity; /* lance_granularity */
+  int mode;        /* lance_mode; must be LANCE_MODE_GEMM */
+} lance_config;
+
+/* lance::QuantParams (quant.hpp:27-37), bit-for-bit. */
+typedef struct {
+  int bits;
+  float t_min, t_max, scale;
+} lance_qparams;
+
+typedef enum {
+  LANCE_OK = 0,
+  LANCE_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument (engines.hpp:46-91,496-499) */
+  LANCE_ERR_NAN = 2,              /* std::invalid_argument("fit_params: NaN in values"), quant.hpp:62 */
+  LANCE_ERR_CUDA = 3,             /* CUDA runtime / launch failure */
+  LANCE_ERR_NO_DEVICE = 4         /* no sm_100 device: the path has no CPU fallback */
+} lance_status;
+
+typedef struct lance_plan_s* lance_plan_t;
+
+LANCE_API int lance_abi_version(void);
+LANCE_API const char* lance_status_string(int status);
+/* Message of the last failure on the calling thread (the what() text the
+ * reference would have thrown). */
+LANCE_API const char* lance_last_error(void);
+
+/* Validation exactly as lance_gemm performs it before any work:
+ * ConvSpec::validate (engines.hpp:46-53), LanceConfig::validate (:66-79),
+ * the Gemm-mode and depth checks (:496-499). */
+LANCE_API int lance_validate(const lance_conv_spec* spec, const lance_config* cfg);
+
+/* Product-stage multiply counts (engines.hpp:568-575). */
+LANCE_API uint64_t lance_winograd_multiply_count(const lance_conv_spec* spec);
+LANCE_API uint64_t lance_direct_multiply_count(const lance_conv_spec* spec);
+
+/* ---------------------------------------------------------------------------
+ * Drop-in for lance::lance_gemm(x, w, spec, cfg) -> y (engines.hpp:492-536):
+ * HOST buffers in and out, synchronous.  x [N][H][W][C], w [K][3][3][C],
+ * y [N][OH][OW][K].  Internally caches one plan per (spec, cfg) per thread.
+ * Pinned (page-locked) host buffers give full-bandwidth copies. */
+LANCE_API int lance_gemm_host(const lance_conv_spec* spec, const lance_config* cfg, const float* x,
+                    const float* w, float* y);
+
+/* ---------------------------------------------------------------------------
+ * Device API.  A plan owns the per-layer state: prepared filter codes (K2),
+ * the int8 input-code workspace, per-position parameters and epilogue
+ * constants.  One plan serves one stream at a time. */
+LANCE_API int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int device,
+                      lance_plan_t* plan);
+LANCE_API int lance_plan_destroy(lance_plan_t plan);
+LANCE_API size_t lance_plan_device_bytes(lance_plan_t plan);
+
+/* K2: filter transform G g G^T + Winograd-domain quantization, once per layer
+ * (domain_from_filters + quantize_domain(u), engines.hpp:215-233,140-183). */
+LANCE_API int lance_plan_set_filters(lance_plan_t plan, const float* w_dev, void* stream);
+
+/* K0 -> K1 -> K3/K4 on a device-resident batch: per-position input ranges
+ * (quantize_domain(v) fit, engines.hpp:157-165), transform + quantize, and the
+ * 16 u8 x u8 -> i32 GEMMs on tcgen05 with the fused affine de-quantization +
+ * A^T m A + merge epilogue.  Asynchronous; NaN inputs are reported by
+ * lance_plan_sync (the reference throws from fit_params). */
+LANCE_API int lance_plan_forward(lance_plan_t plan, const float* x_dev, float* y_dev, void* stream);
+
+/* Static-params variant: the caller supplies the 16 input QuantParams
+ * (no range pass, no batch coupling; SURVEY.md section 8(e) mode 3). */
+LANCE_API int lance_plan_forward_static(lance_plan_t plan, const lance_qparams* in_params16,
+                              const float* x_dev, float* y_dev, void* stream);
+
+/* Optional fused bias + ReLU epilogue for subsequent forwards (north-star
+ * extension; no reference oracle: equals relu(lance_gemm(x, w) + bias)).
+ * bias_dev may be NULL (no bias).  relu is 0 or 1. */
+LANCE_API int lance_plan_set_epilogue(lance_plan_t plan, const float* bias_dev, int relu);
+
+/* Synchronise `stream` and report a NaN seen by the range pass of the last
+ * forward (LANCE_ERR_NAN) or any pending CUDA error. */
+LANCE_API int lance_plan_sync(lance_plan_t plan, void* stream);
+
+/* Parameters of the last forward / set_filters (synchronises the device). */
+LANCE_API int lance_plan_get_params(lance_plan_t plan, lance_qparams* input16, lance_qparams* weight16);
+
+/* Debug / parity access to intermediate stage buffers (synchronising copies to
+ * host memory in the reference layouts):
+ *   LANCE_DBG_CODES_A  u8  [16][M][C]   (vq.codes, engines.hpp:505)
+ *   LANCE_DBG_ROWSUM   i32 [16][M]      (a_row_sum, lowpgemm.hpp:121-123)
+ *   LANCE_DBG_CODES_W  u8  [16][C][K]   (uq.codes, engines.hpp:506)
+ *   LANCE_DBG_COLSUM   i32 [16][K]      (b_col_sum, lowpgemm.hpp:124-126)
+ * M = N * tiles_per_image.  `bytes` must equal the array size. */
+enum { LANCE_DBG_CODES_A = 1, LANCE_DBG_ROWSUM = 2, LANCE_DBG_CODES_W = 3, LANCE_DBG_COLSUM = 4 };
+LANCE_API int lance_plan_debug_read(lance_plan_t plan, int what, void* dst_host, size_t bytes);
+
+/* When acc_dev is non-NULL, subsequent forwards also write the raw int32
+ * accumulators [16][M][K] (gemm_codes per position, lowpgemm.hpp:76-100)
+ * from the same GEMM kernel.  Pass NULL to disable. */
+LANCE_API int lance_plan_set_acc_dump(lance_plan_t plan, int32_t* acc_dev);
+
+/* Kernel launches issued by the most recent forward on this plan. */
+LANCE_API int lance_plan_last_launch_count(lance_plan_t plan);
+
+/* Synthetic-input fixture: lance::UniformSource(seed) stream (rng.hpp:27-47),
+ * mt19937_64 top-24-bit -> U(-1,1).  Host memory. */
+LANCE_API void lance_uniform_fill(uint64_t seed, float* out, size_t count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LANCE_B200_H */

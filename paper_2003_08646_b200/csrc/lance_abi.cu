@@ -1,0 +1,534 @@
+// lance_abi.cu -- host side of the B200 LANCE path behind the C ABI declared
+// in include/lance_b200.h.  Owns validation (mirrors engines.hpp:46-91,
+// 496-499 with the reference's messages), plan/workspace management, TMA
+// tensor-map construction and the stream-ordered launch sequence
+// K0 -> K1 -> K3/K4 (+ K2 once per layer).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <random>
+#include <string>
+#include <tuple>
+
+#include "../../include/lance_b200.h"
+#include "lance_kernels.cuh"
+
+using namespace lance_dev;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(LANCE_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define LANCE_CUDA(call)                                         \
+  do {                                                           \
+    cudaError_t e_ = (call);                                     \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);          \
+  } while (0)
+
+int out_h(const lance_conv_spec& s) { return s.h + 2 * s.pad - 3 + 1; }
+int out_w(const lance_conv_spec& s) { return s.w + 2 * s.pad - 3 + 1; }
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+// ConvSpec::validate (engines.hpp:46-53), LanceConfig::validate (:66-79),
+// lance_gemm's mode / depth checks (:496-499; lowpgemm.hpp:28).
+int validate(const lance_conv_spec* s, const lance_config* c) {
+  if (!s || !c) return fail(LANCE_ERR_INVALID_ARGUMENT, "lance: null spec or config");
+  if (s->n < 1 || s->c < 1 || s->h < 1 || s->w < 1 || s->k < 1)
+    return fail(LANCE_ERR_INVALID_ARGUMENT, "ConvSpec: all dims must be >= 1");
+  if (s->pad != 0 && s->pad != 1)
+    return fail(LANCE_ERR_INVALID_ARGUMENT, "ConvSpec: pad must be 0 or 1");
+  if (out_h(*s) < 1 || out_w(*s) < 1)
+    return fail(LANCE_ERR_INVALID_ARGUMENT, "ConvSpec: output dims collapse to zero");
+  auto ok = [](int b) { return (b >= 2 && b <= 8) || b == 32; };
+  if (!ok(c->bits_w) || !ok(c->bits_i))
+    return fail(LANCE_ERR_INVALID_ARGUMENT, "LanceConfig: bits must be in [2, 8] or 32");
+  if (c->mode == LANCE_MODE_GEMM) {
+    if (c->granularity == LANCE_GRAN_PER_TILE)
+      return fail(LANCE_ERR_INVALID_ARGUMENT,
+                  "LanceConfig: Gemm mode cannot use PerTile granularity; integer "
+                  "accumulation across channels needs one scale per position");
+    if (c->bits_w == 32 || c->bits_i == 32)
+      return fail(LANCE_ERR_INVALID_ARGUMENT,
+                  "LanceConfig: Gemm mode requires quantized operands (bits <= 8)");
+  }
+  if (c->granularity != LANCE_GRAN_PER_TILE && c->granularity != LANCE_GRAN_PER_POSITION &&
+      c->granularity != LANCE_GRAN_PER_TENSOR)
+    return fail(LANCE_ERR_INVALID_ARGUMENT, "LanceConfig: unknown granularity");
+  if (c->mode != LANCE_MODE_GEMM)
+    return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_gemm: cfg.mode must be Gemm");
+  if (s->c > 32768)
+    return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_gemm: channel count exceeds GEMM depth bound");
+  return LANCE_OK;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// [16][rows][C_pad] u8, box = BK bytes x box_rows x 1, swizzle = BK bytes.
+int make_code_map(CUtensorMap* map, void* base, long long rows, int c_pad, int bk, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(LANCE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(c_pad), static_cast<cuuint64_t>(rows), 16};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(c_pad),
+                                 static_cast<cuuint64_t>(rows) * c_pad};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(bk), static_cast<cuuint32_t>(box_rows), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUtensorMapSwizzle sw = bk == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                          : (bk == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                      : CU_TENSOR_MAP_SWIZZLE_32B);
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LANCE_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return LANCE_OK;
+}
+
+}  // namespace
+
+struct lance_plan_s {
+  int device = 0;
+  lance_conv_spec spec{};
+  lance_config cfg{};
+  int OH = 0, OW = 0, TH = 0, TW = 0, P = 0;
+  long long M = 0;
+  int C_pad = 0, K_pad = 0, BK = 32;
+  int sm_count = 148;
+  int range_grid = 1, filter_grid = 1;
+  InGeom in_geom{};
+  FilterGeom f_geom{};
+  GemmGeom gemm_geom{};
+  bool vec4 = false;
+  // device memory
+  uint8_t* codes_a = nullptr;   // [16][M][C_pad]
+  int32_t* rowsum = nullptr;    // [16][M]
+  uint8_t* codes_w = nullptr;   // [16][K_pad][C_pad]
+  int32_t* colsum = nullptr;    // [16][K_pad]
+  float* u_tmp = nullptr;       // [16][K][C]
+  float* partials = nullptr;    // [max(range_grid, filter_grid)][32]
+  LanceDevState* state = nullptr;
+  size_t bytes = 0;
+  CUtensorMap tmA{}, tmB{};
+  bool filters_ready = false;
+  int32_t* acc_dump = nullptr;
+  const float* bias = nullptr;
+  int relu = 0;
+  int last_launches = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+void free_plan(lance_plan_s* p) {
+  cudaFree(p->codes_a);
+  cudaFree(p->rowsum);
+  cudaFree(p->codes_w);
+  cudaFree(p->colsum);
+  cudaFree(p->u_tmp);
+  cudaFree(p->partials);
+  cudaFree(p->state);
+}
+
+template <typename T>
+int dev_alloc(lance_plan_s* p, T** ptr, size_t bytes) {
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(ptr), bytes < 16 ? 16 : bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  p->bytes += bytes;
+  return LANCE_OK;
+}
+
+int pow2ceil(int v) {
+  int r = 1;
+  while (r < v) r <<= 1;
+  return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lance_abi_version(void) { return LANCE_B200_ABI_VERSION; }
+
+const char* lance_status_string(int s) {
+  switch (s) {
+    case LANCE_OK: return "ok";
+    case LANCE_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case LANCE_ERR_NAN: return "NaN in data";
+    case LANCE_ERR_CUDA: return "CUDA error";
+    case LANCE_ERR_NO_DEVICE: return "no sm_100 device";
+    default: return "unknown status";
+  }
+}
+
+const char* lance_last_error(void) { return g_err.c_str(); }
+
+int lance_validate(const lance_conv_spec* spec, const lance_config* cfg) {
+  return validate(spec, cfg);
+}
+
+uint64_t lance_direct_multiply_count(const lance_conv_spec* s) {
+  return uint64_t(s->n) * s->k * s->c * uint64_t(out_h(*s)) * out_w(*s) * 9u;
+}
+
+uint64_t lance_winograd_multiply_count(const lance_conv_spec* s) {
+  const uint64_t tiles = uint64_t((out_h(*s) + 1) / 2) * ((out_w(*s) + 1) / 2);
+  return 16u * tiles * s->n * s->c * uint64_t(s->k);
+}
+
+void lance_uniform_fill(uint64_t seed, float* out, size_t count) {
+  std::mt19937_64 rng(seed);  // UniformSource (rng.hpp:27-47)
+  for (size_t i = 0; i < count; ++i) {
+    const auto top = static_cast<uint32_t>(rng() >> 40);
+    out[i] = float(top) * (1.0f / 8388608.0f) - 1.0f;
+  }
+}
+
+int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int device,
+                      lance_plan_t* out) {
+  if (!out) return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_create: null output");
+  *out = nullptr;
+  int rc = validate(spec, cfg);
+  if (rc) return rc;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(LANCE_ERR_NO_DEVICE,
+                "no CUDA device: the B200 lance_gemm path has no CPU fallback");
+  }
+  if (device < 0 || device >= ndev) return fail(LANCE_ERR_INVALID_ARGUMENT, "bad device index");
+  cudaDeviceProp prop;
+  LANCE_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(LANCE_ERR_NO_DEVICE, std::string("device ") + prop.name +
+                                         " is not sm_100 (this build targets sm_100a only)");
+  DeviceGuard guard(device);
+
+  auto* p = new lance_plan_s();
+  p->device = device;
+  p->spec = *spec;
+  p->cfg = *cfg;
+  p->sm_count = prop.multiProcessorCount;
+  p->OH = out_h(*spec);
+  p->OW = out_w(*spec);
+  p->TH = (p->OH + 1) / 2;
+  p->TW = (p->OW + 1) / 2;
+  p->P = p->TH * p->TW;
+  p->M = static_cast<long long>(spec->n) * p->P;
+  p->C_pad = round_up(spec->c, 32);
+  p->K_pad = round_up(spec->k, kBN);
+  p->BK = (p->C_pad % 128 == 0) ? 128 : (p->C_pad % 64 == 0 ? 64 : 32);
+  p->vec4 = (spec->c % 4) == 0;
+
+  InGeom& g = p->in_geom;
+  g.M = p->M;
+  g.P = p->P;
+  g.TW = p->TW;
+  g.H = spec->h;
+  g.W = spec->w;
+  g.C = spec->c;
+  g.C4 = (spec->c + 3) / 4;
+  g.C_pad = p->C_pad;
+  g.pad = spec->pad;
+  g.G = pow2ceil(g.C4) > 32 ? 32 : pow2ceil(g.C4);
+  g.TPB = 256 / g.G;
+  g.num_tile_blocks = (p->M + g.TPB - 1) / g.TPB;
+  g.granularity = cfg->granularity;
+  p->range_grid = static_cast<int>(std::min<long long>(g.num_tile_blocks, 2LL * p->sm_count));
+
+  FilterGeom& f = p->f_geom;
+  f.K = spec->k;
+  f.C = spec->c;
+  f.K_pad = p->K_pad;
+  f.C_pad = p->C_pad;
+  f.granularity = cfg->granularity;
+  const long long kc = static_cast<long long>(spec->k) * spec->c;
+  p->filter_grid = static_cast<int>(std::min<long long>((kc + 255) / 256, 2LL * p->sm_count));
+
+  GemmGeom& gg = p->gemm_geom;
+  gg.M = p->M;
+  gg.K = spec->k;
+  gg.C = spec->c;
+  gg.P = p->P;
+  gg.TW = p->TW;
+  gg.OH = p->OH;
+  gg.OW = p->OW;
+  gg.num_kchunks = p->C_pad / p->BK;
+  gg.num_n_tiles = p->K_pad / kBN;
+
+  const size_t codes_a_bytes = static_cast<size_t>(16) * p->M * p->C_pad;
+  const size_t codes_w_bytes = static_cast<size_t>(16) * p->K_pad * p->C_pad;
+  const int part_rows = std::max(p->range_grid, p->filter_grid);
+  if ((rc = dev_alloc(p, &p->codes_a, codes_a_bytes)) ||
+      (rc = dev_alloc(p, &p->rowsum, sizeof(int32_t) * 16 * p->M)) ||
+      (rc = dev_alloc(p, &p->codes_w, codes_w_bytes)) ||
+      (rc = dev_alloc(p, &p->colsum, sizeof(int32_t) * 16 * p->K_pad)) ||
+      (rc = dev_alloc(p, &p->u_tmp, sizeof(float) * 16 * kc)) ||
+      (rc = dev_alloc(p, &p->partials, sizeof(float) * 32 * part_rows)) ||
+      (rc = dev_alloc(p, &p->state, sizeof(LanceDevState)))) {
+    free_plan(p);
+    delete p;
+    return rc;
+  }
+  // Channel / filter padding stays zero forever: both GEMM operands are padded
+  // with code 0, which adds nothing to the accumulators.
+  cudaError_t e = cudaMemset(p->codes_a, 0, codes_a_bytes);
+  if (e == cudaSuccess) e = cudaMemset(p->codes_w, 0, codes_w_bytes);
+  if (e == cudaSuccess) e = cudaMemset(p->colsum, 0, sizeof(int32_t) * 16 * p->K_pad);
+  LanceDevState init{};
+  init.bits_i = cfg->bits_i;
+  init.bits_w = cfg->bits_w;
+  if (e == cudaSuccess) e = cudaMemcpy(p->state, &init, sizeof init, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    free_plan(p);
+    delete p;
+    return cuda_fail(e, "plan init");
+  }
+  if ((rc = make_code_map(&p->tmA, p->codes_a, p->M, p->C_pad, p->BK, kBM)) ||
+      (rc = make_code_map(&p->tmB, p->codes_w, p->K_pad, p->C_pad, p->BK, kBN))) {
+    free_plan(p);
+    delete p;
+    return rc;
+  }
+  *out = p;
+  return LANCE_OK;
+}
+
+int lance_plan_destroy(lance_plan_t p) {
+  if (!p) return LANCE_OK;
+  DeviceGuard guard(p->device);
+  free_plan(p);
+  delete p;
+  return LANCE_OK;
+}
+
+size_t lance_plan_device_bytes(lance_plan_t p) { return p ? p->bytes : 0; }
+
+int lance_plan_set_filters(lance_plan_t p, const float* w_dev, void* stream) {
+  if (!p || !w_dev) return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_set_filters: null argument");
+  DeviceGuard guard(p->device);
+  auto s = static_cast<cudaStream_t>(stream);
+  LANCE_CUDA(launch_filter_prepare(w_dev, p->u_tmp, p->partials, p->filter_grid, p->codes_w,
+                                   p->colsum, p->state, p->f_geom, s));
+  p->filters_ready = true;
+  return LANCE_OK;
+}
+
+static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStream_t s,
+                       const lance_qparams* static_params) {
+  if (!p || !x_dev || !y_dev) return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_forward: null argument");
+  if (!p->filters_ready)
+    return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_forward: filters not set");
+  DeviceGuard guard(p->device);
+  int launches = 0;
+  if (static_params) {
+    StaticParams prm{};
+    for (int i = 0; i < 16; ++i) {
+      if (static_params[i].bits != p->cfg.bits_i)
+        return fail(LANCE_ERR_INVALID_ARGUMENT, "static params: bits differ from cfg.bits_i");
+      prm.tmin[i] = static_params[i].t_min;
+      prm.tmax[i] = static_params[i].t_max;
+      prm.scale[i] = static_params[i].scale;
+    }
+    LANCE_CUDA(launch_static_params(p->state, prm, p->spec.c, s));
+  } else {
+    LANCE_CUDA(launch_input_range(x_dev, p->partials, p->range_grid, p->state, p->in_geom,
+                                  p->vec4, s));
+  }
+  ++launches;
+  LANCE_CUDA(launch_input_quant(x_dev, p->codes_a, p->rowsum, p->state, p->in_geom, p->vec4, s));
+  ++launches;
+  LANCE_CUDA(launch_gemm(&p->tmA, &p->tmB, p->BK, p->rowsum, p->colsum, p->state, y_dev,
+                         p->acc_dump, p->bias, p->relu, p->gemm_geom, s));
+  ++launches;
+  p->last_launches = launches;
+  return LANCE_OK;
+}
+
+int lance_plan_forward(lance_plan_t p, const float* x_dev, float* y_dev, void* stream) {
+  return run_forward(p, x_dev, y_dev, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int lance_plan_forward_static(lance_plan_t p, const lance_qparams* in_params16,
+                              const float* x_dev, float* y_dev, void* stream) {
+  if (!in_params16) return fail(LANCE_ERR_INVALID_ARGUMENT, "static params: null");
+  return run_forward(p, x_dev, y_dev, static_cast<cudaStream_t>(stream), in_params16);
+}
+
+int lance_plan_set_epilogue(lance_plan_t p, const float* bias_dev, int relu) {
+  if (!p) return fail(LANCE_ERR_INVALID_ARGUMENT, "null plan");
+  p->bias = bias_dev;
+  p->relu = relu ? 1 : 0;
+  return LANCE_OK;
+}
+
+int lance_plan_set_acc_dump(lance_plan_t p, int32_t* acc_dev) {
+  if (!p) return fail(LANCE_ERR_INVALID_ARGUMENT, "null plan");
+  p->acc_dump = acc_dev;
+  return LANCE_OK;
+}
+
+int lance_plan_last_launch_count(lance_plan_t p) { return p ? p->last_launches : 0; }
+
+int lance_plan_sync(lance_plan_t p, void* stream) {
+  if (!p) return fail(LANCE_ERR_INVALID_ARGUMENT, "null plan");
+  DeviceGuard guard(p->device);
+  LANCE_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  int flags[2];
+  LANCE_CUDA(cudaMemcpy(flags, &p->state->nan_in, sizeof flags, cudaMemcpyDeviceToHost));
+  if (flags[0] || flags[1]) return fail(LANCE_ERR_NAN, "fit_params: NaN in values");
+  return LANCE_OK;
+}
+
+int lance_plan_get_params(lance_plan_t p, lance_qparams* in16, lance_qparams* w16) {
+  if (!p) return fail(LANCE_ERR_INVALID_ARGUMENT, "null plan");
+  DeviceGuard guard(p->device);
+  LanceDevState st;
+  LANCE_CUDA(cudaDeviceSynchronize());
+  LANCE_CUDA(cudaMemcpy(&st, p->state, sizeof st, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < 16; ++i) {
+    if (in16) in16[i] = {p->cfg.bits_i, st.a_tmin[i], st.a_tmax[i], st.a_scale[i]};
+    if (w16) w16[i] = {p->cfg.bits_w, st.w_tmin[i], st.w_tmax[i], st.w_scale[i]};
+  }
+  return LANCE_OK;
+}
+
+int lance_plan_debug_read(lance_plan_t p, int what, void* dst, size_t bytes) {
+  if (!p || !dst) return fail(LANCE_ERR_INVALID_ARGUMENT, "null argument");
+  DeviceGuard guard(p->device);
+  LANCE_CUDA(cudaDeviceSynchronize());
+  const long long M = p->M;
+  const int C = p->spec.c, K = p->spec.k;
+  switch (what) {
+    case LANCE_DBG_CODES_A: {
+      if (bytes != size_t(16) * M * C) return fail(LANCE_ERR_INVALID_ARGUMENT, "bad size");
+      LANCE_CUDA(cudaMemcpy2D(dst, C, p->codes_a, p->C_pad, C, size_t(16) * M,
+                              cudaMemcpyDeviceToHost));
+      return LANCE_OK;
+    }
+    case LANCE_DBG_ROWSUM: {
+      if (bytes != sizeof(int32_t) * 16 * M) return fail(LANCE_ERR_INVALID_ARGUMENT, "bad size");
+      LANCE_CUDA(cudaMemcpy(dst, p->rowsum, bytes, cudaMemcpyDeviceToHost));
+      return LANCE_OK;
+    }
+    case LANCE_DBG_CODES_W: {  // device [16][K_pad][C_pad] -> reference [16][C][K]
+      if (bytes != size_t(16) * C * K) return fail(LANCE_ERR_INVALID_ARGUMENT, "bad size");
+      std::string tmp(size_t(16) * p->K_pad * p->C_pad, '\0');
+      LANCE_CUDA(cudaMemcpy(tmp.data(), p->codes_w, tmp.size(), cudaMemcpyDeviceToHost));
+      auto* out = static_cast<uint8_t*>(dst);
+      for (int q = 0; q < 16; ++q)
+        for (int c = 0; c < C; ++c)
+          for (int k = 0; k < K; ++k)
+            out[(size_t(q) * C + c) * K + k] =
+                static_cast<uint8_t>(tmp[(size_t(q) * p->K_pad + k) * p->C_pad + c]);
+      return LANCE_OK;
+    }
+    case LANCE_DBG_COLSUM: {
+      if (bytes != sizeof(int32_t) * 16 * K) return fail(LANCE_ERR_INVALID_ARGUMENT, "bad size");
+      LANCE_CUDA(cudaMemcpy2D(dst, sizeof(int32_t) * K, p->colsum, sizeof(int32_t) * p->K_pad,
+                              sizeof(int32_t) * K, 16, cudaMemcpyDeviceToHost));
+      return LANCE_OK;
+    }
+    default:
+      return fail(LANCE_ERR_INVALID_ARGUMENT, "unknown debug buffer");
+  }
+}
+
+// --------------------------------------------------------------------------
+// Host-buffer drop-in for lance::lance_gemm (engines.hpp:492-536).
+
+namespace {
+struct HostCtx {
+  lance_plan_t plan = nullptr;
+  float *x = nullptr, *w = nullptr, *y = nullptr;
+  cudaStream_t stream = nullptr;
+};
+using Key = std::tuple<int, int, int, int, int, int, int, int, int, int>;
+thread_local std::map<Key, HostCtx> g_host_ctx;
+}  // namespace
+
+int lance_gemm_host(const lance_conv_spec* spec, const lance_config* cfg, const float* x,
+                    const float* w, float* y) {
+  int rc = validate(spec, cfg);
+  if (rc) return rc;
+  if (!x || !w || !y) return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_gemm: null buffer");
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(LANCE_ERR_NO_DEVICE, "no CUDA device: the B200 lance_gemm path has no CPU fallback");
+  }
+  const Key key{dev, spec->n, spec->c, spec->h, spec->w, spec->k, spec->pad, cfg->bits_w,
+                cfg->bits_i, cfg->granularity};
+  HostCtx& ctx = g_host_ctx[key];
+  const size_t xb = sizeof(float) * size_t(spec->n) * spec->h * spec->w * spec->c;
+  const size_t wb = sizeof(float) * size_t(spec->k) * 9 * spec->c;
+  const size_t yb = sizeof(float) * size_t(spec->n) * out_h(*spec) * out_w(*spec) * spec->k;
+  if (!ctx.plan) {
+    if ((rc = lance_plan_create(spec, cfg, dev, &ctx.plan))) {
+      g_host_ctx.erase(key);
+      return rc;
+    }
+    cudaError_t e = cudaMalloc(&ctx.x, xb);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx.w, wb);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx.y, yb);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx.stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      lance_plan_destroy(ctx.plan);
+      cudaFree(ctx.x);
+      cudaFree(ctx.w);
+      cudaFree(ctx.y);
+      g_host_ctx.erase(key);
+      return cuda_fail(e, "lance_gemm host staging");
+    }
+  }
+  LANCE_CUDA(cudaMemcpyAsync(ctx.w, w, wb, cudaMemcpyHostToDevice, ctx.stream));
+  LANCE_CUDA(cudaMemcpyAsync(ctx.x, x, xb, cudaMemcpyHostToDevice, ctx.stream));
+  if ((rc = lance_plan_set_filters(ctx.plan, ctx.w, ctx.stream))) return rc;
+  if ((rc = lance_plan_forward(ctx.plan, ctx.x, ctx.y, ctx.stream))) return rc;
+  LANCE_CUDA(cudaMemcpyAsync(y, ctx.y, yb, cudaMemcpyDeviceToHost, ctx.stream));
+  // One synchronisation per call; a NaN seen by the range passes is reported
+  // like the reference's throw from fit_params (y is then unspecified).
+  return lance_plan_sync(ctx.plan, ctx.stream);
+}
+
+}  // extern "C"
