@@ -1,0 +1,426 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 LANCE lance_gemm path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2]): the 13 stride-1 3x3 conv layers of
+ResNet-18 -- 4x (C=K=64, 56x56), 3x (128, 28x28), 3x (256, 14x14),
+3x (512, 7x7) -- LANCE 8-bit F(2x2,3x3), PerPosition, pad 1, batch 256 per GPU.
+Each layer runs on its own synthetic input (reference bench convention,
+bench.hpp:128-133: UniformSource(seed), x then w).  One "step" = the 13 layer
+forwards (K0 range -> K1 transform+quantise -> K3/K4 tcgen05 GEMM + fused
+epilogue) on device-resident inputs; filters are prepared once per layer (K2)
+outside the step, as the north star specifies.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N>1 is launched by torchrun (one rank per GPU, NCCL); every rank runs its own
+batch of 256 with no collective on the data path (weak scaling); the step time
+is the max over ranks.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+RESNET18 = [(64, 64, 56)] * 4 + [(128, 128, 28)] * 3 + [(256, 256, 14)] * 3 + [(512, 512, 7)] * 3
+METRIC = "int8 Winograd conv TOPS-equivalent & images/sec vs roofline, 1/2/4/8 B200 vs CPU ref"
+WORKLOAD = "resnet18_3x3_stride1_convs_x13"
+HBM_FALLBACK = 6650.0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def layer_dims(c, k, h, n, pad=1):
+    oh = h + 2 * pad - 2
+    th = (oh + 1) // 2
+    p = th * th
+    m = n * p
+    return oh, p, m
+
+
+def stage_bytes(c, k, h, n):
+    """Algorithmic HBM bytes per launch."""
+    oh, _, m = layer_dims(c, k, h, n)
+    x = 4 * n * h * h * c
+    k0 = x
+    k1 = x + 16 * m * c + 4 * 16 * m
+    k3 = 16 * m * c + 16 * c * k + 4 * 16 * m + 4 * 16 * k + 4 * n * oh * oh * k
+    return k0, k1, k3
+
+
+def direct_macs(c, k, h, n):
+    oh = h
+    return n * k * c * oh * oh * 9
+
+
+def winograd_macs(c, k, h, n):
+    _, _, m = layer_dims(c, k, h, n)
+    return 16 * m * c * k
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.marks = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self):
+        self.marks.append(time.time())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        t0, t1 = (self.marks[0], self.marks[1]) if len(self.marks) >= 2 else (0.0, time.time())
+        rows = [l for (t, l) in self.lines if t0 - 0.06 <= t <= t1 + 0.06] or [l for _, l in self.lines]
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            f = [v.strip() for v in r.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = max(smax, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_reference_images_per_s(batch: int, reps: int, threads: int):
+    """The reference's own lance_gemm (oracle/_ref, compiled from the reference
+    headers) on the 13 layer shapes at `batch` images, median of `reps`
+    steady_clock repeats each (bench.hpp:157-167)."""
+    import oracle
+    ref = oracle.Reference()
+    total = 0.0
+    for i, (c, k, h) in enumerate(RESNET18):
+        med_ns, _ = ref.time_lance_gemm(oracle.Spec(batch, c, h, h, k, 1), threads, 42 + i, reps)
+        total += med_ns * 1e-9
+    return batch / total, total
+
+
+def run_reference_arm(args, ws, rank):
+    """--impl reference: the reference CPU implementation on the host cores."""
+    if rank != 0:
+        return
+    import oracle
+    threads = os.cpu_count() or 1
+    batch = args.ref_batch
+    ref = oracle.Reference()
+    times = []
+    for step in range(args.warmup + args.steps):
+        t = 0.0
+        for i, (c, k, h) in enumerate(RESNET18):
+            med_ns, _ = ref.time_lance_gemm(oracle.Spec(batch, c, h, h, k, 1), threads, 42 + i, 1)
+            t += med_ns * 1e-9
+        if step >= args.warmup:
+            times.append(t)
+    mean_t = sum(times) / len(times)
+    value = batch / mean_t
+    tops = 2 * sum(direct_macs(c, k, h, batch) for c, k, h in RESNET18) / mean_t / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": mean_t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (reference UniformSource, seed 42+layer)",
+        "config": {"workload": WORKLOAD, "batch_per_step": batch,
+                   "note": f"bounded CPU sample: {batch} images per step of the batch-256 workload"},
+        "tops_equivalent": tops,
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "reference",
+                         "sample": f"13 ResNet-18 3x3 layers at batch {batch}, one lance_gemm call each per step"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def int8_peak_tops(device):
+    """Dense INT8 tensor peak measured here (cuBLASLt int8 GEMM via torch._int_mm,
+    8192^3): the denominator for the GEMM stage's tensor fraction."""
+    import torch
+    try:
+        n = 8192
+        a = torch.randint(-64, 64, (n, n), dtype=torch.int8, device=device)
+        b = torch.randint(-64, 64, (n, n), dtype=torch.int8, device=device)
+        for _ in range(3):
+            torch._int_mm(a, b)
+        torch.cuda.synchronize(device)
+        best = 1e9
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1) * 1e-3)
+        return 2 * n ** 3 / best / 1e12
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--ref-batch", type=int, default=2)
+    ap.add_argument("--cpu-batch", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--layers", type=str, default="", help="comma list of layer indices (debug)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference_arm(args, ws, rank)
+        return
+
+    import numpy as np
+    import torch
+    import paper_2003_08646_b200 as lance
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+
+    layers = RESNET18
+    if args.layers:
+        layers = [RESNET18[int(i)] for i in args.layers.split(",")]
+    N = args.batch
+    cfg = lance.LanceConfig(8, 8, lance.Granularity.PerPosition, lance.LanceMode.Gemm)
+
+    # Synthetic inputs: UniformSource(seed) x then w (bench.hpp:129-133), per layer and rank.
+    state = []
+    for i, (c, k, h) in enumerate(layers):
+        spec = lance.ConvSpec(N, c, h, h, k, 1)
+        nx, nw = N * h * h * c, k * 9 * c
+        host = lance.uniform_floats(nx + nw, 42 + 1000 * rank + i)
+        x = torch.from_numpy(host[:nx]).to(dev).view(N, h, h, c)
+        w = torch.from_numpy(host[nx:]).to(dev).view(k, 3, 3, c)
+        conv = lance.LanceConv(spec, cfg, device=local)
+        conv.set_filters(w)
+        y = torch.empty((N, spec.out_h(), spec.out_w(), k), dtype=torch.float32, device=dev)
+        state.append((spec, conv, x, w, y, host))
+    torch.cuda.synchronize(dev)
+
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        for spec, conv, x, w, y, _ in state:
+            conv.forward(x, y, stream=stream)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(args.warmup):
+        step()
+    for _, conv, *_ in state:
+        conv.sync(stream)
+    for _, conv, *_ in state:
+        conv.stage_timing(True)
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    clocks.mark()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks.mark()
+    if pg:
+        pg.barrier()
+    clk = clocks.stop()
+    elapsed = e0.elapsed_time(e1) * 1e-3
+    for _, conv, *_ in state:
+        conv.sync(stream)  # surfaces a NaN error from any range pass
+
+    # per-stage device times over the timed region
+    stage_ms = np.zeros(3)
+    stage_bytes_tot = np.zeros(3)
+    per_layer = []
+    for spec, conv, *_ in state:
+        ms, nf = conv.read_stage_times()
+        conv.stage_timing(False)
+        b = stage_bytes(spec.c, spec.k, spec.h, N)
+        stage_ms += np.array(ms)
+        stage_bytes_tot += np.array(b) * nf
+        per_layer.append({"c": spec.c, "k": spec.k, "h": spec.h,
+                          "us_per_forward": [round(m / max(nf, 1) * 1e3, 2) for m in ms]})
+
+    if pg:
+        t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        elapsed = float(t.item())
+
+    images = N * args.steps * ws
+    value = images / elapsed
+    ms_per_step = elapsed / args.steps * 1e3
+    tops_eq = 2 * sum(direct_macs(c, k, h, N) for c, k, h in layers) * args.steps * ws / elapsed / 1e12
+
+    hbm, hbm_src = peaks()
+    names = ["K0_input_range", "K1_transform_quantize", "K3K4_gemm_epilogue"]
+    stages = {}
+    for i, nm in enumerate(names):
+        gbs = stage_bytes_tot[i] / (stage_ms[i] * 1e-3) / 1e9 if stage_ms[i] > 0 else 0.0
+        stages[nm] = {"ms_per_step": stage_ms[i] / args.steps, "achieved_gbs": gbs,
+                      "frac_hbm": gbs / hbm}
+    dom = int(np.argmax(stage_ms))
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        traffic = tj.get(names[dom])
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "kernel": names[dom], "achieved": stages[names[dom]]["achieved_gbs"],
+                "peak": hbm, "peak_source": hbm_src, "unit": "GB/s",
+                "frac": stages[names[dom]]["achieved_gbs"] / hbm, "traffic": traffic,
+                "algorithmic_bytes_per_step": float(stage_bytes_tot[dom] / args.steps),
+                "stages": stages}
+    i8 = int8_peak_tops(dev) if rank == 0 else None
+    t3 = stage_ms[2] * 1e-3 / args.steps
+    wmacs = sum(winograd_macs(c, k, h, N) for c, k, h in layers)
+    roofline["gemm_stage_int8"] = {"achieved_tops": 2 * wmacs / t3 / 1e12 if t3 > 0 else None,
+                                   "peak_tops": i8, "peak_source": "measured here: torch._int_mm 8192^3",
+                                   "frac": (2 * wmacs / t3 / 1e12 / i8) if (i8 and t3 > 0) else None}
+    roofline["per_layer"] = per_layer
+
+    # ---- e2e through the public host API (reference-facing lance_gemm) ----
+    e2e = None
+    if not args.no_e2e:
+        pinned = []
+        for spec, conv, x, w, y, host in state:
+            hx = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
+            hx.copy_(torch.from_numpy(host[: x.numel()]).view(x.shape))
+            hw = torch.empty(w.shape, dtype=torch.float32, pin_memory=True)
+            hw.copy_(torch.from_numpy(host[x.numel():]).view(w.shape))
+            hy = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
+            pinned.append((spec, hx.numpy(), hw.numpy(), hy.numpy()))
+        h2d = sum(a.nbytes + b.nbytes for _, a, b, _ in pinned)
+        d2h = sum(c.nbytes for _, _, _, c in pinned)
+
+        def e2e_step():
+            for spec, hx, hw, hy in pinned:
+                lance.lance_gemm(hx, hw, spec, cfg, out=hy)
+
+        e2e_step()
+        if pg:
+            pg.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        te = time.perf_counter() - t0
+        if pg:
+            t = torch.tensor([te], device=dev, dtype=torch.float64)
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            te = float(t.item())
+        e2e = {"value": N * args.e2e_steps * ws / te, "unit": "images/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "steps": args.e2e_steps,
+               "api": "lance_gemm(x, w, spec, cfg) host drop-in (K2 + K0 + K1 + K3/K4 per call, pinned host buffers)"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        try:
+            threads = os.cpu_count() or 1
+            v, tot = cpu_reference_images_per_s(args.cpu_batch, 3, threads)
+            cpu = {"value": v, "unit": "images/s", "cores": threads, "kind": "reference",
+                   "sample": f"13 ResNet-18 3x3 layers at batch {args.cpu_batch} (of 256), reference "
+                             f"lance_gemm median of 3 steady_clock repeats per layer ({tot:.2f} s/pass)"}
+        except Exception as e:  # reference shim absent
+            cpu = {"value": None, "unit": "images/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (lance::UniformSource seed 42+layer, x then w; bench.hpp:129-133)",
+            "config": {"workload": WORKLOAD, "batch_per_gpu": N, "global_batch": N * ws,
+                       "layers": [list(l) for l in layers], "winograd": "F(2x2,3x3)",
+                       "bits_w": 8, "bits_i": 8, "granularity": "PerPosition", "pad": 1,
+                       "parallelism": f"batch-shard x{ws}, no collective",
+                       "filters": "prepared once per layer (K2) outside the step",
+                       "l2": "no flush: per-step working set (13 layers x, codes, y) ~4 GB >> 126 MB L2"},
+            "tops_equivalent": tops_eq,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 3 * len(layers) * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -146,6 +146,14 @@ LANCE_API int lance_plan_debug_read(lance_plan_t plan, int what, void* dst_host,
  * from the same GEMM kernel.  Pass NULL to disable. */
 LANCE_API int lance_plan_set_acc_dump(lance_plan_t plan, int32_t* acc_dev);
 
+/* Per-stage device timing (CUDA events recorded on the forward's stream
+ * between the K0 / K1 / K3-K4 launches).  enable != 0 starts recording (up to
+ * 4096 forwards); read_stage_times synchronises those events and returns the
+ * summed milliseconds of {K0 range, K1 quantize, K3/K4 GEMM+epilogue} and the
+ * number of forwards they cover, then clears the record. */
+LANCE_API int lance_plan_stage_timing(lance_plan_t plan, int enable);
+LANCE_API int lance_plan_read_stage_times(lance_plan_t plan, double* sum_ms3, int* nforwards);
+
 /* Kernel launches issued by the most recent forward on this plan. */
 LANCE_API int lance_plan_last_launch_count(lance_plan_t plan);
 

@@ -76,6 +76,9 @@ def lib():
         L.lance_plan_debug_read.argtypes = [P, ct.c_int, P, ct.c_size_t]
         L.lance_plan_set_acc_dump.argtypes = [P, P]
         L.lance_plan_last_launch_count.argtypes = [P]
+        L.lance_plan_stage_timing.argtypes = [P, ct.c_int]
+        L.lance_plan_read_stage_times.argtypes = [P, ct.POINTER(ct.c_double),
+                                                  ct.POINTER(ct.c_int)]
         L.lance_uniform_fill.argtypes = [ct.c_uint64, P, ct.c_size_t]
         L.lance_uniform_fill.restype = None
         _lib = L
@@ -89,5 +92,6 @@ EXPORTED = [
     "lance_plan_set_filters", "lance_plan_forward", "lance_plan_forward_static",
     "lance_plan_set_epilogue", "lance_plan_sync", "lance_plan_get_params",
     "lance_plan_debug_read", "lance_plan_set_acc_dump", "lance_plan_last_launch_count",
+    "lance_plan_stage_timing", "lance_plan_read_stage_times",
     "lance_uniform_fill",
 ]

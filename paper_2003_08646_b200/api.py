@@ -272,6 +272,17 @@ class LanceConv:
     def last_launch_count(self) -> int:
         return int(_lib.lib().lance_plan_last_launch_count(self._plan))
 
+    def stage_timing(self, enable: bool = True):
+        """Record CUDA events between the K0 / K1 / K3-K4 launches of forwards."""
+        _check(_lib.lib().lance_plan_stage_timing(self._plan, int(enable)))
+
+    def read_stage_times(self):
+        """(summed ms of [K0, K1, K3/K4], number of forwards) since enabling."""
+        arr = (ct.c_double * 3)()
+        n = ct.c_int()
+        _check(_lib.lib().lance_plan_read_stage_times(self._plan, arr, ct.byref(n)))
+        return [arr[0], arr[1], arr[2]], n.value
+
     def params(self):
         a = (_lib.CQParams * 16)()
         b = (_lib.CQParams * 16)()

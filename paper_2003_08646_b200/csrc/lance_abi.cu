@@ -14,6 +14,7 @@
 #include <random>
 #include <string>
 #include <tuple>
+#include <vector>
 
 #include "../../include/lance_b200.h"
 #include "lance_kernels.cuh"
@@ -145,6 +146,9 @@ struct lance_plan_s {
   const float* bias = nullptr;
   int relu = 0;
   int last_launches = 0;
+  bool timing = false;
+  std::vector<cudaEvent_t> events;  // 4 per recorded forward
+  int recorded = 0;
 };
 
 namespace {
@@ -161,6 +165,8 @@ struct DeviceGuard {
 };
 
 void free_plan(lance_plan_s* p) {
+  for (cudaEvent_t e : p->events) cudaEventDestroy(e);
+  p->events.clear();
   cudaFree(p->codes_a);
   cudaFree(p->rowsum);
   cudaFree(p->codes_w);
@@ -361,6 +367,17 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
     return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_forward: filters not set");
   DeviceGuard guard(p->device);
   int launches = 0;
+  cudaEvent_t* ev = nullptr;
+  if (p->timing && p->recorded < 4096) {
+    while (p->events.size() < size_t(4) * (p->recorded + 1)) {
+      cudaEvent_t e;
+      LANCE_CUDA(cudaEventCreate(&e));
+      p->events.push_back(e);
+    }
+    ev = &p->events[size_t(4) * p->recorded];
+    ++p->recorded;
+    LANCE_CUDA(cudaEventRecord(ev[0], s));
+  }
   if (static_params) {
     StaticParams prm{};
     for (int i = 0; i < 16; ++i) {
@@ -376,11 +393,14 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
                                   p->vec4, s));
   }
   ++launches;
+  if (ev) LANCE_CUDA(cudaEventRecord(ev[1], s));
   LANCE_CUDA(launch_input_quant(x_dev, p->codes_a, p->rowsum, p->state, p->in_geom, p->vec4, s));
   ++launches;
+  if (ev) LANCE_CUDA(cudaEventRecord(ev[2], s));
   LANCE_CUDA(launch_gemm(&p->tmA, &p->tmB, p->BK, p->rowsum, p->colsum, p->state, y_dev,
                          p->acc_dump, p->bias, p->relu, p->gemm_geom, s));
   ++launches;
+  if (ev) LANCE_CUDA(cudaEventRecord(ev[3], s));
   p->last_launches = launches;
   return LANCE_OK;
 }
@@ -409,6 +429,31 @@ int lance_plan_set_acc_dump(lance_plan_t p, int32_t* acc_dev) {
 }
 
 int lance_plan_last_launch_count(lance_plan_t p) { return p ? p->last_launches : 0; }
+
+int lance_plan_stage_timing(lance_plan_t p, int enable) {
+  if (!p) return fail(LANCE_ERR_INVALID_ARGUMENT, "null plan");
+  p->timing = enable != 0;
+  p->recorded = 0;
+  return LANCE_OK;
+}
+
+int lance_plan_read_stage_times(lance_plan_t p, double* sum_ms3, int* nforwards) {
+  if (!p || !sum_ms3) return fail(LANCE_ERR_INVALID_ARGUMENT, "null argument");
+  DeviceGuard guard(p->device);
+  sum_ms3[0] = sum_ms3[1] = sum_ms3[2] = 0.0;
+  for (int f = 0; f < p->recorded; ++f) {
+    cudaEvent_t* ev = &p->events[size_t(4) * f];
+    LANCE_CUDA(cudaEventSynchronize(ev[3]));
+    for (int i = 0; i < 3; ++i) {
+      float ms = 0.f;
+      LANCE_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+      sum_ms3[i] += ms;
+    }
+  }
+  if (nforwards) *nforwards = p->recorded;
+  p->recorded = 0;
+  return LANCE_OK;
+}
 
 int lance_plan_sync(lance_plan_t p, void* stream) {
   if (!p) return fail(LANCE_ERR_INVALID_ARGUMENT, "null plan");
