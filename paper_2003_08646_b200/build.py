@@ -18,8 +18,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_build")
 LIB = os.path.join(OUT_DIR, "liblance_b200.so")
-SOURCES = ["lance_kernels.cu", "lance_abi.cu"]
-HEADERS = ["lance_kernels.cuh", "lance_ptx.cuh"]
+SOURCES = ["lance_input.cu", "lance_filter.cu", "lance_gemm.cu", "lance_abi.cu"]
+HEADERS = ["lance_common.cuh", "lance_kernels.cuh", "lance_ptx.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
          "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",

@@ -130,7 +130,8 @@ struct lance_plan_s {
   InGeom in_geom{};
   FilterGeom f_geom{};
   GemmGeom gemm_geom{};
-  bool vec4 = false;
+  bool vec2 = false;
+  bool small_acc = false;
   // device memory
   uint8_t* codes_a = nullptr;   // [16][M][C_pad]
   int32_t* rowsum = nullptr;    // [16][M]
@@ -264,23 +265,26 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   p->C_pad = round_up(spec->c, 32);
   p->K_pad = round_up(spec->k, kBN);
   p->BK = (p->C_pad % 128 == 0) ? 128 : (p->C_pad % 64 == 0 ? 64 : 32);
-  p->vec4 = (spec->c % 4) == 0;
+  p->vec2 = (spec->c % 2) == 0;
 
+  if (p->M >= (1LL << 31)) {
+    delete p;
+    return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_gemm: N * tiles exceeds 2^31 rows");
+  }
   InGeom& g = p->in_geom;
-  g.M = p->M;
+  g.M = static_cast<int>(p->M);
   g.P = p->P;
   g.TW = p->TW;
   g.H = spec->h;
   g.W = spec->w;
   g.C = spec->c;
-  g.C4 = (spec->c + 3) / 4;
   g.C_pad = p->C_pad;
   g.pad = spec->pad;
-  g.G = pow2ceil(g.C4) > 32 ? 32 : pow2ceil(g.C4);
-  g.TPB = 256 / g.G;
-  g.num_tile_blocks = (p->M + g.TPB - 1) / g.TPB;
+  g.nchunks = (p->C_pad + kChunk - 1) / kChunk;
   g.granularity = cfg->granularity;
-  p->range_grid = static_cast<int>(std::min<long long>(g.num_tile_blocks, 2LL * p->sm_count));
+  p->range_grid = input_range_grid(g, p->sm_count);
+  p->small_acc = static_cast<double>(spec->c) * ((1 << cfg->bits_i) - 1) *
+                     ((1 << cfg->bits_w) - 1) < 8388608.0;
 
   FilterGeom& f = p->f_geom;
   f.K = spec->k;
@@ -292,7 +296,7 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   p->filter_grid = static_cast<int>(std::min<long long>((kc + 255) / 256, 2LL * p->sm_count));
 
   GemmGeom& gg = p->gemm_geom;
-  gg.M = p->M;
+  gg.M = static_cast<int>(p->M);
   gg.K = spec->k;
   gg.C = spec->c;
   gg.P = p->P;
@@ -390,14 +394,15 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
     LANCE_CUDA(launch_static_params(p->state, prm, p->spec.c, s));
   } else {
     LANCE_CUDA(launch_input_range(x_dev, p->partials, p->range_grid, p->state, p->in_geom,
-                                  p->vec4, s));
+                                  p->vec2, s));
   }
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[1], s));
-  LANCE_CUDA(launch_input_quant(x_dev, p->codes_a, p->rowsum, p->state, p->in_geom, p->vec4, s));
+  LANCE_CUDA(launch_input_quant(x_dev, p->codes_a, p->rowsum, p->state, p->in_geom, p->vec2,
+                                static_params != nullptr, s));
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[2], s));
-  LANCE_CUDA(launch_gemm(&p->tmA, &p->tmB, p->BK, p->rowsum, p->colsum, p->state, y_dev,
+  LANCE_CUDA(launch_gemm(&p->tmA, &p->tmB, p->BK, p->small_acc, p->rowsum, p->colsum, p->state, y_dev,
                          p->acc_dump, p->bias, p->relu, p->gemm_geom, s));
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[3], s));

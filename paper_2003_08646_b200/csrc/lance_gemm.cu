@@ -1,0 +1,293 @@
+// lance_gemm.cu -- K3/K4: the 16 per-position u8 x u8 -> s32 GEMMs of
+// lance_gemm (gemm_codes x 16, lowpgemm.hpp:76-100, engines.hpp:510-525) on
+// tcgen05 kind::i8 with TMA-fed operands and accumulators in TMEM, fused with
+// the affine de-quantisation (affine_term, lowpgemm.hpp:110-114), the output
+// transform A^T m A (winograd.hpp:80-84) and the merge with ragged-edge
+// discard (tensor.hpp:157-182).
+//
+// One CTA = 128 Winograd tiles (UMMA M) x 16 filters (UMMA N) x all 16
+// positions: 16 x 16 s32 = 256 TMEM columns, so two CTAs share an SM and one
+// CTA's epilogue overlaps the other's TMA / MMA.
+//   warp 0      TMA producer (one lane): A box [128 rows x BK ch] of position
+//               p, B box [16 filters x BK ch] of position p per stage
+//   warp 1      TMEM allocator + UMMA issuer (one lane)
+//   warps 2..5  epilogue: TMEM -> registers -> affine -> A^T m A -> y
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "lance_common.cuh"
+
+namespace lance_dev {
+
+template <int BK>
+struct GemmCfg {
+  static constexpr uint32_t kABytes = kBM * BK;
+  static constexpr uint32_t kBBytes = kBN * BK;
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (96 * 1024 / kStageBytes) > 12 ? 12 : (96 * 1024 / kStageBytes);
+  static constexpr uint32_t kLayout = (BK == 128) ? 2u : (BK == 64 ? 4u : 6u);  // SW128/64/32
+  static constexpr uint32_t kTmemCols = 16 * kBN;
+  static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes +
+                                  (2 * kStages + 1) * 8 + 16 + (16 * kBN + 32 + kBN) * 4;
+};
+
+template <int BK, bool SMALL>
+__global__ void __launch_bounds__(kGemmThreads, 2)
+    gemm_epilogue_kernel(const __grid_constant__ CUtensorMap tmA,
+                         const __grid_constant__ CUtensorMap tmB,
+                         const int32_t* __restrict__ rowsum, const int32_t* __restrict__ colsum,
+                         const LanceDevState* __restrict__ st, float* __restrict__ y,
+                         int32_t* __restrict__ acc_dump, const float* __restrict__ bias,
+                         int relu, GemmGeom g) {
+  using Cfg = GemmCfg<BK>;
+  constexpr int kStages = Cfg::kStages;
+  constexpr uint32_t kIdesc = umma_idesc_u8(kBM, kBN);
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* stage_base = smem;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tmem_full_bar = empty_bar + kStages;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full_bar + 1);
+  float* s_cterm = reinterpret_cast<float*>(tmem_holder + 4);  // [16][kBN]
+  float* s_k1 = s_cterm + 16 * kBN;
+  float* s_k4 = s_k1 + 16;
+  float* s_bias = s_k4 + 16;  // [kBN]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tile = blockIdx.x % g.num_n_tiles;
+  const int m_tile = blockIdx.x / g.num_n_tiles;
+  const int m0 = m_tile * kBM;
+  const int n0 = n_tile * kBN;
+  const int K_pad = g.num_n_tiles * kBN;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(tmem_full_bar, 1);
+    fence_barrier_init();
+  }
+  if (warp >= 2) {
+    // c_p[n] = k3[p] * float(colsum[p][n]): the third term of affine_term.
+    const int e = threadIdx.x - 64;
+    for (int i = e; i < 16 * kBN; i += 128) {
+      const int p = i / kBN, kf = n0 + i % kBN;
+      const float cs = (kf < g.K) ? static_cast<float>(colsum[p * K_pad + kf]) : 0.0f;
+      s_cterm[i] = __fmul_rn(st->k3[p], cs);
+    }
+    if (e < 16) {
+      s_k1[e] = st->k1[e];
+      s_k4[e] = st->k4[e];
+    }
+    if (e < kBN) {
+      const int kf = n0 + e;
+      s_bias[e] = (bias != nullptr && kf < g.K) ? bias[kf] : 0.0f;
+    }
+  }
+  __syncthreads();
+
+  const int num_iters = g.num_kchunks * 16;
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      for (int it = 0; it < num_iters; ++it) {
+        const int s = it % kStages;
+        const uint32_t ph = static_cast<uint32_t>(it / kStages) & 1u;
+        const int kc = it >> 4, p = it & 15;
+        mbar_wait(&empty_bar[s], ph ^ 1u);
+        uint8_t* sa = stage_base + s * Cfg::kStageBytes;
+        mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
+        tma_load_3d(sa, &tmA, kc * BK, m0, p, &full_bar[s]);
+        tma_load_3d(sa + Cfg::kABytes, &tmB, kc * BK, n0, p, &full_bar[s]);
+      }
+    }
+  } else if (warp == 1) {
+    tmem_alloc(tmem_holder, Cfg::kTmemCols);
+    tmem_relinquish();
+    tc_fence_before();
+    named_bar_sync(1, 160);
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+    if (lane == 0) {
+      for (int it = 0; it < num_iters; ++it) {
+        const int s = it % kStages;
+        const uint32_t ph = static_cast<uint32_t>(it / kStages) & 1u;
+        const int kc = it >> 4, p = it & 15;
+        mbar_wait(&full_bar[s], ph);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(stage_base + s * Cfg::kStageBytes);
+        const uint32_t sb = sa + Cfg::kABytes;
+#pragma unroll
+        for (int kk = 0; kk < BK / 32; ++kk) {
+          const uint64_t adesc = umma_smem_desc(sa + kk * 32, 8 * BK, Cfg::kLayout);
+          const uint64_t bdesc = umma_smem_desc(sb + kk * 32, 8 * BK, Cfg::kLayout);
+          umma_i8(tmem_base + static_cast<uint32_t>(p * kBN), adesc, bdesc, kIdesc,
+                  (kc > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(&empty_bar[s]);
+      }
+      umma_commit(tmem_full_bar);
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue ----------------
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int r = q * 32 + lane;
+    const int m = m0 + r;
+    const bool row_ok = m < g.M;
+    float rterm[16];  // k2[p] * float(sum_a): second term of affine_term
+#pragma unroll
+    for (int p = 0; p < 16; ++p)
+      rterm[p] = row_ok ? __fmul_rn(st->k2[p], static_cast<float>(rowsum[static_cast<long long>(p) * g.M + m]))
+                        : 0.0f;
+    int img = 0, ti = 0, tj = 0;
+    if (row_ok) {
+      img = m / g.P;
+      const int t = m - img * g.P;
+      ti = t / g.TW;
+      tj = t - ti * g.TW;
+    }
+    named_bar_sync(1, 160);
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+    mbar_wait(tmem_full_bar, 0);
+    tc_fence_after();
+    const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+    const bool vec_ok = (g.K & 3) == 0;
+#pragma unroll 1
+    for (int j = 0; j < kBN / 4; ++j) {
+      uint32_t a[16][4];
+#pragma unroll
+      for (int p = 0; p < 16; ++p) tmem_ld_x4(lane_addr + p * kBN + j * 4, a[p]);
+      tmem_ld_wait();
+      const int kf0 = n0 + j * 4;
+      if (acc_dump != nullptr && row_ok) {
+#pragma unroll
+        for (int p = 0; p < 16; ++p)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (kf0 + i < g.K)
+              acc_dump[(static_cast<long long>(p) * g.M + m) * g.K + kf0 + i] =
+                  static_cast<int32_t>(a[p][i]);
+      }
+      float2 out[4][2];  // [pixel a*2+b][filter pair]
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float2 mv[16];
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+          const float k1 = s_k1[p];
+          float2 t1;
+          if (SMALL) {
+            // dot < 2^23: F = 2^23 + dot exactly, and fma(k1, F, -k1*2^23)
+            // = RN(k1 * dot) (single rounding) = k1 * float(dot) bitwise.
+            const float2 F = make_float2(__uint_as_float(a[p][2 * h] | 0x4B000000u),
+                                         __uint_as_float(a[p][2 * h + 1] | 0x4B000000u));
+            t1 = fma2(bcast2(k1), F, bcast2(__fmul_rn(k1, -8388608.0f)));
+          } else {
+            t1 = mul2(bcast2(k1), make_float2(__int2float_rn(static_cast<int>(a[p][2 * h])),
+                                              __int2float_rn(static_cast<int>(a[p][2 * h + 1]))));
+          }
+          // ((k1*dot + k2*sum_a) + k3*sum_b) + k4, left to right.
+          const float2 ct = *reinterpret_cast<const float2*>(&s_cterm[p * kBN + j * 4 + 2 * h]);
+          mv[p] = add2(add2(add2(t1, bcast2(rterm[p])), ct), bcast2(s_k4[p]));
+        }
+        // S = (A^T m) A (winograd.hpp:80-84 in matrix.hpp:75-84 order).
+        float2 X0[4], X1[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          X0[c] = add2(add2(mv[c], mv[4 + c]), mv[8 + c]);
+          X1[c] = sub2(sub2(mv[4 + c], mv[8 + c]), mv[12 + c]);
+        }
+        float2 s[4];
+        s[0] = add2(add2(X0[0], X0[1]), X0[2]);
+        s[1] = sub2(sub2(X0[1], X0[2]), X0[3]);
+        s[2] = add2(add2(X1[0], X1[1]), X1[2]);
+        s[3] = sub2(sub2(X1[1], X1[2]), X1[3]);
+        const float2 bb = *reinterpret_cast<const float2*>(&s_bias[j * 4 + 2 * h]);
+#pragma unroll
+        for (int ab = 0; ab < 4; ++ab) {
+          float2 v = s[ab];
+          if (bias != nullptr) v = add2(v, bb);
+          if (relu) {
+            v.x = fmaxf(v.x, 0.0f);
+            v.y = fmaxf(v.y, 0.0f);
+          }
+          out[ab][h] = add2(v, bcast2(0.0f));  // the reference never yields -0
+        }
+      }
+      if (row_ok && kf0 < g.K) {
+#pragma unroll
+        for (int ab = 0; ab < 4; ++ab) {
+          const int oy = 2 * ti + (ab >> 1), ox = 2 * tj + (ab & 1);
+          if (oy >= g.OH || ox >= g.OW) continue;  // merge_tiles discard (tensor.hpp:172-175)
+          float* dst = y + ((static_cast<long long>(img) * g.OH + oy) * g.OW + ox) * g.K + kf0;
+          if (vec_ok) {
+            *reinterpret_cast<float4*>(dst) =
+                make_float4(out[ab][0].x, out[ab][0].y, out[ab][1].x, out[ab][1].y);
+          } else {
+            const float o4[4] = {out[ab][0].x, out[ab][0].y, out[ab][1].x, out[ab][1].y};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (kf0 + i < g.K) dst[i] = o4[i];
+          }
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(*tmem_holder, Cfg::kTmemCols);
+  }
+}
+
+template <int BK, bool SMALL>
+static cudaError_t launch_gemm_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
+                                 const int32_t* rowsum, const int32_t* colsum,
+                                 const LanceDevState* st, float* y, int32_t* acc_dump,
+                                 const float* bias, int relu, const GemmGeom& g, cudaStream_t s) {
+  const size_t smem = GemmCfg<BK>::kSmem;
+  static bool configured[64] = {};  // the attribute is per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !configured[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_epilogue_kernel<BK, SMALL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) configured[dev] = true;
+  }
+  const long long m_tiles = (static_cast<long long>(g.M) + kBM - 1) / kBM;
+  const long long grid = m_tiles * g.num_n_tiles;
+  gemm_epilogue_kernel<BK, SMALL><<<static_cast<unsigned>(grid), kGemmThreads, smem, s>>>(
+      *tmA, *tmB, rowsum, colsum, st, y, acc_dump, bias, relu, g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int bk, int small_acc,
+                        const int32_t* rowsum, const int32_t* colsum, const LanceDevState* st,
+                        float* y, int32_t* acc_dump, const float* bias, int relu,
+                        const GemmGeom& g, cudaStream_t s) {
+#define LANCE_GEMM_CASE(BKV)                                                                   \
+  if (bk == BKV)                                                                               \
+    return small_acc ? launch_gemm_t<BKV, true>(tmA, tmB, rowsum, colsum, st, y, acc_dump, bias, \
+                                                relu, g, s)                                    \
+                     : launch_gemm_t<BKV, false>(tmA, tmB, rowsum, colsum, st, y, acc_dump,    \
+                                                 bias, relu, g, s);
+  LANCE_GEMM_CASE(128)
+  LANCE_GEMM_CASE(64)
+  LANCE_GEMM_CASE(32)
+#undef LANCE_GEMM_CASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace lance_dev

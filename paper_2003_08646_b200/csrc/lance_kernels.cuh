@@ -1,5 +1,5 @@
-// lance_kernels.cuh -- device state, launch geometry and kernel entry points
-// of the B200 LANCE path (reference: engines.hpp:492-536).
+// lance_kernels.cuh -- device state, launch geometry and launchers of the B200
+// LANCE path (reference: engines.hpp:492-536).
 #pragma once
 
 #include <cuda.h>
@@ -11,16 +11,17 @@ namespace lance_dev {
 
 constexpr int kPositions = 16;  // (m + r - 1)^2 for F(2x2,3x3)
 constexpr int kBM = 128;        // GEMM rows (Winograd tiles) per CTA = UMMA M
-constexpr int kBN = 32;         // filters per CTA: 16 positions x 32 = 512 TMEM columns
+constexpr int kBN = 16;         // filters per CTA: 16 positions x 16 = 256 TMEM columns
 constexpr int kGemmThreads = 192;
-constexpr int kStages = 8;
+constexpr int kChunk = 64;      // channels per K0/K1 warp item (32 lanes x 2)
+constexpr int kTM = 8;          // tiles (one per warp) per K1 block
 
 // Per-plan device state, written by the range / filter finalisers and read by
 // the quantiser and the GEMM epilogue.  Mirrors QuantParams (quant.hpp:27-37)
 // for both operands plus the hoisted affine constants of affine_term
 // (lowpgemm.hpp:110-114): m = ((k1*dot + k2*sum_a) + k3*sum_b) + k4.
 struct LanceDevState {
-  float a_tmin[kPositions], a_tmax[kPositions], a_scale[kPositions];
+  float a_tmin[kPositions], a_tmax[kPositions], a_scale[kPositions], a_rcp[kPositions];
   float w_tmin[kPositions], w_tmax[kPositions], w_scale[kPositions];
   float k1[kPositions], k2[kPositions], k3[kPositions], k4[kPositions];
   int bits_i, bits_w;
@@ -30,15 +31,13 @@ struct LanceDevState {
 
 // Input-side geometry shared by the range pass (K0) and the quantiser (K1).
 struct InGeom {
-  long long M;         // GEMM rows = N * P
-  int P, TW;           // tiles per image, tiles per image row
-  int H, W, C, C4;     // image dims, channels, ceil(C / 4)
-  int C_pad;           // code row pitch (multiple of 32)
+  int M;          // GEMM rows = N * P (< 2^31, checked at plan creation)
+  int P, TW;      // tiles per image, tiles per image row
+  int H, W, C;    // image dims, channels
+  int C_pad;      // code row pitch (multiple of 32)
   int pad;
-  int G;               // threads per tile (power of two, <= 32)
-  int TPB;             // tiles per 256-thread block
-  long long num_tile_blocks;
-  int granularity;     // 1 = PerPosition, 2 = PerTensor
+  int nchunks;    // ceil(C_pad / kChunk)
+  int granularity;  // 1 = PerPosition, 2 = PerTensor
 };
 
 struct FilterGeom {
@@ -47,28 +46,30 @@ struct FilterGeom {
 };
 
 struct GemmGeom {
-  long long M;
+  int M;
   int K, C;
   int P, TW, OH, OW;
   int num_kchunks;  // C_pad / BK
   int num_n_tiles;  // K_pad / kBN
 };
 
-// Host-side launchers (lance_kernels.cu).  All stream-ordered.
-cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceDevState* st,
-                               const InGeom& g, int vec4, cudaStream_t s);
-cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
-                               const LanceDevState* st, const InGeom& g, int vec4,
-                               cudaStream_t s);
 struct StaticParams {
   float tmin[kPositions], tmax[kPositions], scale[kPositions];
 };
+
+// Host-side launchers.  All stream-ordered.
+int input_range_grid(const InGeom& g, int sm_count);
+cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceDevState* st,
+                               const InGeom& g, int vec2, cudaStream_t s);
+cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
+                               const LanceDevState* st, const InGeom& g, int vec2,
+                               int static_mode, cudaStream_t s);
 cudaError_t launch_static_params(LanceDevState* st, const StaticParams& prm, int C,
                                  cudaStream_t s);
 cudaError_t launch_filter_prepare(const float* w, float* u_tmp, float* partials, int grid,
                                   uint8_t* codes_w, int32_t* colsum, LanceDevState* st,
                                   const FilterGeom& g, cudaStream_t s);
-cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int bk,
+cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int bk, int small_acc,
                         const int32_t* rowsum, const int32_t* colsum, const LanceDevState* st,
                         float* y, int32_t* acc_dump, const float* bias, int relu,
                         const GemmGeom& g, cudaStream_t s);
