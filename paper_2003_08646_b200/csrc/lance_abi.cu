@@ -274,6 +274,7 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   InGeom& g = p->in_geom;
   g.M = static_cast<int>(p->M);
   g.P = p->P;
+  g.TH = p->TH;
   g.TW = p->TW;
   g.H = spec->h;
   g.W = spec->w;
@@ -281,6 +282,15 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   g.C_pad = p->C_pad;
   g.pad = spec->pad;
   g.nchunks = (p->C_pad + kChunk - 1) / kChunk;
+  // Warp strips: whole tile rows unless that leaves too few warps to fill
+  // 148 SMs x 32 warps; then halve the strip length.
+  g.seg_len = p->TW;
+  for (;;) {
+    g.nseg = (p->TW + g.seg_len - 1) / g.seg_len;
+    g.num_items = static_cast<long long>(spec->n) * p->TH * g.nseg * g.nchunks;
+    if (g.num_items >= 32LL * p->sm_count || g.seg_len <= 2) break;
+    g.seg_len = (g.seg_len + 1) / 2;
+  }
   g.granularity = cfg->granularity;
   p->range_grid = input_range_grid(g, p->sm_count);
   p->small_acc = static_cast<double>(spec->c) * ((1 << cfg->bits_i) - 1) *

@@ -28,8 +28,14 @@ namespace lance_dev {
   }
 LANCE_F2_BINOP(add2, "add.rn.f32x2")
 LANCE_F2_BINOP(sub2, "sub.rn.f32x2")
-LANCE_F2_BINOP(mul2, "mul.rn.f32x2")
 #undef LANCE_F2_BINOP
+// NOTE: there is deliberately no packed multiply.  ptxas (CUDA 12.9) contracts
+// mul.rn.f32x2 followed by add.rn.f32x2 into FFMA2 even with .rn and
+// -fmad=false, which changes the rounding; products are issued as scalar
+// __fmul_rn (never contracted) and only the adds are packed.
+__device__ __forceinline__ float2 mul2_rn(float2 a, float2 b) {
+  return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y));
+}
 
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
   float2 r;

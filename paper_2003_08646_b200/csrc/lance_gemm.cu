@@ -30,10 +30,13 @@ struct GemmCfg {
   static constexpr uint32_t kLayout = (BK == 128) ? 2u : (BK == 64 ? 4u : 6u);  // SW128/64/32
   static constexpr uint32_t kTmemCols = 16 * kBN;
   static constexpr size_t kSmem = 1024 + static_cast<size_t>(kStages) * kStageBytes +
-                                  (2 * kStages + 1) * 8 + 16 + (16 * kBN + 32 + kBN) * 4;
+                                  (2 * kStages + 1) * 8 + 16;
 };
 
-template <int BK, bool SMALL>
+// SMALL: C * top_a * top_b < 2^23, so every accumulator fits the fp32
+// significand below 2^23 and k1 * float(dot) is formed exactly by one FFMA
+// (see below).  EPI: fused bias + ReLU (north-star extension).
+template <int BK, bool SMALL, bool EPI>
 __global__ void __launch_bounds__(kGemmThreads, 2)
     gemm_epilogue_kernel(const __grid_constant__ CUtensorMap tmA,
                          const __grid_constant__ CUtensorMap tmB,
@@ -46,6 +49,10 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
   constexpr uint32_t kIdesc = umma_idesc_u8(kBM, kBN);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(16) float s_cterm[16][kBN];  // k3[p] * float(colsum[p][n])
+  __shared__ float s_k1[16], s_nk1m[16], s_k4[16];
+  __shared__ __align__(16) float s_bias[kBN];
+
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* stage_base = smem;
@@ -53,10 +60,6 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tmem_full_bar = empty_bar + kStages;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full_bar + 1);
-  float* s_cterm = reinterpret_cast<float*>(tmem_holder + 4);  // [16][kBN]
-  float* s_k1 = s_cterm + 16 * kBN;
-  float* s_k4 = s_k1 + 16;
-  float* s_bias = s_k4 + 16;  // [kBN]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tile = blockIdx.x % g.num_n_tiles;
@@ -74,20 +77,21 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     fence_barrier_init();
   }
   if (warp >= 2) {
-    // c_p[n] = k3[p] * float(colsum[p][n]): the third term of affine_term.
     const int e = threadIdx.x - 64;
     for (int i = e; i < 16 * kBN; i += 128) {
       const int p = i / kBN, kf = n0 + i % kBN;
       const float cs = (kf < g.K) ? static_cast<float>(colsum[p * K_pad + kf]) : 0.0f;
-      s_cterm[i] = __fmul_rn(st->k3[p], cs);
+      s_cterm[p][i % kBN] = __fmul_rn(st->k3[p], cs);
     }
     if (e < 16) {
-      s_k1[e] = st->k1[e];
+      const float k1 = st->k1[e];
+      s_k1[e] = k1;
+      s_nk1m[e] = __fmul_rn(k1, -8388608.0f);  // -k1 * 2^23, exact
       s_k4[e] = st->k4[e];
     }
     if (e < kBN) {
       const int kf = n0 + e;
-      s_bias[e] = (bias != nullptr && kf < g.K) ? bias[kf] : 0.0f;
+      s_bias[e] = (EPI && bias != nullptr && kf < g.K) ? bias[kf] : 0.0f;
     }
   }
   __syncthreads();
@@ -97,15 +101,19 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmB);
+      int s = 0;
+      uint32_t ph = 0;
       for (int it = 0; it < num_iters; ++it) {
-        const int s = it % kStages;
-        const uint32_t ph = static_cast<uint32_t>(it / kStages) & 1u;
         const int kc = it >> 4, p = it & 15;
         mbar_wait(&empty_bar[s], ph ^ 1u);
         uint8_t* sa = stage_base + s * Cfg::kStageBytes;
         mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
         tma_load_3d(sa, &tmA, kc * BK, m0, p, &full_bar[s]);
         tma_load_3d(sa + Cfg::kABytes, &tmB, kc * BK, n0, p, &full_bar[s]);
+        if (++s == kStages) {
+          s = 0;
+          ph ^= 1u;
+        }
       }
     }
   } else if (warp == 1) {
@@ -116,9 +124,9 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
       for (int it = 0; it < num_iters; ++it) {
-        const int s = it % kStages;
-        const uint32_t ph = static_cast<uint32_t>(it / kStages) & 1u;
         const int kc = it >> 4, p = it & 15;
         mbar_wait(&full_bar[s], ph);
         tc_fence_after();
@@ -132,6 +140,10 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
                   (kc > 0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(&empty_bar[s]);
+        if (++s == kStages) {
+          s = 0;
+          ph ^= 1u;
+        }
       }
       umma_commit(tmem_full_bar);
     }
@@ -139,20 +151,29 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
   } else {
     // ---------------- epilogue ----------------
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
-    const int r = q * 32 + lane;
-    const int m = m0 + r;
+    const int m = m0 + q * 32 + lane;
     const bool row_ok = m < g.M;
     float rterm[16];  // k2[p] * float(sum_a): second term of affine_term
 #pragma unroll
     for (int p = 0; p < 16; ++p)
-      rterm[p] = row_ok ? __fmul_rn(st->k2[p], static_cast<float>(rowsum[static_cast<long long>(p) * g.M + m]))
+      rterm[p] = row_ok ? __fmul_rn(st->k2[p],
+                                    static_cast<float>(rowsum[static_cast<long long>(p) * g.M + m]))
                         : 0.0f;
-    int img = 0, ti = 0, tj = 0;
-    if (row_ok) {
-      img = m / g.P;
-      const int t = m - img * g.P;
-      ti = t / g.TW;
-      tj = t - ti * g.TW;
+    // Output pixels of this tile: (2ti + a, 2tj + b); merge_tiles discards the
+    // ceil-overhang (tensor.hpp:172-175).
+    float* dst[4];
+    bool ok[4];
+    {
+      const int mm = row_ok ? m : 0;
+      const int img = mm / g.P;
+      const int t = mm - img * g.P;
+      const int ti = t / g.TW, tj = t - ti * g.TW;
+#pragma unroll
+      for (int ab = 0; ab < 4; ++ab) {
+        const int oy = 2 * ti + (ab >> 1), ox = 2 * tj + (ab & 1);
+        ok[ab] = row_ok && oy < g.OH && ox < g.OW;
+        dst[ab] = y + ((static_cast<long long>(img) * g.OH + oy) * g.OW + ox) * g.K + n0;
+      }
     }
     named_bar_sync(1, 160);
     tc_fence_after();
@@ -177,66 +198,71 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
               acc_dump[(static_cast<long long>(p) * g.M + m) * g.K + kf0 + i] =
                   static_cast<int32_t>(a[p][i]);
       }
-      float2 out[4][2];  // [pixel a*2+b][filter pair]
+      float2 mv[2][16];  // [filter pair][position]
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float2 mv[16];
+      for (int p = 0; p < 16; ++p) {
+        const float4 ct = *reinterpret_cast<const float4*>(&s_cterm[p][j * 4]);
+        const float k1 = s_k1[p], nk1m = s_nk1m[p];
+        const float k4 = s_k4[p];
 #pragma unroll
-        for (int p = 0; p < 16; ++p) {
-          const float k1 = s_k1[p];
+        for (int h = 0; h < 2; ++h) {
           float2 t1;
           if (SMALL) {
             // dot < 2^23: F = 2^23 + dot exactly, and fma(k1, F, -k1*2^23)
-            // = RN(k1 * dot) (single rounding) = k1 * float(dot) bitwise.
+            // rounds once: RN(k1 * dot) = k1 * float(dot), bitwise.
             const float2 F = make_float2(__uint_as_float(a[p][2 * h] | 0x4B000000u),
                                          __uint_as_float(a[p][2 * h + 1] | 0x4B000000u));
-            t1 = fma2(bcast2(k1), F, bcast2(__fmul_rn(k1, -8388608.0f)));
+            t1 = fma2(bcast2(k1), F, bcast2(nk1m));
           } else {
-            t1 = mul2(bcast2(k1), make_float2(__int2float_rn(static_cast<int>(a[p][2 * h])),
-                                              __int2float_rn(static_cast<int>(a[p][2 * h + 1]))));
+            t1 = make_float2(__fmul_rn(k1, __int2float_rn(static_cast<int>(a[p][2 * h]))),
+                             __fmul_rn(k1, __int2float_rn(static_cast<int>(a[p][2 * h + 1]))));
           }
           // ((k1*dot + k2*sum_a) + k3*sum_b) + k4, left to right.
-          const float2 ct = *reinterpret_cast<const float2*>(&s_cterm[p * kBN + j * 4 + 2 * h]);
-          mv[p] = add2(add2(add2(t1, bcast2(rterm[p])), ct), bcast2(s_k4[p]));
+          const float2 c2 = h ? make_float2(ct.z, ct.w) : make_float2(ct.x, ct.y);
+          mv[h][p] = add2(add2(add2(t1, bcast2(rterm[p])), c2), bcast2(k4));
         }
+      }
+      float2 out[4][2];  // [pixel a*2+b][filter pair]
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
         // S = (A^T m) A (winograd.hpp:80-84 in matrix.hpp:75-84 order).
         float2 X0[4], X1[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          X0[c] = add2(add2(mv[c], mv[4 + c]), mv[8 + c]);
-          X1[c] = sub2(sub2(mv[4 + c], mv[8 + c]), mv[12 + c]);
+          X0[c] = add2(add2(mv[h][c], mv[h][4 + c]), mv[h][8 + c]);
+          X1[c] = sub2(sub2(mv[h][4 + c], mv[h][8 + c]), mv[h][12 + c]);
         }
-        float2 s[4];
-        s[0] = add2(add2(X0[0], X0[1]), X0[2]);
-        s[1] = sub2(sub2(X0[1], X0[2]), X0[3]);
-        s[2] = add2(add2(X1[0], X1[1]), X1[2]);
-        s[3] = sub2(sub2(X1[1], X1[2]), X1[3]);
-        const float2 bb = *reinterpret_cast<const float2*>(&s_bias[j * 4 + 2 * h]);
+        float2 s4[4];
+        s4[0] = add2(add2(X0[0], X0[1]), X0[2]);
+        s4[1] = sub2(sub2(X0[1], X0[2]), X0[3]);
+        s4[2] = add2(add2(X1[0], X1[1]), X1[2]);
+        s4[3] = sub2(sub2(X1[1], X1[2]), X1[3]);
 #pragma unroll
         for (int ab = 0; ab < 4; ++ab) {
-          float2 v = s[ab];
-          if (bias != nullptr) v = add2(v, bb);
-          if (relu) {
-            v.x = fmaxf(v.x, 0.0f);
-            v.y = fmaxf(v.y, 0.0f);
+          float2 v = s4[ab];
+          if (EPI) {
+            if (bias != nullptr) v = add2(v, *reinterpret_cast<const float2*>(&s_bias[j * 4 + 2 * h]));
+            if (relu) {
+              v.x = fmaxf(v.x, 0.0f);
+              v.y = fmaxf(v.y, 0.0f);
+            }
           }
           out[ab][h] = add2(v, bcast2(0.0f));  // the reference never yields -0
         }
       }
-      if (row_ok && kf0 < g.K) {
+      if (kf0 < g.K) {
 #pragma unroll
         for (int ab = 0; ab < 4; ++ab) {
-          const int oy = 2 * ti + (ab >> 1), ox = 2 * tj + (ab & 1);
-          if (oy >= g.OH || ox >= g.OW) continue;  // merge_tiles discard (tensor.hpp:172-175)
-          float* dst = y + ((static_cast<long long>(img) * g.OH + oy) * g.OW + ox) * g.K + kf0;
+          if (!ok[ab]) continue;
+          float* d = dst[ab] + j * 4;
           if (vec_ok) {
-            *reinterpret_cast<float4*>(dst) =
+            *reinterpret_cast<float4*>(d) =
                 make_float4(out[ab][0].x, out[ab][0].y, out[ab][1].x, out[ab][1].y);
           } else {
             const float o4[4] = {out[ab][0].x, out[ab][0].y, out[ab][1].x, out[ab][1].y};
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              if (kf0 + i < g.K) dst[i] = o4[i];
+              if (kf0 + i < g.K) d[i] = o4[i];
           }
         }
       }
@@ -250,7 +276,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2)
   }
 }
 
-template <int BK, bool SMALL>
+template <int BK, bool SMALL, bool EPI>
 static cudaError_t launch_gemm_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
                                  const int32_t* rowsum, const int32_t* colsum,
                                  const LanceDevState* st, float* y, int32_t* acc_dump,
@@ -260,7 +286,7 @@ static cudaError_t launch_gemm_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_epilogue_kernel<BK, SMALL>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_epilogue_kernel<BK, SMALL, EPI>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -268,26 +294,45 @@ static cudaError_t launch_gemm_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
   }
   const long long m_tiles = (static_cast<long long>(g.M) + kBM - 1) / kBM;
   const long long grid = m_tiles * g.num_n_tiles;
-  gemm_epilogue_kernel<BK, SMALL><<<static_cast<unsigned>(grid), kGemmThreads, smem, s>>>(
+  gemm_epilogue_kernel<BK, SMALL, EPI><<<static_cast<unsigned>(grid), kGemmThreads, smem, s>>>(
       *tmA, *tmB, rowsum, colsum, st, y, acc_dump, bias, relu, g);
   return cudaGetLastError();
+}
+
+template <int BK>
+static cudaError_t launch_gemm_bk(const CUtensorMap* tmA, const CUtensorMap* tmB, int small_acc,
+                                  const int32_t* rowsum, const int32_t* colsum,
+                                  const LanceDevState* st, float* y, int32_t* acc_dump,
+                                  const float* bias, int relu, const GemmGeom& g, cudaStream_t s) {
+  const bool epi = bias != nullptr || relu;
+  if (small_acc)
+    return epi ? launch_gemm_t<BK, true, true>(tmA, tmB, rowsum, colsum, st, y, acc_dump, bias,
+                                               relu, g, s)
+               : launch_gemm_t<BK, true, false>(tmA, tmB, rowsum, colsum, st, y, acc_dump, bias,
+                                                relu, g, s);
+  return epi ? launch_gemm_t<BK, false, true>(tmA, tmB, rowsum, colsum, st, y, acc_dump, bias,
+                                              relu, g, s)
+             : launch_gemm_t<BK, false, false>(tmA, tmB, rowsum, colsum, st, y, acc_dump, bias,
+                                               relu, g, s);
 }
 
 cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int bk, int small_acc,
                         const int32_t* rowsum, const int32_t* colsum, const LanceDevState* st,
                         float* y, int32_t* acc_dump, const float* bias, int relu,
                         const GemmGeom& g, cudaStream_t s) {
-#define LANCE_GEMM_CASE(BKV)                                                                   \
-  if (bk == BKV)                                                                               \
-    return small_acc ? launch_gemm_t<BKV, true>(tmA, tmB, rowsum, colsum, st, y, acc_dump, bias, \
-                                                relu, g, s)                                    \
-                     : launch_gemm_t<BKV, false>(tmA, tmB, rowsum, colsum, st, y, acc_dump,    \
-                                                 bias, relu, g, s);
-  LANCE_GEMM_CASE(128)
-  LANCE_GEMM_CASE(64)
-  LANCE_GEMM_CASE(32)
-#undef LANCE_GEMM_CASE
-  return cudaErrorInvalidValue;
+  switch (bk) {
+    case 128:
+      return launch_gemm_bk<128>(tmA, tmB, small_acc, rowsum, colsum, st, y, acc_dump, bias,
+                                 relu, g, s);
+    case 64:
+      return launch_gemm_bk<64>(tmA, tmB, small_acc, rowsum, colsum, st, y, acc_dump, bias,
+                                relu, g, s);
+    case 32:
+      return launch_gemm_bk<32>(tmA, tmB, small_acc, rowsum, colsum, st, y, acc_dump, bias,
+                                relu, g, s);
+    default:
+      return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace lance_dev

@@ -10,10 +10,14 @@
 //                          position GEMMs) plus row sums [16][M]
 //                          (lowpgemm.hpp:121-123).
 //
-// Mapping: one warp = one Winograd tile x 64 channels (2 per lane, float2
-// NHWC loads: 256 contiguous bytes per pixel per warp); the tile gather is
-// extract_tiles (tensor.hpp:116-152): origin (2ti - pad, 2tj - pad), zero pad.
-// Transforms run on packed f32x2 (FADD2), ranges on 3-input FMNMX3.NAN.
+// Mapping: one warp = one segment of a tile row (image img, tile row ti,
+// tiles tj0..tj1) x 64 channels (2 per lane, float2 NHWC loads: 256
+// contiguous bytes per pixel per warp).  The tile gather is extract_tiles
+// (tensor.hpp:116-152): origin (2ti - pad, 2tj - pad), zero padding.
+// Horizontally adjacent tiles share two pixel columns, so the warp slides along
+// the row: per tile it loads 2 new columns (8 pixels) and reuses the first
+// (column) pass of the transform for the 2 shared columns.  Transforms run on
+// packed f32x2 (FADD2), ranges on 3-input FMNMX3.NAN.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -22,46 +26,84 @@
 
 namespace lance_dev {
 
-struct TileOrigin {
-  int img, y0, x0;
+// Warp work item: (img, ti, tile segment, channel chunk).
+struct StripItem {
+  int img, ti, tj0, tj1, ch;
 };
 
-__device__ __forceinline__ TileOrigin tile_origin(const InGeom& g, int m) {
-  const int img = m / g.P;
-  const int t = m - img * g.P;
-  const int ti = t / g.TW, tj = t - ti * g.TW;
-  return {img, 2 * ti - g.pad, 2 * tj - g.pad};
+__device__ __forceinline__ StripItem strip_item(const InGeom& g, long long item, int lane) {
+  const int chunk = static_cast<int>(item % g.nchunks);
+  long long r = item / g.nchunks;
+  const int seg = static_cast<int>(r % g.nseg);
+  r /= g.nseg;
+  const int ti = static_cast<int>(r % g.TH);
+  const int img = static_cast<int>(r / g.TH);
+  const int tj0 = seg * g.seg_len;
+  const int tj1 = min(tj0 + g.seg_len, g.TW);
+  return {img, ti, tj0, tj1, chunk * kChunk + 2 * lane};
 }
 
-// 16 pixels x channels (ch, ch + 1) of one tile; zero outside the image and
-// for channels >= C.
+// Row context of a strip: the 4 input rows of tile row ti for this lane's
+// channel pair, with validity (zero padding above / below the image).
 template <bool VEC2>
-__device__ __forceinline__ void load_tile2(const float* __restrict__ x, const InGeom& g,
-                                           const TileOrigin& o, int ch, float2 (&d)[16]) {
-  const float* base = x + static_cast<long long>(o.img) * g.H * g.W * g.C;
+struct Strip {
+  const float* row[4];
+  bool rok[4];
+  bool c0ok, c1ok;  // channel ch / ch + 1 < C
+  int W, C;
+
+  __device__ __forceinline__ Strip(const float* __restrict__ x, const InGeom& g,
+                                   const StripItem& it) {
+    W = g.W;
+    C = g.C;
+    c0ok = it.ch < g.C;
+    c1ok = it.ch + 1 < g.C;
+    const float* base = x + static_cast<long long>(it.img) * g.H * g.W * g.C + it.ch;
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int yy = o.y0 + a;
-    const bool rok = (yy >= 0) && (yy < g.H);
+    for (int a = 0; a < 4; ++a) {
+      const int yy = 2 * it.ti - g.pad + a;
+      rok[a] = (yy >= 0) && (yy < g.H);
+      row[a] = base + static_cast<long long>(rok[a] ? yy : 0) * g.W * g.C;
+    }
+  }
+
+  // Column pass of B^T d for input column xx: t[a] = (B^T d)(a, col).
+  __device__ __forceinline__ void column(int xx, float2 (&t)[4]) const {
+    const bool cok = (xx >= 0) && (xx < W);
+    float2 d[4];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int xx = o.x0 + b;
-      const bool ok = rok && (xx >= 0) && (xx < g.W);
-      const float* px = base + (static_cast<long long>(yy) * g.W + xx) * g.C + ch;
+    for (int a = 0; a < 4; ++a) {
+      const float* px = row[a] + static_cast<long long>(cok ? xx : 0) * C;
+      const bool ok = cok && rok[a];
       if (VEC2) {
-        d[a * 4 + b] = (ok && ch < g.C) ? __ldg(reinterpret_cast<const float2*>(px))
-                                        : make_float2(0.f, 0.f);
+        d[a] = (ok && c0ok) ? __ldg(reinterpret_cast<const float2*>(px)) : make_float2(0.f, 0.f);
       } else {
-        d[a * 4 + b].x = (ok && ch < g.C) ? __ldg(px) : 0.f;
-        d[a * 4 + b].y = (ok && ch + 1 < g.C) ? __ldg(px + 1) : 0.f;
+        d[a].x = (ok && c0ok) ? __ldg(px) : 0.f;
+        d[a].y = (ok && c1ok) ? __ldg(px + 1) : 0.f;
       }
     }
+    t[0] = sub2(d[0], d[2]);
+    t[1] = add2(d[1], d[2]);
+    t[2] = sub2(d[2], d[1]);
+    t[3] = sub2(d[1], d[3]);
+  }
+};
+
+// Second (row) pass: v[a*4+b] from the column-pass results of 4 columns.
+__device__ __forceinline__ void row_pass(const float2 (&t0)[4], const float2 (&t1)[4],
+                                         const float2 (&t2)[4], const float2 (&t3)[4],
+                                         float2 (&v)[16]) {
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    v[a * 4 + 0] = sub2(t0[a], t2[a]);
+    v[a * 4 + 1] = add2(t1[a], t2[a]);
+    v[a * 4 + 2] = sub2(t2[a], t1[a]);
+    v[a * 4 + 3] = sub2(t1[a], t3[a]);
   }
 }
 
 // --------------------------------------------------------------------------
-// K0: per-position range of v over the whole batch (grid-stride over
-// (tile, 64-channel chunk) warp items).
+// K0: per-position range of v over the whole batch (grid-stride over strips).
 template <bool VEC2>
 __global__ void __launch_bounds__(256, 2) input_range_kernel(const float* __restrict__ x,
                                                              float* __restrict__ partials,
@@ -75,27 +117,39 @@ __global__ void __launch_bounds__(256, 2) input_range_kernel(const float* __rest
     hi[p] = __int_as_float(0xff800000);
   }
   const int lane = threadIdx.x & 31;
-  const long long nitems = static_cast<long long>(g.M) * g.nchunks;
   const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
   for (long long item = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-       item < nitems; item += stride) {
-    const int m = static_cast<int>(item / g.nchunks);
-    const int ch = static_cast<int>(item - static_cast<long long>(m) * g.nchunks) * kChunk + 2 * lane;
-    const TileOrigin o = tile_origin(g, m);
-    float2 d[16], v[16];
-    load_tile2<VEC2>(x, g, o, ch, d);
-    input_transform2(d, v);
-    if (ch + 1 < g.C) {
+       item < g.num_items; item += stride) {
+    const StripItem it = strip_item(g, item, lane);
+    if (it.ch >= g.C) continue;  // lane beyond C (only in the last channel chunk)
+    const Strip<VEC2> sp(x, g, it);
+    const bool two = it.ch + 1 < g.C;
+    float2 ta[4], tb[4], tc[4], td[4];
+    int xx = 2 * it.tj0 - g.pad;
+    sp.column(xx, ta);
+    sp.column(xx + 1, tb);
+    for (int tj = it.tj0; tj < it.tj1; ++tj, xx += 2) {
+      sp.column(xx + 2, tc);
+      sp.column(xx + 3, td);
+      float2 v[16];
+      row_pass(ta, tb, tc, td, v);
+      if (two) {
 #pragma unroll
-      for (int p = 0; p < 16; ++p) {
-        lo[p] = fmin3_nan(lo[p], v[p].x, v[p].y);
-        hi[p] = fmax3_nan(hi[p], v[p].x, v[p].y);
+        for (int p = 0; p < 16; ++p) {
+          lo[p] = fmin3_nan(lo[p], v[p].x, v[p].y);
+          hi[p] = fmax3_nan(hi[p], v[p].x, v[p].y);
+        }
+      } else {  // odd C: the lane's second channel is padding
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+          lo[p] = fmin_nan(lo[p], v[p].x);
+          hi[p] = fmax_nan(hi[p], v[p].x);
+        }
       }
-    } else if (ch < g.C) {  // odd C: last lane holds one real channel
 #pragma unroll
-      for (int p = 0; p < 16; ++p) {
-        lo[p] = fmin_nan(lo[p], v[p].x);
-        hi[p] = fmax_nan(hi[p], v[p].x);
+      for (int a = 0; a < 4; ++a) {
+        ta[a] = tc[a];
+        tb[a] = td[a];
       }
     }
   }
@@ -107,110 +161,133 @@ __global__ void __launch_bounds__(256, 2) input_range_kernel(const float* __rest
   }
 }
 
+// Rare path of K1 (kept out of line so the fast path keeps its registers):
+// re-quantise exactly, with the IEEE formula, every value whose fast-path
+// residual is within 2^-14 of a rounding boundary (or NaN).
+template <bool STATIC>
+__device__ __noinline__ void requantize_flagged(const float2 (&v)[16], const float* s_tmin,
+                                                const float* s_scale, const float* s_rcp,
+                                                float top, uint32_t (&pk)[16]) {
+#pragma unroll 1
+  for (int p = 0; p < 16; ++p) {
+    const float2 dd = sub2(v[p], bcast2(s_tmin[p]));
+    float ra, rb;
+    if (STATIC) {
+      float2 q = mul2_rn(dd, bcast2(s_rcp[p]));
+      q.x = fminf(fmaxf(q.x, 0.0f), top);
+      q.y = fminf(fmaxf(q.y, 0.0f), top);
+      ra = __fsub_rn(q.x, __fsub_rn(__fadd_rn(q.x, kMagic), kMagic));
+      rb = __fsub_rn(q.y, __fsub_rn(__fadd_rn(q.y, kMagic), kMagic));
+    } else {
+      const float2 gq = fma2(dd, bcast2(s_rcp[p]), bcast2(kMagic));
+      const float2 r = fma2(dd, bcast2(s_rcp[p]),
+                            make_float2(-__fsub_rn(gq.x, kMagic), -__fsub_rn(gq.y, kMagic)));
+      ra = r.x;
+      rb = r.y;
+    }
+    if (!(fabsf(ra) < kTieGuard))
+      pk[p] = (pk[p] & 0xFF00u) | quantize_code(v[p].x, s_tmin[p], s_scale[p], top);
+    if (!(fabsf(rb) < kTieGuard))
+      pk[p] = (pk[p] & 0x00FFu) | (quantize_code(v[p].y, s_tmin[p], s_scale[p], top) << 8);
+  }
+}
+
 // --------------------------------------------------------------------------
-// K1: codes + row sums.  Block = kTM tiles (one per warp); channels in chunks
-// of 64; codes staged in shared memory and written with 16-byte stores.
+// K1: codes + row sums, one strip per warp.
+//
+// Dynamic params (the reference's batch fit): d = v - tmin is in [0, range],
+// so the exact product P = d * RN(1/scale) is within 2^-16 of d / scale <= 256.
+// n = rint(P) comes from one FFMA2 with the 1.5 * 2^23 magic addend and
+// r = RN(P - n) from another.  If |r| < 0.5 - 2^-14 then |RN(d / scale) - n|
+// < 0.5, so the reference's roundf((x - t_min) / scale) equals n exactly
+// (no clamp needed: 0 <= n <= top).  Otherwise (probability ~1e-4 per value)
+// the lane re-quantises the flagged values with the IEEE formula.
+// Static params (caller supplied): q may be anywhere, so it is formed with a
+// scalar IEEE multiply, clamped to [0, top] and rounded with the magic addend.
 template <bool VEC2, bool STATIC>
 __global__ void __launch_bounds__(256, 2) input_quant_kernel(const float* __restrict__ x,
                                                              uint8_t* __restrict__ codes,
                                                              int32_t* __restrict__ rowsum,
                                                              const LanceDevState* __restrict__ st,
                                                              InGeom g) {
-  __shared__ __align__(16) uint8_t s_codes[16][kTM][kChunk];
-  __shared__ int s_rs[16][kTM];
   __shared__ float s_tmin[16], s_scale[16], s_rcp[16];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
   if (tid < 16) {
     s_tmin[tid] = st->a_tmin[tid];
     s_scale[tid] = st->a_scale[tid];
     s_rcp[tid] = st->a_rcp[tid];
   }
-  if (tid < 16 * kTM) s_rs[tid / kTM][tid % kTM] = 0;
   const float top = static_cast<float>((1 << st->bits_i) - 1);
   __syncthreads();
-
-  const int m0 = blockIdx.x * kTM;
-  const int m = m0 + warp;
-  const bool valid = m < g.M;
-  const TileOrigin o = tile_origin(g, valid ? m : 0);
-
-  for (int c0 = 0; c0 < g.C_pad; c0 += kChunk) {
-    const int ch = c0 + 2 * lane;
+  const long long item = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
+  if (item >= g.num_items) return;
+  const StripItem it = strip_item(g, item, lane);
+  const bool lane_on = it.ch < g.C;
+  const bool two = it.ch + 1 < g.C;
+  const Strip<VEC2> sp(x, g, it);
+  const long long pstride = static_cast<long long>(g.M) * g.C_pad;
+  float2 ta[4], tb[4], tc[4], td[4];
+  int xx = 2 * it.tj0 - g.pad;
+  if (lane_on) {
+    sp.column(xx, ta);
+    sp.column(xx + 1, tb);
+  }
+  int m = (it.img * g.TH + it.ti) * g.TW + it.tj0;
+  for (int tj = it.tj0; tj < it.tj1; ++tj, xx += 2, ++m) {
     uint32_t pk[16];
 #pragma unroll
     for (int p = 0; p < 16; ++p) pk[p] = 0u;
-    if (valid && ch < g.C) {
-      float2 d[16], v[16];
-      load_tile2<VEC2>(x, g, o, ch, d);
-      input_transform2(d, v);
+    if (lane_on) {
+      sp.column(xx + 2, tc);
+      sp.column(xx + 3, td);
+      float2 v[16];
+      row_pass(ta, tb, tc, td, v);
       float rmax = 0.0f;
 #pragma unroll
       for (int p = 0; p < 16; ++p) {
-        float2 q = mul2(sub2(v[p], bcast2(s_tmin[p])), bcast2(s_rcp[p]));
-        if (STATIC) {  // caller-supplied params: q may be anywhere (NaN -> 0)
-          q.x = fminf(fmaxf(q.x, 0.0f), top);
+        const float2 dd = sub2(v[p], bcast2(s_tmin[p]));
+        float2 gq, r;
+        if (STATIC) {
+          float2 q = mul2_rn(dd, bcast2(s_rcp[p]));
+          q.x = fminf(fmaxf(q.x, 0.0f), top);  // NaN -> 0 like quant.hpp:81
           q.y = fminf(fmaxf(q.y, 0.0f), top);
+          gq = add2(q, bcast2(kMagic));
+          r = sub2(q, sub2(gq, bcast2(kMagic)));
+        } else {
+          gq = fma2(dd, bcast2(s_rcp[p]), bcast2(kMagic));
+          r = fma2(dd, bcast2(s_rcp[p]),
+                   make_float2(-__fsub_rn(gq.x, kMagic), -__fsub_rn(gq.y, kMagic)));
         }
-        const float2 gq = add2(q, bcast2(kMagic));
-        const float2 r = sub2(q, sub2(gq, bcast2(kMagic)));
         rmax = fmax3_nan(rmax, fabsf(r.x), fabsf(r.y));
         pk[p] = __byte_perm(__float_as_uint(gq.x), __float_as_uint(gq.y), 0x0040) & 0xFFFFu;
       }
-      if (!(rmax < kTieGuard)) {
-        // Rare: some q0 lies within 2^-14 of a rounding boundary (or is NaN):
-        // reload the tile and re-quantise exactly those values with the IEEE
-        // reference formula (keeps v out of registers on the fast path).
-        float2 d2[16], w2[16];
-        load_tile2<VEC2>(x, g, o, ch, d2);
-        input_transform2(d2, w2);
+      if (!(rmax < kTieGuard)) requantize_flagged<STATIC>(v, s_tmin, s_scale, s_rcp, top, pk);
+      if (!two) {
 #pragma unroll
-        for (int p = 0; p < 16; ++p) {
-          const float2 q0 = mul2(sub2(w2[p], bcast2(s_tmin[p])), bcast2(s_rcp[p]));
-          float qa = q0.x, qb = q0.y;
-          if (STATIC) {
-            qa = fminf(fmaxf(qa, 0.0f), top);
-            qb = fminf(fmaxf(qb, 0.0f), top);
-          }
-          const float ra = __fsub_rn(qa, __fsub_rn(__fadd_rn(qa, kMagic), kMagic));
-          const float rb = __fsub_rn(qb, __fsub_rn(__fadd_rn(qb, kMagic), kMagic));
-          if (!(fabsf(ra) < kTieGuard))
-            pk[p] = (pk[p] & 0xFF00u) | quantize_code(w2[p].x, s_tmin[p], s_scale[p], top);
-          if (!(fabsf(rb) < kTieGuard))
-            pk[p] = (pk[p] & 0x00FFu) | (quantize_code(w2[p].y, s_tmin[p], s_scale[p], top) << 8);
-        }
+        for (int p = 0; p < 16; ++p) pk[p] &= 0x00FFu;  // odd C: padding channel code 0
       }
-      if (ch + 1 >= g.C) {  // odd C: zero the padding channel's code
 #pragma unroll
-        for (int p = 0; p < 16; ++p) pk[p] &= 0x00FFu;
+      for (int a = 0; a < 4; ++a) {
+        ta[a] = tc[a];
+        tb[a] = td[a];
       }
-    }
+      // Codes: 64 contiguous bytes per warp per position (the A operand row).
+      uint8_t* dst = codes + static_cast<long long>(m) * g.C_pad + it.ch;
 #pragma unroll
-    for (int p = 0; p < 16; ++p)
-      *reinterpret_cast<uint16_t*>(&s_codes[p][warp][2 * lane]) = static_cast<uint16_t>(pk[p]);
-    __syncthreads();
-    // Write-out: 16 positions x kTM tiles x 4 pieces of 16 codes.
-#pragma unroll
-    for (int k = 0; k < (16 * kTM * 4) / 256; ++k) {
-      const int i = tid + 256 * k;
-      const int p = i / (kTM * 4), t = (i / 4) % kTM, part = i % 4;
-      const uint4 val = *reinterpret_cast<const uint4*>(&s_codes[p][t][part * 16]);
-      uint32_t sum = __dp4a(val.x, 0x01010101u, 0u);
-      sum = __dp4a(val.y, 0x01010101u, sum);
-      sum = __dp4a(val.z, 0x01010101u, sum);
-      sum = __dp4a(val.w, 0x01010101u, sum);
-      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-      const int mt = m0 + t;
-      if (mt < g.M && c0 + part * 16 < g.C_pad)
-        *reinterpret_cast<uint4*>(codes + (static_cast<long long>(p) * g.M + mt) * g.C_pad + c0 +
-                                  part * 16) = val;
-      if (part == 0) s_rs[p][t] += static_cast<int>(sum);
+      for (int p = 0; p < 16; ++p)
+        *reinterpret_cast<uint16_t*>(dst + p * pstride) = static_cast<uint16_t>(pk[p]);
     }
-    __syncthreads();
-  }
-  if (tid < 16 * kTM) {
-    const int p = tid / kTM, t = tid % kTM;
-    if (m0 + t < g.M) rowsum[static_cast<long long>(p) * g.M + m0 + t] = s_rs[p][t];
+    // Row sums (lowpgemm.hpp:121-123): per lane the two codes of positions
+    // (2k, 2k+1) as 16-bit halves, one warp reduction (REDUX) per pair.
+    uint32_t mine = 0u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t a = __byte_perm(pk[2 * k], pk[2 * k + 1], 0x5410);  // [p.c0, p.c1, q.c0, q.c1]
+      const uint32_t w = (a & 0x00FF00FFu) + ((a >> 8) & 0x00FF00FFu);  // [p sum | q sum]
+      const uint32_t tot = __reduce_add_sync(0xffffffffu, w);
+      if ((lane >> 1) == k) mine = (lane & 1) ? (tot >> 16) : (tot & 0xFFFFu);
+    }
+    if (lane < 16) rowsum[static_cast<long long>(lane) * g.M + m] = static_cast<int32_t>(mine);
   }
 }
 
@@ -231,9 +308,8 @@ __global__ void static_params_kernel(LanceDevState* st, StaticParams prm, int C)
 
 // --------------------------------------------------------------------------
 int input_range_grid(const InGeom& g, int sm_count) {
-  const long long warps = static_cast<long long>(g.M) * g.nchunks;
-  const long long blocks = (warps + 7) / 8;
-  const long long cap = 3LL * sm_count;  // 3 resident 256-thread blocks per SM
+  const long long blocks = (g.num_items + 7) / 8;
+  const long long cap = 2LL * sm_count;  // 2 resident 256-thread blocks per SM
   return static_cast<int>(blocks < cap ? blocks : cap);
 }
 
@@ -249,7 +325,7 @@ cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceD
 cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
                                const LanceDevState* st, const InGeom& g, int vec2,
                                int static_mode, cudaStream_t s) {
-  const unsigned grid = static_cast<unsigned>((g.M + kTM - 1) / kTM);
+  const unsigned grid = static_cast<unsigned>((g.num_items + 7) / 8);
   if (vec2) {
     if (static_mode)
       input_quant_kernel<true, true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);

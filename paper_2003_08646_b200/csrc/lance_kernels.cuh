@@ -14,7 +14,6 @@ constexpr int kBM = 128;        // GEMM rows (Winograd tiles) per CTA = UMMA M
 constexpr int kBN = 16;         // filters per CTA: 16 positions x 16 = 256 TMEM columns
 constexpr int kGemmThreads = 192;
 constexpr int kChunk = 64;      // channels per K0/K1 warp item (32 lanes x 2)
-constexpr int kTM = 8;          // tiles (one per warp) per K1 block
 
 // Per-plan device state, written by the range / filter finalisers and read by
 // the quantiser and the GEMM epilogue.  Mirrors QuantParams (quant.hpp:27-37)
@@ -32,11 +31,14 @@ struct LanceDevState {
 // Input-side geometry shared by the range pass (K0) and the quantiser (K1).
 struct InGeom {
   int M;          // GEMM rows = N * P (< 2^31, checked at plan creation)
-  int P, TW;      // tiles per image, tiles per image row
+  int P, TH, TW;  // tiles per image, tile rows / columns per image
   int H, W, C;    // image dims, channels
   int C_pad;      // code row pitch (multiple of 32)
   int pad;
   int nchunks;    // ceil(C_pad / kChunk)
+  int seg_len;    // tiles per warp strip (a tile row is split into nseg strips)
+  int nseg;
+  long long num_items;  // N * TH * nseg * nchunks warp items
   int granularity;  // 1 = PerPosition, 2 = PerTensor
 };
 

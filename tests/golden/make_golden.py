@@ -36,6 +36,9 @@ CASES = [
     ("bits_w4_i6_s9", Spec(1, 32, 16, 16, 32, 1), 4, 6, 1, "relu", 9),
     ("bits2_s13", Spec(1, 48, 12, 12, 16, 1), 2, 2, 1, "uniform", 13),
     ("pertensor_s21", Spec(1, 32, 16, 16, 32, 1), 8, 8, 2, "relu", 21),
+    ("c160_nonsmall_s4", Spec(1, 160, 10, 10, 48, 1), 8, 8, 1, "relu", 4),
+    ("c192_k80_pad0_s6", Spec(2, 192, 9, 9, 80, 0), 8, 8, 1, "uniform", 6),
+    ("c130_odd_k17_s8", Spec(1, 130, 11, 13, 17, 1), 7, 8, 1, "relu", 8),
     ("r256_slice_s42", Spec(1, 256, 14, 14, 256, 1), 8, 8, 1, "uniform", 42),
     ("r512_slice_s42", Spec(2, 512, 7, 7, 512, 1), 8, 8, 1, "relu", 42),
 ]
