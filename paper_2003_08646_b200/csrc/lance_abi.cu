@@ -408,6 +408,8 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
   }
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[1], s));
+  if (p->in_geom.nchunks > 1)
+    LANCE_CUDA(cudaMemsetAsync(p->rowsum, 0, sizeof(int32_t) * 16 * p->M, s));
   LANCE_CUDA(launch_input_quant(x_dev, p->codes_a, p->rowsum, p->state, p->in_geom, p->vec2,
                                 static_params != nullptr, s));
   ++launches;
