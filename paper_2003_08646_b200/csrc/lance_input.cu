@@ -161,35 +161,25 @@ __global__ void __launch_bounds__(256, 2) input_range_kernel(const float* __rest
   }
 }
 
-// Rare path of K1 (kept out of line so the fast path keeps its registers):
-// re-quantise exactly, with the IEEE formula, every value whose fast-path
-// residual is within 2^-14 of a rounding boundary (or NaN).
-template <bool STATIC>
-__device__ __noinline__ void requantize_flagged(const float2 (&v)[16], const float* s_tmin,
-                                                const float* s_scale, const float* s_rcp,
-                                                float top, uint32_t (&pk)[16]) {
-#pragma unroll 1
-  for (int p = 0; p < 16; ++p) {
-    const float2 dd = sub2(v[p], bcast2(s_tmin[p]));
-    float ra, rb;
-    if (STATIC) {
-      float2 q = mul2_rn(dd, bcast2(s_rcp[p]));
-      q.x = fminf(fmaxf(q.x, 0.0f), top);
-      q.y = fminf(fmaxf(q.y, 0.0f), top);
-      ra = __fsub_rn(q.x, __fsub_rn(__fadd_rn(q.x, kMagic), kMagic));
-      rb = __fsub_rn(q.y, __fsub_rn(__fadd_rn(q.y, kMagic), kMagic));
-    } else {
-      const float2 gq = fma2(dd, bcast2(s_rcp[p]), bcast2(kMagic));
-      const float2 r = fma2(dd, bcast2(s_rcp[p]),
-                            make_float2(-__fsub_rn(gq.x, kMagic), -__fsub_rn(gq.y, kMagic)));
-      ra = r.x;
-      rb = r.y;
-    }
-    if (!(fabsf(ra) < kTieGuard))
-      pk[p] = (pk[p] & 0xFF00u) | quantize_code(v[p].x, s_tmin[p], s_scale[p], top);
-    if (!(fabsf(rb) < kTieGuard))
-      pk[p] = (pk[p] & 0x00FFu) | (quantize_code(v[p].y, s_tmin[p], s_scale[p], top) << 8);
-  }
+// Exact reference code for a value whose fast-path residual flagged it as
+// being near the rounding boundary h = n + 0.5*sign(r) (dynamic params: d >= 0,
+// scale > 0 normal).  roundf(RN(d/s)) crosses to the upper code iff
+// RN(d/s) >= h, i.e. iff d/s > mid(pred(h), h) (a float quotient is never a
+// midpoint, so there is no tie), i.e. iff d - s*h > -s*delta with
+// delta = (h - pred(h))/2.  d - s*h is exactly representable here
+// (|d - s*h| <= s*2^-13, granularity ulp(s)/2), so one FFMA decides it.
+__device__ __forceinline__ uint32_t exact_code_near_boundary(float d, float s, float gq, float r,
+                                                             float top) {
+  const float n = __fsub_rn(gq, kMagic);
+  const float h = (r > 0.0f) ? __fadd_rn(n, 0.5f) : __fsub_rn(n, 0.5f);
+  const float lower = (r > 0.0f) ? n : __fsub_rn(n, 1.0f);
+  const float upper = __fadd_rn(lower, 1.0f);
+  const float pred_h = __int_as_float(__float_as_int(h) - 1);
+  const float delta = __fmul_rn(__fsub_rn(h, pred_h), 0.5f);
+  const float e = __fmaf_rn(-s, h, d);
+  float c = (e > -__fmul_rn(s, delta)) ? upper : lower;
+  c = fminf(fmaxf(c, 0.0f), top);
+  return static_cast<uint32_t>(c);
 }
 
 // --------------------------------------------------------------------------
@@ -234,55 +224,74 @@ __global__ void __launch_bounds__(256, 2) input_quant_kernel(const float* __rest
   }
   int m = (it.img * g.TH + it.ti) * g.TW + it.tj0;
   for (int tj = it.tj0; tj < it.tj1; ++tj, xx += 2, ++m) {
-    uint32_t pk[16];
-#pragma unroll
-    for (int p = 0; p < 16; ++p) pk[p] = 0u;
+    float2 v[16];
     if (lane_on) {
       sp.column(xx + 2, tc);
       sp.column(xx + 3, td);
-      float2 v[16];
       row_pass(ta, tb, tc, td, v);
-      float rmax = 0.0f;
-#pragma unroll
-      for (int p = 0; p < 16; ++p) {
-        const float2 dd = sub2(v[p], bcast2(s_tmin[p]));
-        float2 gq, r;
-        if (STATIC) {
-          float2 q = mul2_rn(dd, bcast2(s_rcp[p]));
-          q.x = fminf(fmaxf(q.x, 0.0f), top);  // NaN -> 0 like quant.hpp:81
-          q.y = fminf(fmaxf(q.y, 0.0f), top);
-          gq = add2(q, bcast2(kMagic));
-          r = sub2(q, sub2(gq, bcast2(kMagic)));
-        } else {
-          gq = fma2(dd, bcast2(s_rcp[p]), bcast2(kMagic));
-          r = fma2(dd, bcast2(s_rcp[p]),
-                   make_float2(-__fsub_rn(gq.x, kMagic), -__fsub_rn(gq.y, kMagic)));
-        }
-        rmax = fmax3_nan(rmax, fabsf(r.x), fabsf(r.y));
-        pk[p] = __byte_perm(__float_as_uint(gq.x), __float_as_uint(gq.y), 0x0040) & 0xFFFFu;
-      }
-      if (!(rmax < kTieGuard)) requantize_flagged<STATIC>(v, s_tmin, s_scale, s_rcp, top, pk);
-      if (!two) {
-#pragma unroll
-        for (int p = 0; p < 16; ++p) pk[p] &= 0x00FFu;  // odd C: padding channel code 0
-      }
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         ta[a] = tc[a];
         tb[a] = td[a];
       }
-      // Codes: 64 contiguous bytes per warp per position (the A operand row).
-      uint8_t* dst = codes + static_cast<long long>(m) * g.C_pad + it.ch;
-#pragma unroll
-      for (int p = 0; p < 16; ++p)
-        *reinterpret_cast<uint16_t*>(dst + p * pstride) = static_cast<uint16_t>(pk[p]);
     }
-    // Row sums (lowpgemm.hpp:121-123): per lane the two codes of positions
-    // (2k, 2k+1) as 16-bit halves, one warp reduction (REDUX) per pair.
+    uint8_t* dst = codes + static_cast<long long>(m) * g.C_pad + it.ch;
     uint32_t mine = 0u;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const uint32_t a = __byte_perm(pk[2 * k], pk[2 * k + 1], 0x5410);  // [p.c0, p.c1, q.c0, q.c1]
+      uint32_t pk[2] = {0u, 0u};
+      if (lane_on) {
+        float2 dd[2], gq[2], r[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int p = 2 * k + h;
+          dd[h] = sub2(v[p], bcast2(s_tmin[p]));
+          if (STATIC) {
+            float2 q = mul2_rn(dd[h], bcast2(s_rcp[p]));
+            q.x = fminf(fmaxf(q.x, 0.0f), top);  // NaN -> 0 like quant.hpp:81
+            q.y = fminf(fmaxf(q.y, 0.0f), top);
+            gq[h] = add2(q, bcast2(kMagic));
+            r[h] = sub2(q, sub2(gq[h], bcast2(kMagic)));
+          } else {
+            gq[h] = fma2(dd[h], bcast2(s_rcp[p]), bcast2(kMagic));
+            r[h] = fma2(dd[h], bcast2(s_rcp[p]),
+                        make_float2(-__fsub_rn(gq[h].x, kMagic), -__fsub_rn(gq[h].y, kMagic)));
+          }
+          pk[h] = __byte_perm(__float_as_uint(gq[h].x), __float_as_uint(gq[h].y), 0x0040) & 0xFFFFu;
+        }
+        const float rmax = fmax3_nan(fmax3_nan(fabsf(r[0].x), fabsf(r[0].y), fabsf(r[1].x)),
+                                     fabsf(r[1].y), 0.0f);
+        if (!(rmax < kTieGuard)) {
+          // Rare (~1e-4 per value): re-derive the flagged codes exactly.
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int p = 2 * k + h;
+            uint32_t c0, c1;
+            if (STATIC) {
+              c0 = quantize_code(v[p].x, s_tmin[p], s_scale[p], top);
+              c1 = quantize_code(v[p].y, s_tmin[p], s_scale[p], top);
+            } else {
+              c0 = (fabsf(r[h].x) < kTieGuard)
+                       ? (pk[h] & 0xFFu)
+                       : exact_code_near_boundary(dd[h].x, s_scale[p], gq[h].x, r[h].x, top);
+              c1 = (fabsf(r[h].y) < kTieGuard)
+                       ? (pk[h] >> 8)
+                       : exact_code_near_boundary(dd[h].y, s_scale[p], gq[h].y, r[h].y, top);
+            }
+            pk[h] = c0 | (c1 << 8);
+          }
+        }
+        if (!two) {  // odd C: padding channel code 0
+          pk[0] &= 0x00FFu;
+          pk[1] &= 0x00FFu;
+        }
+        // Codes: 64 contiguous bytes per warp per position (the A operand row).
+        *reinterpret_cast<uint16_t*>(dst + (2 * k) * pstride) = static_cast<uint16_t>(pk[0]);
+        *reinterpret_cast<uint16_t*>(dst + (2 * k + 1) * pstride) = static_cast<uint16_t>(pk[1]);
+      }
+      // Row sums (lowpgemm.hpp:121-123): the lane's two codes of positions
+      // (2k, 2k+1) as 16-bit halves, one warp reduction (REDUX) per pair.
+      const uint32_t a = pk[0] | (pk[1] << 16);                          // [p.c0, p.c1, q.c0, q.c1]
       const uint32_t w = (a & 0x00FF00FFu) + ((a >> 8) & 0x00FF00FFu);  // [p sum | q sum]
       const uint32_t tot = __reduce_add_sync(0xffffffffu, w);
       if ((lane >> 1) == k) mine = (lane & 1) ? (tot >> 16) : (tot & 0xFFFFu);
