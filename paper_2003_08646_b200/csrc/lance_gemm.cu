@@ -44,7 +44,7 @@ struct GemmCfg {
                                       (2 * kStages + 4) * 8 + 16;
 };
 
-constexpr size_t kSmemLimit = 227 * 1024;
+constexpr size_t kSmemLimit = 227 * 1024 - 1024;  // leave room for static smem
 
 // SMALL: C * top_a * top_b < 2^23, so every accumulator is below 2^23 and
 // k1 * float(dot) is formed exactly by one FFMA (see below).
@@ -329,19 +329,19 @@ static cudaError_t launch_gemm_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
                                  const float* bias, int relu, const GemmGeom& g, cudaStream_t s) {
   const size_t smem = GemmCfg<BK>::kSmemBase + static_cast<size_t>(16) * g.num_n_tiles * kBN * 4;
   if (smem > kSmemLimit) return cudaErrorInvalidValue;
-  static bool configured[64] = {};  // the attribute is per device
+  static size_t configured[64] = {};  // dynamic-smem attribute set so far, per device
   static int sm_count[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64 || !configured[dev]) {
+  if (dev < 0 || dev >= 64 || configured[dev] < smem) {
     cudaError_t e = cudaFuncSetAttribute(gemm_epilogue_kernel<BK, SMALL, EPI>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmemLimit));
+                                         static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (dev >= 0 && dev < 64) {
-      configured[dev] = true;
+      configured[dev] = smem;
       sm_count[dev] = sms;
     }
   }
