@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -124,7 +125,7 @@ struct lance_plan_s {
   lance_config cfg{};
   int OH = 0, OW = 0, TH = 0, TW = 0, P = 0;
   long long M = 0;
-  int C_pad = 0, K_pad = 0, BK = 32;
+  int C_pad = 0, K_pad = 0, BK = 32, BN = 16;
   int sm_count = 148;
   int range_grid = 1, filter_grid = 1;
   InGeom in_geom{};
@@ -183,12 +184,6 @@ int dev_alloc(lance_plan_s* p, T** ptr, size_t bytes) {
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
   p->bytes += bytes;
   return LANCE_OK;
-}
-
-int pow2ceil(int v) {
-  int r = 1;
-  while (r < v) r <<= 1;
-  return r;
 }
 
 }  // namespace
@@ -263,10 +258,22 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   p->P = p->TH * p->TW;
   p->M = static_cast<long long>(spec->n) * p->P;
   p->C_pad = round_up(spec->c, 32);
-  p->K_pad = round_up(spec->k, kBN);
+  // GEMM tile width: 32 filters (one TMEM accumulator, half the A re-reads
+  // and twice the work per ~44-cycle MMA) for deep layers, 16 (double
+  // buffered accumulators) otherwise.  LANCE_GEMM_BN overrides.
+  p->BN = (round_up(spec->c, 32) >= 256) ? 32 : 16;
+  if (const char* e = std::getenv("LANCE_GEMM_BN")) {
+    const int v = std::atoi(e);
+    if (v == 16 || v == 32) p->BN = v;
+  }
+  p->K_pad = round_up(spec->k, p->BN);
   p->BK = (p->C_pad % 128 == 0) ? 128 : (p->C_pad % 64 == 0 ? 64 : 32);
   p->vec2 = (spec->c % 2) == 0;
 
+  if (static_cast<long long>(spec->n) * p->OH * p->OW >= (1LL << 27)) {
+    delete p;
+    return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_gemm: N * OH * OW exceeds 2^27 output pixels");
+  }
   if (p->M >= (1LL << 31)) {
     delete p;
     return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_gemm: N * tiles exceeds 2^31 rows");
@@ -314,7 +321,7 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   gg.OH = p->OH;
   gg.OW = p->OW;
   gg.num_kchunks = p->C_pad / p->BK;
-  gg.num_n_tiles = p->K_pad / kBN;
+  gg.num_n_tiles = p->K_pad / p->BN;
 
   const size_t codes_a_bytes = static_cast<size_t>(16) * p->M * p->C_pad;
   const size_t codes_w_bytes = static_cast<size_t>(16) * p->K_pad * p->C_pad;
@@ -345,7 +352,7 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
     return cuda_fail(e, "plan init");
   }
   if ((rc = make_code_map(&p->tmA, p->codes_a, p->M, p->C_pad, p->BK, kBM)) ||
-      (rc = make_code_map(&p->tmB, p->codes_w, p->K_pad, p->C_pad, p->BK, kBN))) {
+      (rc = make_code_map(&p->tmB, p->codes_w, p->K_pad, p->C_pad, p->BK, p->BN))) {
     free_plan(p);
     delete p;
     return rc;
@@ -414,7 +421,7 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
                                 static_params != nullptr, s));
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[2], s));
-  LANCE_CUDA(launch_gemm(&p->tmA, &p->tmB, p->BK, p->small_acc, p->rowsum, p->colsum, p->state, y_dev,
+  LANCE_CUDA(launch_gemm(&p->tmA, &p->tmB, p->BK, p->BN, p->small_acc, p->rowsum, p->colsum, p->state, y_dev,
                          p->acc_dump, p->bias, p->relu, p->gemm_geom, s));
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[3], s));

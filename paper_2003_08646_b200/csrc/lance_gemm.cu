@@ -6,18 +6,22 @@
 // discard (tensor.hpp:157-182).
 //
 // Persistent kernel, one CTA per SM.  A tile = 128 Winograd tiles (UMMA M)
-// x 16 filters (UMMA N) x all 16 positions = 16 x 16 s32 = 256 TMEM columns;
-// TMEM holds two such accumulators, so the MMA of tile i+1 overlaps the
-// epilogue of tile i, and the TMA producer runs ahead through an SMEM ring.
+// x BN filters (UMMA N) x all 16 positions = 16*BN s32 TMEM columns; with
+// BN = 16 TMEM holds two accumulators (the MMA of tile i+1 overlaps the
+// epilogue of tile i), with BN = 32 one (twice the MMA work per A byte: a
+// K=32 kind::i8 MMA with M=128 costs ~44 cycles for any N <= 32 because the
+// 4 KB A operand is read from shared memory each time).  The TMA producer runs
+// ahead of the MMA through a shared-memory ring.
 //   warp 0       TMA producer (one lane): per stage the A box
-//                [128 rows x BK ch] and B box [16 filters x BK ch] of one
+//                [128 rows x BK ch] and the B box [BN filters x BK ch] of one
 //                position
 //   warp 1       TMEM allocator + UMMA issuer (one lane)
-//   warps 2..9   epilogue: TMEM -> registers -> affine -> A^T m A -> y; warp
-//                w drains TMEM lane quadrant w % 4, filters 8*((w-2)/4)..+8
-// Tiles are assigned round-robin with the filter tile fastest, so the
-// kBN-wide filter tiles of one row tile run concurrently on neighbouring SMs
-// and share the A operand through L2.
+//   warps 2..9   epilogue: TMEM -> registers -> affine -> A^T m A -> shared
+//                staging -> full-sector stores of y; warp w drains TMEM lane
+//                quadrant w % 4 and filters (BN/2)*((w-2)/4) .. +BN/2
+// Tiles are assigned round-robin with the filter tile fastest, so the filter
+// tiles of one row tile run concurrently on neighbouring SMs and share the A
+// operand through L2.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -29,27 +33,28 @@ namespace lance_dev {
 
 constexpr int kEpiWarps = 8;
 constexpr int kGemmThreadsP = 64 + 32 * kEpiWarps;  // 320
+constexpr size_t kSmemLimit = 226 * 1024;           // dynamic part, leaves room for static smem
 
-template <int BK>
+template <int BK, int BN>
 struct GemmCfg {
+  static constexpr int kBufs = (BN == 16) ? 2 : 1;
   static constexpr uint32_t kABytes = kBM * BK;
-  static constexpr uint32_t kBBytes = kBN * BK;
+  static constexpr uint32_t kBBytes = BN * BK;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  static constexpr int kStagesRaw = (144 * 1024) / kStageBytes;
+  static constexpr int kStagesRaw = (128 * 1024) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 16 ? 16 : kStagesRaw;
   static constexpr uint32_t kLayout = (BK == 128) ? 2u : (BK == 64 ? 4u : 6u);  // SW128/64/32
-  static constexpr uint32_t kAccCols = 16 * kBN;                                // 256
+  static constexpr uint32_t kAccCols = 16 * BN;
+  static constexpr uint32_t kStagingBytes = kEpiWarps * 32 * 4 * 8 * 4;  // 8 filters x 4 px x 32 rows
   // + 16 * K_pad floats of per-filter constants, added at launch.
   static constexpr size_t kSmemBase = 1024 + static_cast<size_t>(kStages) * kStageBytes +
-                                      (2 * kStages + 4) * 8 + 16;
+                                      kStagingBytes + (2 * kStages + 4) * 8 + 16;
 };
-
-constexpr size_t kSmemLimit = 227 * 1024 - 1024;  // leave room for static smem
 
 // SMALL: C * top_a * top_b < 2^23, so every accumulator is below 2^23 and
 // k1 * float(dot) is formed exactly by one FFMA (see below).
 // EPI: fused bias + ReLU (north-star extension).
-template <int BK, bool SMALL, bool EPI>
+template <int BK, int BN, bool SMALL, bool EPI>
 __global__ void __launch_bounds__(kGemmThreadsP, 1)
     gemm_epilogue_kernel(const __grid_constant__ CUtensorMap tmA,
                          const __grid_constant__ CUtensorMap tmB,
@@ -57,9 +62,11 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
                          const LanceDevState* __restrict__ st, float* __restrict__ y,
                          int32_t* __restrict__ acc_dump, const float* __restrict__ bias,
                          int relu, GemmGeom g) {
-  using Cfg = GemmCfg<BK>;
+  using Cfg = GemmCfg<BK, BN>;
   constexpr int kStages = Cfg::kStages;
-  constexpr uint32_t kIdesc = umma_idesc_u8(kBM, kBN);
+  constexpr int kBufs = Cfg::kBufs;
+  constexpr uint32_t kIdesc = umma_idesc_u8(kBM, BN);
+  constexpr int kWarpFilters = BN / 2;  // filters per epilogue warp
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ float s_k1[16], s_nk1m[16], s_k2[16], s_k4[16];
@@ -67,7 +74,9 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* stage_base = smem;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes);
+  float* staging = reinterpret_cast<float*>(smem + kStages * Cfg::kStageBytes);  // [8 warps][1024]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes +
+                                                   Cfg::kStagingBytes);
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* acc_full = empty_bar + kStages;  // [2]
   uint64_t* acc_empty = acc_full + 2;        // [2]
@@ -76,7 +85,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = g.num_n_tiles;
-  const int K_pad = nt * kBN;
+  const int K_pad = nt * BN;
   const int num_tiles = ((g.M + kBM - 1) / kBM) * nt;
   const int num_iters = g.num_kchunks * 16;
 
@@ -117,7 +126,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile / nt) * kBM, n0 = (tile % nt) * kBN;
+        const int m0 = (tile / nt) * kBM, n0 = (tile % nt) * BN;
         for (int it = 0; it < num_iters; ++it) {
           const int kc = it >> 4, p = it & 15;
           mbar_wait(&empty_bar[s], ph ^ 1u);
@@ -134,7 +143,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     }
   } else if (warp == 1) {
     // ---------------- TMEM + UMMA issuer ----------------
-    tmem_alloc(tmem_holder, 2 * Cfg::kAccCols);
+    tmem_alloc(tmem_holder, 512);
     tmem_relinquish();
     tc_fence_before();
     named_bar_sync(1, 32 + 32 * kEpiWarps);
@@ -159,7 +168,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
           for (int kk = 0; kk < BK / 32; ++kk) {
             const uint64_t adesc = umma_smem_desc(sa + kk * 32, 8 * BK, Cfg::kLayout);
             const uint64_t bdesc = umma_smem_desc(sb + kk * 32, 8 * BK, Cfg::kLayout);
-            umma_i8(d_base + static_cast<uint32_t>(p * kBN), adesc, bdesc, kIdesc,
+            umma_i8(d_base + static_cast<uint32_t>(p * BN), adesc, bdesc, kIdesc,
                     (kc > 0 || kk > 0) ? 1u : 0u);
           }
           umma_commit(&empty_bar[s]);
@@ -169,7 +178,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
           }
         }
         umma_commit(&acc_full[buf]);
-        if (++buf == 2) {
+        if (++buf == kBufs) {
           buf = 0;
           acc_ph ^= 1u;
         }
@@ -179,13 +188,14 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   } else {
     // ---------------- epilogue ----------------
     const int ew = warp - 2;
-    const int q = warp & 3;          // TMEM lane quadrant this warp may access
-    const int f0 = (ew >> 2) * 8;    // this warp's 8 filters within the 16-filter tile
+    const int q = warp & 3;                   // TMEM lane quadrant this warp may access
+    const int f0 = (ew >> 2) * kWarpFilters;  // this warp's filters within the tile
+    float* stg = staging + ew * 1024;         // [32 rows][4 px][8 filters], 16-B chunks swizzled
     named_bar_sync(1, 32 + 32 * kEpiWarps);
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-    const bool vec_ok = (g.K & 1) == 0;
+    const bool k4ok = (g.K & 3) == 0;
     int buf = 0;
     uint32_t acc_ph = 0;
     // Row sums of the first tile (later tiles are prefetched one tile ahead).
@@ -194,11 +204,10 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       const int m = (blockIdx.x / nt) * kBM + q * 32 + lane;
 #pragma unroll
       for (int p = 0; p < 16; ++p)
-        rs_next[p] = (blockIdx.x < num_tiles && m < g.M)
-                         ? __ldg(rowsum + static_cast<long long>(p) * g.M + m) : 0;
+        rs_next[p] = (m < g.M) ? __ldg(rowsum + static_cast<long long>(p) * g.M + m) : 0;
     }
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int m0 = (tile / nt) * kBM, n0 = (tile % nt) * kBN;
+      const int m0 = (tile / nt) * kBM, n0 = (tile % nt) * BN;
       const int m = m0 + q * 32 + lane;
       const bool row_ok = m < g.M;
       float rterm[16];  // k2[p] * float(sum_a): second term of affine_term
@@ -212,104 +221,126 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
           rs_next[p] = (nxt < num_tiles && mn < g.M)
                            ? __ldg(rowsum + static_cast<long long>(p) * g.M + mn) : 0;
       }
-      // Output pixels of this tile: (2ti + a, 2tj + b); merge_tiles discards
-      // the ceil-overhang (tensor.hpp:172-175).
-      float* dst[4];
-      bool ok[4];
+      // Output pixels of this lane's tile (2ti + a, 2tj + b) and their
+      // validity (merge_tiles discards the ceil-overhang, tensor.hpp:172-175).
+      // Packed (pixel index << 4 | validity mask): pixel counts < 2^27 are
+      // checked at plan creation.
+      int pixm;
       {
         const int mm = row_ok ? m : 0;
         const int img = mm / g.P;
         const int t = mm - img * g.P;
         const int ti = t / g.TW, tj = t - ti * g.TW;
-#pragma unroll
-        for (int ab = 0; ab < 4; ++ab) {
-          const int oy = 2 * ti + (ab >> 1), ox = 2 * tj + (ab & 1);
-          ok[ab] = row_ok && oy < g.OH && ox < g.OW;
-          dst[ab] = y + ((static_cast<long long>(img) * g.OH + oy) * g.OW + ox) * g.K + n0 + f0;
-        }
+        const int pix0 = (img * g.OH + 2 * ti) * g.OW + 2 * tj;
+        const bool r1 = 2 * ti + 1 < g.OH, c1 = 2 * tj + 1 < g.OW;
+        const int pmask = row_ok ? (1 | (c1 ? 2 : 0) | (r1 ? 4 : 0) | (r1 && c1 ? 8 : 0)) : 0;
+        pixm = (pix0 << 4) | pmask;
       }
       mbar_wait(&acc_full[buf], acc_ph);
       tc_fence_after();
       const uint32_t acc_addr = lane_base + static_cast<uint32_t>(buf) * Cfg::kAccCols + f0;
 #pragma unroll 1
-      for (int j = 0; j < 4; ++j) {  // filter pairs of this warp's 8 filters
-        uint32_t a[16][2];
+      for (int grp = 0; grp < kWarpFilters / 8; ++grp) {
+#pragma unroll 1
+        for (int jj = 0; jj < 4; ++jj) {  // filter pairs of this 8-filter group
+          const int fl = grp * 8 + jj * 2;  // filter offset within the warp's range
+          uint32_t a[16][2];
 #pragma unroll
-        for (int p = 0; p < 16; ++p) tmem_ld_x2(acc_addr + p * kBN + j * 2, a[p]);
-        tmem_ld_wait();
-        if (j == 3) {
-          // All of this warp's accumulators are in registers: hand the TMEM
-          // buffer back to the MMA warp early.
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&acc_empty[buf]);
-        }
-        const int kf0 = n0 + f0 + j * 2;
-        if (acc_dump != nullptr && row_ok) {
-#pragma unroll
-          for (int p = 0; p < 16; ++p)
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-              if (kf0 + i < g.K)
-                acc_dump[(static_cast<long long>(p) * g.M + m) * g.K + kf0 + i] =
-                    static_cast<int32_t>(a[p][i]);
-        }
-        float2 mv[16];
-#pragma unroll
-        for (int p = 0; p < 16; ++p) {
-          const float2 c2 = *reinterpret_cast<const float2*>(&s_cterm[p * K_pad + kf0]);
-          const float k1 = s_k1[p];
-          float2 t1;
-          if (SMALL) {
-            // dot < 2^23: F = 2^23 + dot exactly, and fma(k1, F, -k1*2^23)
-            // rounds once: RN(k1 * dot) = k1 * float(dot), bitwise.
-            const float2 F = make_float2(__uint_as_float(a[p][0] | 0x4B000000u),
-                                         __uint_as_float(a[p][1] | 0x4B000000u));
-            t1 = fma2(bcast2(k1), F, bcast2(s_nk1m[p]));
-          } else {
-            t1 = make_float2(__fmul_rn(k1, __int2float_rn(static_cast<int>(a[p][0]))),
-                             __fmul_rn(k1, __int2float_rn(static_cast<int>(a[p][1]))));
+          for (int p = 0; p < 16; ++p) tmem_ld_x2(acc_addr + p * BN + fl, a[p]);
+          tmem_ld_wait();
+          if (grp == kWarpFilters / 8 - 1 && jj == 3) {
+            // All of this warp's accumulators are in registers: hand the TMEM
+            // buffer back to the MMA warp early.
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[buf]);
           }
-          // ((k1*dot + k2*sum_a) + k3*sum_b) + k4, left to right.
-          mv[p] = add2(add2(add2(t1, bcast2(rterm[p])), c2), bcast2(s_k4[p]));
-        }
-        // S = (A^T m) A (winograd.hpp:80-84 in matrix.hpp:75-84 order).
-        float2 X0[4], X1[4];
+          const int kf0 = n0 + f0 + fl;
+          if (acc_dump != nullptr && row_ok) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          X0[c] = add2(add2(mv[c], mv[4 + c]), mv[8 + c]);
-          X1[c] = sub2(sub2(mv[4 + c], mv[8 + c]), mv[12 + c]);
-        }
-        float2 s4[4];
-        s4[0] = add2(add2(X0[0], X0[1]), X0[2]);
-        s4[1] = sub2(sub2(X0[1], X0[2]), X0[3]);
-        s4[2] = add2(add2(X1[0], X1[1]), X1[2]);
-        s4[3] = sub2(sub2(X1[1], X1[2]), X1[3]);
-        if (kf0 < g.K) {
+            for (int p = 0; p < 16; ++p)
+#pragma unroll
+              for (int i = 0; i < 2; ++i)
+                if (kf0 + i < g.K)
+                  acc_dump[(static_cast<long long>(p) * g.M + m) * g.K + kf0 + i] =
+                      static_cast<int32_t>(a[p][i]);
+          }
+          float2 mv[16];
+#pragma unroll
+          for (int p = 0; p < 16; ++p) {
+            const float2 c2 = *reinterpret_cast<const float2*>(&s_cterm[p * K_pad + kf0]);
+            const float k1 = s_k1[p];
+            float2 t1;
+            if (SMALL) {
+              // dot < 2^23: F = 2^23 + dot exactly, and fma(k1, F, -k1*2^23)
+              // rounds once: RN(k1 * dot) = k1 * float(dot), bitwise.
+              const float2 F = make_float2(__uint_as_float(a[p][0] | 0x4B000000u),
+                                           __uint_as_float(a[p][1] | 0x4B000000u));
+              t1 = fma2(bcast2(k1), F, bcast2(s_nk1m[p]));
+            } else {
+              t1 = make_float2(__fmul_rn(k1, __int2float_rn(static_cast<int>(a[p][0]))),
+                               __fmul_rn(k1, __int2float_rn(static_cast<int>(a[p][1]))));
+            }
+            // ((k1*dot + k2*sum_a) + k3*sum_b) + k4, left to right.
+            mv[p] = add2(add2(add2(t1, bcast2(rterm[p])), c2), bcast2(s_k4[p]));
+          }
+          // S = (A^T m) A (winograd.hpp:80-84 in matrix.hpp:75-84 order).
+          float2 X0[4], X1[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            X0[c] = add2(add2(mv[c], mv[4 + c]), mv[8 + c]);
+            X1[c] = sub2(sub2(mv[4 + c], mv[8 + c]), mv[12 + c]);
+          }
+          float2 s4[4];
+          s4[0] = add2(add2(X0[0], X0[1]), X0[2]);
+          s4[1] = sub2(sub2(X0[1], X0[2]), X0[3]);
+          s4[2] = add2(add2(X1[0], X1[1]), X1[2]);
+          s4[3] = sub2(sub2(X1[1], X1[2]), X1[3]);
 #pragma unroll
           for (int ab = 0; ab < 4; ++ab) {
             float2 v = s4[ab];
             if (EPI) {
               if (bias != nullptr)
-                v = add2(v, make_float2(bias[kf0], kf0 + 1 < g.K ? bias[kf0 + 1] : 0.0f));
+                v = add2(v, make_float2(kf0 < g.K ? bias[kf0] : 0.0f,
+                                        kf0 + 1 < g.K ? bias[kf0 + 1] : 0.0f));
               if (relu) {
                 v.x = fmaxf(v.x, 0.0f);
                 v.y = fmaxf(v.y, 0.0f);
               }
             }
             v = add2(v, bcast2(0.0f));  // the reference never yields -0
-            if (!ok[ab]) continue;
-            float* d = dst[ab] + j * 2;
-            if (vec_ok)
-              *reinterpret_cast<float2*>(d) = v;
-            else {
-              d[0] = v.x;
-              if (kf0 + 1 < g.K) d[1] = v.y;
-            }
+            // staging row = lane (tile), 16-B chunk (ab*2 + jj/2) ^ (lane & 7)
+            const int chunk = (ab * 2 + (jj >> 1)) ^ (lane & 7);
+            *reinterpret_cast<float2*>(&stg[lane * 32 + chunk * 4 + (jj & 1) * 2]) = v;
           }
         }
+        __syncwarp();
+        // Store phase: 32 rows x 4 pixels x 8 filters = 256 16-B chunks, two
+        // lanes per 32-byte pixel segment (full sectors).
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int c = lane + 32 * i;
+          const int r = c >> 3, ab = (c >> 1) & 3, half = c & 1;
+          const int rp = __shfl_sync(0xffffffffu, pixm, r);  // row r's pixel base + mask
+          const float4 val =
+              *reinterpret_cast<const float4*>(&stg[r * 32 + (((ab * 2 + half) ^ (r & 7)) * 4)]);
+          if (!((rp >> ab) & 1)) continue;
+          const int kf = n0 + f0 + grp * 8 + half * 4;
+          if (kf >= g.K) continue;
+          const int pix = (rp >> 4) + (ab >> 1) * g.OW + (ab & 1);
+          float* d = y + static_cast<long long>(pix) * g.K + kf;
+          if (k4ok) {
+            *reinterpret_cast<float4*>(d) = val;
+          } else {
+            const float v4[4] = {val.x, val.y, val.z, val.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (kf + e < g.K) d[e] = v4[e];
+          }
+        }
+        __syncwarp();
       }
-      if (++buf == 2) {
+      if (++buf == kBufs) {
         buf = 0;
         acc_ph ^= 1u;
       }
@@ -318,23 +349,24 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(*tmem_holder, 2 * Cfg::kAccCols);
+    tmem_dealloc(*tmem_holder, 512);
   }
 }
 
-template <int BK, bool SMALL, bool EPI>
+template <int BK, int BN, bool SMALL, bool EPI>
 static cudaError_t launch_gemm_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
                                  const int32_t* rowsum, const int32_t* colsum,
                                  const LanceDevState* st, float* y, int32_t* acc_dump,
                                  const float* bias, int relu, const GemmGeom& g, cudaStream_t s) {
-  const size_t smem = GemmCfg<BK>::kSmemBase + static_cast<size_t>(16) * g.num_n_tiles * kBN * 4;
+  const size_t smem =
+      GemmCfg<BK, BN>::kSmemBase + static_cast<size_t>(16) * g.num_n_tiles * BN * 4;
   if (smem > kSmemLimit) return cudaErrorInvalidValue;
   static size_t configured[64] = {};  // dynamic-smem attribute set so far, per device
   static int sm_count[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || configured[dev] < smem) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_epilogue_kernel<BK, SMALL, EPI>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_epilogue_kernel<BK, BN, SMALL, EPI>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -348,45 +380,44 @@ static cudaError_t launch_gemm_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
   const int sms = (dev >= 0 && dev < 64) ? sm_count[dev] : 148;
   const long long tiles = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * g.num_n_tiles;
   const int grid = static_cast<int>(tiles < sms ? tiles : sms);
-  gemm_epilogue_kernel<BK, SMALL, EPI><<<grid, kGemmThreadsP, smem, s>>>(
+  gemm_epilogue_kernel<BK, BN, SMALL, EPI><<<grid, kGemmThreadsP, smem, s>>>(
       *tmA, *tmB, rowsum, colsum, st, y, acc_dump, bias, relu, g);
   return cudaGetLastError();
 }
 
-template <int BK>
+template <int BK, int BN>
 static cudaError_t launch_gemm_bk(const CUtensorMap* tmA, const CUtensorMap* tmB, int small_acc,
                                   const int32_t* rowsum, const int32_t* colsum,
                                   const LanceDevState* st, float* y, int32_t* acc_dump,
                                   const float* bias, int relu, const GemmGeom& g, cudaStream_t s) {
   const bool epi = bias != nullptr || relu;
   if (small_acc)
-    return epi ? launch_gemm_t<BK, true, true>(tmA, tmB, rowsum, colsum, st, y, acc_dump, bias,
-                                               relu, g, s)
-               : launch_gemm_t<BK, true, false>(tmA, tmB, rowsum, colsum, st, y, acc_dump, bias,
-                                                relu, g, s);
-  return epi ? launch_gemm_t<BK, false, true>(tmA, tmB, rowsum, colsum, st, y, acc_dump, bias,
-                                              relu, g, s)
-             : launch_gemm_t<BK, false, false>(tmA, tmB, rowsum, colsum, st, y, acc_dump, bias,
-                                               relu, g, s);
+    return epi ? launch_gemm_t<BK, BN, true, true>(tmA, tmB, rowsum, colsum, st, y, acc_dump,
+                                                   bias, relu, g, s)
+               : launch_gemm_t<BK, BN, true, false>(tmA, tmB, rowsum, colsum, st, y, acc_dump,
+                                                    bias, relu, g, s);
+  return epi ? launch_gemm_t<BK, BN, false, true>(tmA, tmB, rowsum, colsum, st, y, acc_dump,
+                                                  bias, relu, g, s)
+             : launch_gemm_t<BK, BN, false, false>(tmA, tmB, rowsum, colsum, st, y, acc_dump,
+                                                   bias, relu, g, s);
 }
 
-cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int bk, int small_acc,
-                        const int32_t* rowsum, const int32_t* colsum, const LanceDevState* st,
-                        float* y, int32_t* acc_dump, const float* bias, int relu,
-                        const GemmGeom& g, cudaStream_t s) {
-  switch (bk) {
-    case 128:
-      return launch_gemm_bk<128>(tmA, tmB, small_acc, rowsum, colsum, st, y, acc_dump, bias,
-                                 relu, g, s);
-    case 64:
-      return launch_gemm_bk<64>(tmA, tmB, small_acc, rowsum, colsum, st, y, acc_dump, bias,
-                                relu, g, s);
-    case 32:
-      return launch_gemm_bk<32>(tmA, tmB, small_acc, rowsum, colsum, st, y, acc_dump, bias,
-                                relu, g, s);
-    default:
-      return cudaErrorInvalidValue;
-  }
+cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int bk, int bn,
+                        int small_acc, const int32_t* rowsum, const int32_t* colsum,
+                        const LanceDevState* st, float* y, int32_t* acc_dump, const float* bias,
+                        int relu, const GemmGeom& g, cudaStream_t s) {
+#define LANCE_GEMM_CASE(BKV, BNV)                                                            \
+  if (bk == BKV && bn == BNV)                                                                \
+    return launch_gemm_bk<BKV, BNV>(tmA, tmB, small_acc, rowsum, colsum, st, y, acc_dump,    \
+                                    bias, relu, g, s);
+  LANCE_GEMM_CASE(128, 16)
+  LANCE_GEMM_CASE(64, 16)
+  LANCE_GEMM_CASE(32, 16)
+  LANCE_GEMM_CASE(128, 32)
+  LANCE_GEMM_CASE(64, 32)
+  LANCE_GEMM_CASE(32, 32)
+#undef LANCE_GEMM_CASE
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace lance_dev

@@ -43,6 +43,8 @@ __device__ __forceinline__ StripItem strip_item(const InGeom& g, long long item,
   return {img, ti, tj0, tj1, chunk * kChunk + 2 * lane};
 }
 
+__device__ __forceinline__ void colpass(const float2 (&d)[4], float2 (&t)[4]);
+
 // Row context of a strip: the 4 input rows of tile row ti for this lane's
 // channel pair, with validity (zero padding above / below the image).
 template <bool VEC2>
@@ -67,10 +69,10 @@ struct Strip {
     }
   }
 
-  // Column pass of B^T d for input column xx: t[a] = (B^T d)(a, col).
-  __device__ __forceinline__ void column(int xx, float2 (&t)[4]) const {
+  // The 4 pixels (rows 0..3 of the strip) of input column xx, this lane's
+  // channel pair; zero outside the image.
+  __device__ __forceinline__ void load(int xx, float2 (&d)[4]) const {
     const bool cok = (xx >= 0) && (xx < W);
-    float2 d[4];
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       const float* px = row[a] + static_cast<long long>(cok ? xx : 0) * C;
@@ -82,12 +84,22 @@ struct Strip {
         d[a].y = (ok && c1ok) ? __ldg(px + 1) : 0.f;
       }
     }
-    t[0] = sub2(d[0], d[2]);
-    t[1] = add2(d[1], d[2]);
-    t[2] = sub2(d[2], d[1]);
-    t[3] = sub2(d[1], d[3]);
+  }
+
+  // Column pass of B^T d for input column xx: t[a] = (B^T d)(a, col).
+  __device__ __forceinline__ void column(int xx, float2 (&t)[4]) const {
+    float2 d[4];
+    load(xx, d);
+    colpass(d, t);
   }
 };
+
+__device__ __forceinline__ void colpass(const float2 (&d)[4], float2 (&t)[4]) {
+  t[0] = sub2(d[0], d[2]);
+  t[1] = add2(d[1], d[2]);
+  t[2] = sub2(d[2], d[1]);
+  t[3] = sub2(d[1], d[3]);
+}
 
 // Second (row) pass: v[a*4+b] from the column-pass results of 4 columns.
 __device__ __forceinline__ void row_pass(const float2 (&t0)[4], const float2 (&t1)[4],
@@ -124,13 +136,19 @@ __global__ void __launch_bounds__(256, 2) input_range_kernel(const float* __rest
     if (it.ch >= g.C) continue;  // lane beyond C (only in the last channel chunk)
     const Strip<VEC2> sp(x, g, it);
     const bool two = it.ch + 1 < g.C;
-    float2 ta[4], tb[4], tc[4], td[4];
+    float2 ta[4], tb[4], tc[4], td[4], pc[4], pd[4];
     int xx = 2 * it.tj0 - g.pad;
     sp.column(xx, ta);
     sp.column(xx + 1, tb);
+    sp.load(xx + 2, pc);
+    sp.load(xx + 3, pd);
     for (int tj = it.tj0; tj < it.tj1; ++tj, xx += 2) {
-      sp.column(xx + 2, tc);
-      sp.column(xx + 3, td);
+      colpass(pc, tc);
+      colpass(pd, td);
+      if (tj + 1 < it.tj1) {  // software prefetch of the next tile's two new columns
+        sp.load(xx + 4, pc);
+        sp.load(xx + 5, pd);
+      }
       float2 v[16];
       row_pass(ta, tb, tc, td, v);
       if (two) {
@@ -216,18 +234,24 @@ __global__ void __launch_bounds__(256, 2) input_quant_kernel(const float* __rest
   const bool two = it.ch + 1 < g.C;
   const Strip<VEC2> sp(x, g, it);
   const long long pstride = static_cast<long long>(g.M) * g.C_pad;
-  float2 ta[4], tb[4], tc[4], td[4];
+  float2 ta[4], tb[4], tc[4], td[4], pc[4], pd[4];
   int xx = 2 * it.tj0 - g.pad;
   if (lane_on) {
     sp.column(xx, ta);
     sp.column(xx + 1, tb);
+    sp.load(xx + 2, pc);
+    sp.load(xx + 3, pd);
   }
   int m = (it.img * g.TH + it.ti) * g.TW + it.tj0;
   for (int tj = it.tj0; tj < it.tj1; ++tj, xx += 2, ++m) {
     float2 v[16];
     if (lane_on) {
-      sp.column(xx + 2, tc);
-      sp.column(xx + 3, td);
+      colpass(pc, tc);
+      colpass(pd, td);
+      if (tj + 1 < it.tj1) {  // software prefetch of the next tile's two new columns
+        sp.load(xx + 4, pc);
+        sp.load(xx + 5, pd);
+      }
       row_pass(ta, tb, tc, td, v);
 #pragma unroll
       for (int a = 0; a < 4; ++a) {

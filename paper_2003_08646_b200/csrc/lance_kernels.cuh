@@ -11,7 +11,6 @@ namespace lance_dev {
 
 constexpr int kPositions = 16;  // (m + r - 1)^2 for F(2x2,3x3)
 constexpr int kBM = 128;        // GEMM rows (Winograd tiles) per CTA = UMMA M
-constexpr int kBN = 16;         // filters per CTA: 16 positions x 16 = 256 TMEM columns
 constexpr int kGemmThreads = 192;
 constexpr int kChunk = 64;      // channels per K0/K1 warp item (32 lanes x 2)
 
@@ -52,7 +51,7 @@ struct GemmGeom {
   int K, C;
   int P, TW, OH, OW;
   int num_kchunks;  // C_pad / BK
-  int num_n_tiles;  // K_pad / kBN
+  int num_n_tiles;  // K_pad / bn
 };
 
 struct StaticParams {
@@ -71,9 +70,10 @@ cudaError_t launch_static_params(LanceDevState* st, const StaticParams& prm, int
 cudaError_t launch_filter_prepare(const float* w, float* u_tmp, float* partials, int grid,
                                   uint8_t* codes_w, int32_t* colsum, LanceDevState* st,
                                   const FilterGeom& g, cudaStream_t s);
-cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int bk, int small_acc,
-                        const int32_t* rowsum, const int32_t* colsum, const LanceDevState* st,
-                        float* y, int32_t* acc_dump, const float* bias, int relu,
-                        const GemmGeom& g, cudaStream_t s);
+// bn: filters per GEMM tile, 16 (two TMEM accumulators) or 32 (one).
+cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int bk, int bn,
+                        int small_acc, const int32_t* rowsum, const int32_t* colsum,
+                        const LanceDevState* st, float* y, int32_t* acc_dump, const float* bias,
+                        int relu, const GemmGeom& g, cudaStream_t s);
 
 }  // namespace lance_dev
