@@ -19,9 +19,11 @@
 //   warps 2..9   epilogue: TMEM -> registers -> affine -> A^T m A -> shared
 //                staging -> full-sector stores of y; warp w drains TMEM lane
 //                quadrant w % 4 and filters (BN/2)*((w-2)/4) .. +BN/2
-// Tiles are assigned round-robin with the filter tile fastest, so the filter
-// tiles of one row tile run concurrently on neighbouring SMs and share the A
-// operand through L2.
+// CTAs form clusters of cs (1, 2 or 4) that work on the same row tile and on
+// cs different filter tiles: each CTA loads 128/cs rows of the A box and
+// multicasts them to the whole cluster (TMA .multicast::cluster), so the A
+// operand is read from L2 once per cluster instead of once per filter tile;
+// each CTA's MMA commit releases the stage in every CTA of the cluster.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -86,13 +88,22 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = g.num_n_tiles;
   const int K_pad = nt * BN;
-  const int num_tiles = ((g.M + kBM - 1) / kBM) * nt;
+  const int cs = g.cluster;                       // CTAs per cluster (divides nt)
+  const int rank = cs > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  const int cid = blockIdx.x / cs, ncl = gridDim.x / cs;
+  const int ngrp = nt / cs;                       // filter-tile groups per row tile
+  const int num_groups = ((g.M + kBM - 1) / kBM) * ngrp;
   const int num_iters = g.num_kchunks * 16;
+  const uint16_t cl_mask = static_cast<uint16_t>((1u << cs) - 1u);
+  const int a_rows = kBM / cs;                    // A rows this CTA loads and multicasts
+  // Group index -> (row tile origin, this CTA's filter tile origin).
+  auto tile_m0 = [&](int grp_i) { return (grp_i / ngrp) * kBM; };
+  auto tile_n0 = [&](int grp_i) { return ((grp_i % ngrp) * cs + rank) * BN; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], cs);  // one MMA commit from every CTA of the cluster
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -100,6 +111,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     }
     fence_barrier_init();
   }
+  if (cs > 1) cluster_sync();  // barrier inits visible cluster-wide before any multicast
   if (warp >= 2) {
     // Per-filter third term of affine_term for all filters of the layer.
     for (int i = threadIdx.x - 64; i < 16 * K_pad; i += 32 * kEpiWarps) {
@@ -125,14 +137,18 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       tma_prefetch_desc(&tmB);
       int s = 0;
       uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile / nt) * kBM, n0 = (tile % nt) * BN;
+      for (int grp_i = cid; grp_i < num_groups; grp_i += ncl) {
+        const int m0 = tile_m0(grp_i), n0 = tile_n0(grp_i);
         for (int it = 0; it < num_iters; ++it) {
           const int kc = it >> 4, p = it & 15;
-          mbar_wait(&empty_bar[s], ph ^ 1u);
+          mbar_wait(&empty_bar[s], ph ^ 1u);  // released by all cs consumers
           uint8_t* sa = stage_base + s * Cfg::kStageBytes;
           mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
-          tma_load_3d(sa, &tmA, kc * BK, m0, p, &full_bar[s]);
+          if (cs > 1)
+            tma_load_3d_mc(sa + rank * a_rows * BK, &tmA, kc * BK, m0 + rank * a_rows, p,
+                           &full_bar[s], cl_mask);
+          else
+            tma_load_3d(sa, &tmA, kc * BK, m0, p, &full_bar[s]);
           tma_load_3d(sa + Cfg::kABytes, &tmB, kc * BK, n0, p, &full_bar[s]);
           if (++s == kStages) {
             s = 0;
@@ -154,7 +170,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       uint32_t ph = 0;
       int buf = 0;
       uint32_t acc_ph = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int grp_i = cid; grp_i < num_groups; grp_i += ncl) {
         mbar_wait(&acc_empty[buf], acc_ph ^ 1u);  // epilogue drained this buffer
         tc_fence_after();
         const uint32_t d_base = tmem_base + static_cast<uint32_t>(buf) * Cfg::kAccCols;
@@ -171,7 +187,10 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
             umma_i8(d_base + static_cast<uint32_t>(p * BN), adesc, bdesc, kIdesc,
                     (kc > 0 || kk > 0) ? 1u : 0u);
           }
-          umma_commit(&empty_bar[s]);
+          if (cs > 1)
+            umma_commit_mc(&empty_bar[s], cl_mask);
+          else
+            umma_commit(&empty_bar[s]);
           if (++s == kStages) {
             s = 0;
             ph ^= 1u;
@@ -201,24 +220,25 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     // Row sums of the first tile (later tiles are prefetched one tile ahead).
     int32_t rs_next[16];
     {
-      const int m = (blockIdx.x / nt) * kBM + q * 32 + lane;
+      const int m = tile_m0(cid) + q * 32 + lane;
 #pragma unroll
       for (int p = 0; p < 16; ++p)
-        rs_next[p] = (m < g.M) ? __ldg(rowsum + static_cast<long long>(p) * g.M + m) : 0;
+        rs_next[p] = (cid < num_groups && m < g.M)
+                         ? __ldg(rowsum + static_cast<long long>(p) * g.M + m) : 0;
     }
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int m0 = (tile / nt) * kBM, n0 = (tile % nt) * BN;
+    for (int grp_i = cid; grp_i < num_groups; grp_i += ncl) {
+      const int m0 = tile_m0(grp_i), n0 = tile_n0(grp_i);
       const int m = m0 + q * 32 + lane;
       const bool row_ok = m < g.M;
       float rterm[16];  // k2[p] * float(sum_a): second term of affine_term
 #pragma unroll
       for (int p = 0; p < 16; ++p) rterm[p] = __fmul_rn(s_k2[p], static_cast<float>(rs_next[p]));
       {
-        const int nxt = tile + gridDim.x;
-        const int mn = (nxt / nt) * kBM + q * 32 + lane;
+        const int nxt = grp_i + ncl;
+        const int mn = tile_m0(nxt) + q * 32 + lane;
 #pragma unroll
         for (int p = 0; p < 16; ++p)
-          rs_next[p] = (nxt < num_tiles && mn < g.M)
+          rs_next[p] = (nxt < num_groups && mn < g.M)
                            ? __ldg(rowsum + static_cast<long long>(p) * g.M + mn) : 0;
       }
       // Output pixels of this lane's tile (2ti + a, 2tj + b) and their
@@ -351,6 +371,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     tc_fence_after();
     tmem_dealloc(*tmem_holder, 512);
   }
+  if (cs > 1) cluster_sync();  // no CTA leaves while cluster peers may still signal it
 }
 
 template <int BK, int BN, bool SMALL, bool EPI>
@@ -378,11 +399,24 @@ static cudaError_t launch_gemm_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
     }
   }
   const int sms = (dev >= 0 && dev < 64) ? sm_count[dev] : 148;
-  const long long tiles = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * g.num_n_tiles;
-  const int grid = static_cast<int>(tiles < sms ? tiles : sms);
-  gemm_epilogue_kernel<BK, BN, SMALL, EPI><<<grid, kGemmThreadsP, smem, s>>>(
-      *tmA, *tmB, rowsum, colsum, st, y, acc_dump, bias, relu, g);
-  return cudaGetLastError();
+  const int cs = g.cluster;
+  const long long groups =
+      ((static_cast<long long>(g.M) + kBM - 1) / kBM) * (g.num_n_tiles / cs);
+  const long long clusters = groups < sms / cs ? groups : sms / cs;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(clusters * cs));
+  cfg.blockDim = dim3(kGemmThreadsP);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_epilogue_kernel<BK, BN, SMALL, EPI>, *tmA, *tmB, rowsum,
+                            colsum, st, y, acc_dump, bias, relu, g);
 }
 
 template <int BK, int BN>
