@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 
 namespace lance_dev {
@@ -46,8 +47,19 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
+#ifdef LANCE_DEBUG_HANG
+  long long spins = 0;
+  while (!mbar_try_wait(addr, parity)) {
+    if (++spins == (1ll << 26)) {
+      printf("LANCE hang: block %d thread %d waits on smem barrier 0x%x parity %u\n", blockIdx.x,
+             threadIdx.x, addr, parity);
+      __trap();
+    }
+  }
+#else
   while (!mbar_try_wait(addr, parity)) {
   }
+#endif
 }
 
 // ---------------------------------------------------------------- TMA
