@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         const int m0 = tile_m0(grp_i), n0 = tile_n0(grp_i);
         for (int it = 0; it < num_iters; ++it) {
           const int kc = it >> 4, p = it & 15;
-          mbar_wait(&empty_bar[s], ph ^ 1u);  // released by all cs consumers
+          mbar_wait(&empty_bar[s], ph ^ 1u, 1, grp_i, it);  // released by all cs consumers
           uint8_t* sa = stage_base + s * Cfg::kStageBytes;
           mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
           if (cs > 1)
@@ -171,12 +171,12 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       int buf = 0;
       uint32_t acc_ph = 0;
       for (int grp_i = cid; grp_i < num_groups; grp_i += ncl) {
-        mbar_wait(&acc_empty[buf], acc_ph ^ 1u);  // epilogue drained this buffer
+        mbar_wait(&acc_empty[buf], acc_ph ^ 1u, 2, grp_i, buf);  // epilogue drained this buffer
         tc_fence_after();
         const uint32_t d_base = tmem_base + static_cast<uint32_t>(buf) * Cfg::kAccCols;
         for (int it = 0; it < num_iters; ++it) {
           const int kc = it >> 4, p = it & 15;
-          mbar_wait(&full_bar[s], ph);
+          mbar_wait(&full_bar[s], ph, 3, grp_i, it);
           tc_fence_after();
           const uint32_t sa = smem_u32(stage_base + s * Cfg::kStageBytes);
           const uint32_t sb = sa + Cfg::kABytes;
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         const int pmask = row_ok ? (1 | (c1 ? 2 : 0) | (r1 ? 4 : 0) | (r1 && c1 ? 8 : 0)) : 0;
         pixm = (pix0 << 4) | pmask;
       }
-      mbar_wait(&acc_full[buf], acc_ph);
+      mbar_wait(&acc_full[buf], acc_ph, 4, grp_i, warp);
       tc_fence_after();
       const uint32_t acc_addr = lane_base + static_cast<uint32_t>(buf) * Cfg::kAccCols + f0;
 #pragma unroll 1

@@ -45,18 +45,21 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   return ok != 0;
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int tag = 0, int i0 = 0,
+                                          int i1 = 0) {
   const uint32_t addr = smem_u32(bar);
 #ifdef LANCE_DEBUG_HANG
   long long spins = 0;
   while (!mbar_try_wait(addr, parity)) {
-    if (++spins == (1ll << 26)) {
-      printf("LANCE hang: block %d thread %d waits on smem barrier 0x%x parity %u\n", blockIdx.x,
-             threadIdx.x, addr, parity);
-      __trap();
-    }
+    if (++spins == (1ll << 24))
+      printf("LANCE wait: block %d thread %d tag %d (%d,%d) barrier 0x%x parity %u\n", blockIdx.x,
+             threadIdx.x, tag, i0, i1, addr, parity);
+    if (spins == (1ll << 27)) __trap();
   }
 #else
+  (void)tag;
+  (void)i0;
+  (void)i1;
   while (!mbar_try_wait(addr, parity)) {
   }
 #endif
