@@ -15,6 +15,7 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
 // mode 2: like 0 but expect_tx issued before a cluster barrier, then loads.
 __global__ void mc_kernel(const __grid_constant__ CUtensorMap tm, int cs, int mode, int* out) {
   __shared__ __align__(1024) uint8_t buf[128 * 64];
+  __shared__ __align__(1024) uint8_t buf2[128 * 64];
   __shared__ uint64_t bar;
   const uint32_t rank = cluster_ctarank();
   if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
@@ -22,8 +23,9 @@ __global__ void mc_kernel(const __grid_constant__ CUtensorMap tm, int cs, int mo
   const uint16_t mask = (1u << cs) - 1;
   const int rows = 128 / cs;
   if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(&bar, 128 * 64);
-    if (mode == 2) {}
+    if (mode == 2 && rank == 0) { long long t0 = clock64(); while (clock64() - t0 < 2000000) {} }
+    mbar_arrive_expect_tx(&bar, 128 * 64 + (mode == 3 ? 64 * rows : 0));
+    if (mode == 3) tma_load_3d(buf2, &tm, 0, 0, 0, &bar);
     if (mode == 1) {
       if (rank == 0) tma_load_3d_mc(buf, &tm, 0, 0, 0, &bar, mask);
     } else {
@@ -49,7 +51,7 @@ int main() {
   for (int i = 0; i < 128 * 64; ++i) { h[i] = uint8_t(i * 7 + 3); expect += h[i]; }
   uint8_t* d; cudaMalloc(&d, h.size()); cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice);
   int* out; cudaMalloc(&out, 64 * sizeof(int));
-  for (int cs : {2, 4}) for (int mode : {0, 1}) {
+  for (int cs : {2, 4}) for (int mode : {0, 1, 2, 3}) {
     CUtensorMap tm;
     const cuuint64_t dims[3] = {64, 128, 1};
     const cuuint64_t str[2] = {64, 128 * 64};
