@@ -16,9 +16,9 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
 __global__ void mc_kernel(const __grid_constant__ CUtensorMap tm, int cs, int mode, int* out) {
   __shared__ __align__(1024) uint8_t buf[128 * 64];
   __shared__ __align__(1024) uint8_t buf2[128 * 64];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2, bar3;
   const uint32_t rank = cluster_ctarank();
-  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&bar2, cs); mbar_init(&bar3, 1); fence_barrier_init(); }
   cluster_sync();
   const uint16_t mask = (1u << cs) - 1;
   const int rows = 128 / cs;
@@ -38,6 +38,12 @@ __global__ void mc_kernel(const __grid_constant__ CUtensorMap tm, int cs, int mo
     int sum = 0;
     for (int i = 0; i < 128 * 64; ++i) sum += buf[i];
     out[blockIdx.x] = sum;
+    if (mode == 3) {
+      umma_commit_mc(&bar2, mask);
+      spins = 0;
+      while (!mbar_try_wait(smem_u32(&bar2), 0)) if (++spins > (1ll << 24)) { printf("block %d rank %u commit-mc timeout bar2=0x%x bar3 state\n", blockIdx.x, rank, smem_u32(&bar2)); out[blockIdx.x] = -1; break; }
+      if (mbar_try_wait(smem_u32(&bar3), 0)) printf("block %d rank %u: bar3 unexpectedly completed\n", blockIdx.x, rank);
+    }
   }
   cluster_sync();
 }
