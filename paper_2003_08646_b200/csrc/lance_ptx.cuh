@@ -52,8 +52,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int ta
   long long spins = 0;
   while (!mbar_try_wait(addr, parity)) {
     if (++spins == (1ll << 24))
-      printf("LANCE wait: block %d thread %d tag %d (%d,%d) barrier 0x%x parity %u\n", blockIdx.x,
-             threadIdx.x, tag, i0, i1, addr, parity);
+      printf("LANCE wait: block %d thread %d tag %d (%d,%d) barrier 0x%x parity %u raw 0x%016llx\n",
+             blockIdx.x, threadIdx.x, tag, i0, i1, addr, parity,
+             static_cast<unsigned long long>(*reinterpret_cast<volatile uint64_t*>(bar)));
     if (spins == (1ll << 27)) __trap();
   }
 #else
