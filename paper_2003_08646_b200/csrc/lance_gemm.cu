@@ -112,6 +112,13 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     fence_barrier_init();
   }
   if (cs > 1) cluster_sync();  // barrier inits visible cluster-wide before any multicast
+#ifdef LANCE_DEBUG_HANG
+  if (threadIdx.x == 0 && blockIdx.x < 2)
+    printf("DBG block %d after cluster_sync: full0 0x%016llx empty0 0x%016llx stage_base 0x%x full_bar 0x%x holder 0x%x cterm 0x%x\n",
+           blockIdx.x, (unsigned long long)*reinterpret_cast<volatile uint64_t*>(&full_bar[0]),
+           (unsigned long long)*reinterpret_cast<volatile uint64_t*>(&empty_bar[0]), smem_u32(stage_base),
+           smem_u32(full_bar), smem_u32(tmem_holder), smem_u32(s_cterm));
+#endif
   if (warp >= 2) {
     // Per-filter third term of affine_term for all filters of the layer.
     for (int i = threadIdx.x - 64; i < 16 * K_pad; i += 32 * kEpiWarps) {
@@ -129,6 +136,12 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     }
   }
   __syncthreads();
+#ifdef LANCE_DEBUG_HANG
+  if (threadIdx.x == 0 && blockIdx.x < 2)
+    printf("DBG block %d after syncthreads: full0 0x%016llx empty0 0x%016llx\n", blockIdx.x,
+           (unsigned long long)*reinterpret_cast<volatile uint64_t*>(&full_bar[0]),
+           (unsigned long long)*reinterpret_cast<volatile uint64_t*>(&empty_bar[0]));
+#endif
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
