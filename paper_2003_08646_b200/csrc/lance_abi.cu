@@ -323,6 +323,8 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   gg.num_kchunks = p->C_pad / p->BK;
   gg.num_n_tiles = p->K_pad / p->BN;
   gg.cluster = (gg.num_n_tiles % 4 == 0) ? 4 : (gg.num_n_tiles % 2 == 0 ? 2 : 1);
+  gg.dbg_mode = 0;
+  if (const char* e = std::getenv("LANCE_GEMM_DBG")) gg.dbg_mode = std::atoi(e);
   if (const char* e = std::getenv("LANCE_GEMM_CLUSTER")) {
     const int v = std::atoi(e);
     if ((v == 1 || v == 2 || v == 4) && gg.num_n_tiles % v == 0) gg.cluster = v;

@@ -157,6 +157,12 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
           mbar_wait(&empty_bar[s], ph ^ 1u, 1, grp_i, it);  // released by all cs consumers
           uint8_t* sa = stage_base + s * Cfg::kStageBytes;
           mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
+#ifdef LANCE_DEBUG_HANG
+          if (g.dbg_mode == 1) {  // no multicast: every CTA loads the whole A box in slices
+            for (int rr = 0; rr < cs; ++rr)
+              tma_load_3d(sa + rr * a_rows * BK, &tmA, kc * BK, m0 + rr * a_rows, p, &full_bar[s]);
+          } else
+#endif
           if (cs > 1)
             tma_load_3d_mc(sa + rank * a_rows * BK, &tmA, kc * BK, m0 + rank * a_rows, p,
                            &full_bar[s], cl_mask);
@@ -200,6 +206,11 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
             umma_i8(d_base + static_cast<uint32_t>(p * BN), adesc, bdesc, kIdesc,
                     (kc > 0 || kk > 0) ? 1u : 0u);
           }
+#ifdef LANCE_DEBUG_HANG
+          if (g.dbg_mode == 2) {  // per-CTA release only (empty count stays cs: will hang by design)
+            umma_commit(&empty_bar[s]);
+          } else
+#endif
           if (cs > 1)
             umma_commit_mc(&empty_bar[s], cl_mask);
           else

@@ -52,6 +52,7 @@ struct GemmGeom {
   int P, TW, OH, OW;
   int num_kchunks;  // C_pad / BK
   int num_n_tiles;  // K_pad / bn
+  int dbg_mode;     // debug builds only
   int cluster;      // CTAs per cluster sharing the A operand by multicast (divides num_n_tiles)
 };
 
