@@ -103,7 +103,11 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
+#ifdef LANCE_DEBUG_HANG
+      mbar_init(&empty_bar[s], g.dbg_mode >= 2 ? 1 : cs);
+#else
       mbar_init(&empty_bar[s], cs);  // one MMA commit from every CTA of the cluster
+#endif
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -158,7 +162,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
           uint8_t* sa = stage_base + s * Cfg::kStageBytes;
           mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
 #ifdef LANCE_DEBUG_HANG
-          if (g.dbg_mode == 1) {  // no multicast: every CTA loads the whole A box in slices
+          if (g.dbg_mode == 1 || g.dbg_mode == 3) {  // no multicast: local slices
             for (int rr = 0; rr < cs; ++rr)
               tma_load_3d(sa + rr * a_rows * BK, &tmA, kc * BK, m0 + rr * a_rows, p, &full_bar[s]);
           } else
@@ -207,7 +211,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
                     (kc > 0 || kk > 0) ? 1u : 0u);
           }
 #ifdef LANCE_DEBUG_HANG
-          if (g.dbg_mode == 2) {  // per-CTA release only (empty count stays cs: will hang by design)
+          if (g.dbg_mode >= 2) {  // per-CTA release only
             umma_commit(&empty_bar[s]);
           } else
 #endif
