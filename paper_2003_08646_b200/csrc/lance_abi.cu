@@ -322,7 +322,7 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   gg.OW = p->OW;
   gg.num_kchunks = p->C_pad / p->BK;
   gg.num_n_tiles = p->K_pad / p->BN;
-  gg.cluster = (gg.num_n_tiles % 4 == 0) ? 4 : (gg.num_n_tiles % 2 == 0 ? 2 : 1);
+  gg.cluster = 1;  // multicast clusters are opt-in (LANCE_GEMM_CLUSTER) until validated on the GPU
   gg.dbg_mode = 0;
   if (const char* e = std::getenv("LANCE_GEMM_DBG")) gg.dbg_mode = std::atoi(e);
   if (const char* e = std::getenv("LANCE_GEMM_CLUSTER")) {
