@@ -258,13 +258,12 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   p->P = p->TH * p->TW;
   p->M = static_cast<long long>(spec->n) * p->P;
   p->C_pad = round_up(spec->c, 32);
-  // GEMM tile width: 32 filters (one TMEM accumulator, half the A re-reads
-  // and twice the work per ~44-cycle MMA) for deep layers, 16 (double
-  // buffered accumulators) otherwise.  LANCE_GEMM_BN overrides.
-  p->BN = (round_up(spec->c, 32) >= 256) ? 32 : 16;
+  // GEMM tile width: 64 filters (two j-group accumulators of 4 x 64 TMEM
+  // columns) unless the layer has fewer.  LANCE_GEMM_BN overrides.
+  p->BN = spec->k > 32 ? 64 : (spec->k > 16 ? 32 : 16);
   if (const char* e = std::getenv("LANCE_GEMM_BN")) {
     const int v = std::atoi(e);
-    if (v == 16 || v == 32) p->BN = v;
+    if (v == 16 || v == 32 || v == 64) p->BN = v;
   }
   p->K_pad = round_up(spec->k, p->BN);
   p->BK = (p->C_pad % 128 == 0) ? 128 : (p->C_pad % 64 == 0 ? 64 : 32);
@@ -322,13 +321,7 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   gg.OW = p->OW;
   gg.num_kchunks = p->C_pad / p->BK;
   gg.num_n_tiles = p->K_pad / p->BN;
-  gg.cluster = 1;  // multicast clusters are opt-in (LANCE_GEMM_CLUSTER) until validated on the GPU
-  gg.dbg_mode = 0;
-  if (const char* e = std::getenv("LANCE_GEMM_DBG")) gg.dbg_mode = std::atoi(e);
-  if (const char* e = std::getenv("LANCE_GEMM_CLUSTER")) {
-    const int v = std::atoi(e);
-    if ((v == 1 || v == 2 || v == 4) && gg.num_n_tiles % v == 0) gg.cluster = v;
-  }
+  gg.stages = 0;  // chosen by the launcher
 
   const size_t codes_a_bytes = static_cast<size_t>(16) * p->M * p->C_pad;
   const size_t codes_w_bytes = static_cast<size_t>(16) * p->K_pad * p->C_pad;

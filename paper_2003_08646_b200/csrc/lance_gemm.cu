@@ -5,25 +5,31 @@
 // transform A^T m A (winograd.hpp:80-84) and the merge with ragged-edge
 // discard (tensor.hpp:157-182).
 //
-// Persistent kernel, one CTA per SM.  A tile = 128 Winograd tiles (UMMA M)
-// x BN filters (UMMA N) x all 16 positions = 16*BN s32 TMEM columns; with
-// BN = 16 TMEM holds two accumulators (the MMA of tile i+1 overlaps the
-// epilogue of tile i), with BN = 32 one (twice the MMA work per A byte: a
-// K=32 kind::i8 MMA with M=128 costs ~44 cycles for any N <= 32 because the
-// 4 KB A operand is read from shared memory each time).  The TMA producer runs
-// ahead of the MMA through a shared-memory ring.
+// Position order.  S = (A^T m) A is evaluated as in matrix.hpp:75-84:
+//   T0j = (m_j + m_{4+j}) + m_{8+j},  T1j = (m_{4+j} - m_{8+j}) - m_{12+j}
+//   S00 = (T00 + T01) + T02, S01 = (T01 - T02) - T03   (S1b likewise from T1j)
+// Both folds are left folds, so the positions can be consumed in j-groups
+// {j, 4+j, 8+j, 12+j}, j = 0..3, with four running partials S_ab per
+// (tile, filter): bit-identical to the all-16-resident form.  A j-group
+// needs 4 x BN TMEM columns, so TMEM (512 columns) double-buffers j-groups
+// at BN = 64 filters per tile: a 128 x 64 x 32 kind::i8 UMMA runs at ~2/3 of
+// the tensor peak where the 128 x 32 one needed for all-16-resident tiles
+// runs at ~1/3 (A is re-read from shared memory by every MMA).
+//
+// Persistent kernel, one CTA per SM, tiles = 128 Winograd tiles (UMMA M) x
+// BN filters, n-tile fastest so concurrent CTAs share the A rows in L2.
 //   warp 0       TMA producer (one lane): per stage the A box
 //                [128 rows x BK ch] and the B box [BN filters x BK ch] of one
-//                position
+//                (position, channel chunk)
 //   warp 1       TMEM allocator + UMMA issuer (one lane)
-//   warps 2..9   epilogue: TMEM -> registers -> affine -> A^T m A -> shared
-//                staging -> full-sector stores of y; warp w drains TMEM lane
-//                quadrant w % 4 and filters (BN/2)*((w-2)/4) .. +BN/2
-// CTAs form clusters of cs (1, 2 or 4) that work on the same row tile and on
-// cs different filter tiles: each CTA loads 128/cs rows of the A box and
-// multicasts them to the whole cluster (TMA .multicast::cluster), so the A
-// operand is read from L2 once per cluster instead of once per filter tile;
-// each CTA's MMA commit releases the stage in every CTA of the cluster.
+//   warps 2..17  epilogue: warp w drains TMEM lane quadrant w % 4 and
+//                filters BN/4 * ((w-2)/4) .. +BN/4 of the tile; each thread
+//                owns one Winograd tile (row) and keeps the S partials of its
+//                filters in registers; y is written with 16-byte stores.
+// SMALL (C * top_a * top_b < 2^23): every accumulator is < 2^23, so TMEM is
+// pre-set to the bit pattern of 2^23 (0x4B000000) and the MMAs accumulate on
+// top of it: the result read back is the float 2^23 + dot, and
+// fma(k1, 2^23 + dot, -k1 * 2^23) = RN(k1 * dot) = k1 * float(dot) bitwise.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -33,29 +39,65 @@
 
 namespace lance_dev {
 
-constexpr int kEpiWarps = 8;
-constexpr int kGemmThreadsP = 64 + 32 * kEpiWarps;  // 320
-constexpr size_t kSmemLimit = 226 * 1024;           // dynamic part, leaves room for static smem
+constexpr int kEpiWarps = 16;
+constexpr int kGemmThreadsP = 64 + 32 * kEpiWarps;  // 576
+constexpr size_t kSmemLimit = 225 * 1024;           // dynamic part, leaves room for static smem
+constexpr uint32_t kTwo23Bits = 0x4B000000u;        // float 2^23
 
 template <int BK, int BN>
 struct GemmCfg {
-  static constexpr int kBufs = (BN == 16) ? 2 : 1;
   static constexpr uint32_t kABytes = kBM * BK;
   static constexpr uint32_t kBBytes = BN * BK;
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  static constexpr int kStagesRaw = (128 * 1024) / kStageBytes;
-  static constexpr int kStages = kStagesRaw > 16 ? 16 : kStagesRaw;
   static constexpr uint32_t kLayout = (BK == 128) ? 2u : (BK == 64 ? 4u : 6u);  // SW128/64/32
-  static constexpr uint32_t kAccCols = 16 * BN;
-  static constexpr uint32_t kStagingBytes = kEpiWarps * 32 * 4 * 8 * 4;  // 8 filters x 4 px x 32 rows
-  // + 16 * K_pad floats of per-filter constants, added at launch.
-  static constexpr size_t kSmemBase = 1024 + static_cast<size_t>(kStages) * kStageBytes +
-                                      kStagingBytes + (2 * kStages + 4) * 8 + 16;
+  static constexpr uint32_t kGroupCols = 4 * BN;  // one j-group: 4 positions x BN filters
+  static constexpr int kFPT = BN / 4;             // filters per epilogue thread
+  static constexpr size_t kFixed = 1024 /*align*/ + 16 * 8 /*acc barriers, holder*/;
 };
 
-// SMALL: C * top_a * top_b < 2^23, so every accumulator is below 2^23 and
-// k1 * float(dot) is formed exactly by one FFMA (see below).
-// EPI: fused bias + ReLU (north-star extension).
+template <int BK, int BN>
+__host__ __device__ constexpr size_t gemm_smem_bytes(int stages, int k_pad) {
+  return GemmCfg<BK, BN>::kFixed + static_cast<size_t>(stages) * GemmCfg<BK, BN>::kStageBytes +
+         static_cast<size_t>(stages) * 16 + static_cast<size_t>(16) * k_pad * 4;
+}
+
+// Epilogue of one j-group for 4 filters (one TMEM x4 load per position).
+// acc[a][i]: accumulator of position p = 4a + j, filter f0 + 4c + i.
+template <bool SMALL>
+__device__ __forceinline__ void affine_group4(const uint32_t (&acc)[4][4], const float* s_k1,
+                                              const float* s_nk1m, const float* s_k4,
+                                              const float (&rterm)[4], const float* cterm_j,
+                                              int K_pad, int j, float2 (&T0)[2],
+                                              float2 (&T1)[2]) {
+  float2 m[4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int p = 4 * a + j;
+    const float k1 = s_k1[p];
+    const float4 ct = *reinterpret_cast<const float4*>(cterm_j + a * 4 * K_pad);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float2 t1;
+      if (SMALL) {
+        t1 = fma2(bcast2(k1), make_float2(__uint_as_float(acc[a][2 * h]), __uint_as_float(acc[a][2 * h + 1])),
+                  bcast2(s_nk1m[p]));
+      } else {
+        t1 = make_float2(__fmul_rn(k1, __int2float_rn(static_cast<int>(acc[a][2 * h]))),
+                         __fmul_rn(k1, __int2float_rn(static_cast<int>(acc[a][2 * h + 1]))));
+      }
+      const float2 c2 = h ? make_float2(ct.z, ct.w) : make_float2(ct.x, ct.y);
+      // ((k1*dot + k2*sum_a) + k3*sum_b) + k4, left to right (lowpgemm.hpp:110-114).
+      m[a][h] = add2(add2(add2(t1, bcast2(rterm[a])), c2), bcast2(s_k4[p]));
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    T0[h] = add2(add2(m[0][h], m[1][h]), m[2][h]);
+    T1[h] = sub2(sub2(m[1][h], m[2][h]), m[3][h]);
+  }
+}
+
+// SMALL / EPI: see the file comment; EPI = fused bias + ReLU (north-star extension).
 template <int BK, int BN, bool SMALL, bool EPI>
 __global__ void __launch_bounds__(kGemmThreadsP, 1)
     gemm_epilogue_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -65,49 +107,34 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
                          int32_t* __restrict__ acc_dump, const float* __restrict__ bias,
                          int relu, GemmGeom g) {
   using Cfg = GemmCfg<BK, BN>;
-  constexpr int kStages = Cfg::kStages;
-  constexpr int kBufs = Cfg::kBufs;
+  constexpr int FPT = Cfg::kFPT;
+  constexpr int NCH = FPT / 4;  // 4-filter chunks per thread
   constexpr uint32_t kIdesc = umma_idesc_u8(kBM, BN);
-  constexpr int kWarpFilters = BN / 2;  // filters per epilogue warp
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ float s_k1[16], s_nk1m[16], s_k2[16], s_k4[16];
 
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int stages = g.stages;
   uint8_t* stage_base = smem;
-  float* staging = reinterpret_cast<float*>(smem + kStages * Cfg::kStageBytes);  // [8 warps][1024]
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes +
-                                                   Cfg::kStagingBytes);
-  uint64_t* empty_bar = full_bar + kStages;
-  uint64_t* acc_full = empty_bar + kStages;  // [2]
-  uint64_t* acc_empty = acc_full + 2;        // [2]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(stages) * Cfg::kStageBytes);
+  uint64_t* empty_bar = full_bar + stages;
+  uint64_t* acc_full = empty_bar + stages;  // [2]
+  uint64_t* acc_empty = acc_full + 2;       // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
   float* s_cterm = reinterpret_cast<float*>(tmem_holder + 4);  // [16][K_pad]: k3[p]*colsum[p][k]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = g.num_n_tiles;
   const int K_pad = nt * BN;
-  const int cs = g.cluster;                       // CTAs per cluster (divides nt)
-  const int rank = cs > 1 ? static_cast<int>(cluster_ctarank()) : 0;
-  const int cid = blockIdx.x / cs, ncl = gridDim.x / cs;
-  const int ngrp = nt / cs;                       // filter-tile groups per row tile
-  const int num_groups = ((g.M + kBM - 1) / kBM) * ngrp;
-  const int num_iters = g.num_kchunks * 16;
-  const uint16_t cl_mask = static_cast<uint16_t>((1u << cs) - 1u);
-  const int a_rows = kBM / cs;                    // A rows this CTA loads and multicasts
-  // Group index -> (row tile origin, this CTA's filter tile origin).
-  auto tile_m0 = [&](int grp_i) { return (grp_i / ngrp) * kBM; };
-  auto tile_n0 = [&](int grp_i) { return ((grp_i % ngrp) * cs + rank) * BN; };
+  const int num_tiles = ((g.M + kBM - 1) / kBM) * nt;
+  const int nk = g.num_kchunks;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < stages; ++s) {
       mbar_init(&full_bar[s], 1);
-#ifdef LANCE_DEBUG_HANG
-      mbar_init(&empty_bar[s], g.dbg_mode >= 2 ? 1 : cs);
-#else
-      mbar_init(&empty_bar[s], cs);  // one MMA commit from every CTA of the cluster
-#endif
+      mbar_init(&empty_bar[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -115,20 +142,12 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     }
     fence_barrier_init();
   }
-  if (cs > 1) cluster_sync();  // barrier inits visible cluster-wide before any multicast
-#ifdef LANCE_DEBUG_HANG
-  if (threadIdx.x == 0 && blockIdx.x < 2)
-    printf("DBG block %d after cluster_sync: full0 0x%016llx empty0 0x%016llx stage_base 0x%x full_bar 0x%x holder 0x%x cterm 0x%x\n",
-           blockIdx.x, (unsigned long long)*reinterpret_cast<volatile uint64_t*>(&full_bar[0]),
-           (unsigned long long)*reinterpret_cast<volatile uint64_t*>(&empty_bar[0]), smem_u32(stage_base),
-           smem_u32(full_bar), smem_u32(tmem_holder), smem_u32(s_cterm));
-#endif
   if (warp >= 2) {
-    // Per-filter third term of affine_term for all filters of the layer.
+    // Third term of affine_term for every filter of the layer.
     for (int i = threadIdx.x - 64; i < 16 * K_pad; i += 32 * kEpiWarps) {
       const int p = i / K_pad, kf = i - p * K_pad;
-      const float cs = (kf < g.K) ? static_cast<float>(colsum[i]) : 0.0f;
-      s_cterm[i] = __fmul_rn(st->k3[p], cs);
+      const float csum = (kf < g.K) ? static_cast<float>(colsum[i]) : 0.0f;
+      s_cterm[i] = __fmul_rn(st->k3[p], csum);
     }
     const int e = threadIdx.x - 64;
     if (e < 16) {
@@ -140,12 +159,6 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     }
   }
   __syncthreads();
-#ifdef LANCE_DEBUG_HANG
-  if (threadIdx.x == 0 && blockIdx.x < 2)
-    printf("DBG block %d after syncthreads: full0 0x%016llx empty0 0x%016llx\n", blockIdx.x,
-           (unsigned long long)*reinterpret_cast<volatile uint64_t*>(&full_bar[0]),
-           (unsigned long long)*reinterpret_cast<volatile uint64_t*>(&empty_bar[0]));
-#endif
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -154,30 +167,23 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       tma_prefetch_desc(&tmB);
       int s = 0;
       uint32_t ph = 0;
-      for (int grp_i = cid; grp_i < num_groups; grp_i += ncl) {
-        const int m0 = tile_m0(grp_i), n0 = tile_n0(grp_i);
-        for (int it = 0; it < num_iters; ++it) {
-          const int kc = it >> 4, p = it & 15;
-          mbar_wait(&empty_bar[s], ph ^ 1u, 1, grp_i, it);  // released by all cs consumers
-          uint8_t* sa = stage_base + s * Cfg::kStageBytes;
-          mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
-#ifdef LANCE_DEBUG_HANG
-          if (g.dbg_mode == 1 || g.dbg_mode == 3) {  // no multicast: local slices
-            for (int rr = 0; rr < cs; ++rr)
-              tma_load_3d(sa + rr * a_rows * BK, &tmA, kc * BK, m0 + rr * a_rows, p, &full_bar[s]);
-          } else
-#endif
-          if (cs > 1)
-            tma_load_3d_mc(sa + rank * a_rows * BK, &tmA, kc * BK, m0 + rank * a_rows, p,
-                           &full_bar[s], cl_mask);
-          else
-            tma_load_3d(sa, &tmA, kc * BK, m0, p, &full_bar[s]);
-          tma_load_3d(sa + Cfg::kABytes, &tmB, kc * BK, n0, p, &full_bar[s]);
-          if (++s == kStages) {
-            s = 0;
-            ph ^= 1u;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int m0 = (t / nt) * kBM, n0 = (t % nt) * BN;
+        for (int j = 0; j < 4; ++j)
+          for (int a = 0; a < 4; ++a) {
+            const int p = 4 * a + j;
+            for (int kc = 0; kc < nk; ++kc) {
+              mbar_wait(&empty_bar[s], ph ^ 1u);
+              uint8_t* sa = stage_base + static_cast<size_t>(s) * Cfg::kStageBytes;
+              mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
+              tma_load_3d(sa, &tmA, kc * BK, m0, p, &full_bar[s]);
+              tma_load_3d(sa + Cfg::kABytes, &tmB, kc * BK, n0, p, &full_bar[s]);
+              if (++s == stages) {
+                s = 0;
+                ph ^= 1u;
+              }
+            }
           }
-        }
       }
     }
   } else if (warp == 1) {
@@ -191,43 +197,34 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      int buf = 0;
-      uint32_t acc_ph = 0;
-      for (int grp_i = cid; grp_i < num_groups; grp_i += ncl) {
-        mbar_wait(&acc_empty[buf], acc_ph ^ 1u, 2, grp_i, buf);  // epilogue drained this buffer
-        tc_fence_after();
-        const uint32_t d_base = tmem_base + static_cast<uint32_t>(buf) * Cfg::kAccCols;
-        for (int it = 0; it < num_iters; ++it) {
-          const int kc = it >> 4, p = it & 15;
-          mbar_wait(&full_bar[s], ph, 3, grp_i, it);
+      uint32_t grp = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        for (int j = 0; j < 4; ++j, ++grp) {
+          const uint32_t buf = grp & 1u;
+          mbar_wait(&acc_empty[buf], (grp >> 1) & 1u);  // epilogue drained (and re-armed) it
           tc_fence_after();
-          const uint32_t sa = smem_u32(stage_base + s * Cfg::kStageBytes);
-          const uint32_t sb = sa + Cfg::kABytes;
+          const uint32_t d_base = tmem_base + buf * Cfg::kGroupCols;
+          for (int a = 0; a < 4; ++a) {
+            for (int kc = 0; kc < nk; ++kc) {
+              mbar_wait(&full_bar[s], ph);
+              tc_fence_after();
+              const uint32_t sa = smem_u32(stage_base + static_cast<size_t>(s) * Cfg::kStageBytes);
+              const uint32_t sb = sa + Cfg::kABytes;
 #pragma unroll
-          for (int kk = 0; kk < BK / 32; ++kk) {
-            const uint64_t adesc = umma_smem_desc(sa + kk * 32, 8 * BK, Cfg::kLayout);
-            const uint64_t bdesc = umma_smem_desc(sb + kk * 32, 8 * BK, Cfg::kLayout);
-            umma_i8(d_base + static_cast<uint32_t>(p * BN), adesc, bdesc, kIdesc,
-                    (kc > 0 || kk > 0) ? 1u : 0u);
+              for (int kk = 0; kk < BK / 32; ++kk) {
+                const uint64_t adesc = umma_smem_desc(sa + kk * 32, 8 * BK, Cfg::kLayout);
+                const uint64_t bdesc = umma_smem_desc(sb + kk * 32, 8 * BK, Cfg::kLayout);
+                umma_i8(d_base + static_cast<uint32_t>(a * BN), adesc, bdesc, kIdesc,
+                        (SMALL || kc > 0 || kk > 0) ? 1u : 0u);
+              }
+              umma_commit(&empty_bar[s]);
+              if (++s == stages) {
+                s = 0;
+                ph ^= 1u;
+              }
+            }
           }
-#ifdef LANCE_DEBUG_HANG
-          if (g.dbg_mode >= 2) {  // per-CTA release only
-            umma_commit(&empty_bar[s]);
-          } else
-#endif
-          if (cs > 1)
-            umma_commit_mc(&empty_bar[s], cl_mask);
-          else
-            umma_commit(&empty_bar[s]);
-          if (++s == kStages) {
-            s = 0;
-            ph ^= 1u;
-          }
-        }
-        umma_commit(&acc_full[buf]);
-        if (++buf == kBufs) {
-          buf = 0;
-          acc_ph ^= 1u;
+          umma_commit(&acc_full[buf]);
         }
       }
     }
@@ -235,162 +232,157 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   } else {
     // ---------------- epilogue ----------------
     const int ew = warp - 2;
-    const int q = warp & 3;                   // TMEM lane quadrant this warp may access
-    const int f0 = (ew >> 2) * kWarpFilters;  // this warp's filters within the tile
-    float* stg = staging + ew * 1024;         // [32 rows][4 px][8 filters], 16-B chunks swizzled
+    const int q = warp & 3;          // TMEM lane quadrant this warp may access
+    const int f0 = (ew >> 2) * FPT;  // this thread's filters within the tile
     named_bar_sync(1, 32 + 32 * kEpiWarps);
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
     const bool k4ok = (g.K & 3) == 0;
-    int buf = 0;
-    uint32_t acc_ph = 0;
-    // Row sums of the first tile (later tiles are prefetched one tile ahead).
-    int32_t rs_next[16];
-    {
-      const int m = tile_m0(cid) + q * 32 + lane;
+    // Arm both j-group buffers (SMALL: preset to 2^23; see the file comment).
 #pragma unroll
-      for (int p = 0; p < 16; ++p)
-        rs_next[p] = (cid < num_groups && m < g.M)
-                         ? __ldg(rowsum + static_cast<long long>(p) * g.M + m) : 0;
+    for (int b = 0; b < 2; ++b) {
+      if (SMALL) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+            tmem_st_x4_const(lane_base + b * Cfg::kGroupCols + a * BN + f0 + 4 * c, kTwo23Bits);
+        tmem_st_wait();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[b]);
     }
-    for (int grp_i = cid; grp_i < num_groups; grp_i += ncl) {
-      const int m0 = tile_m0(grp_i), n0 = tile_n0(grp_i);
+    uint32_t grp = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int m0 = (t / nt) * kBM, n0 = (t % nt) * BN;
       const int m = m0 + q * 32 + lane;
       const bool row_ok = m < g.M;
-      float rterm[16];  // k2[p] * float(sum_a): second term of affine_term
-#pragma unroll
-      for (int p = 0; p < 16; ++p) rterm[p] = __fmul_rn(s_k2[p], static_cast<float>(rs_next[p]));
-      {
-        const int nxt = grp_i + ncl;
-        const int mn = tile_m0(nxt) + q * 32 + lane;
-#pragma unroll
-        for (int p = 0; p < 16; ++p)
-          rs_next[p] = (nxt < num_groups && mn < g.M)
-                           ? __ldg(rowsum + static_cast<long long>(p) * g.M + mn) : 0;
-      }
       // Output pixels of this lane's tile (2ti + a, 2tj + b) and their
       // validity (merge_tiles discards the ceil-overhang, tensor.hpp:172-175).
-      // Packed (pixel index << 4 | validity mask): pixel counts < 2^27 are
-      // checked at plan creation.
-      int pixm;
+      int pix0, pmask;
       {
         const int mm = row_ok ? m : 0;
         const int img = mm / g.P;
-        const int t = mm - img * g.P;
-        const int ti = t / g.TW, tj = t - ti * g.TW;
-        const int pix0 = (img * g.OH + 2 * ti) * g.OW + 2 * tj;
+        const int tt = mm - img * g.P;
+        const int ti = tt / g.TW, tj = tt - ti * g.TW;
+        pix0 = (img * g.OH + 2 * ti) * g.OW + 2 * tj;
         const bool r1 = 2 * ti + 1 < g.OH, c1 = 2 * tj + 1 < g.OW;
-        const int pmask = row_ok ? (1 | (c1 ? 2 : 0) | (r1 ? 4 : 0) | (r1 && c1 ? 8 : 0)) : 0;
-        pixm = (pix0 << 4) | pmask;
+        pmask = row_ok ? (1 | (c1 ? 2 : 0) | (r1 ? 4 : 0) | (r1 && c1 ? 8 : 0)) : 0;
       }
-      mbar_wait(&acc_full[buf], acc_ph, 4, grp_i, warp);
-      tc_fence_after();
-      const uint32_t acc_addr = lane_base + static_cast<uint32_t>(buf) * Cfg::kAccCols + f0;
-#pragma unroll 1
-      for (int grp = 0; grp < kWarpFilters / 8; ++grp) {
-#pragma unroll 1
-        for (int jj = 0; jj < 4; ++jj) {  // filter pairs of this 8-filter group
-          const int fl = grp * 8 + jj * 2;  // filter offset within the warp's range
-          uint32_t a[16][2];
+      const int kf0 = n0 + f0;
+      // Store this thread's FPT filters of output pixel ab (0..3).
+      auto store_pixel = [&](int ab, float2 (&v)[FPT / 2]) {
+        if (!((pmask >> ab) & 1)) return;
+        const int pix = pix0 + (ab >> 1) * g.OW + (ab & 1);
+        float* d = y + static_cast<long long>(pix) * g.K + kf0;
 #pragma unroll
-          for (int p = 0; p < 16; ++p) tmem_ld_x2(acc_addr + p * BN + fl, a[p]);
-          tmem_ld_wait();
-          if (grp == kWarpFilters / 8 - 1 && jj == 3) {
-            // All of this warp's accumulators are in registers: hand the TMEM
-            // buffer back to the MMA warp early.
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        for (int i = 0; i < FPT / 2; ++i) {
+          float2 w = v[i];
+          if (EPI) {
+            if (bias != nullptr)
+              w = add2(w, make_float2(kf0 + 2 * i < g.K ? __ldg(bias + kf0 + 2 * i) : 0.0f,
+                                      kf0 + 2 * i + 1 < g.K ? __ldg(bias + kf0 + 2 * i + 1) : 0.0f));
+            if (relu) {
+              w.x = fmaxf(w.x, 0.0f);
+              w.y = fmaxf(w.y, 0.0f);
+            }
           }
-          const int kf0 = n0 + f0 + fl;
+          v[i] = add2(w, bcast2(0.0f));  // the reference never yields -0
+        }
+        if (k4ok && kf0 + FPT <= g.K) {
+#pragma unroll
+          for (int i = 0; i < FPT / 4; ++i)
+            *reinterpret_cast<float4*>(d + 4 * i) =
+                make_float4(v[2 * i].x, v[2 * i].y, v[2 * i + 1].x, v[2 * i + 1].y);
+        } else {
+#pragma unroll
+          for (int i = 0; i < FPT / 2; ++i) {
+            if (kf0 + 2 * i < g.K) d[2 * i] = v[i].x;
+            if (kf0 + 2 * i + 1 < g.K) d[2 * i + 1] = v[i].y;
+          }
+        }
+      };
+      float2 S[4][FPT / 2];  // running S_ab partials, filter pairs
+#pragma unroll
+      for (int j = 0; j < 4; ++j, ++grp) {
+        const uint32_t buf = grp & 1u;
+        float rterm[4];  // k2[p] * float(sum_a): second term of affine_term
+        {
+          int32_t rs[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+            rs[a] = row_ok ? __ldg(rowsum + static_cast<long long>(4 * a + j) * g.M + m) : 0;
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+            rterm[a] = __fmul_rn(s_k2[4 * a + j], static_cast<float>(rs[a]));
+        }
+        mbar_wait(&acc_full[buf], (grp >> 1) & 1u);
+        tc_fence_after();
+        const uint32_t acc_addr = lane_base + buf * Cfg::kGroupCols + f0;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          uint32_t acc[4][4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) tmem_ld_x4(acc_addr + a * BN + 4 * c, acc[a]);
+          tmem_ld_wait();
           if (acc_dump != nullptr && row_ok) {
 #pragma unroll
-            for (int p = 0; p < 16; ++p)
+            for (int a = 0; a < 4; ++a)
 #pragma unroll
-              for (int i = 0; i < 2; ++i)
-                if (kf0 + i < g.K)
-                  acc_dump[(static_cast<long long>(p) * g.M + m) * g.K + kf0 + i] =
-                      static_cast<int32_t>(a[p][i]);
+              for (int i = 0; i < 4; ++i)
+                if (kf0 + 4 * c + i < g.K)
+                  acc_dump[(static_cast<long long>(4 * a + j) * g.M + m) * g.K + kf0 + 4 * c + i] =
+                      static_cast<int32_t>(SMALL ? acc[a][i] - kTwo23Bits : acc[a][i]);
           }
-          float2 mv[16];
+          float2 T0[2], T1[2];
+          affine_group4<SMALL>(acc, s_k1, s_nk1m, s_k4, rterm,
+                               s_cterm + j * K_pad + kf0 + 4 * c, K_pad, j, T0, T1);
 #pragma unroll
-          for (int p = 0; p < 16; ++p) {
-            const float2 c2 = *reinterpret_cast<const float2*>(&s_cterm[p * K_pad + kf0]);
-            const float k1 = s_k1[p];
-            float2 t1;
-            if (SMALL) {
-              // dot < 2^23: F = 2^23 + dot exactly, and fma(k1, F, -k1*2^23)
-              // rounds once: RN(k1 * dot) = k1 * float(dot), bitwise.
-              const float2 F = make_float2(__uint_as_float(a[p][0] | 0x4B000000u),
-                                           __uint_as_float(a[p][1] | 0x4B000000u));
-              t1 = fma2(bcast2(k1), F, bcast2(s_nk1m[p]));
+          for (int h = 0; h < 2; ++h) {
+            float2& s00 = S[0][2 * c + h];
+            float2& s01 = S[1][2 * c + h];
+            float2& s10 = S[2][2 * c + h];
+            float2& s11 = S[3][2 * c + h];
+            if (j == 0) {
+              s00 = T0[h];
+              s10 = T1[h];
+            } else if (j == 1) {
+              s00 = add2(s00, T0[h]);
+              s01 = T0[h];
+              s10 = add2(s10, T1[h]);
+              s11 = T1[h];
+            } else if (j == 2) {
+              s00 = add2(s00, T0[h]);
+              s01 = sub2(s01, T0[h]);
+              s10 = add2(s10, T1[h]);
+              s11 = sub2(s11, T1[h]);
             } else {
-              t1 = make_float2(__fmul_rn(k1, __int2float_rn(static_cast<int>(a[p][0]))),
-                               __fmul_rn(k1, __int2float_rn(static_cast<int>(a[p][1]))));
+              s01 = sub2(s01, T0[h]);
+              s11 = sub2(s11, T1[h]);
             }
-            // ((k1*dot + k2*sum_a) + k3*sum_b) + k4, left to right.
-            mv[p] = add2(add2(add2(t1, bcast2(rterm[p])), c2), bcast2(s_k4[p]));
-          }
-          // S = (A^T m) A (winograd.hpp:80-84 in matrix.hpp:75-84 order).
-          float2 X0[4], X1[4];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            X0[c] = add2(add2(mv[c], mv[4 + c]), mv[8 + c]);
-            X1[c] = sub2(sub2(mv[4 + c], mv[8 + c]), mv[12 + c]);
-          }
-          float2 s4[4];
-          s4[0] = add2(add2(X0[0], X0[1]), X0[2]);
-          s4[1] = sub2(sub2(X0[1], X0[2]), X0[3]);
-          s4[2] = add2(add2(X1[0], X1[1]), X1[2]);
-          s4[3] = sub2(sub2(X1[1], X1[2]), X1[3]);
-#pragma unroll
-          for (int ab = 0; ab < 4; ++ab) {
-            float2 v = s4[ab];
-            if (EPI) {
-              if (bias != nullptr)
-                v = add2(v, make_float2(kf0 < g.K ? bias[kf0] : 0.0f,
-                                        kf0 + 1 < g.K ? bias[kf0 + 1] : 0.0f));
-              if (relu) {
-                v.x = fmaxf(v.x, 0.0f);
-                v.y = fmaxf(v.y, 0.0f);
-              }
-            }
-            v = add2(v, bcast2(0.0f));  // the reference never yields -0
-            // staging row = lane (tile), 16-B chunk (ab*2 + jj/2) ^ (lane & 7)
-            const int chunk = (ab * 2 + (jj >> 1)) ^ (lane & 7);
-            *reinterpret_cast<float2*>(&stg[lane * 32 + chunk * 4 + (jj & 1) * 2]) = v;
           }
         }
-        __syncwarp();
-        // Store phase: 32 rows x 4 pixels x 8 filters = 256 16-B chunks, two
-        // lanes per 32-byte pixel segment (full sectors).
+        // Hand the buffer back (re-armed to 2^23 for SMALL).
+        if (SMALL) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int c = lane + 32 * i;
-          const int r = c >> 3, ab = (c >> 1) & 3, half = c & 1;
-          const int rp = __shfl_sync(0xffffffffu, pixm, r);  // row r's pixel base + mask
-          const float4 val =
-              *reinterpret_cast<const float4*>(&stg[r * 32 + (((ab * 2 + half) ^ (r & 7)) * 4)]);
-          if (!((rp >> ab) & 1)) continue;
-          const int kf = n0 + f0 + grp * 8 + half * 4;
-          if (kf >= g.K) continue;
-          const int pix = (rp >> 4) + (ab >> 1) * g.OW + (ab & 1);
-          float* d = y + static_cast<long long>(pix) * g.K + kf;
-          if (k4ok) {
-            *reinterpret_cast<float4*>(d) = val;
-          } else {
-            const float v4[4] = {val.x, val.y, val.z, val.w};
+          for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if (kf + e < g.K) d[e] = v4[e];
-          }
+            for (int c = 0; c < NCH; ++c)
+              tmem_st_x4_const(acc_addr + a * BN + 4 * c, kTwo23Bits);
+          tmem_st_wait();
         }
+        tc_fence_before();
         __syncwarp();
-      }
-      if (++buf == kBufs) {
-        buf = 0;
-        acc_ph ^= 1u;
+        if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        if (j == 2) {
+          store_pixel(0, S[0]);  // S00 and S10 are final after T_2
+          store_pixel(2, S[2]);
+        } else if (j == 3) {
+          store_pixel(1, S[1]);
+          store_pixel(3, S[3]);
+        }
       }
     }
   }
@@ -399,17 +391,20 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     tc_fence_after();
     tmem_dealloc(*tmem_holder, 512);
   }
-  if (cs > 1) cluster_sync();  // no CTA leaves while cluster peers may still signal it
 }
 
 template <int BK, int BN, bool SMALL, bool EPI>
 static cudaError_t launch_gemm_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
                                  const int32_t* rowsum, const int32_t* colsum,
                                  const LanceDevState* st, float* y, int32_t* acc_dump,
-                                 const float* bias, int relu, const GemmGeom& g, cudaStream_t s) {
-  const size_t smem =
-      GemmCfg<BK, BN>::kSmemBase + static_cast<size_t>(16) * g.num_n_tiles * BN * 4;
+                                 const float* bias, int relu, const GemmGeom& g0, cudaStream_t s) {
+  GemmGeom g = g0;
+  const int k_pad = g.num_n_tiles * BN;
+  int stages = 16;
+  while (stages > 2 && gemm_smem_bytes<BK, BN>(stages, k_pad) > kSmemLimit) --stages;
+  const size_t smem = gemm_smem_bytes<BK, BN>(stages, k_pad);
   if (smem > kSmemLimit) return cudaErrorInvalidValue;
+  g.stages = stages;
   static size_t configured[64] = {};  // dynamic-smem attribute set so far, per device
   static int sm_count[64] = {};
   int dev = 0;
@@ -427,24 +422,11 @@ static cudaError_t launch_gemm_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
     }
   }
   const int sms = (dev >= 0 && dev < 64) ? sm_count[dev] : 148;
-  const int cs = g.cluster;
-  const long long groups =
-      ((static_cast<long long>(g.M) + kBM - 1) / kBM) * (g.num_n_tiles / cs);
-  const long long clusters = groups < sms / cs ? groups : sms / cs;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(clusters * cs));
-  cfg.blockDim = dim3(kGemmThreadsP);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cs;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemm_epilogue_kernel<BK, BN, SMALL, EPI>, *tmA, *tmB, rowsum,
-                            colsum, st, y, acc_dump, bias, relu, g);
+  const long long tiles = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * g.num_n_tiles;
+  const int grid = static_cast<int>(tiles < sms ? tiles : sms);
+  gemm_epilogue_kernel<BK, BN, SMALL, EPI><<<grid, kGemmThreadsP, smem, s>>>(
+      *tmA, *tmB, rowsum, colsum, st, y, acc_dump, bias, relu, g);
+  return cudaGetLastError();
 }
 
 template <int BK, int BN>
@@ -472,12 +454,15 @@ cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int bk, 
   if (bk == BKV && bn == BNV)                                                                \
     return launch_gemm_bk<BKV, BNV>(tmA, tmB, small_acc, rowsum, colsum, st, y, acc_dump,    \
                                     bias, relu, g, s);
-  LANCE_GEMM_CASE(128, 16)
-  LANCE_GEMM_CASE(64, 16)
-  LANCE_GEMM_CASE(32, 16)
+  LANCE_GEMM_CASE(128, 64)
+  LANCE_GEMM_CASE(64, 64)
+  LANCE_GEMM_CASE(32, 64)
   LANCE_GEMM_CASE(128, 32)
   LANCE_GEMM_CASE(64, 32)
   LANCE_GEMM_CASE(32, 32)
+  LANCE_GEMM_CASE(128, 16)
+  LANCE_GEMM_CASE(64, 16)
+  LANCE_GEMM_CASE(32, 16)
 #undef LANCE_GEMM_CASE
   return cudaErrorInvalidValue;
 }

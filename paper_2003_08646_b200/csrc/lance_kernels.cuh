@@ -11,7 +11,6 @@ namespace lance_dev {
 
 constexpr int kPositions = 16;  // (m + r - 1)^2 for F(2x2,3x3)
 constexpr int kBM = 128;        // GEMM rows (Winograd tiles) per CTA = UMMA M
-constexpr int kGemmThreads = 192;
 constexpr int kChunk = 64;      // channels per K0/K1 warp item (32 lanes x 2)
 
 // Per-plan device state, written by the range / filter finalisers and read by
@@ -51,9 +50,8 @@ struct GemmGeom {
   int K, C;
   int P, TW, OH, OW;
   int num_kchunks;  // C_pad / BK
-  int num_n_tiles;  // K_pad / bn
-  int dbg_mode;     // debug builds only
-  int cluster;      // CTAs per cluster sharing the A operand by multicast (divides num_n_tiles)
+  int num_n_tiles;  // K_pad / BN
+  int stages;       // shared-memory ring depth (set by the launcher)
 };
 
 struct StaticParams {
@@ -72,7 +70,7 @@ cudaError_t launch_static_params(LanceDevState* st, const StaticParams& prm, int
 cudaError_t launch_filter_prepare(const float* w, float* u_tmp, float* partials, int grid,
                                   uint8_t* codes_w, int32_t* colsum, LanceDevState* st,
                                   const FilterGeom& g, cudaStream_t s);
-// bn: filters per GEMM tile, 16 (two TMEM accumulators) or 32 (one).
+// bn: filters per GEMM tile (16, 32 or 64); TMEM holds two j-groups of 4 x bn columns.
 cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int bk, int bn,
                         int small_acc, const int32_t* rowsum, const int32_t* colsum,
                         const LanceDevState* st, float* y, int32_t* acc_dump, const float* bias,
