@@ -117,6 +117,21 @@ int make_code_map(CUtensorMap* map, void* base, long long rows, int c_pad, int b
   return LANCE_OK;
 }
 
+// Row sums [16][rows] int32; box = 128 rows x 16 positions (OOB rows read 0).
+int make_rowsum_map(CUtensorMap* map, void* base, long long rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(LANCE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(rows), 16};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(rows) * 4};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBM), 16};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, base, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LANCE_ERR_CUDA, "cuTensorMapEncodeTiled (row sums) failed: " + std::to_string(r));
+  return LANCE_OK;
+}
+
 }  // namespace
 
 struct lance_plan_s {
@@ -142,7 +157,7 @@ struct lance_plan_s {
   float* partials = nullptr;    // [max(range_grid, filter_grid)][32]
   LanceDevState* state = nullptr;
   size_t bytes = 0;
-  CUtensorMap tmA{}, tmB{};
+  CUtensorMap tmA{}, tmB{}, tmR{};
   bool filters_ready = false;
   int32_t* acc_dump = nullptr;
   const float* bias = nullptr;
@@ -258,9 +273,10 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   p->P = p->TH * p->TW;
   p->M = static_cast<long long>(spec->n) * p->P;
   p->C_pad = round_up(spec->c, 32);
-  // GEMM tile width: 64 filters (two j-group accumulators of 4 x 64 TMEM
-  // columns) unless the layer has fewer.  LANCE_GEMM_BN overrides.
-  p->BN = spec->k > 32 ? 64 : (spec->k > 16 ? 32 : 16);
+  // GEMM tile width: 32 filters (four j-group accumulators of 4 x 32 TMEM
+  // columns, 8 S partials per epilogue thread) unless the layer has fewer.
+  // LANCE_GEMM_BN overrides (64: two j-group buffers, 16 partials per thread).
+  p->BN = spec->k > 16 ? 32 : 16;
   if (const char* e = std::getenv("LANCE_GEMM_BN")) {
     const int v = std::atoi(e);
     if (v == 16 || v == 32 || v == 64) p->BN = v;
@@ -352,7 +368,8 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
     return cuda_fail(e, "plan init");
   }
   if ((rc = make_code_map(&p->tmA, p->codes_a, p->M, p->C_pad, p->BK, kBM)) ||
-      (rc = make_code_map(&p->tmB, p->codes_w, p->K_pad, p->C_pad, p->BK, p->BN))) {
+      (rc = make_code_map(&p->tmB, p->codes_w, p->K_pad, p->C_pad, p->BK, p->BN)) ||
+      (rc = make_rowsum_map(&p->tmR, p->rowsum, p->M))) {
     free_plan(p);
     delete p;
     return rc;
@@ -421,7 +438,7 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
                                 static_params != nullptr, s));
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[2], s));
-  LANCE_CUDA(launch_gemm(&p->tmA, &p->tmB, p->BK, p->BN, p->small_acc, p->rowsum, p->colsum, p->state, y_dev,
+  LANCE_CUDA(launch_gemm(&p->tmA, &p->tmB, &p->tmR, p->BK, p->BN, p->small_acc, p->colsum, p->state, y_dev,
                          p->acc_dump, p->bias, p->relu, p->gemm_geom, s));
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[3], s));

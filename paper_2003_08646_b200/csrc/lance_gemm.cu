@@ -51,8 +51,10 @@ struct GemmCfg {
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr uint32_t kLayout = (BK == 128) ? 2u : (BK == 64 ? 4u : 6u);  // SW128/64/32
   static constexpr uint32_t kGroupCols = 4 * BN;  // one j-group: 4 positions x BN filters
+  static constexpr int kAccBufs = (512 / kGroupCols) < 4 ? (512 / kGroupCols) : 4;
   static constexpr int kFPT = BN / 4;             // filters per epilogue thread
-  static constexpr size_t kFixed = 1024 /*align*/ + 16 * 8 /*acc barriers, holder*/;
+  static constexpr uint32_t kRsBytes = 16 * kBM * 4;  // row sums of one tile [16][128] i32
+  static constexpr size_t kFixed = 1024 /*align*/ + 2 * kRsBytes + 16 * 8 /*barriers, holder*/;
 };
 
 template <int BK, int BN>
@@ -97,18 +99,25 @@ __device__ __forceinline__ void affine_group4(const uint32_t (&acc)[4][4], const
   }
 }
 
+__device__ __forceinline__ void tmem_ld_group4(uint32_t addr, int bn, uint32_t (&acc)[4][4]) {
+#pragma unroll
+  for (int a = 0; a < 4; ++a) tmem_ld_x4(addr + a * bn, acc[a]);
+}
+
 // SMALL / EPI: see the file comment; EPI = fused bias + ReLU (north-star extension).
 template <int BK, int BN, bool SMALL, bool EPI>
 __global__ void __launch_bounds__(kGemmThreadsP, 1)
     gemm_epilogue_kernel(const __grid_constant__ CUtensorMap tmA,
                          const __grid_constant__ CUtensorMap tmB,
-                         const int32_t* __restrict__ rowsum, const int32_t* __restrict__ colsum,
+                         const __grid_constant__ CUtensorMap tmR,
+                         const int32_t* __restrict__ colsum,
                          const LanceDevState* __restrict__ st, float* __restrict__ y,
                          int32_t* __restrict__ acc_dump, const float* __restrict__ bias,
                          int relu, GemmGeom g) {
   using Cfg = GemmCfg<BK, BN>;
   constexpr int FPT = Cfg::kFPT;
   constexpr int NCH = FPT / 4;  // 4-filter chunks per thread
+  constexpr int NB = Cfg::kAccBufs;
   constexpr uint32_t kIdesc = umma_idesc_u8(kBM, BN);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -118,11 +127,14 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   const int stages = g.stages;
   uint8_t* stage_base = smem;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(stages) * Cfg::kStageBytes);
+  int32_t* s_rs = reinterpret_cast<int32_t*>(smem + static_cast<size_t>(stages) * Cfg::kStageBytes);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(s_rs + 2 * 16 * kBM);
   uint64_t* empty_bar = full_bar + stages;
-  uint64_t* acc_full = empty_bar + stages;  // [2]
-  uint64_t* acc_empty = acc_full + 2;       // [2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* acc_full = empty_bar + stages;  // [4]
+  uint64_t* acc_empty = acc_full + 4;       // [4]
+  uint64_t* rs_full = acc_empty + 4;        // [2]
+  uint64_t* rs_empty = rs_full + 2;         // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(rs_empty + 2);
   float* s_cterm = reinterpret_cast<float*>(tmem_holder + 4);  // [16][K_pad]: k3[p]*colsum[p][k]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -136,9 +148,13 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < 4; ++b) {
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], kEpiWarps);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&rs_full[b], 1);
+      mbar_init(&rs_empty[b], kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -165,10 +181,17 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmB);
+      tma_prefetch_desc(&tmR);
       int s = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      uint32_t lt = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
         const int m0 = (t / nt) * kBM, n0 = (t % nt) * BN;
+        // Row sums of the tile's 128 rows for all 16 positions (OOB rows read 0).
+        const uint32_t rb = lt & 1u;
+        mbar_wait(&rs_empty[rb], ((lt >> 1) & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&rs_full[rb], Cfg::kRsBytes);
+        tma_load_2d(s_rs + rb * 16 * kBM, &tmR, m0, 0, &rs_full[rb]);
         for (int j = 0; j < 4; ++j)
           for (int a = 0; a < 4; ++a) {
             const int p = 4 * a + j;
@@ -200,8 +223,8 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       uint32_t grp = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         for (int j = 0; j < 4; ++j, ++grp) {
-          const uint32_t buf = grp & 1u;
-          mbar_wait(&acc_empty[buf], (grp >> 1) & 1u);  // epilogue drained (and re-armed) it
+          const uint32_t buf = grp % NB;
+          mbar_wait(&acc_empty[buf], (grp / NB) & 1u);  // epilogue drained (and re-armed) it
           tc_fence_after();
           const uint32_t d_base = tmem_base + buf * Cfg::kGroupCols;
           for (int a = 0; a < 4; ++a) {
@@ -234,14 +257,15 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     const int ew = warp - 2;
     const int q = warp & 3;          // TMEM lane quadrant this warp may access
     const int f0 = (ew >> 2) * FPT;  // this thread's filters within the tile
+    const int row = q * 32 + lane;   // this thread's row (Winograd tile) within the tile
     named_bar_sync(1, 32 + 32 * kEpiWarps);
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
     const bool k4ok = (g.K & 3) == 0;
-    // Arm both j-group buffers (SMALL: preset to 2^23; see the file comment).
+    // Arm all j-group buffers (SMALL: preset to 2^23; see the file comment).
 #pragma unroll
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NB; ++b) {
       if (SMALL) {
 #pragma unroll
         for (int a = 0; a < 4; ++a)
@@ -255,9 +279,10 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       if (lane == 0) mbar_arrive(&acc_empty[b]);
     }
     uint32_t grp = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    uint32_t lt = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
       const int m0 = (t / nt) * kBM, n0 = (t % nt) * BN;
-      const int m = m0 + q * 32 + lane;
+      const int m = m0 + row;
       const bool row_ok = m < g.M;
       // Output pixels of this lane's tile (2ti + a, 2tj + b) and their
       // validity (merge_tiles discards the ceil-overhang, tensor.hpp:172-175).
@@ -304,29 +329,37 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
           }
         }
       };
+      const uint32_t rb = lt & 1u;
+      const int32_t* rs_tile = s_rs + rb * 16 * kBM + row;
+      mbar_wait(&rs_full[rb], (lt >> 1) & 1u);
       float2 S[4][FPT / 2];  // running S_ab partials, filter pairs
 #pragma unroll
       for (int j = 0; j < 4; ++j, ++grp) {
-        const uint32_t buf = grp & 1u;
+        const uint32_t buf = grp % NB;
         float rterm[4];  // k2[p] * float(sum_a): second term of affine_term
-        {
-          int32_t rs[4];
 #pragma unroll
-          for (int a = 0; a < 4; ++a)
-            rs[a] = row_ok ? __ldg(rowsum + static_cast<long long>(4 * a + j) * g.M + m) : 0;
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-            rterm[a] = __fmul_rn(s_k2[4 * a + j], static_cast<float>(rs[a]));
+        for (int a = 0; a < 4; ++a)
+          rterm[a] = __fmul_rn(s_k2[4 * a + j], static_cast<float>(rs_tile[(4 * a + j) * kBM]));
+        if (j == 3) {  // row sums of this tile fully read
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&rs_empty[rb]);
         }
-        mbar_wait(&acc_full[buf], (grp >> 1) & 1u);
+        mbar_wait(&acc_full[buf], (grp / NB) & 1u);
         tc_fence_after();
         const uint32_t acc_addr = lane_base + buf * Cfg::kGroupCols + f0;
+        // Chunk c + 1's TMEM loads are issued while chunk c computes when the
+        // register budget allows (LDB = 2), else one chunk at a time.
+        constexpr int LDB = (NCH > 1 && FPT <= 4) ? 2 : 1;
+        uint32_t acc[LDB][4][4];
+        tmem_ld_group4(acc_addr, BN, acc[0]);
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-          uint32_t acc[4][4];
-#pragma unroll
-          for (int a = 0; a < 4; ++a) tmem_ld_x4(acc_addr + a * BN + 4 * c, acc[a]);
+          if (LDB == 1 && c > 0) tmem_ld_group4(acc_addr + 4 * c, BN, acc[0]);
           tmem_ld_wait();
+#pragma unroll
+          for (int a = 0; a < 4; ++a) reg_fence(acc[c % LDB][a]);
+          if (LDB == 2 && c + 1 < NCH) tmem_ld_group4(acc_addr + 4 * (c + 1), BN, acc[(c + 1) % LDB]);
+          const uint32_t(&ac)[4][4] = acc[c % LDB];
           if (acc_dump != nullptr && row_ok) {
 #pragma unroll
             for (int a = 0; a < 4; ++a)
@@ -334,10 +367,10 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
               for (int i = 0; i < 4; ++i)
                 if (kf0 + 4 * c + i < g.K)
                   acc_dump[(static_cast<long long>(4 * a + j) * g.M + m) * g.K + kf0 + 4 * c + i] =
-                      static_cast<int32_t>(SMALL ? acc[a][i] - kTwo23Bits : acc[a][i]);
+                      static_cast<int32_t>(SMALL ? ac[a][i] - kTwo23Bits : ac[a][i]);
           }
           float2 T0[2], T1[2];
-          affine_group4<SMALL>(acc, s_k1, s_nk1m, s_k4, rterm,
+          affine_group4<SMALL>(ac, s_k1, s_nk1m, s_k4, rterm,
                                s_cterm + j * K_pad + kf0 + 4 * c, K_pad, j, T0, T1);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -395,7 +428,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
 
 template <int BK, int BN, bool SMALL, bool EPI>
 static cudaError_t launch_gemm_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
-                                 const int32_t* rowsum, const int32_t* colsum,
+                                 const CUtensorMap* tmR, const int32_t* colsum,
                                  const LanceDevState* st, float* y, int32_t* acc_dump,
                                  const float* bias, int relu, const GemmGeom& g0, cudaStream_t s) {
   GemmGeom g = g0;
@@ -425,34 +458,34 @@ static cudaError_t launch_gemm_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
   const long long tiles = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * g.num_n_tiles;
   const int grid = static_cast<int>(tiles < sms ? tiles : sms);
   gemm_epilogue_kernel<BK, BN, SMALL, EPI><<<grid, kGemmThreadsP, smem, s>>>(
-      *tmA, *tmB, rowsum, colsum, st, y, acc_dump, bias, relu, g);
+      *tmA, *tmB, *tmR, colsum, st, y, acc_dump, bias, relu, g);
   return cudaGetLastError();
 }
 
 template <int BK, int BN>
 static cudaError_t launch_gemm_bk(const CUtensorMap* tmA, const CUtensorMap* tmB, int small_acc,
-                                  const int32_t* rowsum, const int32_t* colsum,
+                                  const CUtensorMap* tmR, const int32_t* colsum,
                                   const LanceDevState* st, float* y, int32_t* acc_dump,
                                   const float* bias, int relu, const GemmGeom& g, cudaStream_t s) {
   const bool epi = bias != nullptr || relu;
   if (small_acc)
-    return epi ? launch_gemm_t<BK, BN, true, true>(tmA, tmB, rowsum, colsum, st, y, acc_dump,
+    return epi ? launch_gemm_t<BK, BN, true, true>(tmA, tmB, tmR, colsum, st, y, acc_dump,
                                                    bias, relu, g, s)
-               : launch_gemm_t<BK, BN, true, false>(tmA, tmB, rowsum, colsum, st, y, acc_dump,
+               : launch_gemm_t<BK, BN, true, false>(tmA, tmB, tmR, colsum, st, y, acc_dump,
                                                     bias, relu, g, s);
-  return epi ? launch_gemm_t<BK, BN, false, true>(tmA, tmB, rowsum, colsum, st, y, acc_dump,
+  return epi ? launch_gemm_t<BK, BN, false, true>(tmA, tmB, tmR, colsum, st, y, acc_dump,
                                                   bias, relu, g, s)
-             : launch_gemm_t<BK, BN, false, false>(tmA, tmB, rowsum, colsum, st, y, acc_dump,
+             : launch_gemm_t<BK, BN, false, false>(tmA, tmB, tmR, colsum, st, y, acc_dump,
                                                    bias, relu, g, s);
 }
 
-cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int bk, int bn,
-                        int small_acc, const int32_t* rowsum, const int32_t* colsum,
+cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmR,
+                        int bk, int bn, int small_acc, const int32_t* colsum,
                         const LanceDevState* st, float* y, int32_t* acc_dump, const float* bias,
                         int relu, const GemmGeom& g, cudaStream_t s) {
 #define LANCE_GEMM_CASE(BKV, BNV)                                                            \
   if (bk == BKV && bn == BNV)                                                                \
-    return launch_gemm_bk<BKV, BNV>(tmA, tmB, small_acc, rowsum, colsum, st, y, acc_dump,    \
+    return launch_gemm_bk<BKV, BNV>(tmA, tmB, small_acc, tmR, colsum, st, y, acc_dump,       \
                                     bias, relu, g, s);
   LANCE_GEMM_CASE(128, 64)
   LANCE_GEMM_CASE(64, 64)

@@ -71,8 +71,8 @@ cudaError_t launch_filter_prepare(const float* w, float* u_tmp, float* partials,
                                   uint8_t* codes_w, int32_t* colsum, LanceDevState* st,
                                   const FilterGeom& g, cudaStream_t s);
 // bn: filters per GEMM tile (16, 32 or 64); TMEM holds two j-groups of 4 x bn columns.
-cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int bk, int bn,
-                        int small_acc, const int32_t* rowsum, const int32_t* colsum,
+cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmR,
+                        int bk, int bn, int small_acc, const int32_t* colsum,
                         const LanceDevState* st, float* y, int32_t* acc_dump, const float* bias,
                         int relu, const GemmGeom& g, cudaStream_t s);
 

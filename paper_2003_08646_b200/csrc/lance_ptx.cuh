@@ -80,6 +80,15 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int c0,
+                                            int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // Multicast variant: the box lands at the same shared-memory offset in every
 // CTA of `cta_mask` and signals complete_tx on each CTA's barrier at `bar`'s
 // offset.
@@ -196,6 +205,14 @@ __device__ __forceinline__ void tmem_st_wait() {
 
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Pins registers written by tcgen05.ld after the tcgen05.wait::ld that
+// completes them (the compiler sees the ld's outputs as ready at issue).
+template <int N>
+__device__ __forceinline__ void reg_fence(uint32_t (&r)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) asm volatile("" : "+r"(r[i]));
 }
 
 // UMMA shared-memory matrix descriptor (sm_100): K-major operand, swizzled
