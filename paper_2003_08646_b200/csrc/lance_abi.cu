@@ -118,11 +118,11 @@ int make_code_map(CUtensorMap* map, void* base, long long rows, int c_pad, int b
 }
 
 // Row sums [16][rows] int32; box = 128 rows x 16 positions (OOB rows read 0).
-int make_rowsum_map(CUtensorMap* map, void* base, long long rows) {
+int make_rowsum_map(CUtensorMap* map, void* base, long long rows, long long pitch) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(LANCE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(rows), 16};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(rows) * 4};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch) * 4};
   const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBM), 16};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, base, dims, strides, box, estr,
@@ -150,7 +150,8 @@ struct lance_plan_s {
   bool small_acc = false;
   // device memory
   uint8_t* codes_a = nullptr;   // [16][M][C_pad]
-  int32_t* rowsum = nullptr;    // [16][M]
+  int32_t* rowsum = nullptr;    // [16][rs_pitch]
+  long long rs_pitch = 0;       // M rounded up to 4
   uint8_t* codes_w = nullptr;   // [16][K_pad][C_pad]
   int32_t* colsum = nullptr;    // [16][K_pad]
   float* u_tmp = nullptr;       // [16][K][C]
@@ -295,6 +296,8 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   }
   InGeom& g = p->in_geom;
   g.M = static_cast<int>(p->M);
+  p->rs_pitch = (p->M + 3) / 4 * 4;
+  g.rs_pitch = static_cast<int>(p->rs_pitch);
   g.P = p->P;
   g.TH = p->TH;
   g.TW = p->TW;
@@ -343,7 +346,7 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   const size_t codes_w_bytes = static_cast<size_t>(16) * p->K_pad * p->C_pad;
   const int part_rows = std::max(p->range_grid, p->filter_grid);
   if ((rc = dev_alloc(p, &p->codes_a, codes_a_bytes)) ||
-      (rc = dev_alloc(p, &p->rowsum, sizeof(int32_t) * 16 * p->M)) ||
+      (rc = dev_alloc(p, &p->rowsum, sizeof(int32_t) * 16 * p->rs_pitch)) ||
       (rc = dev_alloc(p, &p->codes_w, codes_w_bytes)) ||
       (rc = dev_alloc(p, &p->colsum, sizeof(int32_t) * 16 * p->K_pad)) ||
       (rc = dev_alloc(p, &p->u_tmp, sizeof(float) * 16 * kc)) ||
@@ -369,7 +372,7 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   }
   if ((rc = make_code_map(&p->tmA, p->codes_a, p->M, p->C_pad, p->BK, kBM)) ||
       (rc = make_code_map(&p->tmB, p->codes_w, p->K_pad, p->C_pad, p->BK, p->BN)) ||
-      (rc = make_rowsum_map(&p->tmR, p->rowsum, p->M))) {
+      (rc = make_rowsum_map(&p->tmR, p->rowsum, p->M, p->rs_pitch))) {
     free_plan(p);
     delete p;
     return rc;
@@ -433,7 +436,7 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[1], s));
   if (p->in_geom.nchunks > 1)
-    LANCE_CUDA(cudaMemsetAsync(p->rowsum, 0, sizeof(int32_t) * 16 * p->M, s));
+    LANCE_CUDA(cudaMemsetAsync(p->rowsum, 0, sizeof(int32_t) * 16 * p->rs_pitch, s));
   LANCE_CUDA(launch_input_quant(x_dev, p->codes_a, p->rowsum, p->state, p->in_geom, p->vec2,
                                 static_params != nullptr, s));
   ++launches;
@@ -534,7 +537,8 @@ int lance_plan_debug_read(lance_plan_t p, int what, void* dst, size_t bytes) {
     }
     case LANCE_DBG_ROWSUM: {
       if (bytes != sizeof(int32_t) * 16 * M) return fail(LANCE_ERR_INVALID_ARGUMENT, "bad size");
-      LANCE_CUDA(cudaMemcpy(dst, p->rowsum, bytes, cudaMemcpyDeviceToHost));
+      LANCE_CUDA(cudaMemcpy2D(dst, sizeof(int32_t) * M, p->rowsum, sizeof(int32_t) * p->rs_pitch,
+                              sizeof(int32_t) * M, 16, cudaMemcpyDeviceToHost));
       return LANCE_OK;
     }
     case LANCE_DBG_CODES_W: {  // device [16][K_pad][C_pad] -> reference [16][C][K]

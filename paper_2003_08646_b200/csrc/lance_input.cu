@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(256, 2) input_quant_kernel(const float* __rest
       if ((lane >> 1) == k) mine = (lane & 1) ? (tot >> 16) : (tot & 0xFFFFu);
     }
     if (lane < 16) {
-      int32_t* rs = rowsum + static_cast<long long>(lane) * g.M + m;
+      int32_t* rs = rowsum + static_cast<long long>(lane) * g.rs_pitch + m;
       if (g.nchunks == 1)
         *rs = static_cast<int32_t>(mine);
       else  // channel chunks of one tile run in different warps (rowsum pre-zeroed)

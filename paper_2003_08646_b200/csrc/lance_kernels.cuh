@@ -32,6 +32,7 @@ struct InGeom {
   int P, TH, TW;  // tiles per image, tile rows / columns per image
   int H, W, C;    // image dims, channels
   int C_pad;      // code row pitch (multiple of 32)
+  int rs_pitch;   // row-sum plane pitch (M rounded up to 4: 16-byte TMA strides)
   int pad;
   int nchunks;    // ceil(C_pad / kChunk)
   int seg_len;    // tiles per warp strip (a tile row is split into nseg strips)
