@@ -319,7 +319,7 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   g.granularity = cfg->granularity;
   p->range_grid = input_range_grid(g, p->sm_count);
   p->small_acc = static_cast<double>(spec->c) * ((1 << cfg->bits_i) - 1) *
-                     ((1 << cfg->bits_w) - 1) < 8388608.0;
+                     ((1 << cfg->bits_w) - 1) < 16777216.0;  // every accumulator < 2^24 (exact fp32 bit trick)
 
   FilterGeom& f = p->f_geom;
   f.K = spec->k;

@@ -26,10 +26,14 @@
 //                filters BN/4 * ((w-2)/4) .. +BN/4 of the tile; each thread
 //                owns one Winograd tile (row) and keeps the S partials of its
 //                filters in registers; y is written with 16-byte stores.
-// SMALL (C * top_a * top_b < 2^23): every accumulator is < 2^23, so TMEM is
-// pre-set to the bit pattern of 2^23 (0x4B000000) and the MMAs accumulate on
-// top of it: the result read back is the float 2^23 + dot, and
-// fma(k1, 2^23 + dot, -k1 * 2^23) = RN(k1 * dot) = k1 * float(dot) bitwise.
+// Exact int -> float epilogue without a conversion instruction (SMALL: every
+// accumulator dot < 2^24, i.e. C * top_a * top_b < 2^24).  The int32 bits of
+// dot read as an fp32 are the subnormal / first-binade float D = dot * 2^-149
+// exactly, so with k1s = k1 * 2^126 (exact power-of-two scaling)
+//   u = RN(k1s * D) = RN(k1 * dot) * 2^-23        (one FFMA2, exact scaling)
+//   fma(u, 2^23, rterm) = RN(RN(k1 * dot) + rterm)  (one FFMA2)
+// which is affine_term's first two terms bit for bit, provided k1 * dot stays
+// a normal float (k1 == 0 or 2^-103 <= k1 < 4); other k1 fall back to I2F.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -42,7 +46,8 @@ namespace lance_dev {
 constexpr int kEpiWarps = 16;
 constexpr int kGemmThreadsP = 64 + 32 * kEpiWarps;  // 576
 constexpr size_t kSmemLimit = 225 * 1024;           // dynamic part, leaves room for static smem
-constexpr uint32_t kTwo23Bits = 0x4B000000u;        // float 2^23
+constexpr float kTwo23 = 8388608.0f;
+constexpr float kTwo126 = 8.507059173023462e37f;   // 2^126
 
 template <int BK, int BN>
 struct GemmCfg {
@@ -64,32 +69,32 @@ __host__ __device__ constexpr size_t gemm_smem_bytes(int stages, int k_pad) {
 }
 
 // Epilogue of one j-group for 4 filters (one TMEM x4 load per position).
-// acc[a][i]: accumulator of position p = 4a + j, filter f0 + 4c + i.
-template <bool SMALL>
-__device__ __forceinline__ void affine_group4(const uint32_t (&acc)[4][4], const float* s_k1,
-                                              const float* s_nk1m, const float* s_k4,
-                                              const float (&rterm)[4], const float* cterm_j,
-                                              int K_pad, int j, float2 (&T0)[2],
-                                              float2 (&T1)[2]) {
+// acc[a][i]: accumulator of position p = 4a + j, filter f0 + 4c + i;
+// k1s[a] = k1[p] * 2^126 (fast) or k1[p]; ct_j: cterm row of position j.
+__device__ __forceinline__ void affine_group4(const uint32_t (&acc)[4][4], bool fast,
+                                              const float (&k1s)[4], const float (&k4)[4],
+                                              const float (&rterm)[4], const float* ct_j,
+                                              int K_pad, float2 (&T0)[2], float2 (&T1)[2]) {
   float2 m[4][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
-    const int p = 4 * a + j;
-    const float k1 = s_k1[p];
-    const float4 ct = *reinterpret_cast<const float4*>(cterm_j + a * 4 * K_pad);
+    const float4 ct = *reinterpret_cast<const float4*>(ct_j + a * 4 * K_pad);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      float2 t1;
-      if (SMALL) {
-        t1 = fma2(bcast2(k1), make_float2(__uint_as_float(acc[a][2 * h]), __uint_as_float(acc[a][2 * h + 1])),
-                  bcast2(s_nk1m[p]));
+      const uint32_t d0 = acc[a][2 * h], d1 = acc[a][2 * h + 1];
+      float2 v;  // RN(k1 * dot + k2 * sum_a), both products rounded first
+      if (fast) {
+        const float2 u = fma2(bcast2(k1s[a]), make_float2(__uint_as_float(d0), __uint_as_float(d1)),
+                              bcast2(0.0f));
+        v = fma2(u, bcast2(kTwo23), bcast2(rterm[a]));
       } else {
-        t1 = make_float2(__fmul_rn(k1, __int2float_rn(static_cast<int>(acc[a][2 * h]))),
-                         __fmul_rn(k1, __int2float_rn(static_cast<int>(acc[a][2 * h + 1]))));
+        v = add2(make_float2(__fmul_rn(k1s[a], __int2float_rn(static_cast<int>(d0))),
+                             __fmul_rn(k1s[a], __int2float_rn(static_cast<int>(d1)))),
+                 bcast2(rterm[a]));
       }
       const float2 c2 = h ? make_float2(ct.z, ct.w) : make_float2(ct.x, ct.y);
       // ((k1*dot + k2*sum_a) + k3*sum_b) + k4, left to right (lowpgemm.hpp:110-114).
-      m[a][h] = add2(add2(add2(t1, bcast2(rterm[a])), c2), bcast2(s_k4[p]));
+      m[a][h] = add2(add2(v, c2), bcast2(k4[a]));
     }
   }
 #pragma unroll
@@ -104,8 +109,9 @@ __device__ __forceinline__ void tmem_ld_group4(uint32_t addr, int bn, uint32_t (
   for (int a = 0; a < 4; ++a) tmem_ld_x4(addr + a * bn, acc[a]);
 }
 
-// SMALL / EPI: see the file comment; EPI = fused bias + ReLU (north-star extension).
-template <int BK, int BN, bool SMALL, bool EPI>
+// SMALL: see the file comment.  DUMP: also write the raw int32 accumulators
+// (parity tests).  bias / relu: fused epilogue (north-star extension).
+template <int BK, int BN, bool SMALL, bool DUMP>
 __global__ void __launch_bounds__(kGemmThreadsP, 1)
     gemm_epilogue_kernel(const __grid_constant__ CUtensorMap tmA,
                          const __grid_constant__ CUtensorMap tmB,
@@ -121,10 +127,13 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   constexpr uint32_t kIdesc = umma_idesc_u8(kBM, BN);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ float s_k1[16], s_nk1m[16], s_k2[16], s_k4[16];
+  __shared__ float s_k1[16], s_k2[16], s_k4[16];
+  __shared__ int s_fast;
 
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  // 1024-byte aligned base (SWIZZLE_128B atoms), derived by offsetting the
+  // __shared__ array so every access below stays in the shared window (LDS/STS,
+  // not generic loads).
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stages = g.stages;
   uint8_t* stage_base = smem;
   int32_t* s_rs = reinterpret_cast<int32_t*>(smem + static_cast<size_t>(stages) * Cfg::kStageBytes);
@@ -166,12 +175,16 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       s_cterm[i] = __fmul_rn(st->k3[p], csum);
     }
     const int e = threadIdx.x - 64;
-    if (e < 16) {
-      const float k1 = st->k1[e];
-      s_k1[e] = k1;
-      s_nk1m[e] = __fmul_rn(k1, -8388608.0f);  // -k1 * 2^23, exact
-      s_k2[e] = st->k2[e];
-      s_k4[e] = st->k4[e];
+    if (e < 32) {
+      const float k1 = e < 16 ? st->k1[e] : 0.0f;
+      const bool ok = k1 == 0.0f || (k1 >= 9.860761315262648e-32f /*2^-103*/ && k1 < 4.0f);
+      const bool fast = SMALL && __all_sync(0xffffffffu, ok);
+      if (e < 16) {
+        s_k1[e] = fast ? __fmul_rn(k1, kTwo126) : k1;
+        s_k2[e] = st->k2[e];
+        s_k4[e] = st->k4[e];
+      }
+      if (e == 0) s_fast = fast ? 1 : 0;
     }
   }
   __syncthreads();
@@ -238,7 +251,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
                 const uint64_t adesc = umma_smem_desc(sa + kk * 32, 8 * BK, Cfg::kLayout);
                 const uint64_t bdesc = umma_smem_desc(sb + kk * 32, 8 * BK, Cfg::kLayout);
                 umma_i8(d_base + static_cast<uint32_t>(a * BN), adesc, bdesc, kIdesc,
-                        (SMALL || kc > 0 || kk > 0) ? 1u : 0u);
+                        (kc > 0 || kk > 0) ? 1u : 0u);
               }
               umma_commit(&empty_bar[s]);
               if (++s == stages) {
@@ -263,59 +276,50 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     const uint32_t tmem_base = *tmem_holder;
     const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
     const bool k4ok = (g.K & 3) == 0;
-    // Arm all j-group buffers (SMALL: preset to 2^23; see the file comment).
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      if (SMALL) {
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int c = 0; c < NCH; ++c)
-            tmem_st_x4_const(lane_base + b * Cfg::kGroupCols + a * BN + f0 + 4 * c, kTwo23Bits);
-        tmem_st_wait();
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[b]);
-    }
+    // All j-group buffers start empty.
+    if (lane == 0)
+      for (int b = 0; b < NB; ++b) mbar_arrive(&acc_empty[b]);
+    const bool fast = s_fast != 0;
     uint32_t grp = 0;
     uint32_t lt = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
       const int m0 = (t / nt) * kBM, n0 = (t % nt) * BN;
       const int m = m0 + row;
       const bool row_ok = m < g.M;
+      const int kf0 = n0 + f0;
       // Output pixels of this lane's tile (2ti + a, 2tj + b) and their
       // validity (merge_tiles discards the ceil-overhang, tensor.hpp:172-175).
-      int pix0, pmask;
+      float* ybase;
+      int pmask;
       {
         const int mm = row_ok ? m : 0;
         const int img = mm / g.P;
         const int tt = mm - img * g.P;
         const int ti = tt / g.TW, tj = tt - ti * g.TW;
-        pix0 = (img * g.OH + 2 * ti) * g.OW + 2 * tj;
+        const int pix0 = (img * g.OH + 2 * ti) * g.OW + 2 * tj;
+        ybase = y + static_cast<long long>(pix0) * g.K + kf0;
         const bool r1 = 2 * ti + 1 < g.OH, c1 = 2 * tj + 1 < g.OW;
         pmask = row_ok ? (1 | (c1 ? 2 : 0) | (r1 ? 4 : 0) | (r1 && c1 ? 8 : 0)) : 0;
       }
-      const int kf0 = n0 + f0;
+      const int row_stride = g.OW * g.K;  // one output row, in floats
       // Store this thread's FPT filters of output pixel ab (0..3).
       auto store_pixel = [&](int ab, float2 (&v)[FPT / 2]) {
         if (!((pmask >> ab) & 1)) return;
-        const int pix = pix0 + (ab >> 1) * g.OW + (ab & 1);
-        float* d = y + static_cast<long long>(pix) * g.K + kf0;
+        float* d = ybase + (ab >> 1) * row_stride + (ab & 1) * g.K;
+        if (bias != nullptr || relu) {
 #pragma unroll
-        for (int i = 0; i < FPT / 2; ++i) {
-          float2 w = v[i];
-          if (EPI) {
+          for (int i = 0; i < FPT / 2; ++i) {
             if (bias != nullptr)
-              w = add2(w, make_float2(kf0 + 2 * i < g.K ? __ldg(bias + kf0 + 2 * i) : 0.0f,
-                                      kf0 + 2 * i + 1 < g.K ? __ldg(bias + kf0 + 2 * i + 1) : 0.0f));
+              v[i] = add2(v[i], make_float2(kf0 + 2 * i < g.K ? __ldg(bias + kf0 + 2 * i) : 0.0f,
+                                            kf0 + 2 * i + 1 < g.K ? __ldg(bias + kf0 + 2 * i + 1) : 0.0f));
             if (relu) {
-              w.x = fmaxf(w.x, 0.0f);
-              w.y = fmaxf(w.y, 0.0f);
+              v[i].x = fmaxf(v[i].x, 0.0f);
+              v[i].y = fmaxf(v[i].y, 0.0f);
             }
           }
-          v[i] = add2(w, bcast2(0.0f));  // the reference never yields -0
         }
+#pragma unroll
+        for (int i = 0; i < FPT / 2; ++i) v[i] = add2(v[i], bcast2(0.0f));  // the reference never yields -0
         if (k4ok && kf0 + FPT <= g.K) {
 #pragma unroll
           for (int i = 0; i < FPT / 4; ++i)
@@ -336,10 +340,14 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
 #pragma unroll
       for (int j = 0; j < 4; ++j, ++grp) {
         const uint32_t buf = grp % NB;
-        float rterm[4];  // k2[p] * float(sum_a): second term of affine_term
+        float rterm[4], k1s[4], k4[4];  // per position 4a + j of this j-group
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < 4; ++a) {
+          // k2[p] * float(sum_a): second term of affine_term
           rterm[a] = __fmul_rn(s_k2[4 * a + j], static_cast<float>(rs_tile[(4 * a + j) * kBM]));
+          k1s[a] = s_k1[4 * a + j];
+          k4[a] = s_k4[4 * a + j];
+        }
         if (j == 3) {  // row sums of this tile fully read
           __syncwarp();
           if (lane == 0) mbar_arrive(&rs_empty[rb]);
@@ -347,31 +355,30 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         mbar_wait(&acc_full[buf], (grp / NB) & 1u);
         tc_fence_after();
         const uint32_t acc_addr = lane_base + buf * Cfg::kGroupCols + f0;
-        // Chunk c + 1's TMEM loads are issued while chunk c computes when the
-        // register budget allows (LDB = 2), else one chunk at a time.
-        constexpr int LDB = (NCH > 1 && FPT <= 4) ? 2 : 1;
-        uint32_t acc[LDB][4][4];
-        tmem_ld_group4(acc_addr, BN, acc[0]);
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-          if (LDB == 1 && c > 0) tmem_ld_group4(acc_addr + 4 * c, BN, acc[0]);
+          uint32_t ac[4][4];
+          tmem_ld_group4(acc_addr + 4 * c, BN, ac);
           tmem_ld_wait();
 #pragma unroll
-          for (int a = 0; a < 4; ++a) reg_fence(acc[c % LDB][a]);
-          if (LDB == 2 && c + 1 < NCH) tmem_ld_group4(acc_addr + 4 * (c + 1), BN, acc[(c + 1) % LDB]);
-          const uint32_t(&ac)[4][4] = acc[c % LDB];
-          if (acc_dump != nullptr && row_ok) {
+          for (int a = 0; a < 4; ++a) reg_fence(ac[a]);
+          if (c == NCH - 1) {
+            // Every accumulator of this warp is in registers: release the buffer.
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[buf]);
+          }
+          if (DUMP && row_ok) {
 #pragma unroll
             for (int a = 0; a < 4; ++a)
 #pragma unroll
               for (int i = 0; i < 4; ++i)
                 if (kf0 + 4 * c + i < g.K)
                   acc_dump[(static_cast<long long>(4 * a + j) * g.M + m) * g.K + kf0 + 4 * c + i] =
-                      static_cast<int32_t>(SMALL ? ac[a][i] - kTwo23Bits : ac[a][i]);
+                      static_cast<int32_t>(ac[a][i]);
           }
           float2 T0[2], T1[2];
-          affine_group4<SMALL>(ac, s_k1, s_nk1m, s_k4, rterm,
-                               s_cterm + j * K_pad + kf0 + 4 * c, K_pad, j, T0, T1);
+          affine_group4(ac, fast, k1s, k4, rterm, s_cterm + j * K_pad + kf0 + 4 * c, K_pad, T0, T1);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             float2& s00 = S[0][2 * c + h];
@@ -397,18 +404,6 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
             }
           }
         }
-        // Hand the buffer back (re-armed to 2^23 for SMALL).
-        if (SMALL) {
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int c = 0; c < NCH; ++c)
-              tmem_st_x4_const(acc_addr + a * BN + 4 * c, kTwo23Bits);
-          tmem_st_wait();
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[buf]);
         if (j == 2) {
           store_pixel(0, S[0]);  // S00 and S10 are final after T_2
           store_pixel(2, S[2]);
@@ -426,7 +421,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   }
 }
 
-template <int BK, int BN, bool SMALL, bool EPI>
+template <int BK, int BN, bool SMALL, bool DUMP>
 static cudaError_t launch_gemm_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
                                  const CUtensorMap* tmR, const int32_t* colsum,
                                  const LanceDevState* st, float* y, int32_t* acc_dump,
@@ -443,7 +438,7 @@ static cudaError_t launch_gemm_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || configured[dev] < smem) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_epilogue_kernel<BK, BN, SMALL, EPI>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_epilogue_kernel<BK, BN, SMALL, DUMP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -457,7 +452,7 @@ static cudaError_t launch_gemm_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
   const int sms = (dev >= 0 && dev < 64) ? sm_count[dev] : 148;
   const long long tiles = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * g.num_n_tiles;
   const int grid = static_cast<int>(tiles < sms ? tiles : sms);
-  gemm_epilogue_kernel<BK, BN, SMALL, EPI><<<grid, kGemmThreadsP, smem, s>>>(
+  gemm_epilogue_kernel<BK, BN, SMALL, DUMP><<<grid, kGemmThreadsP, smem, s>>>(
       *tmA, *tmB, *tmR, colsum, st, y, acc_dump, bias, relu, g);
   return cudaGetLastError();
 }
@@ -467,16 +462,16 @@ static cudaError_t launch_gemm_bk(const CUtensorMap* tmA, const CUtensorMap* tmB
                                   const CUtensorMap* tmR, const int32_t* colsum,
                                   const LanceDevState* st, float* y, int32_t* acc_dump,
                                   const float* bias, int relu, const GemmGeom& g, cudaStream_t s) {
-  const bool epi = bias != nullptr || relu;
+  const bool dump = acc_dump != nullptr;
   if (small_acc)
-    return epi ? launch_gemm_t<BK, BN, true, true>(tmA, tmB, tmR, colsum, st, y, acc_dump,
+    return dump ? launch_gemm_t<BK, BN, true, true>(tmA, tmB, tmR, colsum, st, y, acc_dump,
+                                                    bias, relu, g, s)
+                : launch_gemm_t<BK, BN, true, false>(tmA, tmB, tmR, colsum, st, y, acc_dump,
+                                                     bias, relu, g, s);
+  return dump ? launch_gemm_t<BK, BN, false, true>(tmA, tmB, tmR, colsum, st, y, acc_dump,
                                                    bias, relu, g, s)
-               : launch_gemm_t<BK, BN, true, false>(tmA, tmB, tmR, colsum, st, y, acc_dump,
+              : launch_gemm_t<BK, BN, false, false>(tmA, tmB, tmR, colsum, st, y, acc_dump,
                                                     bias, relu, g, s);
-  return epi ? launch_gemm_t<BK, BN, false, true>(tmA, tmB, tmR, colsum, st, y, acc_dump,
-                                                  bias, relu, g, s)
-             : launch_gemm_t<BK, BN, false, false>(tmA, tmB, tmR, colsum, st, y, acc_dump,
-                                                   bias, relu, g, s);
 }
 
 cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmR,
