@@ -59,7 +59,10 @@ struct GemmCfg {
   static constexpr int kAccBufs = (512 / kGroupCols) < 4 ? (512 / kGroupCols) : 4;
   static constexpr int kFPT = BN / 4;             // filters per epilogue thread
   static constexpr uint32_t kRsBytes = 16 * kBM * 4;  // row sums of one tile [16][128] i32
-  static constexpr size_t kFixed = 1024 /*align*/ + 2 * kRsBytes + 16 * 8 /*barriers, holder*/;
+  // Output staging: per lane quadrant 32 tiles x 2 pixels x BN filters fp32.
+  static constexpr uint32_t kOutBytes = 4 * 32 * 2 * BN * 4;
+  static constexpr size_t kFixed =
+      1024 /*align*/ + 2 * kRsBytes + kOutBytes + 16 * 8 /*barriers, holder*/;
 };
 
 template <int BK, int BN>
@@ -137,7 +140,8 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   const int stages = g.stages;
   uint8_t* stage_base = smem;
   int32_t* s_rs = reinterpret_cast<int32_t*>(smem + static_cast<size_t>(stages) * Cfg::kStageBytes);
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(s_rs + 2 * 16 * kBM);
+  float* s_out = reinterpret_cast<float*>(s_rs + 2 * 16 * kBM);  // [4 quadrants][64 segs][BN]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(s_out + Cfg::kOutBytes / 4);
   uint64_t* empty_bar = full_bar + stages;
   uint64_t* acc_full = empty_bar + stages;  // [4]
   uint64_t* acc_empty = acc_full + 4;       // [4]
@@ -289,24 +293,27 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       const int kf0 = n0 + f0;
       // Output pixels of this lane's tile (2ti + a, 2tj + b) and their
       // validity (merge_tiles discards the ceil-overhang, tensor.hpp:172-175).
-      float* ybase;
-      int pmask;
+      int pix0, pmask;
       {
         const int mm = row_ok ? m : 0;
         const int img = mm / g.P;
         const int tt = mm - img * g.P;
         const int ti = tt / g.TW, tj = tt - ti * g.TW;
-        const int pix0 = (img * g.OH + 2 * ti) * g.OW + 2 * tj;
-        ybase = y + static_cast<long long>(pix0) * g.K + kf0;
+        pix0 = (img * g.OH + 2 * ti) * g.OW + 2 * tj;
         const bool r1 = 2 * ti + 1 < g.OH, c1 = 2 * tj + 1 < g.OW;
         pmask = row_ok ? (1 | (c1 ? 2 : 0) | (r1 ? 4 : 0) | (r1 && c1 ? 8 : 0)) : 0;
       }
-      const int row_stride = g.OW * g.K;  // one output row, in floats
-      // Store this thread's FPT filters of output pixel ab (0..3).
-      auto store_pixel = [&](int ab, float2 (&v)[FPT / 2]) {
-        if (!((pmask >> ab) & 1)) return;
-        float* d = ybase + (ab >> 1) * row_stride + (ab & 1) * g.K;
-        if (bias != nullptr || relu) {
+      // Output pixels (a = 0, b) and (a = 1, b) of the quadrant's 32 tiles:
+      // each thread stages its FPT filters (bias / ReLU / +0 applied) into the
+      // quadrant's swizzled buffer [64 segments = (tile, a)][BN filters], then
+      // the quadrant's 4 warps write whole BN-filter segments (8 lanes per 128
+      // bytes) instead of one scattered 16-byte piece per lane.
+      auto store_col = [&](int b, float2 (&v0)[FPT / 2], float2 (&v1)[FPT / 2]) {
+        constexpr int CPR = BN / 4;  // 16-byte chunks per segment
+        float* stg = s_out + q * (64 * BN);
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          float2(&v)[FPT / 2] = a ? v1 : v0;
 #pragma unroll
           for (int i = 0; i < FPT / 2; ++i) {
             if (bias != nullptr)
@@ -316,22 +323,40 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
               v[i].x = fmaxf(v[i].x, 0.0f);
               v[i].y = fmaxf(v[i].y, 0.0f);
             }
+            v[i] = add2(v[i], bcast2(0.0f));  // the reference never yields -0
           }
-        }
+          const int seg = 2 * lane + a;
 #pragma unroll
-        for (int i = 0; i < FPT / 2; ++i) v[i] = add2(v[i], bcast2(0.0f));  // the reference never yields -0
-        if (k4ok && kf0 + FPT <= g.K) {
-#pragma unroll
-          for (int i = 0; i < FPT / 4; ++i)
-            *reinterpret_cast<float4*>(d + 4 * i) =
+          for (int i = 0; i < FPT / 4; ++i) {
+            const int chunk = ((f0 >> 2) + i) ^ (lane & (CPR - 1));
+            *reinterpret_cast<float4*>(stg + seg * BN + chunk * 4) =
                 make_float4(v[2 * i].x, v[2 * i].y, v[2 * i + 1].x, v[2 * i + 1].y);
-        } else {
-#pragma unroll
-          for (int i = 0; i < FPT / 2; ++i) {
-            if (kf0 + 2 * i < g.K) d[2 * i] = v[i].x;
-            if (kf0 + 2 * i + 1 < g.K) d[2 * i + 1] = v[i].y;
           }
         }
+        named_bar_sync(2 + q, 128);
+        const int wq = ew >> 2;  // warp within the quadrant
+#pragma unroll
+        for (int k = 0; k < (64 * CPR) / 128; ++k) {
+          const int id = wq * 32 + lane + 128 * k;
+          const int seg = id / CPR, cc = id % CPR;
+          const int tile = seg >> 1, a = seg & 1;
+          const int tpix = __shfl_sync(0xffffffffu, pix0, tile);
+          const int tmask = __shfl_sync(0xffffffffu, pmask, tile);
+          const int kf = n0 + cc * 4;
+          if (!((tmask >> (2 * a + b)) & 1) || kf >= g.K) continue;
+          const float4 val = *reinterpret_cast<const float4*>(
+              stg + seg * BN + ((cc ^ (tile & (CPR - 1))) * 4));
+          float* d = y + static_cast<long long>(tpix + a * g.OW + b) * g.K + kf;
+          if (k4ok && kf + 4 <= g.K) {
+            *reinterpret_cast<float4*>(d) = val;
+          } else {
+            const float e4[4] = {val.x, val.y, val.z, val.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (kf + e < g.K) d[e] = e4[e];
+          }
+        }
+        named_bar_sync(2 + q, 128);  // staging buffer free again
       };
       const uint32_t rb = lt & 1u;
       const int32_t* rs_tile = s_rs + rb * 16 * kBM + row;
@@ -404,13 +429,10 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
             }
           }
         }
-        if (j == 2) {
-          store_pixel(0, S[0]);  // S00 and S10 are final after T_2
-          store_pixel(2, S[2]);
-        } else if (j == 3) {
-          store_pixel(1, S[1]);
-          store_pixel(3, S[3]);
-        }
+        if (j == 2)
+          store_col(0, S[0], S[2]);  // S00 and S10 are final after T_2
+        else if (j == 3)
+          store_col(1, S[1], S[3]);
       }
     }
   }
