@@ -341,6 +341,8 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   gg.num_kchunks = p->C_pad / p->BK;
   gg.num_n_tiles = p->K_pad / p->BN;
   gg.stages = 0;  // chosen by the launcher
+  gg.exp = 0;
+  if (const char* e = std::getenv("LANCE_GEMM_EXP")) gg.exp = std::atoi(e);
 
   const size_t codes_a_bytes = static_cast<size_t>(16) * p->M * p->C_pad;
   const size_t codes_w_bytes = static_cast<size_t>(16) * p->K_pad * p->C_pad;

@@ -252,6 +252,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
               const uint32_t sb = sa + Cfg::kABytes;
 #pragma unroll
               for (int kk = 0; kk < BK / 32; ++kk) {
+                if (g.exp & 2) break;
                 const uint64_t adesc = umma_smem_desc(sa + kk * 32, 8 * BK, Cfg::kLayout);
                 const uint64_t bdesc = umma_smem_desc(sb + kk * 32, 8 * BK, Cfg::kLayout);
                 umma_i8(d_base + static_cast<uint32_t>(a * BN), adesc, bdesc, kIdesc,
@@ -314,17 +315,20 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
           float2(&v)[FPT / 2] = a ? v1 : v0;
+          if (bias != nullptr || relu) {  // fused epilogue (uniform branch)
 #pragma unroll
-          for (int i = 0; i < FPT / 2; ++i) {
-            if (bias != nullptr)
-              v[i] = add2(v[i], make_float2(kf0 + 2 * i < g.K ? __ldg(bias + kf0 + 2 * i) : 0.0f,
-                                            kf0 + 2 * i + 1 < g.K ? __ldg(bias + kf0 + 2 * i + 1) : 0.0f));
-            if (relu) {
-              v[i].x = fmaxf(v[i].x, 0.0f);
-              v[i].y = fmaxf(v[i].y, 0.0f);
+            for (int i = 0; i < FPT / 2; ++i) {
+              if (bias != nullptr)
+                v[i] = add2(v[i], make_float2(kf0 + 2 * i < g.K ? __ldg(bias + kf0 + 2 * i) : 0.0f,
+                                              kf0 + 2 * i + 1 < g.K ? __ldg(bias + kf0 + 2 * i + 1) : 0.0f));
+              if (relu) {
+                v[i].x = fmaxf(v[i].x, 0.0f);
+                v[i].y = fmaxf(v[i].y, 0.0f);
+              }
             }
-            v[i] = add2(v[i], bcast2(0.0f));  // the reference never yields -0
           }
+#pragma unroll
+          for (int i = 0; i < FPT / 2; ++i) v[i] = add2(v[i], bcast2(0.0f));  // the reference never yields -0
           const int seg = 2 * lane + a;
 #pragma unroll
           for (int i = 0; i < FPT / 4; ++i) {
@@ -335,17 +339,18 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         }
         named_bar_sync(2 + q, 128);
         const int wq = ew >> 2;  // warp within the quadrant
+        // Chunk id = wq * 32 + lane + 128 k: segment id / CPR, chunk id % CPR.
+        const int cc = lane % CPR;
 #pragma unroll
         for (int k = 0; k < (64 * CPR) / 128; ++k) {
-          const int id = wq * 32 + lane + 128 * k;
-          const int seg = id / CPR, cc = id % CPR;
+          const int seg = (wq * 32 + lane + 128 * k) / CPR;
           const int tile = seg >> 1, a = seg & 1;
           const int tpix = __shfl_sync(0xffffffffu, pix0, tile);
           const int tmask = __shfl_sync(0xffffffffu, pmask, tile);
           const int kf = n0 + cc * 4;
-          if (!((tmask >> (2 * a + b)) & 1) || kf >= g.K) continue;
           const float4 val = *reinterpret_cast<const float4*>(
               stg + seg * BN + ((cc ^ (tile & (CPR - 1))) * 4));
+          if (!((tmask >> (2 * a + b)) & 1) || kf >= g.K) continue;
           float* d = y + static_cast<long long>(tpix + a * g.OW + b) * g.K + kf;
           if (k4ok && kf + 4 <= g.K) {
             *reinterpret_cast<float4*>(d) = val;
@@ -402,6 +407,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
                   acc_dump[(static_cast<long long>(4 * a + j) * g.M + m) * g.K + kf0 + 4 * c + i] =
                       static_cast<int32_t>(ac[a][i]);
           }
+          if (g.exp & 1) continue;
           float2 T0[2], T1[2];
           affine_group4(ac, fast, k1s, k4, rterm, s_cterm + j * K_pad + kf0 + 4 * c, K_pad, T0, T1);
 #pragma unroll
@@ -429,6 +435,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
             }
           }
         }
+        if (g.exp & 1) continue;
         if (j == 2)
           store_col(0, S[0], S[2]);  // S00 and S10 are final after T_2
         else if (j == 3)

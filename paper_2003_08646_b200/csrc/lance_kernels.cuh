@@ -53,6 +53,7 @@ struct GemmGeom {
   int num_kchunks;  // C_pad / BK
   int num_n_tiles;  // K_pad / BN
   int stages;       // shared-memory ring depth (set by the launcher)
+  int exp;          // experiment switches (LANCE_GEMM_EXP, profiling only; 0 = normal)
 };
 
 struct StaticParams {
