@@ -98,25 +98,6 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// [16][rows][C_pad] u8, box = BK bytes x box_rows x 1, swizzle = BK bytes.
-int make_code_map(CUtensorMap* map, void* base, long long rows, int c_pad, int bk, int box_rows) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn) return fail(LANCE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(c_pad), static_cast<cuuint64_t>(rows), 16};
-  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(c_pad),
-                                 static_cast<cuuint64_t>(rows) * c_pad};
-  const cuuint32_t box[3] = {static_cast<cuuint32_t>(bk), static_cast<cuuint32_t>(box_rows), 1};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  const CUtensorMapSwizzle sw = bk == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                          : (bk == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                                      : CU_TENSOR_MAP_SWIZZLE_32B);
-  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(LANCE_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
-  return LANCE_OK;
-}
-
 // Row sums [16][rows] int32; box = 128 rows x 16 positions (OOB rows read 0).
 int make_rowsum_map(CUtensorMap* map, void* base, long long rows, long long pitch) {
   EncodeTiledFn fn = encode_fn();
@@ -158,7 +139,7 @@ struct lance_plan_s {
   float* partials = nullptr;    // [max(range_grid, filter_grid)][32]
   LanceDevState* state = nullptr;
   size_t bytes = 0;
-  CUtensorMap tmA{}, tmB{}, tmR{};
+  CUtensorMap tmR{};
   bool filters_ready = false;
   int32_t* acc_dump = nullptr;
   const float* bias = nullptr;
@@ -307,6 +288,8 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   g.C_pad = p->C_pad;
   g.pad = spec->pad;
   g.nchunks = (p->C_pad + kChunk - 1) / kChunk;
+  g.a_bk = p->BK;
+  g.a_nk = p->C_pad / p->BK;
   // Warp strips: whole tile rows unless that leaves too few warps to fill
   // 148 SMs x 32 warps; then halve the strip length.
   g.seg_len = p->TW;
@@ -327,6 +310,9 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   f.K_pad = p->K_pad;
   f.C_pad = p->C_pad;
   f.granularity = cfg->granularity;
+  f.bk = p->BK;
+  f.bn = p->BN;
+  f.nk = p->C_pad / p->BK;
   const long long kc = static_cast<long long>(spec->k) * spec->c;
   p->filter_grid = static_cast<int>(std::min<long long>((kc + 255) / 256, 2LL * p->sm_count));
 
@@ -344,7 +330,8 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   gg.exp = 0;
   if (const char* e = std::getenv("LANCE_GEMM_EXP")) gg.exp = std::atoi(e);
 
-  const size_t codes_a_bytes = static_cast<size_t>(16) * p->M * p->C_pad;
+  // Operand images cover whole 128-row blocks; rows >= M stay code 0.
+  const size_t codes_a_bytes = static_cast<size_t>(16) * ((p->M + kBM - 1) / kBM * kBM) * p->C_pad;
   const size_t codes_w_bytes = static_cast<size_t>(16) * p->K_pad * p->C_pad;
   const int part_rows = std::max(p->range_grid, p->filter_grid);
   if ((rc = dev_alloc(p, &p->codes_a, codes_a_bytes)) ||
@@ -372,9 +359,7 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
     delete p;
     return cuda_fail(e, "plan init");
   }
-  if ((rc = make_code_map(&p->tmA, p->codes_a, p->M, p->C_pad, p->BK, kBM)) ||
-      (rc = make_code_map(&p->tmB, p->codes_w, p->K_pad, p->C_pad, p->BK, p->BN)) ||
-      (rc = make_rowsum_map(&p->tmR, p->rowsum, p->M, p->rs_pitch))) {
+  if ((rc = make_rowsum_map(&p->tmR, p->rowsum, p->M, p->rs_pitch))) {
     free_plan(p);
     delete p;
     return rc;
@@ -443,7 +428,7 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
                                 static_params != nullptr, s));
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[2], s));
-  LANCE_CUDA(launch_gemm(&p->tmA, &p->tmB, &p->tmR, p->BK, p->BN, p->small_acc, p->colsum, p->state, y_dev,
+  LANCE_CUDA(launch_gemm(p->codes_a, p->codes_w, &p->tmR, p->BK, p->BN, p->small_acc, p->colsum, p->state, y_dev,
                          p->acc_dump, p->bias, p->relu, p->gemm_geom, s));
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[3], s));
@@ -531,10 +516,17 @@ int lance_plan_debug_read(lance_plan_t p, int what, void* dst, size_t bytes) {
   const long long M = p->M;
   const int C = p->spec.c, K = p->spec.k;
   switch (what) {
-    case LANCE_DBG_CODES_A: {
+    case LANCE_DBG_CODES_A: {  // device UMMA images -> reference [16][M][C]
       if (bytes != size_t(16) * M * C) return fail(LANCE_ERR_INVALID_ARGUMENT, "bad size");
-      LANCE_CUDA(cudaMemcpy2D(dst, C, p->codes_a, p->C_pad, C, size_t(16) * M,
-                              cudaMemcpyDeviceToHost));
+      std::string tmp(size_t(16) * ((M + kBM - 1) / kBM * kBM) * p->C_pad, '\0');
+      LANCE_CUDA(cudaMemcpy(tmp.data(), p->codes_a, tmp.size(), cudaMemcpyDeviceToHost));
+      auto* out = static_cast<uint8_t*>(dst);
+      const int nk = p->C_pad / p->BK;
+      for (int q = 0; q < 16; ++q)
+        for (long long m = 0; m < M; ++m)
+          for (int c = 0; c < C; ++c)
+            out[(size_t(q) * M + m) * C + c] =
+                static_cast<uint8_t>(tmp[umma_image_offset(m, c, q, kBM, p->BK, nk)]);
       return LANCE_OK;
     }
     case LANCE_DBG_ROWSUM: {
@@ -543,16 +535,17 @@ int lance_plan_debug_read(lance_plan_t p, int what, void* dst, size_t bytes) {
                               sizeof(int32_t) * M, 16, cudaMemcpyDeviceToHost));
       return LANCE_OK;
     }
-    case LANCE_DBG_CODES_W: {  // device [16][K_pad][C_pad] -> reference [16][C][K]
+    case LANCE_DBG_CODES_W: {  // device UMMA images -> reference [16][C][K]
       if (bytes != size_t(16) * C * K) return fail(LANCE_ERR_INVALID_ARGUMENT, "bad size");
       std::string tmp(size_t(16) * p->K_pad * p->C_pad, '\0');
       LANCE_CUDA(cudaMemcpy(tmp.data(), p->codes_w, tmp.size(), cudaMemcpyDeviceToHost));
       auto* out = static_cast<uint8_t*>(dst);
+      const int nk = p->C_pad / p->BK;
       for (int q = 0; q < 16; ++q)
         for (int c = 0; c < C; ++c)
           for (int k = 0; k < K; ++k)
             out[(size_t(q) * C + c) * K + k] =
-                static_cast<uint8_t>(tmp[(size_t(q) * p->K_pad + k) * p->C_pad + c]);
+                static_cast<uint8_t>(tmp[umma_image_offset(k, c, q, p->BN, p->BK, nk)]);
       return LANCE_OK;
     }
     case LANCE_DBG_COLSUM: {

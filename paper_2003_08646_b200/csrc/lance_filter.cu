@@ -46,7 +46,8 @@ __global__ void __launch_bounds__(256) filter_transform_kernel(const float* __re
   }
 }
 
-// K2b: codes_w [16][K_pad][C_pad] (K-major B operand) and column sums [16][K_pad].
+// K2b: codes_w as the B operand's UMMA images (lance_kernels.cuh) and column
+// sums [16][K_pad].
 __global__ void __launch_bounds__(128) filter_quant_kernel(const float* __restrict__ u_tmp,
                                                            uint8_t* __restrict__ codes_w,
                                                            int32_t* __restrict__ colsum,
@@ -62,7 +63,7 @@ __global__ void __launch_bounds__(128) filter_quant_kernel(const float* __restri
     for (int c = threadIdx.x; c < g.C; c += blockDim.x) {
       const uint32_t code =
           quantize_code(u_tmp[p * slice + static_cast<long long>(k) * g.C + c], tmin, scale, top);
-      codes_w[(static_cast<long long>(p) * g.K_pad + k) * g.C_pad + c] = static_cast<uint8_t>(code);
+      codes_w[umma_image_offset(k, c, p, g.bn, g.bk, g.nk)] = static_cast<uint8_t>(code);
       sum += static_cast<int>(code);
     }
 #pragma unroll

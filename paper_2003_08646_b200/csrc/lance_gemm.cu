@@ -116,8 +116,8 @@ __device__ __forceinline__ void tmem_ld_group4(uint32_t addr, int bn, uint32_t (
 // (parity tests).  bias / relu: fused epilogue (north-star extension).
 template <int BK, int BN, bool SMALL, bool DUMP>
 __global__ void __launch_bounds__(kGemmThreadsP, 1)
-    gemm_epilogue_kernel(const __grid_constant__ CUtensorMap tmA,
-                         const __grid_constant__ CUtensorMap tmB,
+    gemm_epilogue_kernel(const uint8_t* __restrict__ codes_a,
+                         const uint8_t* __restrict__ codes_w,
                          const __grid_constant__ CUtensorMap tmR,
                          const int32_t* __restrict__ colsum,
                          const LanceDevState* __restrict__ st, float* __restrict__ y,
@@ -196,14 +196,16 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      tma_prefetch_desc(&tmA);
-      tma_prefetch_desc(&tmB);
       tma_prefetch_desc(&tmR);
       int s = 0;
       uint32_t ph = 0;
       uint32_t lt = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
-        const int m0 = (t / nt) * kBM, n0 = (t % nt) * BN;
+        const int mt = t / nt, ntile = t % nt;
+        const int m0 = mt * kBM;
+        // Operand images of this tile (lance_kernels.cuh umma_image_offset).
+        const uint8_t* a_tile = codes_a + static_cast<long long>(mt) * 16 * nk * Cfg::kABytes;
+        const uint8_t* b_tile = codes_w + static_cast<long long>(ntile) * 16 * nk * Cfg::kBBytes;
         // Row sums of the tile's 128 rows for all 16 positions (OOB rows read 0).
         const uint32_t rb = lt & 1u;
         mbar_wait(&rs_empty[rb], ((lt >> 1) & 1u) ^ 1u);
@@ -216,8 +218,9 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
               mbar_wait(&empty_bar[s], ph ^ 1u);
               uint8_t* sa = stage_base + static_cast<size_t>(s) * Cfg::kStageBytes;
               mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
-              tma_load_3d(sa, &tmA, kc * BK, m0, p, &full_bar[s]);
-              tma_load_3d(sa + Cfg::kABytes, &tmB, kc * BK, n0, p, &full_bar[s]);
+              bulk_load(sa, a_tile + (p * nk + kc) * Cfg::kABytes, Cfg::kABytes, &full_bar[s]);
+              bulk_load(sa + Cfg::kABytes, b_tile + (p * nk + kc) * Cfg::kBBytes, Cfg::kBBytes,
+                        &full_bar[s]);
               if (++s == stages) {
                 s = 0;
                 ph ^= 1u;
@@ -451,7 +454,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
 }
 
 template <int BK, int BN, bool SMALL, bool DUMP>
-static cudaError_t launch_gemm_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
+static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
                                  const CUtensorMap* tmR, const int32_t* colsum,
                                  const LanceDevState* st, float* y, int32_t* acc_dump,
                                  const float* bias, int relu, const GemmGeom& g0, cudaStream_t s) {
@@ -482,34 +485,34 @@ static cudaError_t launch_gemm_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
   const long long tiles = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * g.num_n_tiles;
   const int grid = static_cast<int>(tiles < sms ? tiles : sms);
   gemm_epilogue_kernel<BK, BN, SMALL, DUMP><<<grid, kGemmThreadsP, smem, s>>>(
-      *tmA, *tmB, *tmR, colsum, st, y, acc_dump, bias, relu, g);
+      codes_a, codes_w, *tmR, colsum, st, y, acc_dump, bias, relu, g);
   return cudaGetLastError();
 }
 
 template <int BK, int BN>
-static cudaError_t launch_gemm_bk(const CUtensorMap* tmA, const CUtensorMap* tmB, int small_acc,
+static cudaError_t launch_gemm_bk(const uint8_t* codes_a, const uint8_t* codes_w, int small_acc,
                                   const CUtensorMap* tmR, const int32_t* colsum,
                                   const LanceDevState* st, float* y, int32_t* acc_dump,
                                   const float* bias, int relu, const GemmGeom& g, cudaStream_t s) {
   const bool dump = acc_dump != nullptr;
   if (small_acc)
-    return dump ? launch_gemm_t<BK, BN, true, true>(tmA, tmB, tmR, colsum, st, y, acc_dump,
+    return dump ? launch_gemm_t<BK, BN, true, true>(codes_a, codes_w, tmR, colsum, st, y, acc_dump,
                                                     bias, relu, g, s)
-                : launch_gemm_t<BK, BN, true, false>(tmA, tmB, tmR, colsum, st, y, acc_dump,
+                : launch_gemm_t<BK, BN, true, false>(codes_a, codes_w, tmR, colsum, st, y, acc_dump,
                                                      bias, relu, g, s);
-  return dump ? launch_gemm_t<BK, BN, false, true>(tmA, tmB, tmR, colsum, st, y, acc_dump,
+  return dump ? launch_gemm_t<BK, BN, false, true>(codes_a, codes_w, tmR, colsum, st, y, acc_dump,
                                                    bias, relu, g, s)
-              : launch_gemm_t<BK, BN, false, false>(tmA, tmB, tmR, colsum, st, y, acc_dump,
+              : launch_gemm_t<BK, BN, false, false>(codes_a, codes_w, tmR, colsum, st, y, acc_dump,
                                                     bias, relu, g, s);
 }
 
-cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmR,
+cudaError_t launch_gemm(const uint8_t* codes_a, const uint8_t* codes_w, const CUtensorMap* tmR,
                         int bk, int bn, int small_acc, const int32_t* colsum,
                         const LanceDevState* st, float* y, int32_t* acc_dump, const float* bias,
                         int relu, const GemmGeom& g, cudaStream_t s) {
 #define LANCE_GEMM_CASE(BKV, BNV)                                                            \
   if (bk == BKV && bn == BNV)                                                                \
-    return launch_gemm_bk<BKV, BNV>(tmA, tmB, small_acc, tmR, colsum, st, y, acc_dump,       \
+    return launch_gemm_bk<BKV, BNV>(codes_a, codes_w, small_acc, tmR, colsum, st, y, acc_dump, \
                                     bias, relu, g, s);
   LANCE_GEMM_CASE(128, 64)
   LANCE_GEMM_CASE(64, 64)

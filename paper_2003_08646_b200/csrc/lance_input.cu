@@ -233,7 +233,9 @@ __global__ void __launch_bounds__(256, 2) input_quant_kernel(const float* __rest
   const bool lane_on = it.ch < g.C;
   const bool two = it.ch + 1 < g.C;
   const Strip<VEC2> sp(x, g, it);
-  const long long pstride = static_cast<long long>(g.M) * g.C_pad;
+  // Codes go to the A operand's UMMA images (lance_kernels.cuh): position
+  // planes are nk images apart within a 128-row block.
+  const long long pstride = static_cast<long long>(g.a_nk) * kBM * g.a_bk;
   float2 ta[4], tb[4], tc[4], td[4], pc[4], pd[4];
   int xx = 2 * it.tj0 - g.pad;
   if (lane_on) {
@@ -259,7 +261,7 @@ __global__ void __launch_bounds__(256, 2) input_quant_kernel(const float* __rest
         tb[a] = td[a];
       }
     }
-    uint8_t* dst = codes + static_cast<long long>(m) * g.C_pad + it.ch;
+    uint8_t* dst = codes + umma_image_offset(m, it.ch, 0, kBM, g.a_bk, g.a_nk);
     uint32_t mine = 0u;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {

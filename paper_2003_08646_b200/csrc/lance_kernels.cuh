@@ -33,6 +33,8 @@ struct InGeom {
   int H, W, C;    // image dims, channels
   int C_pad;      // code row pitch (multiple of 32)
   int rs_pitch;   // row-sum plane pitch (M rounded up to 4: 16-byte TMA strides)
+  int a_bk;       // GEMM K chunk (32, 64 or 128 channels): codes are stored as UMMA images
+  int a_nk;       // C_pad / a_bk
   int pad;
   int nchunks;    // ceil(C_pad / kChunk)
   int seg_len;    // tiles per warp strip (a tile row is split into nseg strips)
@@ -44,6 +46,7 @@ struct InGeom {
 struct FilterGeom {
   int K, C, K_pad, C_pad;
   int granularity;
+  int bk, bn, nk;  // UMMA image geometry of the B operand (see umma_image_offset)
 };
 
 struct GemmGeom {
@@ -55,6 +58,27 @@ struct GemmGeom {
   int stages;       // shared-memory ring depth (set by the launcher)
   int exp;          // experiment switches (LANCE_GEMM_EXP, profiling only; 0 = normal)
 };
+
+// Operand codes are stored in global memory exactly as the GEMM's shared-memory
+// stages hold them, so one contiguous bulk copy fills a stage: the operand
+// [rows][C_pad] u8 is cut into images of `rows_per_img` rows x bk channels
+// (128 for A, BN for B), each image K-major with the UMMA / TMA swizzle of a
+// bk-byte row (SWIZZLE_128B / 64B / 32B: 16-byte chunk c of row r sits at
+// chunk c ^ f(r), i.e. byte bit 4+ ^= bits 7+), ordered
+// [row block][position 0..15][k chunk][image].
+__host__ __device__ __forceinline__ uint32_t umma_swizzle(uint32_t lin, int bk) {
+  const uint32_t mask = bk == 128 ? 7u : (bk == 64 ? 3u : 1u);
+  return lin ^ (((lin >> 7) & mask) << 4);
+}
+__host__ __device__ __forceinline__ long long umma_image_offset(long long row, int c, int p,
+                                                                 int rows_per_img, int bk,
+                                                                 int nk) {
+  const long long blk = row / rows_per_img;
+  const int r = static_cast<int>(row - blk * rows_per_img);
+  const int kc = c / bk, cb = c - kc * bk;
+  return ((blk * 16 + p) * nk + kc) * static_cast<long long>(rows_per_img * bk) +
+         umma_swizzle(static_cast<uint32_t>(r * bk + cb), bk);
+}
 
 struct StaticParams {
   float tmin[kPositions], tmax[kPositions], scale[kPositions];
@@ -73,7 +97,7 @@ cudaError_t launch_filter_prepare(const float* w, float* u_tmp, float* partials,
                                   uint8_t* codes_w, int32_t* colsum, LanceDevState* st,
                                   const FilterGeom& g, cudaStream_t s);
 // bn: filters per GEMM tile (16, 32 or 64); TMEM holds two j-groups of 4 x bn columns.
-cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmR,
+cudaError_t launch_gemm(const uint8_t* codes_a, const uint8_t* codes_w, const CUtensorMap* tmR,
                         int bk, int bn, int small_acc, const int32_t* colsum,
                         const LanceDevState* st, float* y, int32_t* acc_dump, const float* bias,
                         int relu, const GemmGeom& g, cudaStream_t s);
