@@ -107,6 +107,11 @@ __device__ __forceinline__ void affine_group4(const uint32_t (&acc)[4][4], bool 
   }
 }
 
+// Profiling trace (LANCE_GEMM_TRACE): CTA 0 records globaltimer-free SM clocks.
+__device__ __forceinline__ void trace_event(unsigned long long* tr, int slot, int i) {
+  if (tr != nullptr && blockIdx.x == 0 && i < 100000) tr[slot * 100000 + i] = clock64();
+}
+
 __device__ __forceinline__ void tmem_ld_group4(uint32_t addr, int bn, uint32_t (&acc)[4][4]) {
 #pragma unroll
   for (int a = 0; a < 4; ++a) tmem_ld_x4(addr + a * bn, acc[a]);
@@ -200,6 +205,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       int s = 0;
       uint32_t ph = 0;
       uint32_t lt = 0;
+      int pst = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
         const int mt = t / nt, ntile = t % nt;
         const int m0 = mt * kBM;
@@ -221,6 +227,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
               bulk_load(sa, a_tile + (p * nk + kc) * Cfg::kABytes, Cfg::kABytes, &full_bar[s]);
               bulk_load(sa + Cfg::kABytes, b_tile + (p * nk + kc) * Cfg::kBBytes, Cfg::kBBytes,
                         &full_bar[s]);
+              trace_event(g.trace, 0, pst++);
               if (++s == stages) {
                 s = 0;
                 ph ^= 1u;
@@ -241,15 +248,18 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       int s = 0;
       uint32_t ph = 0;
       uint32_t grp = 0;
+      int mst = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         for (int j = 0; j < 4; ++j, ++grp) {
           const uint32_t buf = grp % NB;
-          mbar_wait(&acc_empty[buf], (grp / NB) & 1u);  // epilogue drained (and re-armed) it
+          mbar_wait(&acc_empty[buf], (grp / NB) & 1u);  // epilogue drained it
+          trace_event(g.trace, 2, grp);
           tc_fence_after();
           const uint32_t d_base = tmem_base + buf * Cfg::kGroupCols;
           for (int a = 0; a < 4; ++a) {
             for (int kc = 0; kc < nk; ++kc) {
               mbar_wait(&full_bar[s], ph);
+              trace_event(g.trace, 1, mst++);
               tc_fence_after();
               const uint32_t sa = smem_u32(stage_base + static_cast<size_t>(s) * Cfg::kStageBytes);
               const uint32_t sb = sa + Cfg::kABytes;
@@ -386,6 +396,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
           if (lane == 0) mbar_arrive(&rs_empty[rb]);
         }
         mbar_wait(&acc_full[buf], (grp / NB) & 1u);
+        if (ew == 0 && lane == 0) trace_event(g.trace, 3, grp);
         tc_fence_after();
         const uint32_t acc_addr = lane_base + buf * Cfg::kGroupCols + f0;
 #pragma unroll
@@ -400,6 +411,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[buf]);
+            if (ew == 0 && lane == 0) trace_event(g.trace, 4, grp);
           }
           if (DUMP && row_ok) {
 #pragma unroll
