@@ -66,8 +66,8 @@ struct GemmCfg {
 };
 
 template <int BK, int BN>
-__host__ __device__ constexpr size_t gemm_smem_bytes(int stages, int k_pad) {
-  return GemmCfg<BK, BN>::kFixed + static_cast<size_t>(stages) * GemmCfg<BK, BN>::kStageBytes +
+__host__ __device__ constexpr size_t gemm_smem_bytes(int stages, int ups, int k_pad) {
+  return GemmCfg<BK, BN>::kFixed + static_cast<size_t>(stages) * ups * GemmCfg<BK, BN>::kStageBytes +
          static_cast<size_t>(stages) * 16 + static_cast<size_t>(16) * k_pad * 4;
 }
 
@@ -143,8 +143,10 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   // not generic loads).
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stages = g.stages;
+  const int ups = g.ups;  // (position, k chunk) units per stage
+  const uint32_t stage_bytes = ups * Cfg::kStageBytes;
   uint8_t* stage_base = smem;
-  int32_t* s_rs = reinterpret_cast<int32_t*>(smem + static_cast<size_t>(stages) * Cfg::kStageBytes);
+  int32_t* s_rs = reinterpret_cast<int32_t*>(smem + static_cast<size_t>(stages) * stage_bytes);
   float* s_out = reinterpret_cast<float*>(s_rs + 2 * 16 * kBM);  // [4 quadrants][64 segs][BN]
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(s_out + Cfg::kOutBytes / 4);
   uint64_t* empty_bar = full_bar + stages;
@@ -217,23 +219,21 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         mbar_wait(&rs_empty[rb], ((lt >> 1) & 1u) ^ 1u);
         mbar_arrive_expect_tx(&rs_full[rb], Cfg::kRsBytes);
         tma_load_2d(s_rs + rb * 16 * kBM, &tmR, m0, 0, &rs_full[rb]);
-        for (int j = 0; j < 4; ++j)
-          for (int a = 0; a < 4; ++a) {
-            const int p = 4 * a + j;
-            for (int kc = 0; kc < nk; ++kc) {
-              mbar_wait(&empty_bar[s], ph ^ 1u);
-              uint8_t* sa = stage_base + static_cast<size_t>(s) * Cfg::kStageBytes;
-              mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
-              bulk_load(sa, a_tile + (p * nk + kc) * Cfg::kABytes, Cfg::kABytes, &full_bar[s]);
-              bulk_load(sa + Cfg::kABytes, b_tile + (p * nk + kc) * Cfg::kBBytes, Cfg::kBBytes,
-                        &full_bar[s]);
-              trace_event(g.trace, 0, pst++);
-              if (++s == stages) {
-                s = 0;
-                ph ^= 1u;
-              }
-            }
+        // The tile's 16 * nk (position, k chunk) units are contiguous in j-major
+        // order; a stage is `ups` consecutive units (one bulk copy per operand).
+        for (int u0 = 0; u0 < 16 * nk; u0 += ups) {
+          mbar_wait(&empty_bar[s], ph ^ 1u);
+          uint8_t* sa = stage_base + static_cast<size_t>(s) * stage_bytes;
+          mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
+          bulk_load(sa, a_tile + u0 * Cfg::kABytes, ups * Cfg::kABytes, &full_bar[s]);
+          bulk_load(sa + ups * Cfg::kABytes, b_tile + u0 * Cfg::kBBytes, ups * Cfg::kBBytes,
+                    &full_bar[s]);
+          trace_event(g.trace, 0, pst++);
+          if (++s == stages) {
+            s = 0;
+            ph ^= 1u;
           }
+        }
       }
     }
   } else if (warp == 1) {
@@ -249,36 +249,43 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       uint32_t ph = 0;
       uint32_t grp = 0;
       int mst = 0;
+      const int upg = 4 * nk;  // units per j-group
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        for (int j = 0; j < 4; ++j, ++grp) {
-          const uint32_t buf = grp % NB;
-          mbar_wait(&acc_empty[buf], (grp / NB) & 1u);  // epilogue drained it
-          trace_event(g.trace, 2, grp);
+        for (int u0 = 0; u0 < 16 * nk; u0 += ups) {
+          mbar_wait(&full_bar[s], ph);
+          trace_event(g.trace, 1, mst++);
           tc_fence_after();
-          const uint32_t d_base = tmem_base + buf * Cfg::kGroupCols;
-          for (int a = 0; a < 4; ++a) {
-            for (int kc = 0; kc < nk; ++kc) {
-              mbar_wait(&full_bar[s], ph);
-              trace_event(g.trace, 1, mst++);
+          const uint32_t sa = smem_u32(stage_base + static_cast<size_t>(s) * stage_bytes);
+          const uint32_t sb = sa + ups * Cfg::kABytes;
+          for (int ui = 0; ui < ups; ++ui) {
+            const int u = u0 + ui;
+            const int a = (u / nk) & 3, kc = u % nk;
+            const uint32_t buf = grp % NB;
+            if (u % upg == 0) {  // first unit of a j-group: its TMEM buffer must be drained
+              mbar_wait(&acc_empty[buf], (grp / NB) & 1u);
+              trace_event(g.trace, 2, grp);
               tc_fence_after();
-              const uint32_t sa = smem_u32(stage_base + static_cast<size_t>(s) * Cfg::kStageBytes);
-              const uint32_t sb = sa + Cfg::kABytes;
+            }
+            const uint32_t d = tmem_base + buf * Cfg::kGroupCols + static_cast<uint32_t>(a * BN);
 #pragma unroll
-              for (int kk = 0; kk < BK / 32; ++kk) {
-                if (g.exp & 2) break;
-                const uint64_t adesc = umma_smem_desc(sa + kk * 32, 8 * BK, Cfg::kLayout);
-                const uint64_t bdesc = umma_smem_desc(sb + kk * 32, 8 * BK, Cfg::kLayout);
-                umma_i8(d_base + static_cast<uint32_t>(a * BN), adesc, bdesc, kIdesc,
-                        (kc > 0 || kk > 0) ? 1u : 0u);
-              }
-              umma_commit(&empty_bar[s]);
-              if (++s == stages) {
-                s = 0;
-                ph ^= 1u;
-              }
+            for (int kk = 0; kk < BK / 32; ++kk) {
+              if (g.exp & 2) break;
+              const uint64_t adesc =
+                  umma_smem_desc(sa + ui * Cfg::kABytes + kk * 32, 8 * BK, Cfg::kLayout);
+              const uint64_t bdesc =
+                  umma_smem_desc(sb + ui * Cfg::kBBytes + kk * 32, 8 * BK, Cfg::kLayout);
+              umma_i8(d, adesc, bdesc, kIdesc, (kc > 0 || kk > 0) ? 1u : 0u);
+            }
+            if (u % upg == upg - 1) {  // last unit of the j-group
+              umma_commit(&acc_full[buf]);
+              ++grp;
             }
           }
-          umma_commit(&acc_full[buf]);
+          umma_commit(&empty_bar[s]);
+          if (++s == stages) {
+            s = 0;
+            ph ^= 1u;
+          }
         }
       }
     }
@@ -472,9 +479,17 @@ static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
                                  const float* bias, int relu, const GemmGeom& g0, cudaStream_t s) {
   GemmGeom g = g0;
   const int k_pad = g.num_n_tiles * BN;
+  // Stages of ~32-40 KB: the producer's per-stage issue cost (~500 cycles)
+  // must stay well below the stage's HBM time.
+  const int units = 16 * g.num_kchunks;
+  int ups = 1;
+  while (ups * 2 <= 4 && units % (ups * 2) == 0 &&
+         ups * 2 * GemmCfg<BK, BN>::kStageBytes <= 40 * 1024)
+    ups *= 2;
   int stages = 16;
-  while (stages > 2 && gemm_smem_bytes<BK, BN>(stages, k_pad) > kSmemLimit) --stages;
-  const size_t smem = gemm_smem_bytes<BK, BN>(stages, k_pad);
+  while (stages > 2 && gemm_smem_bytes<BK, BN>(stages, ups, k_pad) > kSmemLimit) --stages;
+  const size_t smem = gemm_smem_bytes<BK, BN>(stages, ups, k_pad);
+  g.ups = ups;
   if (smem > kSmemLimit) return cudaErrorInvalidValue;
   g.stages = stages;
   static size_t configured[64] = {};  // dynamic-smem attribute set so far, per device

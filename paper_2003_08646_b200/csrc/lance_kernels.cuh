@@ -56,6 +56,7 @@ struct GemmGeom {
   int num_kchunks;  // C_pad / BK
   int num_n_tiles;  // K_pad / BN
   int stages;       // shared-memory ring depth (set by the launcher)
+  int ups;          // (position, k chunk) units per stage (set by the launcher)
   int exp;          // experiment switches (LANCE_GEMM_EXP, profiling only; 0 = normal)
   unsigned long long* trace;  // CTA-0 event timestamps (LANCE_GEMM_TRACE, profiling only)
 };
@@ -66,7 +67,8 @@ struct GemmGeom {
 // (128 for A, BN for B), each image K-major with the UMMA / TMA swizzle of a
 // bk-byte row (SWIZZLE_128B / 64B / 32B: 16-byte chunk c of row r sits at
 // chunk c ^ f(r), i.e. byte bit 4+ ^= bits 7+), ordered
-// [row block][position 0..15][k chunk][image].
+// [row block][j][a][k chunk][image] for position p = 4a + j (j-major: the
+// GEMM consumes positions in j-groups, and a stage copies consecutive units).
 __host__ __device__ __forceinline__ uint32_t umma_swizzle(uint32_t lin, int bk) {
   const uint32_t mask = bk == 128 ? 7u : (bk == 64 ? 3u : 1u);
   return lin ^ (((lin >> 7) & mask) << 4);
@@ -77,7 +79,8 @@ __host__ __device__ __forceinline__ long long umma_image_offset(long long row, i
   const long long blk = row / rows_per_img;
   const int r = static_cast<int>(row - blk * rows_per_img);
   const int kc = c / bk, cb = c - kc * bk;
-  return ((blk * 16 + p) * nk + kc) * static_cast<long long>(rows_per_img * bk) +
+  const int pj = (p & 3) * 4 + (p >> 2);
+  return ((blk * 16 + pj) * nk + kc) * static_cast<long long>(rows_per_img * bk) +
          umma_swizzle(static_cast<uint32_t>(r * bk + cb), bk);
 }
 
