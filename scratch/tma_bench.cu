@@ -9,15 +9,20 @@
 #include "../paper_2003_08646_b200/csrc/lance_ptx.cuh"
 using namespace lance_dev;
 
-__global__ void __launch_bounds__(128, 1) stream_kernel(const uint8_t* src, size_t bytes, int stage_bytes,
-                                                        int stages, int mode, unsigned long long* sink) {
+__global__ void __launch_bounds__(640, 1) stream_kernel(const uint8_t* src, size_t bytes, int stage_bytes,
+                                                        int stages, int mode, unsigned long long* sink,
+                                                        size_t wrap) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
   uint64_t* empty = full + stages;
   __shared__ uint32_t holder;
+  __shared__ uint64_t spin_bar;
+  __shared__ volatile int done;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(&spin_bar, 1);
+    done = 0;
     fence_barrier_init();
   }
   if (warp == 1) { tmem_alloc(&holder, 32); tmem_relinquish(); }
@@ -30,7 +35,10 @@ __global__ void __launch_bounds__(128, 1) stream_kernel(const uint8_t* src, size
     for (size_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
       mbar_wait(&empty[s], ph ^ 1u);
       mbar_arrive_expect_tx(&full[s], stage_bytes);
-      bulk_load(smem + (size_t)s * stage_bytes, src + c * stage_bytes, stage_bytes, &full[s]);
+      const int pieces = mode >= 2 ? 4 : 1;  // mode 2/3: the stage as 4 separate copies
+      for (int pc = 0; pc < pieces; ++pc)
+        bulk_load(smem + (size_t)s * stage_bytes + pc * (stage_bytes / pieces),
+                  src + (c * stage_bytes) % wrap + pc * (stage_bytes / pieces), stage_bytes / pieces, &full[s]);
       if (++s == stages) { s = 0; ph ^= 1u; }
     }
   } else if (warp == 1 && lane == 0) {
@@ -43,6 +51,12 @@ __global__ void __launch_bounds__(128, 1) stream_kernel(const uint8_t* src, size
       if (++s == stages) { s = 0; ph ^= 1u; }
     }
     sink[blockIdx.x] = acc;
+    done = 1;
+  } else if (warp >= 4 && (mode & 1)) {
+    // mode 1/3: 16 warps spin on a barrier that completes only at the end.
+    while (!mbar_try_wait(smem_u32(&spin_bar), 0u)) {
+      if (done) break;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -58,19 +72,23 @@ int main() {
   cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   const int sizes[] = {8192, 16384, 32768};
-  const int depths[] = {2, 4, 8, 16};
-  for (int mode = 0; mode < 2; ++mode)
+  const int depths[] = {4, 8, 16};
+  const size_t wraps[] = {bytes, size_t(32) << 20};
+  const char* names[] = {"plain", "spin16", "split4", "split4+spin16"};
+  for (size_t wrap : wraps)
+  for (int mode = 0; mode < 4; ++mode)
     for (int sb : sizes)
       for (int d : depths) {
         const size_t smem = (size_t)d * sb + 2 * d * 8 + 64;
         if (smem > 200 * 1024) continue;
-        stream_kernel<<<sms, 128, smem>>>(src, bytes, sb, d, mode, sink);
+        const int thr = (mode & 1) ? 640 : 128;
+        stream_kernel<<<sms, thr, smem>>>(src, bytes, sb, d, mode, sink, wrap);
         cudaEventRecord(e0);
-        for (int r = 0; r < 3; ++r) stream_kernel<<<sms, 128, smem>>>(src, bytes, sb, d, mode, sink);
+        for (int r = 0; r < 3; ++r) stream_kernel<<<sms, thr, smem>>>(src, bytes, sb, d, mode, sink, wrap);
         cudaEventRecord(e1); cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1);
-        printf("mode=%s stage=%6d depth=%2d : %7.0f GB/s  (%s)\n", mode ? "commit" : "arrive", sb, d,
-               3.0 * bytes / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+        printf("%s %-14s stage=%6d depth=%2d : %7.0f GB/s  (%s)\n", wrap == bytes ? "HBM" : "L2 ",
+               names[mode], sb, d, 3.0 * bytes / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
       }
   return 0;
 }
