@@ -38,6 +38,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "lance_common.cuh"
 
@@ -223,6 +224,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         // order; a stage is `ups` consecutive units (one bulk copy per operand).
         for (int u0 = 0; u0 < 16 * nk; u0 += ups) {
           mbar_wait(&empty_bar[s], ph ^ 1u);
+          trace_event(g.trace, 2, pst);
           uint8_t* sa = stage_base + static_cast<size_t>(s) * stage_bytes;
           mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
           bulk_load(sa, a_tile + u0 * Cfg::kABytes, ups * Cfg::kABytes, &full_bar[s]);
@@ -263,7 +265,6 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
             const uint32_t buf = grp % NB;
             if (u % upg == 0) {  // first unit of a j-group: its TMEM buffer must be drained
               mbar_wait(&acc_empty[buf], (grp / NB) & 1u);
-              trace_event(g.trace, 2, grp);
               tc_fence_after();
             }
             const uint32_t d = tmem_base + buf * Cfg::kGroupCols + static_cast<uint32_t>(a * BN);
@@ -483,9 +484,9 @@ static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
   // must stay well below the stage's HBM time.
   const int units = 16 * g.num_kchunks;
   int ups = 1;
-  while (ups * 2 <= 4 && units % (ups * 2) == 0 &&
-         ups * 2 * GemmCfg<BK, BN>::kStageBytes <= 40 * 1024)
-    ups *= 2;
+  int ups_cap = 1;
+  if (const char* e = std::getenv("LANCE_GEMM_UPS")) ups_cap = std::atoi(e);
+  while (ups * 2 <= ups_cap && units % (ups * 2) == 0) ups *= 2;
   int stages = 16;
   while (stages > 2 && gemm_smem_bytes<BK, BN>(stages, ups, k_pad) > kSmemLimit) --stages;
   const size_t smem = gemm_smem_bytes<BK, BN>(stages, ups, k_pad);

@@ -1,4 +1,4 @@
-"""Summarise a GEMM CTA-0 trace: slots 0 producer issue / 1 MMA full-ready / 2 MMA acc-empty-ready /
+"""Summarise a GEMM CTA-0 trace: slots 0 producer issued / 1 MMA full-ready / 2 producer slot-free /
 3 epilogue acc-full-ready / 4 epilogue release (clock64 cycles)."""
 import sys
 import numpy as np
@@ -15,8 +15,9 @@ m = min(len(prod), len(full))
 print("stage latency (issue->ready)  median %d  p90 %d" % (np.median(full[:m] - prod[:m]), np.percentile(full[:m] - prod[:m], 90)))
 g = min(len(afull), len(rel), len(aempty))
 print("group: epi ready->release median %d; group interval %d" % (np.median(rel[:g] - afull[:g]), np.median(d(afull))))
-print("MMA waited for acc-empty: median gap ready-vs-first-stage? first 12 groups:")
-print(" acc_empty_ready", aempty[:12])
+g2=min(len(prod),len(aempty))
+print("producer: slot-free -> issued median %d; issued -> next slot-free median %d" % (np.median(prod[:g2]-aempty[:g2]), np.median(aempty[1:g2]-prod[:g2-1])))
+print(" slot_free first 20", aempty[:20])
 print(" epi_acc_full   ", afull[:12])
 print(" epi_release    ", rel[:12])
 print(" prod first 20  ", prod[:20])
