@@ -35,10 +35,20 @@ __global__ void __launch_bounds__(640, 1) stream_kernel(const uint8_t* src, size
     for (size_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
       mbar_wait(&empty[s], ph ^ 1u);
       mbar_arrive_expect_tx(&full[s], stage_bytes);
-      const int pieces = mode >= 2 ? 4 : 1;  // mode 2/3: the stage as 4 separate copies
-      for (int pc = 0; pc < pieces; ++pc)
-        bulk_load(smem + (size_t)s * stage_bytes + pc * (stage_bytes / pieces),
-                  src + (c * stage_bytes) % wrap + pc * (stage_bytes / pieces), stage_bytes / pieces, &full[s]);
+      // mode 0: one copy; mode 1: 4/5 of the stage streamed + 1/5 from a shared
+      // 64 KB region (all CTAs); mode 2: stage as 2 copies, both streamed.
+      const size_t off = c * (size_t)stage_bytes;
+      if (mode == 0) {
+        bulk_load(smem + (size_t)s * stage_bytes, src + off, stage_bytes, &full[s]);
+      } else if (mode == 1) {
+        const int a = stage_bytes / 5 * 4 / 16 * 16, b = stage_bytes - a;
+        bulk_load(smem + (size_t)s * stage_bytes, src + off, a, &full[s]);
+        bulk_load(smem + (size_t)s * stage_bytes + a, src + (c * b) % 65536, b, &full[s]);
+      } else {
+        const int a = stage_bytes / 5 * 4 / 16 * 16, b = stage_bytes - a;
+        bulk_load(smem + (size_t)s * stage_bytes, src + off, a, &full[s]);
+        bulk_load(smem + (size_t)s * stage_bytes + a, src + off + a, b, &full[s]);
+      }
       if (++s == stages) { s = 0; ph ^= 1u; }
     }
   } else if (warp == 1 && lane == 0) {
@@ -52,7 +62,7 @@ __global__ void __launch_bounds__(640, 1) stream_kernel(const uint8_t* src, size
     }
     sink[blockIdx.x] = acc;
     done = 1;
-  } else if (warp >= 4 && (mode & 1)) {
+  } else if (warp >= 4 && mode == 7) {
     // mode 1/3: 16 warps spin on a barrier that completes only at the end.
     while (!mbar_try_wait(smem_u32(&spin_bar), 0u)) {
       if (done) break;
@@ -71,17 +81,18 @@ int main() {
   int sms = 148; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  const int sizes[] = {8192, 16384, 32768};
+  const int sizes[] = {10240, 20480, 40960};
   const int depths[] = {4, 8, 16};
-  const size_t wraps[] = {bytes, size_t(32) << 20};
-  const char* names[] = {"plain", "spin16", "split4", "split4+spin16"};
+  const size_t wraps[] = {bytes};
+  const char* names[] = {"one copy", "A+sharedB", "two copies"};
   for (size_t wrap : wraps)
-  for (int mode = 0; mode < 4; ++mode)
+  for (int mode = 0; mode < 3; ++mode)
     for (int sb : sizes)
       for (int d : depths) {
         const size_t smem = (size_t)d * sb + 2 * d * 8 + 64;
         if (smem > 200 * 1024) continue;
-        const int thr = (mode & 1) ? 640 : 128;
+        (void)wrap;
+        const int thr = 128;
         stream_kernel<<<sms, thr, smem>>>(src, bytes, sb, d, mode, sink, wrap);
         cudaEventRecord(e0);
         for (int r = 0; r < 3; ++r) stream_kernel<<<sms, thr, smem>>>(src, bytes, sb, d, mode, sink, wrap);
