@@ -344,6 +344,8 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   gg.exp = 0;
   if (const char* e = std::getenv("LANCE_GEMM_EXP")) gg.exp = std::atoi(e);
   gg.trace = nullptr;
+  gg.prefetch = 1;
+  if (const char* e = std::getenv("LANCE_GEMM_PF")) gg.prefetch = std::atoi(e);
 
   // Operand images cover whole 128-row blocks; rows >= M stay code 0.
   const size_t codes_a_bytes = static_cast<size_t>(16) * ((p->M + kBM - 1) / kBM * kBM) * p->C_pad;

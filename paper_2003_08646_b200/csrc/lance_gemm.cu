@@ -215,6 +215,17 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         // Operand images of this tile (lance_kernels.cuh umma_image_offset).
         const uint8_t* a_tile = codes_a + static_cast<long long>(mt) * 16 * nk * Cfg::kABytes;
         const uint8_t* b_tile = codes_w + static_cast<long long>(ntile) * 16 * nk * Cfg::kBBytes;
+        // Prefetch the next tile's operand images into L2 so its stage copies
+        // hit L2 (bulk copies that miss to HBM have a long per-copy latency).
+        if (g.prefetch && t + static_cast<int>(gridDim.x) < num_tiles) {
+          const int t2 = t + gridDim.x;
+          const uint8_t* a2 = codes_a + static_cast<long long>(t2 / nt) * 16 * nk * Cfg::kABytes;
+          const uint8_t* b2 = codes_w + static_cast<long long>(t2 % nt) * 16 * nk * Cfg::kBBytes;
+          for (int jg = 0; jg < 4; ++jg) {
+            bulk_prefetch_l2(a2 + jg * 4 * nk * Cfg::kABytes, 4 * nk * Cfg::kABytes);
+            bulk_prefetch_l2(b2 + jg * 4 * nk * Cfg::kBBytes, 4 * nk * Cfg::kBBytes);
+          }
+        }
         // Row sums of the tile's 128 rows for all 16 positions (OOB rows read 0).
         const uint32_t rb = lt & 1u;
         mbar_wait(&rs_empty[rb], ((lt >> 1) & 1u) ^ 1u);

@@ -57,6 +57,7 @@ struct GemmGeom {
   int num_n_tiles;  // K_pad / BN
   int stages;       // shared-memory ring depth (set by the launcher)
   int ups;          // (position, k chunk) units per stage (set by the launcher)
+  int prefetch;     // L2-prefetch the next tile's operand images (LANCE_GEMM_PF, default 1)
   int exp;          // experiment switches (LANCE_GEMM_EXP, profiling only; 0 = normal)
   unsigned long long* trace;  // CTA-0 event timestamps (LANCE_GEMM_TRACE, profiling only)
 };

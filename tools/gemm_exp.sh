@@ -6,7 +6,9 @@ TAG=${1:-exp}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
-for cfg in "EXP=0" "EXP=1" "EXP=2" "EXP=3" "BN=64" "BN=64 EXP=1" "BN=16"; do
+CFG_LIST=${CFG_LIST:-"EXP=0;EXP=1;EXP=2;EXP=3;BN=64;BN=64 EXP=1;BN=16"}
+IFS=';' read -ra CFGS <<< "$CFG_LIST"
+for cfg in "${CFGS[@]}"; do
   envs=""
   for kv in $cfg; do envs="$envs LANCE_GEMM_$kv"; done
   echo "== $cfg" >> $OUT/exp.txt
