@@ -110,7 +110,13 @@ __device__ __forceinline__ void affine_group4(const uint32_t (&acc)[4][4], bool 
 
 // Profiling trace (LANCE_GEMM_TRACE): CTA 0 records globaltimer-free SM clocks.
 __device__ __forceinline__ void trace_event(unsigned long long* tr, int slot, int i) {
+#ifdef LANCE_GEMM_TRACE
   if (tr != nullptr && blockIdx.x == 0 && i < 100000) tr[slot * 100000 + i] = clock64();
+#else
+  (void)tr;
+  (void)slot;
+  (void)i;
+#endif
 }
 
 __device__ __forceinline__ void tmem_ld_group4(uint32_t addr, int bn, uint32_t (&acc)[4][4]) {
@@ -146,6 +152,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   const int stages = g.stages;
   const int ups = g.ups;  // (position, k chunk) units per stage
   const uint32_t stage_bytes = ups * Cfg::kStageBytes;
+  const int nstage_tile = 16 * g.num_kchunks / ups;  // stages per tile
   uint8_t* stage_base = smem;
   int32_t* s_rs = reinterpret_cast<int32_t*>(smem + static_cast<size_t>(stages) * stage_bytes);
   float* s_out = reinterpret_cast<float*>(s_rs + 2 * 16 * kBM);  // [4 quadrants][64 segs][BN]
@@ -233,14 +240,18 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         tma_load_2d(s_rs + rb * 16 * kBM, &tmR, m0, 0, &rs_full[rb]);
         // The tile's 16 * nk (position, k chunk) units are contiguous in j-major
         // order; a stage is `ups` consecutive units (one bulk copy per operand).
-        for (int u0 = 0; u0 < 16 * nk; u0 += ups) {
+        const uint8_t* pa = a_tile;
+        const uint8_t* pb = b_tile;
+        const uint32_t abytes = ups * Cfg::kABytes, bbytes = ups * Cfg::kBBytes;
+        for (int st = 0; st < nstage_tile; ++st) {
           mbar_wait(&empty_bar[s], ph ^ 1u);
           trace_event(g.trace, 2, pst);
           uint8_t* sa = stage_base + static_cast<size_t>(s) * stage_bytes;
           mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
-          bulk_load(sa, a_tile + u0 * Cfg::kABytes, ups * Cfg::kABytes, &full_bar[s]);
-          bulk_load(sa + ups * Cfg::kABytes, b_tile + u0 * Cfg::kBBytes, ups * Cfg::kBBytes,
-                    &full_bar[s]);
+          bulk_load(sa, pa, abytes, &full_bar[s]);
+          bulk_load(sa + abytes, pb, bbytes, &full_bar[s]);
+          pa += abytes;
+          pb += bbytes;
           trace_event(g.trace, 0, pst++);
           if (++s == stages) {
             s = 0;
@@ -262,23 +273,24 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       uint32_t ph = 0;
       uint32_t grp = 0;
       int mst = 0;
-      const int upg = 4 * nk;  // units per j-group
+      int a = 0, kc = 0;  // position within the j-group and k chunk of the next unit
+      uint32_t d_base = tmem_base;
+      uint32_t buf = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        for (int u0 = 0; u0 < 16 * nk; u0 += ups) {
+        for (int st = 0; st < nstage_tile; ++st) {
           mbar_wait(&full_bar[s], ph);
           trace_event(g.trace, 1, mst++);
           tc_fence_after();
           const uint32_t sa = smem_u32(stage_base + static_cast<size_t>(s) * stage_bytes);
           const uint32_t sb = sa + ups * Cfg::kABytes;
           for (int ui = 0; ui < ups; ++ui) {
-            const int u = u0 + ui;
-            const int a = (u / nk) & 3, kc = u % nk;
-            const uint32_t buf = grp % NB;
-            if (u % upg == 0) {  // first unit of a j-group: its TMEM buffer must be drained
+            if (a == 0 && kc == 0) {  // first unit of a j-group: its TMEM buffer must be drained
+              buf = grp % NB;
               mbar_wait(&acc_empty[buf], (grp / NB) & 1u);
               tc_fence_after();
+              d_base = tmem_base + buf * Cfg::kGroupCols;
             }
-            const uint32_t d = tmem_base + buf * Cfg::kGroupCols + static_cast<uint32_t>(a * BN);
+            const uint32_t d = d_base + static_cast<uint32_t>(a * BN);
 #pragma unroll
             for (int kk = 0; kk < BK / 32; ++kk) {
               if (g.exp & 2) break;
@@ -288,9 +300,13 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
                   umma_smem_desc(sb + ui * Cfg::kBBytes + kk * 32, 8 * BK, Cfg::kLayout);
               umma_i8(d, adesc, bdesc, kIdesc, (kc > 0 || kk > 0) ? 1u : 0u);
             }
-            if (u % upg == upg - 1) {  // last unit of the j-group
-              umma_commit(&acc_full[buf]);
-              ++grp;
+            if (++kc == nk) {
+              kc = 0;
+              if (++a == 4) {  // j-group complete
+                a = 0;
+                umma_commit(&acc_full[buf]);
+                ++grp;
+              }
             }
           }
           umma_commit(&empty_bar[s]);
@@ -493,11 +509,10 @@ static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
   const int k_pad = g.num_n_tiles * BN;
   // Stages of ~32-40 KB: the producer's per-stage issue cost (~500 cycles)
   // must stay well below the stage's HBM time.
-  const int units = 16 * g.num_kchunks;
   int ups = 1;
   int ups_cap = 1;
   if (const char* e = std::getenv("LANCE_GEMM_UPS")) ups_cap = std::atoi(e);
-  while (ups * 2 <= ups_cap && units % (ups * 2) == 0) ups *= 2;
+  while (ups * 2 <= ups_cap && (4 * g.num_kchunks) % (ups * 2) == 0) ups *= 2;
   int stages = 16;
   while (stages > 2 && gemm_smem_bytes<BK, BN>(stages, ups, k_pad) > kSmemLimit) --stages;
   const size_t smem = gemm_smem_bytes<BK, BN>(stages, ups, k_pad);
