@@ -21,7 +21,7 @@ LIB = os.path.join(OUT_DIR, "liblance_b200.so")
 SOURCES = ["lance_input.cu", "lance_filter.cu", "lance_gemm.cu", "lance_abi.cu"]
 HEADERS = ["lance_common.cuh", "lance_kernels.cuh", "lance_ptx.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
+FLAGS = ["-DLANCE_JMAJOR=" + os.environ.get("LANCE_JMAJOR", "0"), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
          "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "-I" + os.path.join(ROOT, "include")]
 

@@ -240,18 +240,24 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         tma_load_2d(s_rs + rb * 16 * kBM, &tmR, m0, 0, &rs_full[rb]);
         // The tile's 16 * nk (position, k chunk) units are contiguous in j-major
         // order; a stage is `ups` consecutive units (one bulk copy per operand).
-        const uint8_t* pa = a_tile;
-        const uint8_t* pb = b_tile;
         const uint32_t abytes = ups * Cfg::kABytes, bbytes = ups * Cfg::kBBytes;
+        int ua = 0, ukc = 0, uj = 0;  // unit (a, kc) of j-group uj, consumed j-major
         for (int st = 0; st < nstage_tile; ++st) {
           mbar_wait(&empty_bar[s], ph ^ 1u);
           trace_event(g.trace, 2, pst);
           uint8_t* sa = stage_base + static_cast<size_t>(s) * stage_bytes;
           mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
-          bulk_load(sa, pa, abytes, &full_bar[s]);
-          bulk_load(sa + abytes, pb, bbytes, &full_bar[s]);
-          pa += abytes;
-          pb += bbytes;
+          const int u = (image_plane(4 * ua + uj) * nk + ukc);
+          bulk_load(sa, a_tile + u * Cfg::kABytes, abytes, &full_bar[s]);
+          bulk_load(sa + abytes, b_tile + u * Cfg::kBBytes, bbytes, &full_bar[s]);
+          ukc += ups;
+          while (ukc >= nk) {
+            ukc -= nk;
+            if (++ua == 4) {
+              ua = 0;
+              ++uj;
+            }
+          }
           trace_event(g.trace, 0, pst++);
           if (++s == stages) {
             s = 0;
@@ -512,7 +518,11 @@ static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
   int ups = 1;
   int ups_cap = 1;
   if (const char* e = std::getenv("LANCE_GEMM_UPS")) ups_cap = std::atoi(e);
-  while (ups * 2 <= ups_cap && (4 * g.num_kchunks) % (ups * 2) == 0) ups *= 2;
+  // A stage's units must be contiguous images: j-major planes allow any
+  // divisor of the j-group's 4 * nk units, p-major planes only of nk.
+  while (ups * 2 <= ups_cap &&
+         (kJMajorImages ? (4 * g.num_kchunks) % (ups * 2) : g.num_kchunks % (ups * 2)) == 0)
+    ups *= 2;
   int stages = 16;
   while (stages > 2 && gemm_smem_bytes<BK, BN>(stages, ups, k_pad) > kSmemLimit) --stages;
   const size_t smem = gemm_smem_bytes<BK, BN>(stages, ups, k_pad);

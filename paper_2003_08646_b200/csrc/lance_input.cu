@@ -314,10 +314,8 @@ __global__ void __launch_bounds__(256, 2) input_quant_kernel(const float* __rest
         // Codes: 64 contiguous bytes per warp per position (the A operand row).
         // position planes in j-major image order (umma_image_offset)
         const int p0 = 2 * k, p1 = 2 * k + 1;
-        *reinterpret_cast<uint16_t*>(dst + ((p0 & 3) * 4 + (p0 >> 2)) * pstride) =
-            static_cast<uint16_t>(pk[0]);
-        *reinterpret_cast<uint16_t*>(dst + ((p1 & 3) * 4 + (p1 >> 2)) * pstride) =
-            static_cast<uint16_t>(pk[1]);
+        *reinterpret_cast<uint16_t*>(dst + image_plane(p0) * pstride) = static_cast<uint16_t>(pk[0]);
+        *reinterpret_cast<uint16_t*>(dst + image_plane(p1) * pstride) = static_cast<uint16_t>(pk[1]);
       }
       // Row sums (lowpgemm.hpp:121-123): the lane's two codes of positions
       // (2k, 2k+1) as 16-bit halves, one warp reduction (REDUX) per pair.

@@ -7,6 +7,10 @@
 
 #include <cstdint>
 
+#ifndef LANCE_JMAJOR
+#define LANCE_JMAJOR 0
+#endif
+
 namespace lance_dev {
 
 constexpr int kPositions = 16;  // (m + r - 1)^2 for F(2x2,3x3)
@@ -70,6 +74,11 @@ struct GemmGeom {
 // chunk c ^ f(r), i.e. byte bit 4+ ^= bits 7+), ordered
 // [row block][j][a][k chunk][image] for position p = 4a + j (j-major: the
 // GEMM consumes positions in j-groups, and a stage copies consecutive units).
+// Plane order of the 16 positions inside a row block (kJMajorImages: j-major).
+constexpr bool kJMajorImages = LANCE_JMAJOR;
+__host__ __device__ __forceinline__ constexpr int image_plane(int p) {
+  return kJMajorImages ? (p & 3) * 4 + (p >> 2) : p;
+}
 __host__ __device__ __forceinline__ uint32_t umma_swizzle(uint32_t lin, int bk) {
   const uint32_t mask = bk == 128 ? 7u : (bk == 64 ? 3u : 1u);
   return lin ^ (((lin >> 7) & mask) << 4);
@@ -80,7 +89,7 @@ __host__ __device__ __forceinline__ long long umma_image_offset(long long row, i
   const long long blk = row / rows_per_img;
   const int r = static_cast<int>(row - blk * rows_per_img);
   const int kc = c / bk, cb = c - kc * bk;
-  const int pj = (p & 3) * 4 + (p >> 2);
+  const int pj = image_plane(p);
   return ((blk * 16 + pj) * nk + kc) * static_cast<long long>(rows_per_img * bk) +
          umma_swizzle(static_cast<uint32_t>(r * bk + cb), bk);
 }
