@@ -12,7 +12,7 @@ import threading
 
 from . import build as _build
 
-LIB_PATH = _build.LIB
+LIB_PATH = os.environ.get("LANCE_LIB_PATH", _build.LIB)  # override: A/B experiments only
 
 LANCE_OK = 0
 LANCE_ERR_INVALID_ARGUMENT = 1

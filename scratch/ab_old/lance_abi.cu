@@ -164,20 +164,6 @@ struct DeviceGuard {
 };
 
 void free_plan(lance_plan_s* p) {
-  if (p->gemm_geom.trace != nullptr) {
-    if (const char* path = std::getenv("LANCE_GEMM_TRACE")) {
-      std::vector<unsigned long long> h(500000);
-      if (cudaMemcpy(h.data(), p->gemm_geom.trace, h.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess) {
-        const std::string f = std::string(path) + "_c" + std::to_string(p->spec.c) + "_h" +
-                              std::to_string(p->spec.h) + ".bin";
-        if (FILE* fp = std::fopen(f.c_str(), "wb")) {
-          std::fwrite(h.data(), 8, h.size(), fp);
-          std::fclose(fp);
-        }
-      }
-    }
-    cudaFree(p->gemm_geom.trace);
-  }
   for (cudaEvent_t e : p->events) cudaEventDestroy(e);
   p->events.clear();
   cudaFree(p->codes_a);
@@ -269,10 +255,10 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   p->P = p->TH * p->TW;
   p->M = static_cast<long long>(spec->n) * p->P;
   p->C_pad = round_up(spec->c, 32);
-  // GEMM tile width: 64 filters (two j-group accumulators of 4 x 64 TMEM
-  // columns, 16 filters' S partials per epilogue thread) unless the layer has
-  // fewer.  LANCE_GEMM_BN overrides.
-  p->BN = spec->k > 32 ? 64 : (spec->k > 16 ? 32 : 16);
+  // GEMM tile width: 32 filters (four j-group accumulators of 4 x 32 TMEM
+  // columns, 8 S partials per epilogue thread) unless the layer has fewer.
+  // LANCE_GEMM_BN overrides (64: two j-group buffers, 16 partials per thread).
+  p->BN = spec->k > 16 ? 32 : 16;
   if (const char* e = std::getenv("LANCE_GEMM_BN")) {
     const int v = std::atoi(e);
     if (v == 16 || v == 32 || v == 64) p->BN = v;
@@ -343,8 +329,6 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   gg.stages = 0;  // chosen by the launcher
   gg.exp = 0;
   if (const char* e = std::getenv("LANCE_GEMM_EXP")) gg.exp = std::atoi(e);
-  gg.trace = nullptr;
-  gg.b_resident = 0;
 
   // Operand images cover whole 128-row blocks; rows >= M stay code 0.
   const size_t codes_a_bytes = static_cast<size_t>(16) * ((p->M + kBM - 1) / kBM * kBM) * p->C_pad;
@@ -374,12 +358,6 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
     free_plan(p);
     delete p;
     return cuda_fail(e, "plan init");
-  }
-  if (std::getenv("LANCE_GEMM_TRACE") != nullptr &&
-      (rc = dev_alloc(p, &p->gemm_geom.trace, sizeof(unsigned long long) * 500000))) {
-    free_plan(p);
-    delete p;
-    return rc;
   }
   if ((rc = make_rowsum_map(&p->tmR, p->rowsum, p->M, p->rs_pitch))) {
     free_plan(p);

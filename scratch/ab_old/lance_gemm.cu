@@ -38,18 +38,13 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <cstdlib>
 
 #include "lance_common.cuh"
 
 namespace lance_dev {
 
-constexpr int kEpiWarps = 16;                      // warps 0..15: epilogue (4 warpgroups)
-constexpr int kProducerWarp = 16, kMmaWarp = 17;  // warpgroup 4: producer, MMA, 2 idle
-constexpr int kGemmThreadsP = 32 * 20;            // 640
-// Register split (setmaxnreg): the control warpgroup gives its registers to
-// the epilogue warpgroups (S partials of 64-filter tiles live in registers).
-constexpr int kCtrlRegs = 32, kEpiRegs = 112;
+constexpr int kEpiWarps = 16;
+constexpr int kGemmThreadsP = 64 + 32 * kEpiWarps;  // 576
 constexpr size_t kSmemLimit = 225 * 1024;           // dynamic part, leaves room for static smem
 constexpr float kTwo23 = 8388608.0f;
 constexpr float kTwo126 = 8.507059173023462e37f;   // 2^126
@@ -70,14 +65,9 @@ struct GemmCfg {
       1024 /*align*/ + 2 * kRsBytes + kOutBytes + 16 * 8 /*barriers, holder*/;
 };
 
-// b_res: the whole B operand of the (single) filter tile stays resident in
-// shared memory and stages carry only A.
 template <int BK, int BN>
-__host__ __device__ constexpr size_t gemm_smem_bytes(int stages, int nk, int b_res, int k_pad) {
-  return GemmCfg<BK, BN>::kFixed +
-         static_cast<size_t>(stages) *
-             (b_res ? GemmCfg<BK, BN>::kABytes : GemmCfg<BK, BN>::kStageBytes) +
-         (b_res ? static_cast<size_t>(16) * nk * GemmCfg<BK, BN>::kBBytes : 0) +
+__host__ __device__ constexpr size_t gemm_smem_bytes(int stages, int k_pad) {
+  return GemmCfg<BK, BN>::kFixed + static_cast<size_t>(stages) * GemmCfg<BK, BN>::kStageBytes +
          static_cast<size_t>(stages) * 16 + static_cast<size_t>(16) * k_pad * 4;
 }
 
@@ -117,17 +107,6 @@ __device__ __forceinline__ void affine_group4(const uint32_t (&acc)[4][4], bool 
   }
 }
 
-// Profiling trace (LANCE_GEMM_TRACE): CTA 0 records globaltimer-free SM clocks.
-__device__ __forceinline__ void trace_event(unsigned long long* tr, int slot, int i) {
-#ifdef LANCE_GEMM_TRACE
-  if (tr != nullptr && blockIdx.x == 0 && i < 100000) tr[slot * 100000 + i] = clock64();
-#else
-  (void)tr;
-  (void)slot;
-  (void)i;
-#endif
-}
-
 __device__ __forceinline__ void tmem_ld_group4(uint32_t addr, int bn, uint32_t (&acc)[4][4]) {
 #pragma unroll
   for (int a = 0; a < 4; ++a) tmem_ld_x4(addr + a * bn, acc[a]);
@@ -159,12 +138,8 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   // not generic loads).
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stages = g.stages;
-  const int nk = g.num_kchunks;
-  const bool b_res = g.b_resident != 0;
-  const uint32_t stage_bytes = b_res ? Cfg::kABytes : Cfg::kStageBytes;
   uint8_t* stage_base = smem;
-  uint8_t* b_base = smem + static_cast<size_t>(stages) * stage_bytes;  // resident B images
-  int32_t* s_rs = reinterpret_cast<int32_t*>(b_base + (b_res ? 16 * nk * Cfg::kBBytes : 0));
+  int32_t* s_rs = reinterpret_cast<int32_t*>(smem + static_cast<size_t>(stages) * Cfg::kStageBytes);
   float* s_out = reinterpret_cast<float*>(s_rs + 2 * 16 * kBM);  // [4 quadrants][64 segs][BN]
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(s_out + Cfg::kOutBytes / 4);
   uint64_t* empty_bar = full_bar + stages;
@@ -172,14 +147,14 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   uint64_t* acc_empty = acc_full + 4;       // [4]
   uint64_t* rs_full = acc_empty + 4;        // [2]
   uint64_t* rs_empty = rs_full + 2;         // [2]
-  uint64_t* b_full = rs_empty + 2;          // [1]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(b_full + 2);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(rs_empty + 2);
   float* s_cterm = reinterpret_cast<float*>(tmem_holder + 4);  // [16][K_pad]: k3[p]*colsum[p][k]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = g.num_n_tiles;
   const int K_pad = nt * BN;
   const int num_tiles = ((g.M + kBM - 1) / kBM) * nt;
+  const int nk = g.num_kchunks;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -194,17 +169,16 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       mbar_init(&rs_full[b], 1);
       mbar_init(&rs_empty[b], kEpiWarps);
     }
-    mbar_init(b_full, 1);
     fence_barrier_init();
   }
-  if (warp < kEpiWarps) {
+  if (warp >= 2) {
     // Third term of affine_term for every filter of the layer.
-    for (int i = threadIdx.x; i < 16 * K_pad; i += 32 * kEpiWarps) {
+    for (int i = threadIdx.x - 64; i < 16 * K_pad; i += 32 * kEpiWarps) {
       const int p = i / K_pad, kf = i - p * K_pad;
       const float csum = (kf < g.K) ? static_cast<float>(colsum[i]) : 0.0f;
       s_cterm[i] = __fmul_rn(st->k3[p], csum);
     }
-    const int e = threadIdx.x;
+    const int e = threadIdx.x - 64;
     if (e < 32) {
       const float k1 = e < 16 ? st->k1[e] : 0.0f;
       const bool ok = k1 == 0.0f || (k1 >= 9.860761315262648e-32f /*2^-103*/ && k1 < 4.0f);
@@ -219,15 +193,10 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   }
   __syncthreads();
 
-  if (warp >= kEpiWarps) {
-    setmaxnreg_dec<kCtrlRegs>();
-    if (warp == kProducerWarp && lane == 0) {
-      // ---------------- TMA producer ----------------
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
       tma_prefetch_desc(&tmR);
-      if (b_res) {  // the single filter tile's B images, once
-        mbar_arrive_expect_tx(b_full, 16 * nk * Cfg::kBBytes);
-        bulk_load(b_base, codes_w, 16 * nk * Cfg::kBBytes, b_full);
-      }
       int s = 0;
       uint32_t ph = 0;
       uint32_t lt = 0;
@@ -244,15 +213,14 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         tma_load_2d(s_rs + rb * 16 * kBM, &tmR, m0, 0, &rs_full[rb]);
         for (int j = 0; j < 4; ++j)
           for (int a = 0; a < 4; ++a) {
-            const int u0 = image_plane(4 * a + j) * nk;
+            const int p = 4 * a + j;
             for (int kc = 0; kc < nk; ++kc) {
               mbar_wait(&empty_bar[s], ph ^ 1u);
-              uint8_t* sa = stage_base + static_cast<size_t>(s) * stage_bytes;
-              mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
-              bulk_load(sa, a_tile + (u0 + kc) * Cfg::kABytes, Cfg::kABytes, &full_bar[s]);
-              if (!b_res)
-                bulk_load(sa + Cfg::kABytes, b_tile + (u0 + kc) * Cfg::kBBytes, Cfg::kBBytes,
-                          &full_bar[s]);
+              uint8_t* sa = stage_base + static_cast<size_t>(s) * Cfg::kStageBytes;
+              mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
+              bulk_load(sa, a_tile + (p * nk + kc) * Cfg::kABytes, Cfg::kABytes, &full_bar[s]);
+              bulk_load(sa + Cfg::kABytes, b_tile + (p * nk + kc) * Cfg::kBBytes, Cfg::kBBytes,
+                        &full_bar[s]);
               if (++s == stages) {
                 s = 0;
                 ph ^= 1u;
@@ -260,59 +228,54 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
             }
           }
       }
-    } else if (warp == kMmaWarp) {
-      // ---------------- TMEM + UMMA issuer ----------------
-      tmem_alloc(tmem_holder, 512);
-      tmem_relinquish();
-      tc_fence_before();
-      named_bar_sync(1, 32 + 32 * kEpiWarps);
-      tc_fence_after();
-      const uint32_t tmem_base = *tmem_holder;
-      if (lane == 0) {
-        if (b_res) mbar_wait(b_full, 0);
-        const uint32_t b_res_base = smem_u32(b_base);
-        int s = 0;
-        uint32_t ph = 0;
-        uint32_t grp = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-          for (int j = 0; j < 4; ++j, ++grp) {
-            const uint32_t buf = grp % NB;
-            mbar_wait(&acc_empty[buf], (grp / NB) & 1u);  // epilogue drained it
-            tc_fence_after();
-            const uint32_t d_base = tmem_base + buf * Cfg::kGroupCols;
-            for (int a = 0; a < 4; ++a) {
-              const int u0 = image_plane(4 * a + j) * nk;
-              for (int kc = 0; kc < nk; ++kc) {
-                mbar_wait(&full_bar[s], ph);
-                tc_fence_after();
-                const uint32_t sa = smem_u32(stage_base + static_cast<size_t>(s) * stage_bytes);
-                const uint32_t sb =
-                    b_res ? b_res_base + (u0 + kc) * Cfg::kBBytes : sa + Cfg::kABytes;
+    }
+  } else if (warp == 1) {
+    // ---------------- TMEM + UMMA issuer ----------------
+    tmem_alloc(tmem_holder, 512);
+    tmem_relinquish();
+    tc_fence_before();
+    named_bar_sync(1, 32 + 32 * kEpiWarps);
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      uint32_t grp = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        for (int j = 0; j < 4; ++j, ++grp) {
+          const uint32_t buf = grp % NB;
+          mbar_wait(&acc_empty[buf], (grp / NB) & 1u);  // epilogue drained (and re-armed) it
+          tc_fence_after();
+          const uint32_t d_base = tmem_base + buf * Cfg::kGroupCols;
+          for (int a = 0; a < 4; ++a) {
+            for (int kc = 0; kc < nk; ++kc) {
+              mbar_wait(&full_bar[s], ph);
+              tc_fence_after();
+              const uint32_t sa = smem_u32(stage_base + static_cast<size_t>(s) * Cfg::kStageBytes);
+              const uint32_t sb = sa + Cfg::kABytes;
 #pragma unroll
-                for (int kk = 0; kk < BK / 32; ++kk) {
-                  if (g.exp & 2) break;
-                  const uint64_t adesc = umma_smem_desc(sa + kk * 32, 8 * BK, Cfg::kLayout);
-                  const uint64_t bdesc = umma_smem_desc(sb + kk * 32, 8 * BK, Cfg::kLayout);
-                  umma_i8(d_base + static_cast<uint32_t>(a * BN), adesc, bdesc, kIdesc,
-                          (kc > 0 || kk > 0) ? 1u : 0u);
-                }
-                umma_commit(&empty_bar[s]);
-                if (++s == stages) {
-                  s = 0;
-                  ph ^= 1u;
-                }
+              for (int kk = 0; kk < BK / 32; ++kk) {
+                if (g.exp & 2) break;
+                const uint64_t adesc = umma_smem_desc(sa + kk * 32, 8 * BK, Cfg::kLayout);
+                const uint64_t bdesc = umma_smem_desc(sb + kk * 32, 8 * BK, Cfg::kLayout);
+                umma_i8(d_base + static_cast<uint32_t>(a * BN), adesc, bdesc, kIdesc,
+                        (kc > 0 || kk > 0) ? 1u : 0u);
+              }
+              umma_commit(&empty_bar[s]);
+              if (++s == stages) {
+                s = 0;
+                ph ^= 1u;
               }
             }
-            umma_commit(&acc_full[buf]);
           }
+          umma_commit(&acc_full[buf]);
         }
       }
-      __syncwarp();
     }
+    __syncwarp();
   } else {
     // ---------------- epilogue ----------------
-    setmaxnreg_inc<kEpiRegs>();
-    const int ew = warp;
+    const int ew = warp - 2;
     const int q = warp & 3;          // TMEM lane quadrant this warp may access
     const int f0 = (ew >> 2) * FPT;  // this thread's filters within the tile
     const int row = q * 32 + lane;   // this thread's row (Winograd tile) within the tile
@@ -423,7 +386,6 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
           if (lane == 0) mbar_arrive(&rs_empty[rb]);
         }
         mbar_wait(&acc_full[buf], (grp / NB) & 1u);
-        if (ew == 0 && lane == 0) trace_event(g.trace, 3, grp);
         tc_fence_after();
         const uint32_t acc_addr = lane_base + buf * Cfg::kGroupCols + f0;
 #pragma unroll
@@ -438,7 +400,6 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[buf]);
-            if (ew == 0 && lane == 0) trace_event(g.trace, 4, grp);
           }
           if (DUMP && row_ok) {
 #pragma unroll
@@ -486,7 +447,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     }
   }
   __syncthreads();
-  if (warp == kMmaWarp) {
+  if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(*tmem_holder, 512);
   }
@@ -499,14 +460,10 @@ static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
                                  const float* bias, int relu, const GemmGeom& g0, cudaStream_t s) {
   GemmGeom g = g0;
   const int k_pad = g.num_n_tiles * BN;
-  const int nk = g.num_kchunks;
-  // Resident B: one filter tile whose 16 positions x C_pad images fit in 64 KB.
-  const int b_res = (g.num_n_tiles == 1 && 16 * nk * GemmCfg<BK, BN>::kBBytes <= 64 * 1024) ? 1 : 0;
   int stages = 16;
-  while (stages > 2 && gemm_smem_bytes<BK, BN>(stages, nk, b_res, k_pad) > kSmemLimit) --stages;
-  const size_t smem = gemm_smem_bytes<BK, BN>(stages, nk, b_res, k_pad);
+  while (stages > 2 && gemm_smem_bytes<BK, BN>(stages, k_pad) > kSmemLimit) --stages;
+  const size_t smem = gemm_smem_bytes<BK, BN>(stages, k_pad);
   if (smem > kSmemLimit) return cudaErrorInvalidValue;
-  g.b_resident = b_res;
   g.stages = stages;
   static size_t configured[64] = {};  // dynamic-smem attribute set so far, per device
   static int sm_count[64] = {};

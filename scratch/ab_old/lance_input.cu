@@ -1,0 +1,390 @@
+// lance_input.cu -- input side of the LANCE path on sm_100a.
+//
+//   K0 input_range_kernel  per-position (min, max) of v = B^T d B over the whole
+//                          batch (quantize_domain PerPosition / PerTensor fit,
+//                          engines.hpp:151-165, fit_params quant.hpp:54-72);
+//                          the last block folds the partials into
+//                          QuantParams[16] and the epilogue constants.
+//   K1 input_quant_kernel  v recomputed and quantised (quant.hpp:77-84) to u8
+//                          codes [16][M][C_pad] (the K-major A operand of the
+//                          position GEMMs) plus row sums [16][M]
+//                          (lowpgemm.hpp:121-123).
+//
+// Mapping: one warp = one segment of a tile row (image img, tile row ti,
+// tiles tj0..tj1) x 64 channels (2 per lane, float2 NHWC loads: 256
+// contiguous bytes per pixel per warp).  The tile gather is extract_tiles
+// (tensor.hpp:116-152): origin (2ti - pad, 2tj - pad), zero padding.
+// Horizontally adjacent tiles share two pixel columns, so the warp slides along
+// the row: per tile it loads 2 new columns (8 pixels) and reuses the first
+// (column) pass of the transform for the 2 shared columns.  Transforms run on
+// packed f32x2 (FADD2), ranges on 3-input FMNMX3.NAN.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "lance_common.cuh"
+
+namespace lance_dev {
+
+// Warp work item: (img, ti, tile segment, channel chunk).
+struct StripItem {
+  int img, ti, tj0, tj1, ch;
+};
+
+__device__ __forceinline__ StripItem strip_item(const InGeom& g, long long item, int lane) {
+  const int chunk = static_cast<int>(item % g.nchunks);
+  long long r = item / g.nchunks;
+  const int seg = static_cast<int>(r % g.nseg);
+  r /= g.nseg;
+  const int ti = static_cast<int>(r % g.TH);
+  const int img = static_cast<int>(r / g.TH);
+  const int tj0 = seg * g.seg_len;
+  const int tj1 = min(tj0 + g.seg_len, g.TW);
+  return {img, ti, tj0, tj1, chunk * kChunk + 2 * lane};
+}
+
+__device__ __forceinline__ void colpass(const float2 (&d)[4], float2 (&t)[4]);
+
+// Row context of a strip: the 4 input rows of tile row ti for this lane's
+// channel pair, with validity (zero padding above / below the image).
+template <bool VEC2>
+struct Strip {
+  const float* row[4];
+  bool rok[4];
+  bool c0ok, c1ok;  // channel ch / ch + 1 < C
+  int W, C;
+
+  __device__ __forceinline__ Strip(const float* __restrict__ x, const InGeom& g,
+                                   const StripItem& it) {
+    W = g.W;
+    C = g.C;
+    c0ok = it.ch < g.C;
+    c1ok = it.ch + 1 < g.C;
+    const float* base = x + static_cast<long long>(it.img) * g.H * g.W * g.C + it.ch;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int yy = 2 * it.ti - g.pad + a;
+      rok[a] = (yy >= 0) && (yy < g.H);
+      row[a] = base + static_cast<long long>(rok[a] ? yy : 0) * g.W * g.C;
+    }
+  }
+
+  // The 4 pixels (rows 0..3 of the strip) of input column xx, this lane's
+  // channel pair; zero outside the image.
+  __device__ __forceinline__ void load(int xx, float2 (&d)[4]) const {
+    const bool cok = (xx >= 0) && (xx < W);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const float* px = row[a] + static_cast<long long>(cok ? xx : 0) * C;
+      const bool ok = cok && rok[a];
+      if (VEC2) {
+        d[a] = (ok && c0ok) ? __ldg(reinterpret_cast<const float2*>(px)) : make_float2(0.f, 0.f);
+      } else {
+        d[a].x = (ok && c0ok) ? __ldg(px) : 0.f;
+        d[a].y = (ok && c1ok) ? __ldg(px + 1) : 0.f;
+      }
+    }
+  }
+
+  // Column pass of B^T d for input column xx: t[a] = (B^T d)(a, col).
+  __device__ __forceinline__ void column(int xx, float2 (&t)[4]) const {
+    float2 d[4];
+    load(xx, d);
+    colpass(d, t);
+  }
+};
+
+__device__ __forceinline__ void colpass(const float2 (&d)[4], float2 (&t)[4]) {
+  t[0] = sub2(d[0], d[2]);
+  t[1] = add2(d[1], d[2]);
+  t[2] = sub2(d[2], d[1]);
+  t[3] = sub2(d[1], d[3]);
+}
+
+// Second (row) pass: v[a*4+b] from the column-pass results of 4 columns.
+__device__ __forceinline__ void row_pass(const float2 (&t0)[4], const float2 (&t1)[4],
+                                         const float2 (&t2)[4], const float2 (&t3)[4],
+                                         float2 (&v)[16]) {
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    v[a * 4 + 0] = sub2(t0[a], t2[a]);
+    v[a * 4 + 1] = add2(t1[a], t2[a]);
+    v[a * 4 + 2] = sub2(t2[a], t1[a]);
+    v[a * 4 + 3] = sub2(t1[a], t3[a]);
+  }
+}
+
+// --------------------------------------------------------------------------
+// K0: per-position range of v over the whole batch (grid-stride over strips).
+template <bool VEC2>
+__global__ void __launch_bounds__(256, 2) input_range_kernel(const float* __restrict__ x,
+                                                             float* __restrict__ partials,
+                                                             LanceDevState* __restrict__ st,
+                                                             InGeom g) {
+  __shared__ float s_red[256];
+  float lo[16], hi[16];
+#pragma unroll
+  for (int p = 0; p < 16; ++p) {
+    lo[p] = __int_as_float(0x7f800000);
+    hi[p] = __int_as_float(0xff800000);
+  }
+  const int lane = threadIdx.x & 31;
+  const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  for (long long item = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       item < g.num_items; item += stride) {
+    const StripItem it = strip_item(g, item, lane);
+    if (it.ch >= g.C) continue;  // lane beyond C (only in the last channel chunk)
+    const Strip<VEC2> sp(x, g, it);
+    const bool two = it.ch + 1 < g.C;
+    float2 ta[4], tb[4], tc[4], td[4], pc[4], pd[4];
+    int xx = 2 * it.tj0 - g.pad;
+    sp.column(xx, ta);
+    sp.column(xx + 1, tb);
+    sp.load(xx + 2, pc);
+    sp.load(xx + 3, pd);
+    for (int tj = it.tj0; tj < it.tj1; ++tj, xx += 2) {
+      colpass(pc, tc);
+      colpass(pd, td);
+      if (tj + 1 < it.tj1) {  // software prefetch of the next tile's two new columns
+        sp.load(xx + 4, pc);
+        sp.load(xx + 5, pd);
+      }
+      float2 v[16];
+      row_pass(ta, tb, tc, td, v);
+      if (two) {
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+          lo[p] = fmin3_nan(lo[p], v[p].x, v[p].y);
+          hi[p] = fmax3_nan(hi[p], v[p].x, v[p].y);
+        }
+      } else {  // odd C: the lane's second channel is padding
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+          lo[p] = fmin_nan(lo[p], v[p].x);
+          hi[p] = fmax_nan(hi[p], v[p].x);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        ta[a] = tc[a];
+        tb[a] = td[a];
+      }
+    }
+  }
+  if (block_minmax_and_ticket(lo, hi, partials, &st->ticket_in, s_red)) {
+    fit_from_ranges(s_red, g.granularity, st->bits_i, st->a_tmin, st->a_tmax, st->a_scale,
+                    st->a_rcp, &st->nan_in);
+    __syncthreads();
+    make_epilogue_consts(st, g.C);
+  }
+}
+
+// Exact reference code for a value whose fast-path residual flagged it as
+// being near the rounding boundary h = n + 0.5*sign(r) (dynamic params: d >= 0,
+// scale > 0 normal).  roundf(RN(d/s)) crosses to the upper code iff
+// RN(d/s) >= h, i.e. iff d/s > mid(pred(h), h) (a float quotient is never a
+// midpoint, so there is no tie), i.e. iff d - s*h > -s*delta with
+// delta = (h - pred(h))/2.  d - s*h is exactly representable here
+// (|d - s*h| <= s*2^-13, granularity ulp(s)/2), so one FFMA decides it.
+__device__ __forceinline__ uint32_t exact_code_near_boundary(float d, float s, float gq, float r,
+                                                             float top) {
+  const float n = __fsub_rn(gq, kMagic);
+  const float h = (r > 0.0f) ? __fadd_rn(n, 0.5f) : __fsub_rn(n, 0.5f);
+  const float lower = (r > 0.0f) ? n : __fsub_rn(n, 1.0f);
+  const float upper = __fadd_rn(lower, 1.0f);
+  const float pred_h = __int_as_float(__float_as_int(h) - 1);
+  const float delta = __fmul_rn(__fsub_rn(h, pred_h), 0.5f);
+  const float e = __fmaf_rn(-s, h, d);
+  float c = (e > -__fmul_rn(s, delta)) ? upper : lower;
+  c = fminf(fmaxf(c, 0.0f), top);
+  return static_cast<uint32_t>(c);
+}
+
+// --------------------------------------------------------------------------
+// K1: codes + row sums, one strip per warp.
+//
+// Dynamic params (the reference's batch fit): d = v - tmin is in [0, range],
+// so the exact product P = d * RN(1/scale) is within 2^-16 of d / scale <= 256.
+// n = rint(P) comes from one FFMA2 with the 1.5 * 2^23 magic addend and
+// r = RN(P - n) from another.  If |r| < 0.5 - 2^-14 then |RN(d / scale) - n|
+// < 0.5, so the reference's roundf((x - t_min) / scale) equals n exactly
+// (no clamp needed: 0 <= n <= top).  Otherwise (probability ~1e-4 per value)
+// the lane re-quantises the flagged values with the IEEE formula.
+// Static params (caller supplied): q may be anywhere, so it is formed with a
+// scalar IEEE multiply, clamped to [0, top] and rounded with the magic addend.
+template <bool VEC2, bool STATIC>
+__global__ void __launch_bounds__(256, 2) input_quant_kernel(const float* __restrict__ x,
+                                                             uint8_t* __restrict__ codes,
+                                                             int32_t* __restrict__ rowsum,
+                                                             const LanceDevState* __restrict__ st,
+                                                             InGeom g) {
+  __shared__ float s_tmin[16], s_scale[16], s_rcp[16];
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < 16) {
+    s_tmin[tid] = st->a_tmin[tid];
+    s_scale[tid] = st->a_scale[tid];
+    s_rcp[tid] = st->a_rcp[tid];
+  }
+  const float top = static_cast<float>((1 << st->bits_i) - 1);
+  __syncthreads();
+  const long long item = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
+  if (item >= g.num_items) return;
+  const StripItem it = strip_item(g, item, lane);
+  const bool lane_on = it.ch < g.C;
+  const bool two = it.ch + 1 < g.C;
+  const Strip<VEC2> sp(x, g, it);
+  // Codes go to the A operand's UMMA images (lance_kernels.cuh): position
+  // planes are nk images apart within a 128-row block.
+  const long long pstride = static_cast<long long>(g.a_nk) * kBM * g.a_bk;
+  float2 ta[4], tb[4], tc[4], td[4], pc[4], pd[4];
+  int xx = 2 * it.tj0 - g.pad;
+  if (lane_on) {
+    sp.column(xx, ta);
+    sp.column(xx + 1, tb);
+    sp.load(xx + 2, pc);
+    sp.load(xx + 3, pd);
+  }
+  int m = (it.img * g.TH + it.ti) * g.TW + it.tj0;
+  for (int tj = it.tj0; tj < it.tj1; ++tj, xx += 2, ++m) {
+    float2 v[16];
+    if (lane_on) {
+      colpass(pc, tc);
+      colpass(pd, td);
+      if (tj + 1 < it.tj1) {  // software prefetch of the next tile's two new columns
+        sp.load(xx + 4, pc);
+        sp.load(xx + 5, pd);
+      }
+      row_pass(ta, tb, tc, td, v);
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        ta[a] = tc[a];
+        tb[a] = td[a];
+      }
+    }
+    uint8_t* dst = codes + umma_image_offset(m, it.ch, 0, kBM, g.a_bk, g.a_nk);
+    uint32_t mine = 0u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      uint32_t pk[2] = {0u, 0u};
+      if (lane_on) {
+        float2 dd[2], gq[2], r[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int p = 2 * k + h;
+          dd[h] = sub2(v[p], bcast2(s_tmin[p]));
+          if (STATIC) {
+            float2 q = mul2_rn(dd[h], bcast2(s_rcp[p]));
+            q.x = fminf(fmaxf(q.x, 0.0f), top);  // NaN -> 0 like quant.hpp:81
+            q.y = fminf(fmaxf(q.y, 0.0f), top);
+            gq[h] = add2(q, bcast2(kMagic));
+            r[h] = sub2(q, sub2(gq[h], bcast2(kMagic)));
+          } else {
+            gq[h] = fma2(dd[h], bcast2(s_rcp[p]), bcast2(kMagic));
+            r[h] = fma2(dd[h], bcast2(s_rcp[p]),
+                        make_float2(-__fsub_rn(gq[h].x, kMagic), -__fsub_rn(gq[h].y, kMagic)));
+          }
+          pk[h] = __byte_perm(__float_as_uint(gq[h].x), __float_as_uint(gq[h].y), 0x0040) & 0xFFFFu;
+        }
+        const float rmax = fmax3_nan(fmax3_nan(fabsf(r[0].x), fabsf(r[0].y), fabsf(r[1].x)),
+                                     fabsf(r[1].y), 0.0f);
+        if (!(rmax < kTieGuard)) {
+          // Rare (~1e-4 per value): re-derive the flagged codes exactly.
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int p = 2 * k + h;
+            uint32_t c0, c1;
+            if (STATIC) {
+              c0 = quantize_code(v[p].x, s_tmin[p], s_scale[p], top);
+              c1 = quantize_code(v[p].y, s_tmin[p], s_scale[p], top);
+            } else {
+              c0 = (fabsf(r[h].x) < kTieGuard)
+                       ? (pk[h] & 0xFFu)
+                       : exact_code_near_boundary(dd[h].x, s_scale[p], gq[h].x, r[h].x, top);
+              c1 = (fabsf(r[h].y) < kTieGuard)
+                       ? (pk[h] >> 8)
+                       : exact_code_near_boundary(dd[h].y, s_scale[p], gq[h].y, r[h].y, top);
+            }
+            pk[h] = c0 | (c1 << 8);
+          }
+        }
+        if (!two) {  // odd C: padding channel code 0
+          pk[0] &= 0x00FFu;
+          pk[1] &= 0x00FFu;
+        }
+        // Codes: 64 contiguous bytes per warp per position (the A operand row).
+        *reinterpret_cast<uint16_t*>(dst + (2 * k) * pstride) = static_cast<uint16_t>(pk[0]);
+        *reinterpret_cast<uint16_t*>(dst + (2 * k + 1) * pstride) = static_cast<uint16_t>(pk[1]);
+      }
+      // Row sums (lowpgemm.hpp:121-123): the lane's two codes of positions
+      // (2k, 2k+1) as 16-bit halves, one warp reduction (REDUX) per pair.
+      const uint32_t a = pk[0] | (pk[1] << 16);                          // [p.c0, p.c1, q.c0, q.c1]
+      const uint32_t w = (a & 0x00FF00FFu) + ((a >> 8) & 0x00FF00FFu);  // [p sum | q sum]
+      const uint32_t tot = __reduce_add_sync(0xffffffffu, w);
+      if ((lane >> 1) == k) mine = (lane & 1) ? (tot >> 16) : (tot & 0xFFFFu);
+    }
+    if (lane < 16) {
+      int32_t* rs = rowsum + static_cast<long long>(lane) * g.rs_pitch + m;
+      if (g.nchunks == 1)
+        *rs = static_cast<int32_t>(mine);
+      else  // channel chunks of one tile run in different warps (rowsum pre-zeroed)
+        atomicAdd(rs, static_cast<int32_t>(mine));
+    }
+  }
+}
+
+// Static-params mode: caller-supplied input QuantParams[16].
+__global__ void static_params_kernel(LanceDevState* st, StaticParams prm, int C) {
+  if (threadIdx.x < 16) {
+    const int p = threadIdx.x;
+    const float s = prm.scale[p];
+    st->a_tmin[p] = prm.tmin[p];
+    st->a_tmax[p] = prm.tmax[p];
+    st->a_scale[p] = s;
+    st->a_rcp[p] = (s == 0.0f) ? 0.0f : __frcp_rn(s);
+    if (p == 0) st->nan_in = 0;
+  }
+  __syncwarp();
+  make_epilogue_consts(st, C);
+}
+
+// --------------------------------------------------------------------------
+int input_range_grid(const InGeom& g, int sm_count) {
+  const long long blocks = (g.num_items + 7) / 8;
+  const long long cap = 2LL * sm_count;  // 2 resident 256-thread blocks per SM
+  return static_cast<int>(blocks < cap ? blocks : cap);
+}
+
+cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceDevState* st,
+                               const InGeom& g, int vec2, cudaStream_t s) {
+  if (vec2)
+    input_range_kernel<true><<<grid, 256, 0, s>>>(x, partials, st, g);
+  else
+    input_range_kernel<false><<<grid, 256, 0, s>>>(x, partials, st, g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
+                               const LanceDevState* st, const InGeom& g, int vec2,
+                               int static_mode, cudaStream_t s) {
+  const unsigned grid = static_cast<unsigned>((g.num_items + 7) / 8);
+  if (vec2) {
+    if (static_mode)
+      input_quant_kernel<true, true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
+    else
+      input_quant_kernel<true, false><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
+  } else {
+    if (static_mode)
+      input_quant_kernel<false, true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
+    else
+      input_quant_kernel<false, false><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_static_params(LanceDevState* st, const StaticParams& prm, int C,
+                                 cudaStream_t s) {
+  static_params_kernel<<<1, 32, 0, s>>>(st, prm, C);
+  return cudaGetLastError();
+}
+
+}  // namespace lance_dev

@@ -7,10 +7,6 @@
 
 #include <cstdint>
 
-#ifndef LANCE_JMAJOR
-#define LANCE_JMAJOR 0
-#endif
-
 namespace lance_dev {
 
 constexpr int kPositions = 16;  // (m + r - 1)^2 for F(2x2,3x3)
@@ -60,9 +56,7 @@ struct GemmGeom {
   int num_kchunks;  // C_pad / BK
   int num_n_tiles;  // K_pad / BN
   int stages;       // shared-memory ring depth (set by the launcher)
-  int b_resident;   // B operand resident in shared memory (set by the launcher)
   int exp;          // experiment switches (LANCE_GEMM_EXP, profiling only; 0 = normal)
-  unsigned long long* trace;  // CTA-0 event timestamps (LANCE_GEMM_TRACE, profiling only)
 };
 
 // Operand codes are stored in global memory exactly as the GEMM's shared-memory
@@ -71,13 +65,7 @@ struct GemmGeom {
 // (128 for A, BN for B), each image K-major with the UMMA / TMA swizzle of a
 // bk-byte row (SWIZZLE_128B / 64B / 32B: 16-byte chunk c of row r sits at
 // chunk c ^ f(r), i.e. byte bit 4+ ^= bits 7+), ordered
-// [row block][j][a][k chunk][image] for position p = 4a + j (j-major: the
-// GEMM consumes positions in j-groups, and a stage copies consecutive units).
-// Plane order of the 16 positions inside a row block (kJMajorImages: j-major).
-constexpr bool kJMajorImages = LANCE_JMAJOR;
-__host__ __device__ __forceinline__ constexpr int image_plane(int p) {
-  return kJMajorImages ? (p & 3) * 4 + (p >> 2) : p;
-}
+// [row block][position 0..15][k chunk][image].
 __host__ __device__ __forceinline__ uint32_t umma_swizzle(uint32_t lin, int bk) {
   const uint32_t mask = bk == 128 ? 7u : (bk == 64 ? 3u : 1u);
   return lin ^ (((lin >> 7) & mask) << 4);
@@ -88,8 +76,7 @@ __host__ __device__ __forceinline__ long long umma_image_offset(long long row, i
   const long long blk = row / rows_per_img;
   const int r = static_cast<int>(row - blk * rows_per_img);
   const int kc = c / bk, cb = c - kc * bk;
-  const int pj = image_plane(p);
-  return ((blk * 16 + pj) * nk + kc) * static_cast<long long>(rows_per_img * bk) +
+  return ((blk * 16 + p) * nk + kc) * static_cast<long long>(rows_per_img * bk) +
          umma_swizzle(static_cast<uint32_t>(r * bk + cb), bk);
 }
 
