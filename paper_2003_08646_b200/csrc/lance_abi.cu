@@ -113,6 +113,25 @@ int make_rowsum_map(CUtensorMap* map, void* base, long long rows, long long pitc
   return LANCE_OK;
 }
 
+// x viewed as [N][H][W][C] fp32; box = chb channels x box_w pixels x 1 row x
+// 1 image.  Out-of-bounds pixels / rows read as 0 (the reference's zero pad).
+int make_input_map(CUtensorMap* map, const float* x, const lance_conv_spec& s, const BandGeom& b) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(LANCE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(s.c), static_cast<cuuint64_t>(s.w),
+                              static_cast<cuuint64_t>(s.h), static_cast<cuuint64_t>(s.n)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(s.c) * 4,
+                                 static_cast<cuuint64_t>(s.c) * 4 * s.w,
+                                 static_cast<cuuint64_t>(s.c) * 4 * s.w * s.h};
+  const cuuint32_t box[4] = {static_cast<cuuint32_t>(b.chb), static_cast<cuuint32_t>(b.box_w), 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(LANCE_ERR_CUDA, "cuTensorMapEncodeTiled (input) failed: " + std::to_string(r));
+  return LANCE_OK;
+}
+
 }  // namespace
 
 struct lance_plan_s {
@@ -125,6 +144,9 @@ struct lance_plan_s {
   int sm_count = 148;
   int range_grid = 1, filter_grid = 1;
   InGeom in_geom{};
+  BandGeom band{};
+  CUtensorMap tmX{};
+  const float* tmX_ptr = nullptr;
   FilterGeom f_geom{};
   GemmGeom gemm_geom{};
   bool vec2 = false;
@@ -315,6 +337,42 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   }
   g.granularity = cfg->granularity;
   p->range_grid = input_range_grid(g, p->sm_count);
+  {
+    // v4 band kernels: C % 4 == 0 (16-byte TMA strides), a box row of 2 TW + 2
+    // pixels (<= 256), a channel band of 64/128/256 (a multiple of BK that
+    // divides C_pad) with TW * chb / 4 <= 512 threads, and the ring + staging
+    // within shared memory.
+    BandGeom& b = p->band;
+    b.enabled = 0;
+    const char* off = std::getenv("LANCE_BAND_OFF");
+    if (!(off && std::atoi(off)) && spec->c % 4 == 0 && 2 * p->TW + 2 <= 256) {
+      for (int chb : {256, 128, 64}) {
+        if (p->C_pad % chb || chb % p->BK || p->TW * (chb / 4) > 512) continue;
+        b.chb = chb;
+        b.nbc = p->C_pad / chb;
+        b.nkb = chb / p->BK;
+        b.box_w = 2 * p->TW + 2;
+        b.slot_bytes = b.box_w * chb * 4;
+        b.run_bytes = p->TW * p->BK;
+        b.stg_bytes = 16 * b.nkb * b.run_bytes;
+        b.ring = 8;
+        while (b.ring > 4 && (size_t(b.ring) * b.slot_bytes + 2 * size_t(b.stg_bytes) + 16 * 1024 + 128) > 200 * 1024)
+          --b.ring;
+        if (size_t(b.ring) * b.slot_bytes + 2 * size_t(b.stg_bytes) + 16 * 1024 + 128 > 200 * 1024) break;
+        // Tile rows per item: enough items for ~3 waves of CTAs.
+        const long long per = static_cast<long long>(spec->n) * b.nbc;
+        b.nseg = 1;
+        while (per * b.nseg < 3LL * p->sm_count && b.nseg < p->TH) ++b.nseg;
+        b.trs = (p->TH + b.nseg - 1) / b.nseg;
+        b.nseg = (p->TH + b.trs - 1) / b.trs;
+        b.items = per * b.nseg;
+        b.grid = static_cast<int>(std::min<long long>(b.items, p->sm_count));
+        b.enabled = 1;
+        break;
+      }
+    }
+    if (b.enabled) p->range_grid = std::max(p->range_grid, b.grid);
+  }
   p->small_acc = static_cast<double>(spec->c) * ((1 << cfg->bits_i) - 1) *
                      ((1 << cfg->bits_w) - 1) < 16777216.0;  // every accumulator < 2^24 (exact fp32 bit trick)
 
@@ -438,16 +496,36 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
       prm.scale[i] = static_params[i].scale;
     }
     LANCE_CUDA(launch_static_params(p->state, prm, p->spec.c, s));
+  } else if (p->band.enabled) {
+    if (p->tmX_ptr != x_dev) {
+      int rc = make_input_map(&p->tmX, x_dev, p->spec, p->band);
+      if (rc) return rc;
+      p->tmX_ptr = x_dev;
+    }
+    LANCE_CUDA(launch_band(&p->tmX, p->codes_a, p->rowsum, p->partials, p->state, p->in_geom,
+                           p->band, 0, 0, s));
   } else {
     LANCE_CUDA(launch_input_range(x_dev, p->partials, p->range_grid, p->state, p->in_geom,
                                   p->vec2, s));
   }
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[1], s));
-  if (p->in_geom.nchunks > 1)
-    LANCE_CUDA(cudaMemsetAsync(p->rowsum, 0, sizeof(int32_t) * 16 * p->rs_pitch, s));
-  LANCE_CUDA(launch_input_quant(x_dev, p->codes_a, p->rowsum, p->state, p->in_geom, p->vec2,
-                                static_params != nullptr, s));
+  if (p->band.enabled) {
+    if (p->tmX_ptr != x_dev) {
+      int rc = make_input_map(&p->tmX, x_dev, p->spec, p->band);
+      if (rc) return rc;
+      p->tmX_ptr = x_dev;
+    }
+    if (p->band.nbc > 1)
+      LANCE_CUDA(cudaMemsetAsync(p->rowsum, 0, sizeof(int32_t) * 16 * p->rs_pitch, s));
+    LANCE_CUDA(launch_band(&p->tmX, p->codes_a, p->rowsum, p->partials, p->state, p->in_geom,
+                           p->band, 1, static_params != nullptr, s));
+  } else {
+    if (p->in_geom.nchunks > 1)
+      LANCE_CUDA(cudaMemsetAsync(p->rowsum, 0, sizeof(int32_t) * 16 * p->rs_pitch, s));
+    LANCE_CUDA(launch_input_quant(x_dev, p->codes_a, p->rowsum, p->state, p->in_geom, p->vec2,
+                                  static_params != nullptr, s));
+  }
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[2], s));
   LANCE_CUDA(launch_gemm(p->codes_a, p->codes_w, &p->tmR, p->BK, p->BN, p->small_acc, p->colsum, p->state, y_dev,

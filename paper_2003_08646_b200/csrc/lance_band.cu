@@ -1,0 +1,372 @@
+// lance_band.cu -- input side of the LANCE path, v4 ("band" kernels).
+//
+//   K0 band_kernel<RANGE>  per-position (min, max) of v = B^T d B over the
+//                          batch (quantize_domain PerPosition / PerTensor fit,
+//                          engines.hpp:151-165, fit_params quant.hpp:54-72); the
+//                          last CTA folds the partials into QuantParams[16].
+//   K1 band_kernel<QUANT>  v recomputed and quantised (quant.hpp:77-84) into
+//                          the A operand's UMMA images (lance_kernels.cuh),
+//                          plus row sums [16][M] (lowpgemm.hpp:121-123).
+//
+// Work item = (image, channel band of chb channels, run of tile rows).  A CTA
+// walks its tile rows top to bottom; the zero-padded input rows of the band
+// (2*TW + 2 pixels from x = -pad, chb channels) arrive by 4-D TMA into a ring
+// of shared-memory row slots -- the TMA's out-of-bounds zero fill is exactly
+// extract_tiles' zero padding (tensor.hpp:141-147) -- and each row is loaded
+// once per run (tile rows share two input rows).  Thread (tile tj, channel
+// quad q) reads its 4 x 4 pixels with conflict-free 16-byte shared loads,
+// transforms 4 channels with packed f32x2 adds in the reference order
+// (column pass first, matrix.hpp:75-84) and, for K1, quantises them, packs
+// the 4 codes of each position into one word and stages them in shared memory
+// in the final UMMA-image byte order; one thread then writes each (position,
+// k chunk) run of rows with a bulk copy.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "lance_common.cuh"
+
+namespace lance_dev {
+
+constexpr int kBandThreads = 512;
+constexpr int kRangeMode = 0, kQuantMode = 1;
+
+// ---------------------------------------------------------------- PTX bits
+__device__ __forceinline__ void tma_load_4d(void* smem_dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                   reinterpret_cast<uint64_t>(gdst)),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ float4 lds128(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
+
+// ---------------------------------------------------------------- item decode
+struct BandItem {
+  int img, band, ti0, ti1;
+};
+
+__device__ __forceinline__ BandItem band_item(const BandGeom& b, const InGeom& g, long long it) {
+  const int seg = static_cast<int>(it % b.nseg);
+  long long r = it / b.nseg;
+  const int band = static_cast<int>(r % b.nbc);
+  const int img = static_cast<int>(r / b.nbc);
+  const int ti0 = seg * b.trs;
+  return {img, band, ti0, min(ti0 + b.trs, g.TH)};
+}
+
+// Exact reference code for a value whose fast-path residual r flagged it as
+// near a rounding boundary (see lance_input.cu exact_code_near_boundary).
+__device__ __forceinline__ uint32_t band_exact_code(float d, float s, float gq, float r, float top) {
+  const float n = __fsub_rn(gq, kMagic);
+  const float h = (r > 0.0f) ? __fadd_rn(n, 0.5f) : __fsub_rn(n, 0.5f);
+  const float lower = (r > 0.0f) ? n : __fsub_rn(n, 1.0f);
+  const float upper = __fadd_rn(lower, 1.0f);
+  const float pred_h = __int_as_float(__float_as_int(h) - 1);
+  const float delta = __fmul_rn(__fsub_rn(h, pred_h), 0.5f);
+  const float e = __fmaf_rn(-s, h, d);
+  float c = (e > -__fmul_rn(s, delta)) ? upper : lower;
+  c = fminf(fmaxf(c, 0.0f), top);
+  return static_cast<uint32_t>(c);
+}
+
+// Transform of one channel pair: d[a][b] (4 x 4 pixels) -> v (in place),
+// column pass (over a) first, then the row pass (over b).
+__device__ __forceinline__ void band_transform(float2 (&d)[4][4]) {
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const float2 d0 = d[0][b], d1 = d[1][b], d2 = d[2][b], d3 = d[3][b];
+    d[0][b] = sub2(d0, d2);
+    d[1][b] = add2(d1, d2);
+    d[2][b] = sub2(d2, d1);
+    d[3][b] = sub2(d1, d3);
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const float2 t0 = d[a][0], t1 = d[a][1], t2 = d[a][2], t3 = d[a][3];
+    d[a][0] = sub2(t0, t2);
+    d[a][1] = add2(t1, t2);
+    d[a][2] = sub2(t2, t1);
+    d[a][3] = sub2(t1, t3);
+  }
+}
+
+// ---------------------------------------------------------------- kernel
+template <int MODE, bool STATIC>
+__global__ void __launch_bounds__(kBandThreads, 1)
+    band_kernel(const __grid_constant__ CUtensorMap tmX, uint8_t* __restrict__ codes,
+                int32_t* __restrict__ rowsum, float* __restrict__ partials,
+                LanceDevState* __restrict__ st, InGeom g, BandGeom b) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  __shared__ float s_tmin[16], s_scale[16], s_rcp[16];
+  __shared__ uint64_t row_full[16];
+  __shared__ float s_red[kBandThreads];
+
+  uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  float* ring = reinterpret_cast<float*>(smem);                   // [ring][box_w][chb]
+  uint8_t* stg = smem + static_cast<size_t>(b.ring) * b.slot_bytes;  // [2][16][TW][chb] codes
+  int32_t* rs_acc = reinterpret_cast<int32_t*>(stg + 2 * b.stg_bytes);  // [16][TW]
+
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int QPT = b.chb >> 2;       // threads (channel quads) per tile
+  const int tj = tid / QPT, q = tid - tj * QPT;
+  const bool active = tj < g.TW;
+  const int slot_floats = b.slot_bytes >> 2;
+
+  if (tid < 16 && MODE == kQuantMode) {
+    s_tmin[tid] = st->a_tmin[tid];
+    s_scale[tid] = st->a_scale[tid];
+    s_rcp[tid] = st->a_rcp[tid];
+  }
+  if (tid < b.ring) mbar_init(&row_full[tid], 1);
+  if (MODE == kQuantMode)
+    for (int i = tid; i < 16 * g.TW; i += kBandThreads) rs_acc[i] = 0;
+  fence_barrier_init();
+  __syncthreads();
+  const float top = static_cast<float>((1 << st->bits_i) - 1);
+
+  float lo[16], hi[16];
+#pragma unroll
+  for (int p = 0; p < 16; ++p) {
+    lo[p] = __int_as_float(0x7f800000);
+    hi[p] = __int_as_float(0xff800000);
+  }
+
+  // Row loads: rows of the current item are numbered k = 0, 1, ... (input row
+  // y = 2 * ti0 - pad + k); a CTA-wide counter gives the ring slot / phase.
+  uint32_t kbase = 0;  // global row counter at the current item's row 0
+  const uint32_t bytes_row = static_cast<uint32_t>(b.slot_bytes);
+  auto issue_row = [&](const BandItem& it, int k) {
+    const uint32_t kg = kbase + k;
+    const int slot = static_cast<int>(kg % b.ring);
+    mbar_arrive_expect_tx(&row_full[slot], bytes_row);
+    tma_load_4d(ring + static_cast<size_t>(slot) * slot_floats, &tmX, it.band * b.chb, -g.pad,
+                2 * it.ti0 - g.pad + k, it.img, &row_full[slot]);
+  };
+
+  uint32_t iter = 0;  // tile rows processed by this CTA (staging buffer parity)
+  for (long long itn = blockIdx.x; itn < b.items; itn += gridDim.x) {
+    const BandItem it = band_item(b, g, itn);
+    const int nrows = 2 * (it.ti1 - it.ti0) + 2;
+    if (tid == 0) {
+      const int first = nrows < b.ring ? nrows : b.ring;
+      for (int k = 0; k < first; ++k) issue_row(it, k);
+    }
+    const int c0 = it.band * b.chb + 4 * q;  // this thread's first channel
+    const bool cvalid = active && c0 < g.C;  // C % 4 == 0 on this path
+    for (int ti = it.ti0; ti < it.ti1; ++ti, ++iter) {
+      const int kr = 2 * (ti - it.ti0);  // first of the 4 rows of this tile row
+      float2 dA[4][4], dB[4][4];         // channels (c0, c0+1) and (c0+2, c0+3)
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const uint32_t kg = kbase + kr + a;
+        const int slot = static_cast<int>(kg % b.ring);
+        mbar_wait(&row_full[slot], (kg / b.ring) & 1u);
+        if (cvalid) {
+          const float* row = ring + static_cast<size_t>(slot) * slot_floats + (2 * tj) * b.chb + 4 * q;
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb) {
+            const float4 v = lds128(row + bb * b.chb);
+            dA[a][bb] = make_float2(v.x, v.y);
+            dB[a][bb] = make_float2(v.z, v.w);
+          }
+        }
+      }
+      if (cvalid) {
+        band_transform(dA);
+        band_transform(dB);
+      }
+      if (MODE == kRangeMode) {
+        if (cvalid) {
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) {
+              const int p = 4 * a + bb;
+              lo[p] = fmin3_nan(fmin3_nan(lo[p], dA[a][bb].x, dA[a][bb].y), dB[a][bb].x, dB[a][bb].y);
+              hi[p] = fmax3_nan(fmax3_nan(hi[p], dA[a][bb].x, dA[a][bb].y), dB[a][bb].x, dB[a][bb].y);
+            }
+        }
+        __syncthreads();  // every thread is done with this tile row's rows
+      } else {
+        // ---- quantise (quant.hpp:77-84) into the staging buffer ----
+        uint8_t* sbuf = stg + (iter & 1u) * b.stg_bytes;
+        const int m = (it.img * g.TH + ti) * g.TW + tj;
+        // Byte offset of (row m, channels c0..c0+3) inside a staged run of the
+        // tile row's TW image rows: row tj, 16-byte chunk swizzled with the
+        // row's index inside its 128-row image (umma_swizzle keeps the row).
+        const int rg = m & (kBM - 1);
+        const int cb = (4 * q) & (g.a_bk - 1);
+        const int stg_off = (4 * q / g.a_bk) * b.run_bytes + tj * g.a_bk +
+                            static_cast<int>(umma_swizzle(static_cast<uint32_t>(rg * g.a_bk + cb), g.a_bk)) -
+                            rg * g.a_bk;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb) {
+            const int p = 4 * a + bb;
+            uint32_t word = 0;
+            if (cvalid) {
+              const float tmin = s_tmin[p], rcp = s_rcp[p];
+              const float2 v2[2] = {dA[a][bb], dB[a][bb]};
+              float2 dd[2], gq[2], r[2];
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                dd[h] = sub2(v2[h], bcast2(tmin));
+                if (STATIC) {
+                  float2 qq = mul2_rn(dd[h], bcast2(rcp));
+                  qq.x = fminf(fmaxf(qq.x, 0.0f), top);  // NaN -> 0 like quant.hpp:81
+                  qq.y = fminf(fmaxf(qq.y, 0.0f), top);
+                  gq[h] = add2(qq, bcast2(kMagic));
+                  r[h] = sub2(qq, sub2(gq[h], bcast2(kMagic)));
+                } else {
+                  // n = rint(d * rcp) via the magic addend, r = d * rcp - n
+                  // exactly (one rounding); see input_quant_kernel.
+                  gq[h] = fma2(dd[h], bcast2(rcp), bcast2(kMagic));
+                  r[h] = fma2(dd[h], bcast2(rcp), sub2(bcast2(kMagic), gq[h]));
+                }
+              }
+              const uint32_t w01 = __byte_perm(__float_as_uint(gq[0].x), __float_as_uint(gq[0].y), 0x0040);
+              const uint32_t w23 = __byte_perm(__float_as_uint(gq[1].x), __float_as_uint(gq[1].y), 0x0040);
+              word = __byte_perm(w01, w23, 0x5410);
+              const float rmax = fmax3_nan(fmax3_nan(fabsf(r[0].x), fabsf(r[0].y), fabsf(r[1].x)),
+                                           fabsf(r[1].y), 0.0f);
+              if (!(rmax < kTieGuard)) {
+                // Rare (~1e-4 per value): re-derive the 4 codes exactly.
+                const float sc = s_scale[p];
+                const float vv[4] = {v2[0].x, v2[0].y, v2[1].x, v2[1].y};
+                const float dv[4] = {dd[0].x, dd[0].y, dd[1].x, dd[1].y};
+                const float gv[4] = {gq[0].x, gq[0].y, gq[1].x, gq[1].y};
+                const float rv[4] = {r[0].x, r[0].y, r[1].x, r[1].y};
+                word = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  uint32_t c;
+                  if (STATIC)
+                    c = quantize_code(vv[e], tmin, sc, top);
+                  else
+                    c = (fabsf(rv[e]) < kTieGuard) ? (__float_as_uint(gv[e]) & 0xFFu)
+                                                   : band_exact_code(dv[e], sc, gv[e], rv[e], top);
+                  word |= c << (8 * e);
+                }
+              }
+            }
+            if (active)
+              *reinterpret_cast<uint32_t*>(sbuf + image_plane(p) * b.nkb * b.run_bytes + stg_off) = word;
+            // Row sums (lowpgemm.hpp:121-123): the thread's 4 codes, then the
+            // tile's QPT threads (two tiles per warp at QPT = 16: 16-bit halves).
+            uint32_t part = __dp4a(word, 0x01010101u, 0u);
+            if (QPT == 16) part <<= 16 * ((lane >> 4) & 1);
+            const uint32_t tot = __reduce_add_sync(0xffffffffu, part);
+            if (active && (lane & (QPT == 16 ? 15 : 31)) == 0) {
+              const uint32_t mine = (QPT == 16) ? ((tot >> (16 * ((lane >> 4) & 1))) & 0xFFFFu) : tot;
+              if (QPT <= 32)
+                rs_acc[p * g.TW + tj] = static_cast<int32_t>(mine);
+              else
+                atomicAdd(&rs_acc[p * g.TW + tj], static_cast<int32_t>(mine));
+            }
+          }
+        fence_proxy_async_smem();
+        if (tid == 0) bulk_wait_read_all();  // the store that used this buffer 2 rows ago
+        __syncthreads();
+        // Row sums of this tile row -> global (channel bands > 1 accumulate).
+        for (int i = tid; i < 16 * g.TW; i += kBandThreads) {
+          const int p = i / g.TW, t = i - p * g.TW;
+          const int mm = (it.img * g.TH + ti) * g.TW + t;
+          int32_t* dst = rowsum + static_cast<long long>(p) * g.rs_pitch + mm;
+          if (b.nbc == 1)
+            *dst = rs_acc[i];
+          else
+            atomicAdd(dst, rs_acc[i]);
+          if (QPT > 32) rs_acc[i] = 0;
+        }
+        if (tid == 0) {
+          // Codes: per (position, k chunk) the tile row's TW image rows are
+          // contiguous in global memory, except across a 128-row block edge.
+          const int m0 = (it.img * g.TH + ti) * g.TW;
+          const int r0 = m0 & (kBM - 1);
+          const int first = (kBM - r0) < g.TW ? (kBM - r0) : g.TW;  // rows before the edge
+          for (int pj = 0; pj < 16; ++pj)
+            for (int kc = 0; kc < b.nkb; ++kc) {
+              const uint8_t* src = sbuf + (pj * b.nkb + kc) * b.run_bytes;
+              const int kcg = kc + it.band * b.nkb;  // global k chunk
+              const long long blk0 = m0 / kBM;
+              uint8_t* dst0 = codes + ((blk0 * 16 + pj) * g.a_nk + kcg) * static_cast<long long>(kBM * g.a_bk) +
+                              r0 * g.a_bk;
+              bulk_store(dst0, src, first * g.a_bk);
+              if (first < g.TW) {
+                uint8_t* dst1 = codes + (((blk0 + 1) * 16 + pj) * g.a_nk + kcg) *
+                                            static_cast<long long>(kBM * g.a_bk);
+                bulk_store(dst1, src + first * g.a_bk, (g.TW - first) * g.a_bk);
+              }
+            }
+          bulk_commit();
+        }
+      }
+      // Rows 2(ti - ti0) and +1 are free: load the rows ring slots ahead.
+      if (tid == 0) {
+        const int knext = kr + 2 + b.ring - 2;  // first row not yet issued: kr + 4 + (ring - 4)
+        for (int k = knext; k < knext + 2 && k < nrows; ++k)
+          if (k >= b.ring) issue_row(it, k);
+      }
+    }
+    kbase += nrows;
+    __syncthreads();  // the next item reuses the ring
+  }
+
+  if (MODE == kRangeMode) {
+    if (block_minmax_and_ticket(lo, hi, partials, &st->ticket_in, s_red)) {
+      fit_from_ranges(s_red, g.granularity, st->bits_i, st->a_tmin, st->a_tmax, st->a_scale,
+                      st->a_rcp, &st->nan_in);
+      __syncthreads();
+      make_epilogue_consts(st, g.C);
+    }
+  } else {
+    if (tid == 0) bulk_wait_all();
+  }
+}
+
+size_t band_smem_bytes(const BandGeom& b, int mode) {
+  return 128 + static_cast<size_t>(b.ring) * b.slot_bytes +
+         (mode == kQuantMode ? 2 * static_cast<size_t>(b.stg_bytes) + 16 * 4 * 256 : 0);
+}
+
+cudaError_t launch_band(const CUtensorMap* tmX, uint8_t* codes, int32_t* rowsum, float* partials,
+                        LanceDevState* st, const InGeom& g, const BandGeom& b, int mode,
+                        int static_mode, cudaStream_t s) {
+  const size_t smem = band_smem_bytes(b, mode);
+  static size_t configured[4] = {};
+  auto fn = mode == kRangeMode ? band_kernel<kRangeMode, false>
+                               : (static_mode ? band_kernel<kQuantMode, true> : band_kernel<kQuantMode, false>);
+  const int fi = mode == kRangeMode ? 0 : (static_mode ? 1 : 2);
+  if (configured[fi] < smem) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured[fi] = smem;
+  }
+  fn<<<b.grid, kBandThreads, smem, s>>>(*tmX, codes, rowsum, partials, st, g, b);
+  return cudaGetLastError();
+}
+
+}  // namespace lance_dev

@@ -47,6 +47,23 @@ struct InGeom {
   int granularity;  // 1 = PerPosition, 2 = PerTensor
 };
 
+// v4 input kernels (lance_band.cu): bands of tile rows fed by 4-D TMA.
+struct BandGeom {
+  int enabled;     // shape supported (C % 4 == 0, 2 * TW + 2 <= 256, chb | C_pad, ...)
+  int chb;         // channels per band (64, 128 or 256; a multiple of the GEMM's BK)
+  int nbc;         // channel bands per image (C_pad / chb)
+  int nkb;         // GEMM k chunks per band (chb / BK)
+  int trs;         // tile rows per work item
+  int nseg;        // items per (image, band) = ceil(TH / trs)
+  long long items; // N * nbc * nseg
+  int box_w;       // pixels per loaded row: 2 * TW + 2 from x = -pad
+  int slot_bytes;  // box_w * chb * 4
+  int ring;        // shared-memory row slots (<= 16)
+  int run_bytes;   // TW * BK: one staged (position, k chunk) run of image rows
+  int stg_bytes;   // 16 * nkb * run_bytes
+  int grid;
+};
+
 struct FilterGeom {
   int K, C, K_pad, C_pad;
   int granularity;
@@ -104,6 +121,11 @@ cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceD
 cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
                                const LanceDevState* st, const InGeom& g, int vec2,
                                int static_mode, cudaStream_t s);
+size_t band_smem_bytes(const BandGeom& b, int mode);
+// mode 0: K0 range pass, 1: K1 quantise (static_mode: caller params).
+cudaError_t launch_band(const CUtensorMap* tmX, uint8_t* codes, int32_t* rowsum, float* partials,
+                        LanceDevState* st, const InGeom& g, const BandGeom& b, int mode,
+                        int static_mode, cudaStream_t s);
 cudaError_t launch_static_params(LanceDevState* st, const StaticParams& prm, int C,
                                  cudaStream_t s);
 cudaError_t launch_filter_prepare(const float* w, float* u_tmp, float* partials, int grid,
