@@ -287,7 +287,9 @@ __global__ void __launch_bounds__(kBandThreads, 1)
             }
           }
         fence_proxy_async_smem();
-        if (tid == 0) bulk_wait_read_all();  // the store that used this buffer 2 rows ago
+        // The bulk stores that read the staging buffer we are about to refill
+        // (two tile rows ago) were issued by each warp's lane 0.
+        if (lane == 0) bulk_wait_read_all();
         __syncthreads();
         // Row sums of this tile row -> global (channel bands > 1 accumulate).
         for (int i = tid; i < 16 * g.TW; i += kBandThreads) {
@@ -300,17 +302,20 @@ __global__ void __launch_bounds__(kBandThreads, 1)
             atomicAdd(dst, rs_acc[i]);
           if (QPT > 32) rs_acc[i] = 0;
         }
-        if (tid == 0) {
-          // Codes: per (position, k chunk) the tile row's TW image rows are
-          // contiguous in global memory, except across a 128-row block edge.
+        // Codes: per (position plane, k chunk) the tile row's TW image rows
+        // are contiguous in global memory, except across a 128-row block edge.
+        // Warp w's lane 0 writes runs w, w + 16, ...
+        {
+          const int warp = tid >> 5;
           const int m0 = (it.img * g.TH + ti) * g.TW;
           const int r0 = m0 & (kBM - 1);
           const int first = (kBM - r0) < g.TW ? (kBM - r0) : g.TW;  // rows before the edge
-          for (int pj = 0; pj < 16; ++pj)
-            for (int kc = 0; kc < b.nkb; ++kc) {
-              const uint8_t* src = sbuf + (pj * b.nkb + kc) * b.run_bytes;
+          const long long blk0 = m0 / kBM;
+          if (lane == 0) {
+            for (int run = warp; run < 16 * b.nkb; run += kBandThreads / 32) {
+              const int pj = run / b.nkb, kc = run - pj * b.nkb;
+              const uint8_t* src = sbuf + run * b.run_bytes;
               const int kcg = kc + it.band * b.nkb;  // global k chunk
-              const long long blk0 = m0 / kBM;
               uint8_t* dst0 = codes + ((blk0 * 16 + pj) * g.a_nk + kcg) * static_cast<long long>(kBM * g.a_bk) +
                               r0 * g.a_bk;
               bulk_store(dst0, src, first * g.a_bk);
@@ -320,7 +325,8 @@ __global__ void __launch_bounds__(kBandThreads, 1)
                 bulk_store(dst1, src + first * g.a_bk, (g.TW - first) * g.a_bk);
               }
             }
-          bulk_commit();
+            bulk_commit();
+          }
         }
       }
       // Rows 2(ti - ti0) and +1 are free: load the rows ring slots ahead.
@@ -342,7 +348,7 @@ __global__ void __launch_bounds__(kBandThreads, 1)
       make_epilogue_consts(st, g.C);
     }
   } else {
-    if (tid == 0) bulk_wait_all();
+    if (lane == 0) bulk_wait_all();
   }
 }
 
