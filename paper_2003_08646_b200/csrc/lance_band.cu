@@ -125,7 +125,6 @@ __global__ void __launch_bounds__(kBandThreads, 1)
   uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   float* ring = reinterpret_cast<float*>(smem);                   // [ring][box_w][chb]
   uint8_t* stg = smem + static_cast<size_t>(b.ring) * b.slot_bytes;  // [2][16][TW][chb] codes
-  int32_t* rs_acc = reinterpret_cast<int32_t*>(stg + 2 * b.stg_bytes);  // [16][TW]
 
   const int tid = threadIdx.x, lane = tid & 31;
   const int QPT = b.chb >> 2;       // threads (channel quads) per tile
@@ -139,8 +138,6 @@ __global__ void __launch_bounds__(kBandThreads, 1)
     s_rcp[tid] = st->a_rcp[tid];
   }
   if (tid < b.ring) mbar_init(&row_full[tid], 1);
-  if (MODE == kQuantMode)
-    for (int i = tid; i < 16 * g.TW; i += kBandThreads) rs_acc[i] = 0;
   fence_barrier_init();
   __syncthreads();
   const float top = static_cast<float>((1 << st->bits_i) - 1);
@@ -182,7 +179,7 @@ __global__ void __launch_bounds__(kBandThreads, 1)
         const uint32_t kg = kbase + kr + a;
         const int slot = static_cast<int>(kg % b.ring);
         mbar_wait(&row_full[slot], (kg / b.ring) & 1u);
-        if (cvalid) {
+        if (active) {
           const float* row = ring + static_cast<size_t>(slot) * slot_floats + (2 * tj) * b.chb + 4 * q;
 #pragma unroll
           for (int bb = 0; bb < 4; ++bb) {
@@ -192,10 +189,8 @@ __global__ void __launch_bounds__(kBandThreads, 1)
           }
         }
       }
-      if (cvalid) {
-        band_transform(dA);
-        band_transform(dB);
-      }
+      band_transform(dA);
+      band_transform(dB);
       if (MODE == kRangeMode) {
         if (cvalid) {
 #pragma unroll
@@ -220,87 +215,86 @@ __global__ void __launch_bounds__(kBandThreads, 1)
         const int stg_off = (4 * q / g.a_bk) * b.run_bytes + tj * g.a_bk +
                             static_cast<int>(umma_swizzle(static_cast<uint32_t>(rg * g.a_bk + cb), g.a_bk)) -
                             rg * g.a_bk;
+        uint32_t* sdst = reinterpret_cast<uint32_t*>(sbuf + stg_off);
+        const int pstride_w = (b.nkb * b.run_bytes) >> 2;  // one position plane, in words
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
           for (int bb = 0; bb < 4; ++bb) {
             const int p = 4 * a + bb;
-            uint32_t word = 0;
-            if (cvalid) {
-              const float tmin = s_tmin[p], rcp = s_rcp[p];
-              const float2 v2[2] = {dA[a][bb], dB[a][bb]};
-              float2 dd[2], gq[2], r[2];
+            const float tmin = s_tmin[p], rcp = s_rcp[p];
+            const float2 v2[2] = {dA[a][bb], dB[a][bb]};
+            float2 dd[2], gq[2], r[2];
 #pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                dd[h] = sub2(v2[h], bcast2(tmin));
-                if (STATIC) {
-                  float2 qq = mul2_rn(dd[h], bcast2(rcp));
-                  qq.x = fminf(fmaxf(qq.x, 0.0f), top);  // NaN -> 0 like quant.hpp:81
-                  qq.y = fminf(fmaxf(qq.y, 0.0f), top);
-                  gq[h] = add2(qq, bcast2(kMagic));
-                  r[h] = sub2(qq, sub2(gq[h], bcast2(kMagic)));
-                } else {
-                  // n = rint(d * rcp) via the magic addend, r = d * rcp - n
-                  // exactly (one rounding); see input_quant_kernel.
-                  gq[h] = fma2(dd[h], bcast2(rcp), bcast2(kMagic));
-                  r[h] = fma2(dd[h], bcast2(rcp), sub2(bcast2(kMagic), gq[h]));
-                }
-              }
-              const uint32_t w01 = __byte_perm(__float_as_uint(gq[0].x), __float_as_uint(gq[0].y), 0x0040);
-              const uint32_t w23 = __byte_perm(__float_as_uint(gq[1].x), __float_as_uint(gq[1].y), 0x0040);
-              word = __byte_perm(w01, w23, 0x5410);
-              const float rmax = fmax3_nan(fmax3_nan(fabsf(r[0].x), fabsf(r[0].y), fabsf(r[1].x)),
-                                           fabsf(r[1].y), 0.0f);
-              if (!(rmax < kTieGuard)) {
-                // Rare (~1e-4 per value): re-derive the 4 codes exactly.
-                const float sc = s_scale[p];
-                const float vv[4] = {v2[0].x, v2[0].y, v2[1].x, v2[1].y};
-                const float dv[4] = {dd[0].x, dd[0].y, dd[1].x, dd[1].y};
-                const float gv[4] = {gq[0].x, gq[0].y, gq[1].x, gq[1].y};
-                const float rv[4] = {r[0].x, r[0].y, r[1].x, r[1].y};
-                word = 0;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  uint32_t c;
-                  if (STATIC)
-                    c = quantize_code(vv[e], tmin, sc, top);
-                  else
-                    c = (fabsf(rv[e]) < kTieGuard) ? (__float_as_uint(gv[e]) & 0xFFu)
-                                                   : band_exact_code(dv[e], sc, gv[e], rv[e], top);
-                  word |= c << (8 * e);
-                }
+            for (int h = 0; h < 2; ++h) {
+              dd[h] = sub2(v2[h], bcast2(tmin));
+              if (STATIC) {
+                float2 qq = mul2_rn(dd[h], bcast2(rcp));
+                qq.x = fminf(fmaxf(qq.x, 0.0f), top);  // NaN -> 0 like quant.hpp:81
+                qq.y = fminf(fmaxf(qq.y, 0.0f), top);
+                gq[h] = add2(qq, bcast2(kMagic));
+                r[h] = sub2(qq, sub2(gq[h], bcast2(kMagic)));
+              } else {
+                // n = rint(d * rcp) via the magic addend, r = d * rcp - n
+                // exactly (one rounding); see input_quant_kernel.
+                gq[h] = fma2(dd[h], bcast2(rcp), bcast2(kMagic));
+                r[h] = fma2(dd[h], bcast2(rcp), sub2(bcast2(kMagic), gq[h]));
               }
             }
-            if (active)
-              *reinterpret_cast<uint32_t*>(sbuf + image_plane(p) * b.nkb * b.run_bytes + stg_off) = word;
-            // Row sums (lowpgemm.hpp:121-123): the thread's 4 codes, then the
-            // tile's QPT threads (two tiles per warp at QPT = 16: 16-bit halves).
-            uint32_t part = __dp4a(word, 0x01010101u, 0u);
-            if (QPT == 16) part <<= 16 * ((lane >> 4) & 1);
-            const uint32_t tot = __reduce_add_sync(0xffffffffu, part);
-            if (active && (lane & (QPT == 16 ? 15 : 31)) == 0) {
-              const uint32_t mine = (QPT == 16) ? ((tot >> (16 * ((lane >> 4) & 1))) & 0xFFFFu) : tot;
-              if (QPT <= 32)
-                rs_acc[p * g.TW + tj] = static_cast<int32_t>(mine);
-              else
-                atomicAdd(&rs_acc[p * g.TW + tj], static_cast<int32_t>(mine));
+            const uint32_t w01 = __byte_perm(__float_as_uint(gq[0].x), __float_as_uint(gq[0].y), 0x0040);
+            const uint32_t w23 = __byte_perm(__float_as_uint(gq[1].x), __float_as_uint(gq[1].y), 0x0040);
+            uint32_t word = __byte_perm(w01, w23, 0x5410);
+            const float rmax = fmax3_nan(fmax3_nan(fabsf(r[0].x), fabsf(r[0].y), fabsf(r[1].x)),
+                                         fabsf(r[1].y), 0.0f);
+            if (__builtin_expect(!(rmax < kTieGuard), 0)) {
+              // Rare (~1e-4 per value): re-derive the 4 codes exactly.
+              const float sc = s_scale[p];
+              const float vv[4] = {v2[0].x, v2[0].y, v2[1].x, v2[1].y};
+              const float dv[4] = {dd[0].x, dd[0].y, dd[1].x, dd[1].y};
+              const float gv[4] = {gq[0].x, gq[0].y, gq[1].x, gq[1].y};
+              const float rv[4] = {r[0].x, r[0].y, r[1].x, r[1].y};
+              word = 0;
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                uint32_t c;
+                if (STATIC)
+                  c = quantize_code(vv[e], tmin, sc, top);
+                else
+                  c = (fabsf(rv[e]) < kTieGuard) ? (__float_as_uint(gv[e]) & 0xFFu)
+                                                 : band_exact_code(dv[e], sc, gv[e], rv[e], top);
+                word |= c << (8 * e);
+              }
             }
+            if (active) sdst[image_plane(p) * pstride_w] = cvalid ? word : 0u;
           }
         fence_proxy_async_smem();
         // The bulk stores that read the staging buffer we are about to refill
         // (two tile rows ago) were issued by each warp's lane 0.
         if (lane == 0) bulk_wait_read_all();
         __syncthreads();
-        // Row sums of this tile row -> global (channel bands > 1 accumulate).
+        // Row sums (lowpgemm.hpp:121-123) from the staged codes: thread i sums
+        // the band's chb codes of (position i / TW, tile i % TW) -- whole
+        // swizzled image rows, so the chunk order does not matter.
         for (int i = tid; i < 16 * g.TW; i += kBandThreads) {
           const int p = i / g.TW, t = i - p * g.TW;
+          const uint8_t* rowp = sbuf + image_plane(p) * b.nkb * b.run_bytes + t * g.a_bk;
+          uint32_t sum = 0;
+          for (int kc = 0; kc < b.nkb; ++kc) {
+            const uint4* r4 = reinterpret_cast<const uint4*>(rowp + kc * b.run_bytes);
+            for (int c16 = 0; c16 < g.a_bk / 16; ++c16) {
+              const uint4 w = r4[c16];
+              sum = __dp4a(w.x, 0x01010101u, sum);
+              sum = __dp4a(w.y, 0x01010101u, sum);
+              sum = __dp4a(w.z, 0x01010101u, sum);
+              sum = __dp4a(w.w, 0x01010101u, sum);
+            }
+          }
           const int mm = (it.img * g.TH + ti) * g.TW + t;
           int32_t* dst = rowsum + static_cast<long long>(p) * g.rs_pitch + mm;
           if (b.nbc == 1)
-            *dst = rs_acc[i];
+            *dst = static_cast<int32_t>(sum);
           else
-            atomicAdd(dst, rs_acc[i]);
-          if (QPT > 32) rs_acc[i] = 0;
+            atomicAdd(dst, static_cast<int32_t>(sum));
         }
         // Codes: per (position plane, k chunk) the tile row's TW image rows
         // are contiguous in global memory, except across a 128-row block edge.
@@ -354,7 +348,7 @@ __global__ void __launch_bounds__(kBandThreads, 1)
 
 size_t band_smem_bytes(const BandGeom& b, int mode) {
   return 128 + static_cast<size_t>(b.ring) * b.slot_bytes +
-         (mode == kQuantMode ? 2 * static_cast<size_t>(b.stg_bytes) + 16 * 4 * 256 : 0);
+         (mode == kQuantMode ? 2 * static_cast<size_t>(b.stg_bytes) : 0);
 }
 
 cudaError_t launch_band(const CUtensorMap* tmX, uint8_t* codes, int32_t* rowsum, float* partials,
