@@ -345,28 +345,36 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
     BandGeom& b = p->band;
     b.enabled = 0;
     const char* off = std::getenv("LANCE_BAND_OFF");
-    if (!(off && std::atoi(off)) && spec->c % 4 == 0 && 2 * p->TW + 2 <= 256) {
+    if (!(off && std::atoi(off)) && spec->c % 4 == 0) {
       for (int chb : {256, 128, 64}) {
-        if (p->C_pad % chb || chb % p->BK || p->TW * (chb / 4) > 512) continue;
+        if (p->C_pad % chb || chb % p->BK) continue;
+        const int qpt = chb / 4;
+        if (qpt > 256) continue;
         b.chb = chb;
         b.nbc = p->C_pad / chb;
         b.nkb = chb / p->BK;
-        b.box_w = 2 * p->TW + 2;
+        // Column slices of <= 256 / qpt tiles (one thread per tile x channel quad).
+        const int maxt = 256 / qpt;
+        b.ncs = (p->TW + maxt - 1) / maxt;
+        b.tws = (p->TW + b.ncs - 1) / b.ncs;
+        b.box_w = 2 * b.tws + 2;
+        if (b.box_w > 256) continue;
         b.slot_bytes = b.box_w * chb * 4;
-        b.run_bytes = p->TW * p->BK;
+        b.run_bytes = b.tws * p->BK;
         b.stg_bytes = 16 * b.nkb * b.run_bytes;
-        b.ring = 8;
-        while (b.ring > 4 && (size_t(b.ring) * b.slot_bytes + 2 * size_t(b.stg_bytes) + 16 * 1024 + 128) > 200 * 1024)
-          --b.ring;
-        if (size_t(b.ring) * b.slot_bytes + 2 * size_t(b.stg_bytes) + 16 * 1024 + 128 > 200 * 1024) break;
-        // Tile rows per item: enough items for ~3 waves of CTAs.
-        const long long per = static_cast<long long>(spec->n) * b.nbc;
+        b.ring = 6;
+        if (size_t(b.ring) * b.slot_bytes + 2 * size_t(b.stg_bytes) + 128 > 110 * 1024) continue;
+        // Tile rows per item: enough items for ~4 waves of 2 CTAs per SM.
+        const long long per = static_cast<long long>(spec->n) * b.nbc * b.ncs;
         b.nseg = 1;
-        while (per * b.nseg < 3LL * p->sm_count && b.nseg < p->TH) ++b.nseg;
+        while (per * b.nseg < 8LL * p->sm_count && b.nseg < p->TH) ++b.nseg;
         b.trs = (p->TH + b.nseg - 1) / b.nseg;
         b.nseg = (p->TH + b.trs - 1) / b.trs;
         b.items = per * b.nseg;
-        b.grid = static_cast<int>(std::min<long long>(b.items, p->sm_count));
+        const size_t smem = size_t(b.ring) * b.slot_bytes + 2 * size_t(b.stg_bytes) + 128;
+        const int per_sm = 2;  // ~120 registers x 256 threads
+        (void)smem;
+        b.grid = static_cast<int>(std::min<long long>(b.items, static_cast<long long>(per_sm) * p->sm_count));
         b.enabled = 1;
         break;
       }

@@ -29,7 +29,7 @@
 
 namespace lance_dev {
 
-constexpr int kBandThreads = 512;
+constexpr int kBandThreads = 256;  // several CTAs per SM overlap their barrier phases
 constexpr int kRangeMode = 0, kQuantMode = 1;
 
 // ---------------------------------------------------------------- PTX bits
@@ -63,16 +63,19 @@ __device__ __forceinline__ float4 lds128(const float* p) {
 
 // ---------------------------------------------------------------- item decode
 struct BandItem {
-  int img, band, ti0, ti1;
+  int img, band, ti0, ti1, tj0, ntj;  // tile rows [ti0, ti1), tiles [tj0, tj0 + ntj)
 };
 
 __device__ __forceinline__ BandItem band_item(const BandGeom& b, const InGeom& g, long long it) {
   const int seg = static_cast<int>(it % b.nseg);
   long long r = it / b.nseg;
+  const int cs = static_cast<int>(r % b.ncs);
+  r /= b.ncs;
   const int band = static_cast<int>(r % b.nbc);
   const int img = static_cast<int>(r / b.nbc);
   const int ti0 = seg * b.trs;
-  return {img, band, ti0, min(ti0 + b.trs, g.TH)};
+  const int tj0 = cs * b.tws;
+  return {img, band, ti0, min(ti0 + b.trs, g.TH), tj0, min(b.tws, g.TW - tj0)};
 }
 
 // Exact reference code for a value whose fast-path residual r flagged it as
@@ -113,7 +116,7 @@ __device__ __forceinline__ void band_transform(float2 (&d)[4][4]) {
 
 // ---------------------------------------------------------------- kernel
 template <int MODE, bool STATIC>
-__global__ void __launch_bounds__(kBandThreads, 1)
+__global__ void __launch_bounds__(kBandThreads, 2)
     band_kernel(const __grid_constant__ CUtensorMap tmX, uint8_t* __restrict__ codes,
                 int32_t* __restrict__ rowsum, float* __restrict__ partials,
                 LanceDevState* __restrict__ st, InGeom g, BandGeom b) {
@@ -129,7 +132,7 @@ __global__ void __launch_bounds__(kBandThreads, 1)
   const int tid = threadIdx.x, lane = tid & 31;
   const int QPT = b.chb >> 2;       // threads (channel quads) per tile
   const int tj = tid / QPT, q = tid - tj * QPT;
-  const bool active = tj < g.TW;
+  const bool in_slice = tj < b.tws;
   const int slot_floats = b.slot_bytes >> 2;
 
   if (tid < 16 && MODE == kQuantMode) {
@@ -157,7 +160,7 @@ __global__ void __launch_bounds__(kBandThreads, 1)
     const uint32_t kg = kbase + k;
     const int slot = static_cast<int>(kg % b.ring);
     mbar_arrive_expect_tx(&row_full[slot], bytes_row);
-    tma_load_4d(ring + static_cast<size_t>(slot) * slot_floats, &tmX, it.band * b.chb, -g.pad,
+    tma_load_4d(ring + static_cast<size_t>(slot) * slot_floats, &tmX, it.band * b.chb, 2 * it.tj0 - g.pad,
                 2 * it.ti0 - g.pad + k, it.img, &row_full[slot]);
   };
 
@@ -170,6 +173,7 @@ __global__ void __launch_bounds__(kBandThreads, 1)
       for (int k = 0; k < first; ++k) issue_row(it, k);
     }
     const int c0 = it.band * b.chb + 4 * q;  // this thread's first channel
+    const bool active = in_slice && tj < it.ntj;
     const bool cvalid = active && c0 < g.C;  // C % 4 == 0 on this path
     for (int ti = it.ti0; ti < it.ti1; ++ti, ++iter) {
       const int kr = 2 * (ti - it.ti0);  // first of the 4 rows of this tile row
@@ -206,7 +210,7 @@ __global__ void __launch_bounds__(kBandThreads, 1)
       } else {
         // ---- quantise (quant.hpp:77-84) into the staging buffer ----
         uint8_t* sbuf = stg + (iter & 1u) * b.stg_bytes;
-        const int m = (it.img * g.TH + ti) * g.TW + tj;
+        const int m = (it.img * g.TH + ti) * g.TW + it.tj0 + tj;
         // Byte offset of (row m, channels c0..c0+3) inside a staged run of the
         // tile row's TW image rows: row tj, 16-byte chunk swizzled with the
         // row's index inside its 128-row image (umma_swizzle keeps the row).
@@ -275,8 +279,8 @@ __global__ void __launch_bounds__(kBandThreads, 1)
         // Row sums (lowpgemm.hpp:121-123) from the staged codes: thread i sums
         // the band's chb codes of (position i / TW, tile i % TW) -- whole
         // swizzled image rows, so the chunk order does not matter.
-        for (int i = tid; i < 16 * g.TW; i += kBandThreads) {
-          const int p = i / g.TW, t = i - p * g.TW;
+        for (int i = tid; i < 16 * it.ntj; i += kBandThreads) {
+          const int p = i / it.ntj, t = i - p * it.ntj;
           const uint8_t* rowp = sbuf + image_plane(p) * b.nkb * b.run_bytes + t * g.a_bk;
           uint32_t sum = 0;
           for (int kc = 0; kc < b.nkb; ++kc) {
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(kBandThreads, 1)
               sum = __dp4a(w.w, 0x01010101u, sum);
             }
           }
-          const int mm = (it.img * g.TH + ti) * g.TW + t;
+          const int mm = (it.img * g.TH + ti) * g.TW + it.tj0 + t;
           int32_t* dst = rowsum + static_cast<long long>(p) * g.rs_pitch + mm;
           if (b.nbc == 1)
             *dst = static_cast<int32_t>(sum);
@@ -301,9 +305,9 @@ __global__ void __launch_bounds__(kBandThreads, 1)
         // Warp w's lane 0 writes runs w, w + 16, ...
         {
           const int warp = tid >> 5;
-          const int m0 = (it.img * g.TH + ti) * g.TW;
+          const int m0 = (it.img * g.TH + ti) * g.TW + it.tj0;
           const int r0 = m0 & (kBM - 1);
-          const int first = (kBM - r0) < g.TW ? (kBM - r0) : g.TW;  // rows before the edge
+          const int first = (kBM - r0) < it.ntj ? (kBM - r0) : it.ntj;  // rows before the edge
           const long long blk0 = m0 / kBM;
           if (lane == 0) {
             for (int run = warp; run < 16 * b.nkb; run += kBandThreads / 32) {
@@ -313,10 +317,10 @@ __global__ void __launch_bounds__(kBandThreads, 1)
               uint8_t* dst0 = codes + ((blk0 * 16 + pj) * g.a_nk + kcg) * static_cast<long long>(kBM * g.a_bk) +
                               r0 * g.a_bk;
               bulk_store(dst0, src, first * g.a_bk);
-              if (first < g.TW) {
+              if (first < it.ntj) {
                 uint8_t* dst1 = codes + (((blk0 + 1) * 16 + pj) * g.a_nk + kcg) *
                                             static_cast<long long>(kBM * g.a_bk);
-                bulk_store(dst1, src + first * g.a_bk, (g.TW - first) * g.a_bk);
+                bulk_store(dst1, src + first * g.a_bk, (it.ntj - first) * g.a_bk);
               }
             }
             bulk_commit();

@@ -49,17 +49,19 @@ struct InGeom {
 
 // v4 input kernels (lance_band.cu): bands of tile rows fed by 4-D TMA.
 struct BandGeom {
-  int enabled;     // shape supported (C % 4 == 0, 2 * TW + 2 <= 256, chb | C_pad, ...)
+  int enabled;     // shape supported (C % 4 == 0, chb | C_pad, chb % BK == 0, ...)
   int chb;         // channels per band (64, 128 or 256; a multiple of the GEMM's BK)
   int nbc;         // channel bands per image (C_pad / chb)
   int nkb;         // GEMM k chunks per band (chb / BK)
   int trs;         // tile rows per work item
-  int nseg;        // items per (image, band) = ceil(TH / trs)
-  long long items; // N * nbc * nseg
-  int box_w;       // pixels per loaded row: 2 * TW + 2 from x = -pad
+  int nseg;        // tile-row segments per image = ceil(TH / trs)
+  int tws;         // tiles per column slice (a CTA handles tws tiles of a tile row)
+  int ncs;         // column slices = ceil(TW / tws)
+  long long items; // N * nbc * ncs * nseg
+  int box_w;       // pixels per loaded row: 2 * tws + 2 from x = 2 * tj0 - pad
   int slot_bytes;  // box_w * chb * 4
   int ring;        // shared-memory row slots (<= 16)
-  int run_bytes;   // TW * BK: one staged (position, k chunk) run of image rows
+  int run_bytes;   // tws * BK: one staged (position, k chunk) run of image rows
   int stg_bytes;   // 16 * nkb * run_bytes
   int grid;
 };
