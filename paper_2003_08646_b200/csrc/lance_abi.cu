@@ -524,7 +524,7 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
       if (rc) return rc;
       p->tmX_ptr = x_dev;
     }
-    if (p->band.nbc > 1)
+    if (p->band.nbc > 1 || p->band.chb == 256)  // row sums accumulate atomically
       LANCE_CUDA(cudaMemsetAsync(p->rowsum, 0, sizeof(int32_t) * 16 * p->rs_pitch, s));
     LANCE_CUDA(launch_band(&p->tmX, p->codes_a, p->rowsum, p->partials, p->state, p->in_geom,
                            p->band, 1, static_params != nullptr, s));

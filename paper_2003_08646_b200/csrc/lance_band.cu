@@ -115,24 +115,33 @@ __device__ __forceinline__ void band_transform(float2 (&d)[4][4]) {
 }
 
 // ---------------------------------------------------------------- kernel
+// Warp-specialised: warps 0 .. NCW-1 compute (thread = tile x channel quad),
+// the last warp's lane 0 streams input rows into the ring and writes staged
+// codes back.  All hand-offs are mbarriers; there is no CTA-wide barrier in
+// the loop:
+//   row_full[slot]   TMA transaction barrier of a ring slot
+//   stage_full[buf]  compute warps staged a tile row's codes (count NCW);
+//                    also implies they are done with that tile row's rows
+//   stage_empty[buf] the bulk stores of that staging buffer finished reading
 template <int MODE, bool STATIC>
-__global__ void __launch_bounds__(kBandThreads, 2)
+__global__ void __launch_bounds__(kBandThreads + 32, 2)
     band_kernel(const __grid_constant__ CUtensorMap tmX, uint8_t* __restrict__ codes,
                 int32_t* __restrict__ rowsum, float* __restrict__ partials,
                 LanceDevState* __restrict__ st, InGeom g, BandGeom b) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ float s_tmin[16], s_scale[16], s_rcp[16];
-  __shared__ uint64_t row_full[16];
-  __shared__ float s_red[kBandThreads];
+  __shared__ uint64_t row_full[16], stage_full[2], stage_empty[2];
+  __shared__ float s_red[kBandThreads + 32];
 
   uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-  float* ring = reinterpret_cast<float*>(smem);                   // [ring][box_w][chb]
-  uint8_t* stg = smem + static_cast<size_t>(b.ring) * b.slot_bytes;  // [2][16][TW][chb] codes
+  float* ring = reinterpret_cast<float*>(smem);                       // [ring][box_w][chb]
+  uint8_t* stg = smem + static_cast<size_t>(b.ring) * b.slot_bytes;  // [2][16][nkb][tws][BK]
 
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int QPT = b.chb >> 2;       // threads (channel quads) per tile
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int QPT = b.chb >> 2;  // threads (channel quads) per tile
+  constexpr int NCW = kBandThreads / 32;  // compute warps (all arrive on stage_full)
+  const bool is_ctrl = warp == kBandThreads / 32;
   const int tj = tid / QPT, q = tid - tj * QPT;
-  const bool in_slice = tj < b.tws;
   const int slot_floats = b.slot_bytes >> 2;
 
   if (tid < 16 && MODE == kQuantMode) {
@@ -141,6 +150,10 @@ __global__ void __launch_bounds__(kBandThreads, 2)
     s_rcp[tid] = st->a_rcp[tid];
   }
   if (tid < b.ring) mbar_init(&row_full[tid], 1);
+  if (tid < 2) {
+    mbar_init(&stage_full[tid], NCW);
+    mbar_init(&stage_empty[tid], 1);
+  }
   fence_barrier_init();
   __syncthreads();
   const float top = static_cast<float>((1 << st->bits_i) - 1);
@@ -152,168 +165,40 @@ __global__ void __launch_bounds__(kBandThreads, 2)
     hi[p] = __int_as_float(0xff800000);
   }
 
-  // Row loads: rows of the current item are numbered k = 0, 1, ... (input row
-  // y = 2 * ti0 - pad + k); a CTA-wide counter gives the ring slot / phase.
-  uint32_t kbase = 0;  // global row counter at the current item's row 0
-  const uint32_t bytes_row = static_cast<uint32_t>(b.slot_bytes);
-  auto issue_row = [&](const BandItem& it, int k) {
-    const uint32_t kg = kbase + k;
-    const int slot = static_cast<int>(kg % b.ring);
-    mbar_arrive_expect_tx(&row_full[slot], bytes_row);
-    tma_load_4d(ring + static_cast<size_t>(slot) * slot_floats, &tmX, it.band * b.chb, 2 * it.tj0 - g.pad,
-                2 * it.ti0 - g.pad + k, it.img, &row_full[slot]);
-  };
-
-  uint32_t iter = 0;  // tile rows processed by this CTA (staging buffer parity)
-  for (long long itn = blockIdx.x; itn < b.items; itn += gridDim.x) {
-    const BandItem it = band_item(b, g, itn);
-    const int nrows = 2 * (it.ti1 - it.ti0) + 2;
-    if (tid == 0) {
-      const int first = nrows < b.ring ? nrows : b.ring;
-      for (int k = 0; k < first; ++k) issue_row(it, k);
-    }
-    const int c0 = it.band * b.chb + 4 * q;  // this thread's first channel
-    const bool active = in_slice && tj < it.ntj;
-    const bool cvalid = active && c0 < g.C;  // C % 4 == 0 on this path
-    for (int ti = it.ti0; ti < it.ti1; ++ti, ++iter) {
-      const int kr = 2 * (ti - it.ti0);  // first of the 4 rows of this tile row
-      float2 dA[4][4], dB[4][4];         // channels (c0, c0+1) and (c0+2, c0+3)
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const uint32_t kg = kbase + kr + a;
+  if (is_ctrl) {
+    // ------------------------------------------------ loader / storer
+    if (lane == 0) {
+      uint32_t kbase = 0;  // CTA row counter at the current item's row 0
+      uint32_t iter = 0;   // tile rows of this CTA (staging parity)
+      auto issue_row = [&](const BandItem& it, int k) {
+        const uint32_t kg = kbase + k;
         const int slot = static_cast<int>(kg % b.ring);
-        mbar_wait(&row_full[slot], (kg / b.ring) & 1u);
-        if (active) {
-          const float* row = ring + static_cast<size_t>(slot) * slot_floats + (2 * tj) * b.chb + 4 * q;
-#pragma unroll
-          for (int bb = 0; bb < 4; ++bb) {
-            const float4 v = lds128(row + bb * b.chb);
-            dA[a][bb] = make_float2(v.x, v.y);
-            dB[a][bb] = make_float2(v.z, v.w);
-          }
-        }
-      }
-      band_transform(dA);
-      band_transform(dB);
-      if (MODE == kRangeMode) {
-        if (cvalid) {
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int bb = 0; bb < 4; ++bb) {
-              const int p = 4 * a + bb;
-              lo[p] = fmin3_nan(fmin3_nan(lo[p], dA[a][bb].x, dA[a][bb].y), dB[a][bb].x, dB[a][bb].y);
-              hi[p] = fmax3_nan(fmax3_nan(hi[p], dA[a][bb].x, dA[a][bb].y), dB[a][bb].x, dB[a][bb].y);
-            }
-        }
-        __syncthreads();  // every thread is done with this tile row's rows
-      } else {
-        // ---- quantise (quant.hpp:77-84) into the staging buffer ----
-        uint8_t* sbuf = stg + (iter & 1u) * b.stg_bytes;
-        const int m = (it.img * g.TH + ti) * g.TW + it.tj0 + tj;
-        // Byte offset of (row m, channels c0..c0+3) inside a staged run of the
-        // tile row's TW image rows: row tj, 16-byte chunk swizzled with the
-        // row's index inside its 128-row image (umma_swizzle keeps the row).
-        const int rg = m & (kBM - 1);
-        const int cb = (4 * q) & (g.a_bk - 1);
-        const int stg_off = (4 * q / g.a_bk) * b.run_bytes + tj * g.a_bk +
-                            static_cast<int>(umma_swizzle(static_cast<uint32_t>(rg * g.a_bk + cb), g.a_bk)) -
-                            rg * g.a_bk;
-        uint32_t* sdst = reinterpret_cast<uint32_t*>(sbuf + stg_off);
-        const int pstride_w = (b.nkb * b.run_bytes) >> 2;  // one position plane, in words
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int bb = 0; bb < 4; ++bb) {
-            const int p = 4 * a + bb;
-            const float tmin = s_tmin[p], rcp = s_rcp[p];
-            const float2 v2[2] = {dA[a][bb], dB[a][bb]};
-            float2 dd[2], gq[2], r[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              dd[h] = sub2(v2[h], bcast2(tmin));
-              if (STATIC) {
-                float2 qq = mul2_rn(dd[h], bcast2(rcp));
-                qq.x = fminf(fmaxf(qq.x, 0.0f), top);  // NaN -> 0 like quant.hpp:81
-                qq.y = fminf(fmaxf(qq.y, 0.0f), top);
-                gq[h] = add2(qq, bcast2(kMagic));
-                r[h] = sub2(qq, sub2(gq[h], bcast2(kMagic)));
-              } else {
-                // n = rint(d * rcp) via the magic addend, r = d * rcp - n
-                // exactly (one rounding); see input_quant_kernel.
-                gq[h] = fma2(dd[h], bcast2(rcp), bcast2(kMagic));
-                r[h] = fma2(dd[h], bcast2(rcp), sub2(bcast2(kMagic), gq[h]));
-              }
-            }
-            const uint32_t w01 = __byte_perm(__float_as_uint(gq[0].x), __float_as_uint(gq[0].y), 0x0040);
-            const uint32_t w23 = __byte_perm(__float_as_uint(gq[1].x), __float_as_uint(gq[1].y), 0x0040);
-            uint32_t word = __byte_perm(w01, w23, 0x5410);
-            const float rmax = fmax3_nan(fmax3_nan(fabsf(r[0].x), fabsf(r[0].y), fabsf(r[1].x)),
-                                         fabsf(r[1].y), 0.0f);
-            if (__builtin_expect(!(rmax < kTieGuard), 0)) {
-              // Rare (~1e-4 per value): re-derive the 4 codes exactly.
-              const float sc = s_scale[p];
-              const float vv[4] = {v2[0].x, v2[0].y, v2[1].x, v2[1].y};
-              const float dv[4] = {dd[0].x, dd[0].y, dd[1].x, dd[1].y};
-              const float gv[4] = {gq[0].x, gq[0].y, gq[1].x, gq[1].y};
-              const float rv[4] = {r[0].x, r[0].y, r[1].x, r[1].y};
-              word = 0;
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                uint32_t c;
-                if (STATIC)
-                  c = quantize_code(vv[e], tmin, sc, top);
-                else
-                  c = (fabsf(rv[e]) < kTieGuard) ? (__float_as_uint(gv[e]) & 0xFFu)
-                                                 : band_exact_code(dv[e], sc, gv[e], rv[e], top);
-                word |= c << (8 * e);
-              }
-            }
-            if (active) sdst[image_plane(p) * pstride_w] = cvalid ? word : 0u;
-          }
-        fence_proxy_async_smem();
-        // The bulk stores that read the staging buffer we are about to refill
-        // (two tile rows ago) were issued by each warp's lane 0.
-        if (lane == 0) bulk_wait_read_all();
-        __syncthreads();
-        // Row sums (lowpgemm.hpp:121-123) from the staged codes: thread i sums
-        // the band's chb codes of (position i / TW, tile i % TW) -- whole
-        // swizzled image rows, so the chunk order does not matter.
-        for (int i = tid; i < 16 * it.ntj; i += kBandThreads) {
-          const int p = i / it.ntj, t = i - p * it.ntj;
-          const uint8_t* rowp = sbuf + image_plane(p) * b.nkb * b.run_bytes + t * g.a_bk;
-          uint32_t sum = 0;
-          for (int kc = 0; kc < b.nkb; ++kc) {
-            const uint4* r4 = reinterpret_cast<const uint4*>(rowp + kc * b.run_bytes);
-            for (int c16 = 0; c16 < g.a_bk / 16; ++c16) {
-              const uint4 w = r4[c16];
-              sum = __dp4a(w.x, 0x01010101u, sum);
-              sum = __dp4a(w.y, 0x01010101u, sum);
-              sum = __dp4a(w.z, 0x01010101u, sum);
-              sum = __dp4a(w.w, 0x01010101u, sum);
-            }
-          }
-          const int mm = (it.img * g.TH + ti) * g.TW + it.tj0 + t;
-          int32_t* dst = rowsum + static_cast<long long>(p) * g.rs_pitch + mm;
-          if (b.nbc == 1)
-            *dst = static_cast<int32_t>(sum);
-          else
-            atomicAdd(dst, static_cast<int32_t>(sum));
-        }
-        // Codes: per (position plane, k chunk) the tile row's TW image rows
-        // are contiguous in global memory, except across a 128-row block edge.
-        // Warp w's lane 0 writes runs w, w + 16, ...
-        {
-          const int warp = tid >> 5;
-          const int m0 = (it.img * g.TH + ti) * g.TW + it.tj0;
-          const int r0 = m0 & (kBM - 1);
-          const int first = (kBM - r0) < it.ntj ? (kBM - r0) : it.ntj;  // rows before the edge
-          const long long blk0 = m0 / kBM;
-          if (lane == 0) {
-            for (int run = warp; run < 16 * b.nkb; run += kBandThreads / 32) {
+        mbar_arrive_expect_tx(&row_full[slot], static_cast<uint32_t>(b.slot_bytes));
+        tma_load_4d(ring + static_cast<size_t>(slot) * slot_floats, &tmX, it.band * b.chb,
+                    2 * it.tj0 - g.pad, 2 * it.ti0 - g.pad + k, it.img, &row_full[slot]);
+      };
+      for (long long itn = blockIdx.x; itn < b.items; itn += gridDim.x) {
+        const BandItem it = band_item(b, g, itn);
+        const int nrows = 2 * (it.ti1 - it.ti0) + 2;
+        for (int k = 0; k < nrows && k < b.ring; ++k) issue_row(it, k);
+        for (int ti = it.ti0; ti < it.ti1; ++ti, ++iter) {
+          const int i = ti - it.ti0;
+          const uint32_t buf = iter & 1u;
+          mbar_wait(&stage_full[buf], (iter >> 1) & 1u);  // computed (and done reading rows)
+          // Rows 2i, 2i+1 are free: refill their slots ring rows ahead.
+          for (int k = 2 * i + b.ring; k < 2 * i + b.ring + 2 && k < nrows; ++k) issue_row(it, k);
+          if (MODE == kQuantMode) {
+            // Codes: per (position plane, k chunk) the slice's ntj image rows
+            // are contiguous in global memory, except across a 128-row edge.
+            const uint8_t* sbuf = stg + buf * b.stg_bytes;
+            const int m0 = (it.img * g.TH + ti) * g.TW + it.tj0;
+            const int r0 = m0 & (kBM - 1);
+            const int first = (kBM - r0) < it.ntj ? (kBM - r0) : it.ntj;
+            const long long blk0 = m0 / kBM;
+            for (int run = 0; run < 16 * b.nkb; ++run) {
               const int pj = run / b.nkb, kc = run - pj * b.nkb;
               const uint8_t* src = sbuf + run * b.run_bytes;
-              const int kcg = kc + it.band * b.nkb;  // global k chunk
+              const int kcg = kc + it.band * b.nkb;
               uint8_t* dst0 = codes + ((blk0 * 16 + pj) * g.a_nk + kcg) * static_cast<long long>(kBM * g.a_bk) +
                               r0 * g.a_bk;
               bulk_store(dst0, src, first * g.a_bk);
@@ -324,18 +209,158 @@ __global__ void __launch_bounds__(kBandThreads, 2)
               }
             }
             bulk_commit();
+            bulk_wait_read_all();  // this buffer may be refilled now
+          }
+          mbar_arrive(&stage_empty[buf]);
+        }
+        kbase += nrows;
+      }
+      if (MODE == kQuantMode) bulk_wait_all();
+    }
+  } else {
+    // ------------------------------------------------ compute warps
+    uint32_t kbase = 0, iter = 0;
+    for (long long itn = blockIdx.x; itn < b.items; itn += gridDim.x) {
+      const BandItem it = band_item(b, g, itn);
+      const int nrows = 2 * (it.ti1 - it.ti0) + 2;
+      const int c0 = it.band * b.chb + 4 * q;  // this thread's first channel
+      const bool active = tj < it.ntj;
+      const bool cvalid = active && c0 < g.C;  // C % 4 == 0 on this path
+      for (int ti = it.ti0; ti < it.ti1; ++ti, ++iter) {
+        const int kr = 2 * (ti - it.ti0);  // first of the 4 rows of this tile row
+        float2 dA[4][4], dB[4][4];         // channels (c0, c0+1) and (c0+2, c0+3)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const uint32_t kg = kbase + kr + a;
+          const int slot = static_cast<int>(kg % b.ring);
+          mbar_wait(&row_full[slot], (kg / b.ring) & 1u);
+          const float* row = ring + static_cast<size_t>(slot) * slot_floats + (2 * tj) * b.chb + 4 * q;
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb) {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (active) v = lds128(row + bb * b.chb);
+            dA[a][bb] = make_float2(v.x, v.y);
+            dB[a][bb] = make_float2(v.z, v.w);
+          }
+        }
+        band_transform(dA);
+        band_transform(dB);
+        const uint32_t buf = iter & 1u;
+        if (MODE == kRangeMode) {
+          if (cvalid) {
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int bb = 0; bb < 4; ++bb) {
+                const int p = 4 * a + bb;
+                lo[p] = fmin3_nan(fmin3_nan(lo[p], dA[a][bb].x, dA[a][bb].y), dB[a][bb].x, dB[a][bb].y);
+                hi[p] = fmax3_nan(fmax3_nan(hi[p], dA[a][bb].x, dA[a][bb].y), dB[a][bb].x, dB[a][bb].y);
+              }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&stage_full[buf]);  // rows of this tile row consumed
+        } else {
+          // ---- quantise (quant.hpp:77-84) into the staging buffer ----
+          mbar_wait(&stage_empty[buf], ((iter >> 1) & 1u) ^ 1u);
+          uint8_t* sbuf = stg + buf * b.stg_bytes;
+          const int m = (it.img * g.TH + ti) * g.TW + it.tj0 + tj;
+          // Byte offset of (row m, channels c0..c0+3) inside a staged run of
+          // the slice's image rows: row tj, 16-byte chunk swizzled with the
+          // row's index inside its 128-row image (umma_swizzle keeps the row).
+          const int rg = m & (kBM - 1);
+          const int cb = (4 * q) & (g.a_bk - 1);
+          const int stg_off = (4 * q / g.a_bk) * b.run_bytes + tj * g.a_bk +
+                              static_cast<int>(umma_swizzle(static_cast<uint32_t>(rg * g.a_bk + cb), g.a_bk)) -
+                              rg * g.a_bk;
+          uint32_t* sdst = reinterpret_cast<uint32_t*>(sbuf + stg_off);
+          const int pstride_w = (b.nkb * b.run_bytes) >> 2;  // one position plane, in words
+          uint32_t rs_mine = 0;  // row sum of position (lane & 15), see below
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) {
+              const int p = 4 * a + bb;
+              const float tmin = s_tmin[p], rcp = s_rcp[p];
+              const float2 v2[2] = {dA[a][bb], dB[a][bb]};
+              float2 dd[2], gq[2], r[2];
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                dd[h] = sub2(v2[h], bcast2(tmin));
+                if (STATIC) {
+                  float2 qq = mul2_rn(dd[h], bcast2(rcp));
+                  qq.x = fminf(fmaxf(qq.x, 0.0f), top);  // NaN -> 0 like quant.hpp:81
+                  qq.y = fminf(fmaxf(qq.y, 0.0f), top);
+                  gq[h] = add2(qq, bcast2(kMagic));
+                  r[h] = sub2(qq, sub2(gq[h], bcast2(kMagic)));
+                } else {
+                  // n = rint(d * rcp) via the magic addend, r = d * rcp - n
+                  // exactly (one rounding); see input_quant_kernel.
+                  gq[h] = fma2(dd[h], bcast2(rcp), bcast2(kMagic));
+                  r[h] = fma2(dd[h], bcast2(rcp), sub2(bcast2(kMagic), gq[h]));
+                }
+              }
+              const uint32_t w01 = __byte_perm(__float_as_uint(gq[0].x), __float_as_uint(gq[0].y), 0x0040);
+              const uint32_t w23 = __byte_perm(__float_as_uint(gq[1].x), __float_as_uint(gq[1].y), 0x0040);
+              uint32_t word = __byte_perm(w01, w23, 0x5410);
+              const float rmax = fmax3_nan(fmax3_nan(fabsf(r[0].x), fabsf(r[0].y), fabsf(r[1].x)),
+                                           fabsf(r[1].y), 0.0f);
+              if (__builtin_expect(!(rmax < kTieGuard), 0)) {
+                // Rare (~1e-4 per value): re-derive the 4 codes exactly.
+                const float sc = s_scale[p];
+                const float vv[4] = {v2[0].x, v2[0].y, v2[1].x, v2[1].y};
+                const float dv[4] = {dd[0].x, dd[0].y, dd[1].x, dd[1].y};
+                const float gv[4] = {gq[0].x, gq[0].y, gq[1].x, gq[1].y};
+                const float rv[4] = {r[0].x, r[0].y, r[1].x, r[1].y};
+                word = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  uint32_t c;
+                  if (STATIC)
+                    c = quantize_code(vv[e], tmin, sc, top);
+                  else
+                    c = (fabsf(rv[e]) < kTieGuard) ? (__float_as_uint(gv[e]) & 0xFFu)
+                                                   : band_exact_code(dv[e], sc, gv[e], rv[e], top);
+                  word |= c << (8 * e);
+                }
+              }
+              word = cvalid ? word : 0u;
+              if (active) sdst[image_plane(p) * pstride_w] = word;
+              // Row sums (lowpgemm.hpp:121-123): the thread's 4 codes, then one
+              // warp reduction; at QPT = 16 a warp holds two tiles (16-bit halves).
+              uint32_t part = __dp4a(word, 0x01010101u, 0u);
+              if (QPT == 16) part <<= 16 * ((lane >> 4) & 1);
+              const uint32_t tot = __reduce_add_sync(0xffffffffu, part);
+              if ((lane & 15) == p) rs_mine = tot;
+            }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&stage_full[buf]);
+          // Lane l writes the row sum of position l & 15 for its tile.
+          {
+            const int half = (lane >> 4) & 1;
+            uint32_t val;
+            int tl;
+            if (QPT == 16) {
+              val = (rs_mine >> (16 * half)) & 0xFFFFu;
+              tl = (warp * 32 + half * 16) / QPT;
+            } else {
+              val = rs_mine;
+              tl = (warp * 32) / QPT;
+            }
+            const bool writer = (QPT == 16) || lane < 16;
+            if (writer && tl < it.ntj) {
+              const int mm = (it.img * g.TH + ti) * g.TW + it.tj0 + tl;
+              int32_t* dst = rowsum + static_cast<long long>(lane & 15) * g.rs_pitch + mm;
+              if (b.nbc == 1 && QPT <= 32)
+                *dst = static_cast<int32_t>(val);
+              else
+                atomicAdd(dst, static_cast<int32_t>(val));
+            }
           }
         }
       }
-      // Rows 2(ti - ti0) and +1 are free: load the rows ring slots ahead.
-      if (tid == 0) {
-        const int knext = kr + 2 + b.ring - 2;  // first row not yet issued: kr + 4 + (ring - 4)
-        for (int k = knext; k < knext + 2 && k < nrows; ++k)
-          if (k >= b.ring) issue_row(it, k);
-      }
+      kbase += nrows;
     }
-    kbase += nrows;
-    __syncthreads();  // the next item reuses the ring
   }
 
   if (MODE == kRangeMode) {
@@ -345,8 +370,6 @@ __global__ void __launch_bounds__(kBandThreads, 2)
       __syncthreads();
       make_epilogue_consts(st, g.C);
     }
-  } else {
-    if (lane == 0) bulk_wait_all();
   }
 }
 
@@ -369,7 +392,7 @@ cudaError_t launch_band(const CUtensorMap* tmX, uint8_t* codes, int32_t* rowsum,
     if (e != cudaSuccess) return e;
     configured[fi] = smem;
   }
-  fn<<<b.grid, kBandThreads, smem, s>>>(*tmX, codes, rowsum, partials, st, g, b);
+  fn<<<b.grid, kBandThreads + 32, smem, s>>>(*tmX, codes, rowsum, partials, st, g, b);
   return cudaGetLastError();
 }
 
