@@ -362,8 +362,13 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
         b.slot_bytes = b.box_w * chb * 4;
         b.run_bytes = b.tws * p->BK;
         b.stg_bytes = 16 * b.nkb * b.run_bytes;
-        b.ring = 6;
-        if (size_t(b.ring) * b.slot_bytes + 2 * size_t(b.stg_bytes) + 128 > 110 * 1024) continue;
+        // Ring depth: as many row slots as two CTAs per SM can hold (the
+        // loader runs ring - 4 rows ahead of the compute warps), <= 16.
+        b.ring = 16;
+        while (b.ring > 6 &&
+               2 * (size_t(b.ring) * b.slot_bytes + 2 * size_t(b.stg_bytes) + 2048) > 225 * 1024)
+          --b.ring;
+        if (2 * (size_t(b.ring) * b.slot_bytes + 2 * size_t(b.stg_bytes) + 2048) > 225 * 1024) continue;
         // Tile rows per item: enough items for ~4 waves of 2 CTAs per SM.
         const long long per = static_cast<long long>(spec->n) * b.nbc * b.ncs;
         b.nseg = 1;
