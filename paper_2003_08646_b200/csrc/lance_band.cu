@@ -114,6 +114,20 @@ __device__ __forceinline__ void band_transform(float2 (&d)[4][4]) {
   }
 }
 
+// Profiling trace (built with -DLANCE_BAND_TRACE): CTA 0 clock64 stamps.
+#ifdef LANCE_BAND_TRACE
+__device__ unsigned long long g_band_trace[8 * 4096];
+#endif
+template <int MODE>
+__device__ __forceinline__ void band_trace(int slot, int i) {
+#ifdef LANCE_BAND_TRACE
+  if (blockIdx.x == 0 && i < 4096) g_band_trace[(slot + 4 * MODE) * 4096 + i] = clock64();
+#else
+  (void)slot;
+  (void)i;
+#endif
+}
+
 // ---------------------------------------------------------------- kernel
 // Warp-specialised: warps 0 .. NCW-1 compute (thread = tile x channel quad),
 // the last warp's lane 0 streams input rows into the ring and writes staged
@@ -176,6 +190,7 @@ __global__ void __launch_bounds__(kBandThreads + 32, 2)
         mbar_arrive_expect_tx(&row_full[slot], static_cast<uint32_t>(b.slot_bytes));
         tma_load_4d(ring + static_cast<size_t>(slot) * slot_floats, &tmX, it.band * b.chb,
                     2 * it.tj0 - g.pad, 2 * it.ti0 - g.pad + k, it.img, &row_full[slot]);
+        band_trace<MODE>(0, static_cast<int>(kg));
       };
       for (long long itn = blockIdx.x; itn < b.items; itn += gridDim.x) {
         const BandItem it = band_item(b, g, itn);
@@ -185,6 +200,7 @@ __global__ void __launch_bounds__(kBandThreads + 32, 2)
           const int i = ti - it.ti0;
           const uint32_t buf = iter & 1u;
           mbar_wait(&stage_full[buf], (iter >> 1) & 1u);  // computed (and done reading rows)
+          band_trace<MODE>(3, static_cast<int>(iter));
           // Rows 2i, 2i+1 are free: refill their slots ring rows ahead.
           for (int k = 2 * i + b.ring; k < 2 * i + b.ring + 2 && k < nrows; ++k) issue_row(it, k);
           if (MODE == kQuantMode) {
@@ -234,6 +250,7 @@ __global__ void __launch_bounds__(kBandThreads + 32, 2)
           const uint32_t kg = kbase + kr + a;
           const int slot = static_cast<int>(kg % b.ring);
           mbar_wait(&row_full[slot], (kg / b.ring) & 1u);
+          if (tid == 0) band_trace<MODE>(1, static_cast<int>(kg));
           const float* row = ring + static_cast<size_t>(slot) * slot_floats + (2 * tj) * b.chb + 4 * q;
 #pragma unroll
           for (int bb = 0; bb < 4; ++bb) {
@@ -259,6 +276,7 @@ __global__ void __launch_bounds__(kBandThreads + 32, 2)
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&stage_full[buf]);  // rows of this tile row consumed
+          if (tid == 0) band_trace<MODE>(2, static_cast<int>(iter));
         } else {
           // ---- quantise (quant.hpp:77-84) into the staging buffer ----
           mbar_wait(&stage_empty[buf], ((iter >> 1) & 1u) ^ 1u);
@@ -397,3 +415,9 @@ cudaError_t launch_band(const CUtensorMap* tmX, uint8_t* codes, int32_t* rowsum,
 }
 
 }  // namespace lance_dev
+
+#ifdef LANCE_BAND_TRACE
+extern "C" __attribute__((visibility("default"))) int lance_debug_band_trace(void* host, size_t bytes) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, lance_dev::g_band_trace, bytes));
+}
+#endif
