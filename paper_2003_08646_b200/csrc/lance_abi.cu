@@ -364,10 +364,10 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
         b.stg_bytes = 16 * b.nkb * b.run_bytes;
         // Ring depth: as many row slots as two CTAs per SM can hold (the
         // loader runs ring - 4 rows ahead of the compute warps), <= 16.
-        b.ring = 16;
+        b.ring = 16;  // even: slots are used in row pairs
         while (b.ring > 6 &&
                2 * (size_t(b.ring) * b.slot_bytes + 2 * size_t(b.stg_bytes) + 2048) > 225 * 1024)
-          --b.ring;
+          b.ring -= 2;
         if (2 * (size_t(b.ring) * b.slot_bytes + 2 * size_t(b.stg_bytes) + 2048) > 225 * 1024) continue;
         // Tile rows per item: enough items for ~4 waves of 2 CTAs per SM.
         const long long per = static_cast<long long>(spec->n) * b.nbc * b.ncs;

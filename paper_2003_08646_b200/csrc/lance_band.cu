@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kBandThreads + 32, 2)
     s_scale[tid] = st->a_scale[tid];
     s_rcp[tid] = st->a_rcp[tid];
   }
-  if (tid < b.ring) mbar_init(&row_full[tid], 1);
+  if (tid < (b.ring >> 1)) mbar_init(&row_full[tid], 1);
   if (tid < 2) {
     mbar_init(&stage_full[tid], NCW);
     mbar_init(&stage_empty[tid], 1);
@@ -182,27 +182,30 @@ __global__ void __launch_bounds__(kBandThreads + 32, 2)
   if (is_ctrl) {
     // ------------------------------------------------ loader / storer
     if (lane == 0) {
-      uint32_t kbase = 0;  // CTA row counter at the current item's row 0
+      uint32_t kbase = 0;  // CTA row-pair counter at the current item's pair 0
       uint32_t iter = 0;   // tile rows of this CTA (staging parity)
-      auto issue_row = [&](const BandItem& it, int k) {
-        const uint32_t kg = kbase + k;
-        const int slot = static_cast<int>(kg % b.ring);
-        mbar_arrive_expect_tx(&row_full[slot], static_cast<uint32_t>(b.slot_bytes));
-        tma_load_4d(ring + static_cast<size_t>(slot) * slot_floats, &tmX, it.band * b.chb,
-                    2 * it.tj0 - g.pad, 2 * it.ti0 - g.pad + k, it.img, &row_full[slot]);
+      const int npr = b.ring >> 1;  // pair slots
+      // Pair kp = input rows 2kp, 2kp + 1 of the item -> slots 2ps, 2ps + 1, one barrier.
+      auto issue_pair = [&](const BandItem& it, int kp) {
+        const uint32_t kg = kbase + kp;
+        const int ps = static_cast<int>(kg % npr);
+        mbar_arrive_expect_tx(&row_full[ps], 2u * static_cast<uint32_t>(b.slot_bytes));
+        for (int r = 0; r < 2; ++r)
+          tma_load_4d(ring + static_cast<size_t>(2 * ps + r) * slot_floats, &tmX, it.band * b.chb,
+                      2 * it.tj0 - g.pad, 2 * it.ti0 - g.pad + 2 * kp + r, it.img, &row_full[ps]);
         band_trace<MODE>(0, static_cast<int>(kg));
       };
       for (long long itn = blockIdx.x; itn < b.items; itn += gridDim.x) {
         const BandItem it = band_item(b, g, itn);
-        const int nrows = 2 * (it.ti1 - it.ti0) + 2;
-        for (int k = 0; k < nrows && k < b.ring; ++k) issue_row(it, k);
+        const int npairs = (it.ti1 - it.ti0) + 1;
+        for (int kp = 0; kp < npairs && kp < npr; ++kp) issue_pair(it, kp);
         for (int ti = it.ti0; ti < it.ti1; ++ti, ++iter) {
           const int i = ti - it.ti0;
           const uint32_t buf = iter & 1u;
           mbar_wait(&stage_full[buf], (iter >> 1) & 1u);  // computed (and done reading rows)
           band_trace<MODE>(3, static_cast<int>(iter));
-          // Rows 2i, 2i+1 are free: refill their slots ring rows ahead.
-          for (int k = 2 * i + b.ring; k < 2 * i + b.ring + 2 && k < nrows; ++k) issue_row(it, k);
+          // Pair i (rows 2i, 2i+1) is free: refill its slots npr pairs ahead.
+          if (i + npr < npairs) issue_pair(it, i + npr);
           if (MODE == kQuantMode) {
             // Codes: per (position plane, k chunk) the slice's ntj image rows
             // are contiguous in global memory, except across a 128-row edge.
@@ -229,28 +232,33 @@ __global__ void __launch_bounds__(kBandThreads + 32, 2)
           }
           mbar_arrive(&stage_empty[buf]);
         }
-        kbase += nrows;
+        kbase += npairs;
       }
       if (MODE == kQuantMode) bulk_wait_all();
     }
   } else {
     // ------------------------------------------------ compute warps
     uint32_t kbase = 0, iter = 0;
+    const int npr = b.ring >> 1;
     for (long long itn = blockIdx.x; itn < b.items; itn += gridDim.x) {
       const BandItem it = band_item(b, g, itn);
-      const int nrows = 2 * (it.ti1 - it.ti0) + 2;
+      const int npairs = (it.ti1 - it.ti0) + 1;
       const int c0 = it.band * b.chb + 4 * q;  // this thread's first channel
       const bool active = tj < it.ntj;
       const bool cvalid = active && c0 < g.C;  // C % 4 == 0 on this path
+      {
+        const uint32_t kg = kbase;  // pair 0 of the item
+        mbar_wait(&row_full[kg % npr], (kg / npr) & 1u);
+      }
       for (int ti = it.ti0; ti < it.ti1; ++ti, ++iter) {
-        const int kr = 2 * (ti - it.ti0);  // first of the 4 rows of this tile row
-        float2 dA[4][4], dB[4][4];         // channels (c0, c0+1) and (c0+2, c0+3)
+        const int i = ti - it.ti0;  // tile row i uses pairs i and i + 1
+        const uint32_t kg1 = kbase + i + 1;
+        mbar_wait(&row_full[kg1 % npr], (kg1 / npr) & 1u);
+        if (tid == 0) band_trace<MODE>(1, static_cast<int>(kg1));
+        float2 dA[4][4], dB[4][4];  // channels (c0, c0+1) and (c0+2, c0+3)
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
-          const uint32_t kg = kbase + kr + a;
-          const int slot = static_cast<int>(kg % b.ring);
-          mbar_wait(&row_full[slot], (kg / b.ring) & 1u);
-          if (tid == 0) band_trace<MODE>(1, static_cast<int>(kg));
+          const int slot = static_cast<int>((2 * ((kbase + i + (a >> 1)) % npr)) + (a & 1));
           const float* row = ring + static_cast<size_t>(slot) * slot_floats + (2 * tj) * b.chb + 4 * q;
 #pragma unroll
           for (int bb = 0; bb < 4; ++bb) {
@@ -377,7 +385,7 @@ __global__ void __launch_bounds__(kBandThreads + 32, 2)
           }
         }
       }
-      kbase += nrows;
+      kbase += npairs;
     }
   }
 

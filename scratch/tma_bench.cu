@@ -37,7 +37,11 @@ __global__ void __launch_bounds__(640, 1) stream_kernel(const uint8_t* src, size
       mbar_arrive_expect_tx(&full[s], stage_bytes);
       // mode 0: one copy; mode 1: 4/5 of the stage streamed + 1/5 from a shared
       // 64 KB region (all CTAs); mode 2: stage as 2 copies, both streamed.
-      const size_t off = c * (size_t)stage_bytes;
+      // wrap == 1: CTA-private contiguous regions (each CTA streams its own
+      // slab) instead of the grid-interleaved sweep.
+      const size_t nper = nchunks / gridDim.x;
+      const size_t off = (wrap == 1) ? ((size_t)blockIdx.x * nper + (c / gridDim.x)) * stage_bytes
+                                     : c * (size_t)stage_bytes;
       if (mode == 0) {
         bulk_load(smem + (size_t)s * stage_bytes, src + off, stage_bytes, &full[s]);
       } else if (mode == 1) {
@@ -81,12 +85,12 @@ int main() {
   int sms = 148; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  const int sizes[] = {10240, 20480, 40960};
+  const int sizes[] = {8192, 16384};
   const int depths[] = {4, 8, 16};
-  const size_t wraps[] = {bytes};
+  const size_t wraps[] = {bytes, 1};
   const char* names[] = {"one copy", "A+sharedB", "two copies"};
   for (size_t wrap : wraps)
-  for (int mode = 0; mode < 3; ++mode)
+  for (int mode = 0; mode < 1; ++mode)
     for (int sb : sizes)
       for (int d : depths) {
         const size_t smem = (size_t)d * sb + 2 * d * 8 + 64;
@@ -98,7 +102,7 @@ int main() {
         for (int r = 0; r < 3; ++r) stream_kernel<<<sms, thr, smem>>>(src, bytes, sb, d, mode, sink, wrap);
         cudaEventRecord(e1); cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1);
-        printf("%s %-14s stage=%6d depth=%2d : %7.0f GB/s  (%s)\n", wrap == bytes ? "HBM" : "L2 ",
+        printf("%s %-14s stage=%6d depth=%2d : %7.0f GB/s  (%s)\n", wrap == bytes ? "interleaved" : "cta-slabs  ",
                names[mode], sb, d, 3.0 * bytes / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
       }
   return 0;
