@@ -144,7 +144,8 @@ __global__ void __launch_bounds__(kBandThreads + 32, 2)
                 LanceDevState* __restrict__ st, InGeom g, BandGeom b) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ float s_tmin[16], s_scale[16], s_rcp[16];
-  __shared__ uint64_t row_full[16], stage_full[2], stage_empty[2];
+  __shared__ uint64_t row_full[16], stage_full[2], stage_empty[2], item_full[4], item_empty[4];
+  __shared__ long long s_items[4];
   __shared__ float s_red[kBandThreads + 32];
 
   uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
@@ -168,6 +169,10 @@ __global__ void __launch_bounds__(kBandThreads + 32, 2)
     mbar_init(&stage_full[tid], NCW);
     mbar_init(&stage_empty[tid], 1);
   }
+  if (tid < 4) {
+    mbar_init(&item_full[tid], 1);
+    mbar_init(&item_empty[tid], NCW);
+  }
   fence_barrier_init();
   __syncthreads();
   const float top = static_cast<float>((1 << st->bits_i) - 1);
@@ -181,31 +186,70 @@ __global__ void __launch_bounds__(kBandThreads + 32, 2)
 
   if (is_ctrl) {
     // ------------------------------------------------ loader / storer
+    // Items are taken dynamically (one atomic counter per launch) and
+    // published to the compute warps through a 4-slot item ring; row pairs are
+    // streamed continuously across item boundaries (flat pair numbering).
     if (lane == 0) {
-      uint32_t kbase = 0;  // CTA row-pair counter at the current item's pair 0
-      uint32_t iter = 0;   // tile rows of this CTA (staging parity)
       const int npr = b.ring >> 1;  // pair slots
-      // Pair kp = input rows 2kp, 2kp + 1 of the item -> slots 2ps, 2ps + 1, one barrier.
-      auto issue_pair = [&](const BandItem& it, int kp) {
-        const uint32_t kg = kbase + kp;
-        const int ps = static_cast<int>(kg % npr);
+      struct QItem {
+        BandItem it;
+        int ntr;
+        bool last;  // the sentinel
+      };
+      // Loader-private copies: the loader issues at most npr <= 8 pairs ahead
+      // and every item has >= 2 pairs, so <= 5 items are in flight: 8 slots.
+      QItem q[8];
+      int k_pub = 0;                 // items published (incl. the final sentinel)
+      bool exhausted = false;
+      int ci_k = -1, ci_next = 0;    // item being issued (queue index), its next pair
+      uint32_t flat_issued = 0;      // row pairs issued so far
+      auto fetch_item = [&]() -> bool {
+        const int slot = k_pub & 3;
+        mbar_wait(&item_empty[slot], ((k_pub >> 2) & 1u) ^ 1u);
+        long long idx = static_cast<long long>(atomicAdd(&st->band_ctr[MODE], 1u));
+        if (idx >= b.items) idx = -1;
+        s_items[slot] = idx;
+        mbar_arrive(&item_full[slot]);
+        QItem& qi = q[k_pub & 7];
+        qi.last = idx < 0;
+        if (idx < 0) {
+          exhausted = true;
+          ++k_pub;
+          return false;
+        }
+        qi.it = band_item(b, g, idx);
+        qi.ntr = qi.it.ti1 - qi.it.ti0;
+        ci_k = k_pub++;
+        ci_next = 0;
+        return true;
+      };
+      auto issue_next_pair = [&]() -> bool {
+        if (exhausted) return false;
+        if (ci_k < 0 || ci_next == q[ci_k & 7].ntr + 1)
+          if (!fetch_item()) return false;
+        const BandItem& it = q[ci_k & 7].it;
+        const int ps = static_cast<int>(flat_issued % npr);
         mbar_arrive_expect_tx(&row_full[ps], 2u * static_cast<uint32_t>(b.slot_bytes));
         for (int r = 0; r < 2; ++r)
           tma_load_4d(ring + static_cast<size_t>(2 * ps + r) * slot_floats, &tmX, it.band * b.chb,
-                      2 * it.tj0 - g.pad, 2 * it.ti0 - g.pad + 2 * kp + r, it.img, &row_full[ps]);
-        band_trace<MODE>(0, static_cast<int>(kg));
+                      2 * it.tj0 - g.pad, 2 * it.ti0 - g.pad + 2 * ci_next + r, it.img, &row_full[ps]);
+        band_trace<MODE>(0, static_cast<int>(flat_issued));
+        ++ci_next;
+        ++flat_issued;
+        return true;
       };
-      for (long long itn = blockIdx.x; itn < b.items; itn += gridDim.x) {
-        const BandItem it = band_item(b, g, itn);
-        const int npairs = (it.ti1 - it.ti0) + 1;
-        for (int kp = 0; kp < npairs && kp < npr; ++kp) issue_pair(it, kp);
-        for (int ti = it.ti0; ti < it.ti1; ++ti, ++iter) {
-          const int i = ti - it.ti0;
+      while (flat_issued < static_cast<uint32_t>(npr) && issue_next_pair()) {
+      }
+      uint32_t freed = 0, iter = 0;
+      for (int k_con = 0; k_con < k_pub; ++k_con) {
+        if (q[k_con & 7].last) break;  // sentinel
+        const BandItem it = q[k_con & 7].it;
+        const int ntr = q[k_con & 7].ntr;
+        for (int i = 0; i < ntr; ++i, ++iter) {
+          const int ti = it.ti0 + i;
           const uint32_t buf = iter & 1u;
           mbar_wait(&stage_full[buf], (iter >> 1) & 1u);  // computed (and done reading rows)
           band_trace<MODE>(3, static_cast<int>(iter));
-          // Pair i (rows 2i, 2i+1) is free: refill its slots npr pairs ahead.
-          if (i + npr < npairs) issue_pair(it, i + npr);
           if (MODE == kQuantMode) {
             // Codes: per (position plane, k chunk) the slice's ntj image rows
             // are contiguous in global memory, except across a 128-row edge.
@@ -231,16 +275,35 @@ __global__ void __launch_bounds__(kBandThreads + 32, 2)
             bulk_wait_read_all();  // this buffer may be refilled now
           }
           mbar_arrive(&stage_empty[buf]);
+          // Tile row i frees pair i (and, being the item's last, pair i + 1).
+          freed += (i == ntr - 1) ? 2u : 1u;
+          while (flat_issued < freed + npr && issue_next_pair()) {
+          }
         }
-        kbase += npairs;
+      }
+      if (!exhausted) {  // publish the sentinel if the issue side never needed to
+        while (issue_next_pair()) {
+        }
       }
       if (MODE == kQuantMode) bulk_wait_all();
+      // The last CTA to finish fetching resets the counter for the next launch.
+      if (atomicAdd(&st->band_done[MODE], 1u) == gridDim.x - 1) {
+        st->band_ctr[MODE] = 0u;
+        st->band_done[MODE] = 0u;
+        __threadfence();
+      }
     }
   } else {
     // ------------------------------------------------ compute warps
     uint32_t kbase = 0, iter = 0;
     const int npr = b.ring >> 1;
-    for (long long itn = blockIdx.x; itn < b.items; itn += gridDim.x) {
+    for (int k = 0;; ++k) {
+      const int islot = k & 3;
+      mbar_wait(&item_full[islot], (k >> 2) & 1u);
+      const long long itn = s_items[islot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&item_empty[islot]);
+      if (itn < 0) break;
       const BandItem it = band_item(b, g, itn);
       const int npairs = (it.ti1 - it.ti0) + 1;
       const int c0 = it.band * b.chb + 4 * q;  // this thread's first channel

@@ -28,6 +28,7 @@ struct LanceDevState {
   int bits_i, bits_w;
   int nan_in, nan_w;
   unsigned int ticket_in, ticket_w;
+  unsigned int band_ctr[2], band_done[2];  // dynamic work counters of the band kernels
 };
 
 // Input-side geometry shared by the range pass (K0) and the quantiser (K1).
