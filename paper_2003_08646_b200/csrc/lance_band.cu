@@ -334,6 +334,9 @@ __global__ void __launch_bounds__(kBandThreads + 32, 2)
         band_transform(dA);
         band_transform(dB);
         const uint32_t buf = iter & 1u;
+        // Both modes: at most two tile rows ahead of the loader, so the
+        // stage_full phases it waits for can never alias.
+        mbar_wait(&stage_empty[buf], ((iter >> 1) & 1u) ^ 1u);
         if (MODE == kRangeMode) {
           if (cvalid) {
 #pragma unroll
@@ -350,7 +353,6 @@ __global__ void __launch_bounds__(kBandThreads + 32, 2)
           if (tid == 0) band_trace<MODE>(2, static_cast<int>(iter));
         } else {
           // ---- quantise (quant.hpp:77-84) into the staging buffer ----
-          mbar_wait(&stage_empty[buf], ((iter >> 1) & 1u) ^ 1u);
           uint8_t* sbuf = stg + buf * b.stg_bytes;
           const int m = (it.img * g.TH + ti) * g.TW + it.tj0 + tj;
           // Byte offset of (row m, channels c0..c0+3) inside a staged run of
