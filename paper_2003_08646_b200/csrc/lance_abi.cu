@@ -145,6 +145,7 @@ struct lance_plan_s {
   int range_grid = 1, filter_grid = 1;
   InGeom in_geom{};
   BandGeom band{};
+  bool band_k0 = true, band_k1 = false;  // which stages use the band kernels (LANCE_BAND_K0/K1)
   CUtensorMap tmX{};
   const float* tmX_ptr = nullptr;
   FilterGeom f_geom{};
@@ -385,6 +386,8 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
       }
     }
     if (b.enabled) p->range_grid = std::max(p->range_grid, b.grid);
+    if (const char* e = std::getenv("LANCE_BAND_K0")) p->band_k0 = std::atoi(e) != 0;
+    if (const char* e = std::getenv("LANCE_BAND_K1")) p->band_k1 = std::atoi(e) != 0;
   }
   p->small_acc = static_cast<double>(spec->c) * ((1 << cfg->bits_i) - 1) *
                      ((1 << cfg->bits_w) - 1) < 16777216.0;  // every accumulator < 2^24 (exact fp32 bit trick)
@@ -509,7 +512,7 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
       prm.scale[i] = static_params[i].scale;
     }
     LANCE_CUDA(launch_static_params(p->state, prm, p->spec.c, s));
-  } else if (p->band.enabled) {
+  } else if (p->band.enabled && p->band_k0) {
     if (p->tmX_ptr != x_dev) {
       int rc = make_input_map(&p->tmX, x_dev, p->spec, p->band);
       if (rc) return rc;
@@ -523,7 +526,7 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
   }
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[1], s));
-  if (p->band.enabled) {
+  if (p->band.enabled && p->band_k1) {
     if (p->tmX_ptr != x_dev) {
       int rc = make_input_map(&p->tmX, x_dev, p->spec, p->band);
       if (rc) return rc;

@@ -334,6 +334,110 @@ __global__ void __launch_bounds__(256, 2) input_quant_kernel(const float* __rest
   }
 }
 
+// K1 fast path: dynamic params, C % 64 == 0 (every lane owns two real
+// channels), even C.  Same arithmetic as input_quant_kernel without the
+// per-lane validity branches; BK is a template parameter so the UMMA-image
+// address is a handful of shifts per tile, and the tie fix-up is one
+// warp-uniform branch per position pair.
+template <int BK>
+__global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* __restrict__ x,
+                                                                  uint8_t* __restrict__ codes,
+                                                                  int32_t* __restrict__ rowsum,
+                                                                  const LanceDevState* __restrict__ st,
+                                                                  InGeom g) {
+  __shared__ float s_tmin[16], s_scale[16], s_rcp[16];
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < 16) {
+    s_tmin[tid] = st->a_tmin[tid];
+    s_scale[tid] = st->a_scale[tid];
+    s_rcp[tid] = st->a_rcp[tid];
+  }
+  const float top = static_cast<float>((1 << st->bits_i) - 1);
+  __syncthreads();
+  const long long item = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
+  if (item >= g.num_items) return;
+  const StripItem it = strip_item(g, item, lane);
+  const Strip<true> sp(x, g, it);
+  constexpr int kImg = kBM * BK;                       // bytes of one image
+  constexpr uint32_t kMask = BK == 128 ? 7u : (BK == 64 ? 3u : 1u);
+  const int kc = it.ch / BK, cb = it.ch % BK;
+  const long long pstride = static_cast<long long>(g.a_nk) * kImg;  // one position plane
+  const long long blkstride = 16 * pstride;                        // one 128-row block
+  uint8_t* const cbase = codes + static_cast<long long>(kc) * kImg;
+  float2 ta[4], tb[4], tc[4], td[4], pc[4], pd[4];
+  int xx = 2 * it.tj0 - g.pad;
+  sp.column(xx, ta);
+  sp.column(xx + 1, tb);
+  sp.load(xx + 2, pc);
+  sp.load(xx + 3, pd);
+  int m = (it.img * g.TH + it.ti) * g.TW + it.tj0;
+  for (int tj = it.tj0; tj < it.tj1; ++tj, xx += 2, ++m) {
+    float2 v[16];
+    colpass(pc, tc);
+    colpass(pd, td);
+    if (tj + 1 < it.tj1) {  // software prefetch of the next tile's two new columns
+      sp.load(xx + 4, pc);
+      sp.load(xx + 5, pd);
+    }
+    row_pass(ta, tb, tc, td, v);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      ta[a] = tc[a];
+      tb[a] = td[a];
+    }
+    const uint32_t lin = static_cast<uint32_t>((m & (kBM - 1)) * BK + cb);
+    uint8_t* dst = cbase + (m >> 7) * blkstride + (lin ^ (((lin >> 7) & kMask) << 4));
+    uint32_t mine = 0u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float2 dd[2], gq[2], r[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int p = 2 * k + h;
+        const float rcp = s_rcp[p];
+        dd[h] = sub2(v[p], bcast2(s_tmin[p]));
+        gq[h] = fma2(dd[h], bcast2(rcp), bcast2(kMagic));
+        r[h] = fma2(dd[h], bcast2(rcp), sub2(bcast2(kMagic), gq[h]));
+      }
+      uint32_t pk0 = __byte_perm(__float_as_uint(gq[0].x), __float_as_uint(gq[0].y), 0x0040);
+      uint32_t pk1 = __byte_perm(__float_as_uint(gq[1].x), __float_as_uint(gq[1].y), 0x0040);
+      const float rmax = fmax3_nan(fmax3_nan(fabsf(r[0].x), fabsf(r[0].y), fabsf(r[1].x)),
+                                   fabsf(r[1].y), 0.0f);
+      if (__builtin_expect(__any_sync(0xffffffffu, !(rmax < kTieGuard)), 0)) {
+        // Rare (~1e-4 per value): re-derive flagged codes exactly.
+        if (!(rmax < kTieGuard)) {
+          uint32_t c[4];
+          const float dv[4] = {dd[0].x, dd[0].y, dd[1].x, dd[1].y};
+          const float gv[4] = {gq[0].x, gq[0].y, gq[1].x, gq[1].y};
+          const float rv[4] = {r[0].x, r[0].y, r[1].x, r[1].y};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float sc = s_scale[2 * k + (e >> 1)];
+            c[e] = (fabsf(rv[e]) < kTieGuard) ? (__float_as_uint(gv[e]) & 0xFFu)
+                                              : exact_code_near_boundary(dv[e], sc, gv[e], rv[e], top);
+          }
+          pk0 = c[0] | (c[1] << 8);
+          pk1 = c[2] | (c[3] << 8);
+        }
+      }
+      *reinterpret_cast<uint16_t*>(dst + image_plane(2 * k) * pstride) = static_cast<uint16_t>(pk0);
+      *reinterpret_cast<uint16_t*>(dst + image_plane(2 * k + 1) * pstride) = static_cast<uint16_t>(pk1);
+      // Row sums (lowpgemm.hpp:121-123): positions (2k, 2k+1) as 16-bit halves.
+      const uint32_t a = (pk0 & 0xFFFFu) | (pk1 << 16);                  // [p.c0, p.c1, q.c0, q.c1]
+      const uint32_t w = (a & 0x00FF00FFu) + ((a >> 8) & 0x00FF00FFu);  // [p sum | q sum]
+      const uint32_t tot = __reduce_add_sync(0xffffffffu, w);
+      if ((lane >> 1) == k) mine = (lane & 1) ? (tot >> 16) : (tot & 0xFFFFu);
+    }
+    if (lane < 16) {
+      int32_t* rs = rowsum + static_cast<long long>(lane) * g.rs_pitch + m;
+      if (g.nchunks == 1)
+        *rs = static_cast<int32_t>(mine);
+      else  // channel chunks of one tile run in different warps (rowsum pre-zeroed)
+        atomicAdd(rs, static_cast<int32_t>(mine));
+    }
+  }
+}
+
 // Static-params mode: caller-supplied input QuantParams[16].
 __global__ void static_params_kernel(LanceDevState* st, StaticParams prm, int C) {
   if (threadIdx.x < 16) {
@@ -369,6 +473,15 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
                                const LanceDevState* st, const InGeom& g, int vec2,
                                int static_mode, cudaStream_t s) {
   const unsigned grid = static_cast<unsigned>((g.num_items + 7) / 8);
+  if (!static_mode && g.C % 64 == 0) {  // fast path: every lane owns two real channels
+    if (g.a_bk == 128)
+      input_quant_fast_kernel<128><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
+    else if (g.a_bk == 64)
+      input_quant_fast_kernel<64><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
+    else
+      input_quant_fast_kernel<32><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
+    return cudaGetLastError();
+  }
   if (vec2) {
     if (static_mode)
       input_quant_kernel<true, true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
