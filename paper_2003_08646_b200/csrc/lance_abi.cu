@@ -145,7 +145,7 @@ struct lance_plan_s {
   int range_grid = 1, filter_grid = 1;
   InGeom in_geom{};
   BandGeom band{};
-  bool band_k0 = true, band_k1 = false;  // which stages use the band kernels (LANCE_BAND_K0/K1)
+  bool band_k0 = false, band_k1 = false;  // which stages use the band kernels (LANCE_BAND_K0/K1)
   CUtensorMap tmX{};
   const float* tmX_ptr = nullptr;
   FilterGeom f_geom{};

@@ -179,6 +179,60 @@ __global__ void __launch_bounds__(256, 2) input_range_kernel(const float* __rest
   }
 }
 
+// K0 fast path (C % 64 == 0: every lane owns two real channels): the range
+// pass without per-lane validity branches.
+__global__ void __launch_bounds__(256, 2) input_range_fast_kernel(const float* __restrict__ x,
+                                                                  float* __restrict__ partials,
+                                                                  LanceDevState* __restrict__ st,
+                                                                  InGeom g) {
+  __shared__ float s_red[256];
+  float lo[16], hi[16];
+#pragma unroll
+  for (int p = 0; p < 16; ++p) {
+    lo[p] = __int_as_float(0x7f800000);
+    hi[p] = __int_as_float(0xff800000);
+  }
+  const int lane = threadIdx.x & 31;
+  const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  for (long long item = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       item < g.num_items; item += stride) {
+    const StripItem it = strip_item(g, item, lane);
+    const Strip<true> sp(x, g, it);
+    float2 ta[4], tb[4], tc[4], td[4], pc[4], pd[4];
+    int xx = 2 * it.tj0 - g.pad;
+    sp.column(xx, ta);
+    sp.column(xx + 1, tb);
+    sp.load(xx + 2, pc);
+    sp.load(xx + 3, pd);
+    for (int tj = it.tj0; tj < it.tj1; ++tj, xx += 2) {
+      colpass(pc, tc);
+      colpass(pd, td);
+      if (tj + 1 < it.tj1) {  // software prefetch of the next tile's two new columns
+        sp.load(xx + 4, pc);
+        sp.load(xx + 5, pd);
+      }
+      float2 v[16];
+      row_pass(ta, tb, tc, td, v);
+#pragma unroll
+      for (int p = 0; p < 16; ++p) {
+        lo[p] = fmin3_nan(lo[p], v[p].x, v[p].y);
+        hi[p] = fmax3_nan(hi[p], v[p].x, v[p].y);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        ta[a] = tc[a];
+        tb[a] = td[a];
+      }
+    }
+  }
+  if (block_minmax_and_ticket(lo, hi, partials, &st->ticket_in, s_red)) {
+    fit_from_ranges(s_red, g.granularity, st->bits_i, st->a_tmin, st->a_tmax, st->a_scale,
+                    st->a_rcp, &st->nan_in);
+    __syncthreads();
+    make_epilogue_consts(st, g.C);
+  }
+}
+
 // Exact reference code for a value whose fast-path residual flagged it as
 // being near the rounding boundary h = n + 0.5*sign(r) (dynamic params: d >= 0,
 // scale > 0 normal).  roundf(RN(d/s)) crosses to the upper code iff
@@ -462,7 +516,9 @@ int input_range_grid(const InGeom& g, int sm_count) {
 
 cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceDevState* st,
                                const InGeom& g, int vec2, cudaStream_t s) {
-  if (vec2)
+  if (g.C % 64 == 0)
+    input_range_fast_kernel<<<grid, 256, 0, s>>>(x, partials, st, g);
+  else if (vec2)
     input_range_kernel<true><<<grid, 256, 0, s>>>(x, partials, st, g);
   else
     input_range_kernel<false><<<grid, 256, 0, s>>>(x, partials, st, g);
