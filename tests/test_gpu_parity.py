@@ -165,3 +165,34 @@ def test_launch_count_and_native_library():
     assert conv.last_launch_count == 3
     maps = open("/proc/self/maps").read()
     assert "liblance_b200.so" in maps
+
+
+def test_global_params_across_shards(lo):
+    # SURVEY 8(e) mode 2 on one device: two batch shards each run the range
+    # pass, their (min, max) are combined (what the 128-byte all-reduce does
+    # across GPUs), and both shards quantise with the full-batch params: the
+    # concatenated output equals one full-batch reference call bitwise.
+    from paper_2003_08646_b200 import shard
+    spec = Spec(4, 64, 14, 14, 32, 1)
+    x, w = make_inputs(lo.uniform, spec, "relu", 41)
+    wd = torch.from_numpy(w).cuda()
+    convs, los, his = [], [], []
+    for r in range(2):
+        a, b = shard.shard_range(spec.n, 2, r)
+        c = lance.LanceConv(lance.ConvSpec(b - a, spec.c, spec.h, spec.w, spec.k, 1), gemm_cfg())
+        c.set_filters(wd)
+        c.forward(torch.from_numpy(np.ascontiguousarray(x[a:b])).cuda())
+        c.sync()
+        pa, _ = c.params()
+        los.append([q.t_min for q in pa])
+        his.append([q.t_max for q in pa])
+        convs.append((c, a, b))
+    params = shard.params_from_minmax(np.min(los, axis=0), np.max(his, axis=0), 8)
+    ys = []
+    for c, a, b in convs:
+        y = c.forward(torch.from_numpy(np.ascontiguousarray(x[a:b])).cuda(), params=params)
+        c.sync()
+        ys.append(y.cpu().numpy())
+    got = np.concatenate(ys)
+    ref = lo.lance_gemm(spec, x, w)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), mismatch_report(got, ref)
