@@ -547,9 +547,9 @@ static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
   }
   const int sms = (dev >= 0 && dev < 64) ? sm_count[dev] : 148;
   // Cluster size: cs CTAs per m-tile (divides the filter tiles; no resident B).
+  // Default 1: measured, A multicast does not pay off here (profiles/).
   int cs = 1;
   if (!b_res) {
-    cs = (g.num_n_tiles % 4 == 0) ? 4 : (g.num_n_tiles % 2 == 0 ? 2 : 1);
     if (const char* e = std::getenv("LANCE_GEMM_CLUSTER")) {
       const int v = std::atoi(e);
       if ((v == 1 || v == 2 || v == 4) && g.num_n_tiles % v == 0) cs = v;
@@ -570,8 +570,13 @@ static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
   attr[0].val.clusterDim.z = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  cudaError_t le = cudaLaunchKernelEx(&lc, gemm_epilogue_kernel<BK, BN, SMALL, DUMP>, codes_a, codes_w,
-                                      *tmR, colsum, st, y, acc_dump, bias, relu, g);
+  cudaError_t le = cudaSuccess;
+  if (cs == 1)
+    gemm_epilogue_kernel<BK, BN, SMALL, DUMP><<<lc.gridDim, kGemmThreadsP, smem, s>>>(
+        codes_a, codes_w, *tmR, colsum, st, y, acc_dump, bias, relu, g);
+  else
+    le = cudaLaunchKernelEx(&lc, gemm_epilogue_kernel<BK, BN, SMALL, DUMP>, codes_a, codes_w, *tmR,
+                            colsum, st, y, acc_dump, bias, relu, g);
   if (le != cudaSuccess) return le;
   return cudaGetLastError();
 }
