@@ -179,19 +179,12 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = g.num_n_tiles;
   const int K_pad = nt * BN;
-  // Clusters of cs CTAs share an m-tile and take cs consecutive filter tiles;
-  // each CTA loads 1/cs of every A image and multicasts it to the cluster.
-  const int cs = g.cluster;
-  const int crank = cs > 1 ? static_cast<int>(cluster_ctarank()) : 0;
-  const uint16_t cmask = static_cast<uint16_t>((1u << cs) - 1u);
-  const int cid = blockIdx.x / cs, ncl = gridDim.x / cs;
-  const int ngrp = nt / cs;
-  const int num_groups = ((g.M + kBM - 1) / kBM) * ngrp;
+  const int num_tiles = ((g.M + kBM - 1) / kBM) * nt;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], cs);  // every cluster CTA's MMA releases the slot
+      mbar_init(&empty_bar[s], 1);
     }
     for (int b = 0; b < 4; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -224,10 +217,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       if (e == 0) s_fast = fast ? 1 : 0;
     }
   }
-  if (cs > 1)
-    cluster_sync();  // barrier inits visible cluster-wide before any multicast
-  else
-    __syncthreads();
+  __syncthreads();
 
   if (warp >= kEpiWarps) {
     setmaxnreg_dec<kCtrlRegs>();
@@ -241,8 +231,8 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       int s = 0;
       uint32_t ph = 0;
       uint32_t lt = 0;
-      for (int gi = cid; gi < num_groups; gi += ncl, ++lt) {
-        const int mt = gi / ngrp, ntile = (gi - mt * ngrp) * cs + crank;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+        const int mt = t / nt, ntile = t % nt;
         const int m0 = mt * kBM;
         // Operand images of this tile (lance_kernels.cuh umma_image_offset).
         const uint8_t* a_tile = codes_a + static_cast<long long>(mt) * 16 * nk * Cfg::kABytes;
@@ -259,13 +249,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
               mbar_wait(&empty_bar[s], ph ^ 1u);
               uint8_t* sa = stage_base + static_cast<size_t>(s) * stage_bytes;
               mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
-              if (cs > 1) {
-                const uint32_t part = Cfg::kABytes / cs;  // 128 / cs whole image rows
-                bulk_load_mc(sa + crank * part, a_tile + (u0 + kc) * Cfg::kABytes + crank * part, part,
-                             &full_bar[s], cmask);
-              } else {
-                bulk_load(sa, a_tile + (u0 + kc) * Cfg::kABytes, Cfg::kABytes, &full_bar[s]);
-              }
+              bulk_load(sa, a_tile + (u0 + kc) * Cfg::kABytes, Cfg::kABytes, &full_bar[s]);
               if (!b_res)
                 bulk_load(sa + Cfg::kABytes, b_tile + (u0 + kc) * Cfg::kBBytes, Cfg::kBBytes,
                           &full_bar[s]);
@@ -290,7 +274,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         int s = 0;
         uint32_t ph = 0;
         uint32_t grp = 0;
-        for (int gi = cid; gi < num_groups; gi += ncl) {
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
           for (int j = 0; j < 4; ++j, ++grp) {
             const uint32_t buf = grp % NB;
             mbar_wait(&acc_empty[buf], (grp / NB) & 1u);  // epilogue drained it
@@ -312,10 +296,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
                   umma_i8(d_base + static_cast<uint32_t>(a * BN), adesc, bdesc, kIdesc,
                           (kc > 0 || kk > 0) ? 1u : 0u);
                 }
-                if (cs > 1)
-                  umma_commit_mc(&empty_bar[s], cmask);
-                else
-                  umma_commit(&empty_bar[s]);
+                umma_commit(&empty_bar[s]);
                 if (++s == stages) {
                   s = 0;
                   ph ^= 1u;
@@ -346,9 +327,8 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     const bool fast = s_fast != 0;
     uint32_t grp = 0;
     uint32_t lt = 0;
-    for (int gi = cid; gi < num_groups; gi += ncl, ++lt) {
-      const int mt = gi / ngrp;
-      const int m0 = mt * kBM, n0 = ((gi - mt * ngrp) * cs + crank) * BN;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+      const int m0 = (t / nt) * kBM, n0 = (t % nt) * BN;
       const int m = m0 + row;
       const bool row_ok = m < g.M;
       const int kf0 = n0 + f0;
@@ -510,7 +490,6 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     tc_fence_after();
     tmem_dealloc(*tmem_holder, 512);
   }
-  if (cs > 1) cluster_sync();  // no CTA leaves while cluster peers may still signal it
 }
 
 template <int BK, int BN, bool SMALL, bool DUMP>
@@ -546,38 +525,10 @@ static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
     }
   }
   const int sms = (dev >= 0 && dev < 64) ? sm_count[dev] : 148;
-  // Cluster size: cs CTAs per m-tile (divides the filter tiles; no resident B).
-  // Default 1: measured, A multicast does not pay off here (profiles/).
-  int cs = 1;
-  if (!b_res) {
-    if (const char* e = std::getenv("LANCE_GEMM_CLUSTER")) {
-      const int v = std::atoi(e);
-      if ((v == 1 || v == 2 || v == 4) && g.num_n_tiles % v == 0) cs = v;
-    }
-  }
-  g.cluster = cs;
-  const long long groups = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * (g.num_n_tiles / cs);
-  const long long clusters = groups < sms / cs ? groups : sms / cs;
-  cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(static_cast<unsigned>(clusters * cs));
-  lc.blockDim = dim3(kGemmThreadsP);
-  lc.dynamicSmemBytes = smem;
-  lc.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cs;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  lc.attrs = attr;
-  lc.numAttrs = 1;
-  cudaError_t le = cudaSuccess;
-  if (cs == 1)
-    gemm_epilogue_kernel<BK, BN, SMALL, DUMP><<<lc.gridDim, kGemmThreadsP, smem, s>>>(
-        codes_a, codes_w, *tmR, colsum, st, y, acc_dump, bias, relu, g);
-  else
-    le = cudaLaunchKernelEx(&lc, gemm_epilogue_kernel<BK, BN, SMALL, DUMP>, codes_a, codes_w, *tmR,
-                            colsum, st, y, acc_dump, bias, relu, g);
-  if (le != cudaSuccess) return le;
+  const long long tiles = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * g.num_n_tiles;
+  const int grid = static_cast<int>(tiles < sms ? tiles : sms);
+  gemm_epilogue_kernel<BK, BN, SMALL, DUMP><<<grid, kGemmThreadsP, smem, s>>>(
+      codes_a, codes_w, *tmR, colsum, st, y, acc_dump, bias, relu, g);
   return cudaGetLastError();
 }
 

@@ -81,7 +81,6 @@ struct GemmGeom {
   int num_n_tiles;  // K_pad / BN
   int stages;       // shared-memory ring depth (set by the launcher)
   int b_resident;   // B operand resident in shared memory (set by the launcher)
-  int cluster;      // CTAs per cluster sharing A by multicast (set by the launcher)
   int exp;          // experiment switches (LANCE_GEMM_EXP, profiling only; 0 = normal)
   unsigned long long* trace;  // CTA-0 event timestamps (LANCE_GEMM_TRACE, profiling only)
 };
