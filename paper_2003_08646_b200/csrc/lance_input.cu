@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(256, 2) input_quant_kernel(const float* __rest
 // per-lane validity branches; BK is a template parameter so the UMMA-image
 // address is a handful of shifts per tile, and the tie fix-up is one
 // warp-uniform branch per position pair.
-template <int BK>
+template <int BK, int NK>
 __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* __restrict__ x,
                                                                   uint8_t* __restrict__ codes,
                                                                   int32_t* __restrict__ rowsum,
@@ -415,8 +415,8 @@ __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* _
   constexpr int kImg = kBM * BK;                       // bytes of one image
   constexpr uint32_t kMask = BK == 128 ? 7u : (BK == 64 ? 3u : 1u);
   const int kc = it.ch / BK, cb = it.ch % BK;
-  const long long pstride = static_cast<long long>(g.a_nk) * kImg;  // one position plane
-  const long long blkstride = 16 * pstride;                        // one 128-row block
+  constexpr int pstride = NK * kImg;           // one position plane (compile-time: immediate offsets)
+  constexpr long long blkstride = 16LL * pstride;  // one 128-row block
   uint8_t* const cbase = codes + static_cast<long long>(kc) * kImg;
   float2 ta[4], tb[4], tc[4], td[4], pc[4], pd[4];
   int xx = 2 * it.tj0 - g.pad;
@@ -530,13 +530,19 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
                                int static_mode, cudaStream_t s) {
   const unsigned grid = static_cast<unsigned>((g.num_items + 7) / 8);
   if (!static_mode && g.C % 64 == 0) {  // fast path: every lane owns two real channels
-    if (g.a_bk == 128)
-      input_quant_fast_kernel<128><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
-    else if (g.a_bk == 64)
-      input_quant_fast_kernel<64><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
-    else
-      input_quant_fast_kernel<32><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
-    return cudaGetLastError();
+#define LANCE_K1_FAST(BKV, NKV)                                                       \
+  if (g.a_bk == BKV && g.a_nk == NKV) {                                               \
+    input_quant_fast_kernel<BKV, NKV><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g); \
+    return cudaGetLastError();                                                        \
+  }
+    LANCE_K1_FAST(64, 1)
+    LANCE_K1_FAST(128, 1)
+    LANCE_K1_FAST(128, 2)
+    LANCE_K1_FAST(128, 3)
+    LANCE_K1_FAST(128, 4)
+    LANCE_K1_FAST(64, 3)
+    LANCE_K1_FAST(64, 5)
+#undef LANCE_K1_FAST
   }
   if (vec2) {
     if (static_mode)
