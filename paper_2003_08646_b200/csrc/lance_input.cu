@@ -428,26 +428,20 @@ __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* _
   constexpr int pstride = NK * kImg;           // one position plane (compile-time: immediate offsets)
   constexpr long long blkstride = 16LL * pstride;  // one 128-row block
   uint8_t* const cbase = codes + static_cast<long long>(kc) * kImg;
-  // Two tiles of new columns in flight (pc/pd slots 0 and 1): the loads for
-  // tile tj + 2 are issued while tile tj computes.
-  float2 ta[4], tb[4], tc[4], td[4], pc[2][4], pd[2][4];
+  float2 ta[4], tb[4], tc[4], td[4], pc[4], pd[4];
   int xx = 2 * it.tj0 - g.pad;
   sp.column(xx, ta);
   sp.column(xx + 1, tb);
-  sp.load(xx + 2, pc[0]);
-  sp.load(xx + 3, pd[0]);
-  if (it.tj0 + 1 < it.tj1) {
-    sp.load(xx + 4, pc[1]);
-    sp.load(xx + 5, pd[1]);
-  }
-  const int m_first = (it.img * g.TH + it.ti) * g.TW + it.tj0;
-  auto tile = [&](int sl, int tj, int xb, int m) {
+  sp.load(xx + 2, pc);
+  sp.load(xx + 3, pd);
+  int m = (it.img * g.TH + it.ti) * g.TW + it.tj0;
+  for (int tj = it.tj0; tj < it.tj1; ++tj, xx += 2, ++m) {
     float2 v[16];
-    colpass(pc[sl], tc);
-    colpass(pd[sl], td);
-    if (tj + 2 < it.tj1) {  // prefetch two tiles ahead
-      sp.load(xb + 6, pc[sl]);
-      sp.load(xb + 7, pd[sl]);
+    colpass(pc, tc);
+    colpass(pd, td);
+    if (tj + 1 < it.tj1) {  // software prefetch of the next tile's two new columns
+      sp.load(xx + 4, pc);
+      sp.load(xx + 5, pd);
     }
     row_pass(ta, tb, tc, td, v);
 #pragma unroll
@@ -505,10 +499,6 @@ __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* _
       else  // channel chunks of one tile run in different warps (rowsum pre-zeroed)
         atomicAdd(rs, static_cast<int32_t>(mine));
     }
-  };
-  for (int tj = it.tj0; tj < it.tj1; tj += 2, xx += 4) {
-    tile(0, tj, xx, m_first + (tj - it.tj0));
-    if (tj + 1 < it.tj1) tile(1, tj + 1, xx + 2, m_first + (tj + 1 - it.tj0));
   }
 }
 
