@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "lance_common.cuh"
 
@@ -502,6 +503,115 @@ __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* _
   }
 }
 
+template <int BK, int NK>
+__global__ void __launch_bounds__(192, 2) input_quant_fast2_kernel(const float* __restrict__ x,
+                                                                  uint8_t* __restrict__ codes,
+                                                                  int32_t* __restrict__ rowsum,
+                                                                  const LanceDevState* __restrict__ st,
+                                                                  InGeom g) {
+  __shared__ float s_tmin[16], s_scale[16], s_rcp[16];
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < 16) {
+    s_tmin[tid] = st->a_tmin[tid];
+    s_scale[tid] = st->a_scale[tid];
+    s_rcp[tid] = st->a_rcp[tid];
+  }
+  const float top = static_cast<float>((1 << st->bits_i) - 1);
+  __syncthreads();
+  const long long item = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
+  if (item >= g.num_items) return;
+  const StripItem it = strip_item(g, item, lane);
+  const Strip<true> sp(x, g, it);
+  constexpr int kImg = kBM * BK;                       // bytes of one image
+  constexpr uint32_t kMask = BK == 128 ? 7u : (BK == 64 ? 3u : 1u);
+  const int kc = it.ch / BK, cb = it.ch % BK;
+  constexpr int pstride = NK * kImg;           // one position plane (compile-time: immediate offsets)
+  constexpr long long blkstride = 16LL * pstride;  // one 128-row block
+  uint8_t* const cbase = codes + static_cast<long long>(kc) * kImg;
+  // Two tiles of new columns in flight (pc/pd slots 0 and 1): the loads for
+  // tile tj + 2 are issued while tile tj computes.
+  float2 ta[4], tb[4], tc[4], td[4], pc[2][4], pd[2][4];
+  int xx = 2 * it.tj0 - g.pad;
+  sp.column(xx, ta);
+  sp.column(xx + 1, tb);
+  sp.load(xx + 2, pc[0]);
+  sp.load(xx + 3, pd[0]);
+  if (it.tj0 + 1 < it.tj1) {
+    sp.load(xx + 4, pc[1]);
+    sp.load(xx + 5, pd[1]);
+  }
+  const int m_first = (it.img * g.TH + it.ti) * g.TW + it.tj0;
+  auto tile = [&](int sl, int tj, int xb, int m) {
+    float2 v[16];
+    colpass(pc[sl], tc);
+    colpass(pd[sl], td);
+    if (tj + 2 < it.tj1) {  // prefetch two tiles ahead
+      sp.load(xb + 6, pc[sl]);
+      sp.load(xb + 7, pd[sl]);
+    }
+    row_pass(ta, tb, tc, td, v);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      ta[a] = tc[a];
+      tb[a] = td[a];
+    }
+    const uint32_t lin = static_cast<uint32_t>((m & (kBM - 1)) * BK + cb);
+    uint8_t* dst = cbase + (m >> 7) * blkstride + (lin ^ (((lin >> 7) & kMask) << 4));
+    uint32_t mine = 0u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float2 dd[2], gq[2], r[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int p = 2 * k + h;
+        const float rcp = s_rcp[p];
+        dd[h] = sub2(v[p], bcast2(s_tmin[p]));
+        gq[h] = fma2(dd[h], bcast2(rcp), bcast2(kMagic));
+        r[h] = fma2(dd[h], bcast2(rcp), sub2(bcast2(kMagic), gq[h]));
+      }
+      uint32_t pk0 = __byte_perm(__float_as_uint(gq[0].x), __float_as_uint(gq[0].y), 0x0040);
+      uint32_t pk1 = __byte_perm(__float_as_uint(gq[1].x), __float_as_uint(gq[1].y), 0x0040);
+      const float rmax = fmax3_nan(fmax3_nan(fabsf(r[0].x), fabsf(r[0].y), fabsf(r[1].x)),
+                                   fabsf(r[1].y), 0.0f);
+      if (__builtin_expect(__any_sync(0xffffffffu, !(rmax < kTieGuard)), 0)) {
+        // Rare (~1e-4 per value): re-derive flagged codes exactly.
+        if (!(rmax < kTieGuard)) {
+          uint32_t c[4];
+          const float dv[4] = {dd[0].x, dd[0].y, dd[1].x, dd[1].y};
+          const float gv[4] = {gq[0].x, gq[0].y, gq[1].x, gq[1].y};
+          const float rv[4] = {r[0].x, r[0].y, r[1].x, r[1].y};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float sc = s_scale[2 * k + (e >> 1)];
+            c[e] = (fabsf(rv[e]) < kTieGuard) ? (__float_as_uint(gv[e]) & 0xFFu)
+                                              : exact_code_near_boundary(dv[e], sc, gv[e], rv[e], top);
+          }
+          pk0 = c[0] | (c[1] << 8);
+          pk1 = c[2] | (c[3] << 8);
+        }
+      }
+      *reinterpret_cast<uint16_t*>(dst + image_plane(2 * k) * pstride) = static_cast<uint16_t>(pk0);
+      *reinterpret_cast<uint16_t*>(dst + image_plane(2 * k + 1) * pstride) = static_cast<uint16_t>(pk1);
+      // Row sums (lowpgemm.hpp:121-123): positions (2k, 2k+1) as 16-bit halves.
+      const uint32_t a = (pk0 & 0xFFFFu) | (pk1 << 16);                  // [p.c0, p.c1, q.c0, q.c1]
+      const uint32_t w = (a & 0x00FF00FFu) + ((a >> 8) & 0x00FF00FFu);  // [p sum | q sum]
+      const uint32_t tot = __reduce_add_sync(0xffffffffu, w);
+      if ((lane >> 1) == k) mine = (lane & 1) ? (tot >> 16) : (tot & 0xFFFFu);
+    }
+    if (lane < 16) {
+      int32_t* rs = rowsum + static_cast<long long>(lane) * g.rs_pitch + m;
+      if (g.nchunks == 1)
+        *rs = static_cast<int32_t>(mine);
+      else  // channel chunks of one tile run in different warps (rowsum pre-zeroed)
+        atomicAdd(rs, static_cast<int32_t>(mine));
+    }
+  };
+  for (int tj = it.tj0; tj < it.tj1; tj += 2, xx += 4) {
+    tile(0, tj, xx, m_first + (tj - it.tj0));
+    if (tj + 1 < it.tj1) tile(1, tj + 1, xx + 2, m_first + (tj + 1 - it.tj0));
+  }
+}
+
 // Static-params mode: caller-supplied input QuantParams[16].
 __global__ void static_params_kernel(LanceDevState* st, StaticParams prm, int C) {
   if (threadIdx.x < 16) {
@@ -540,10 +650,18 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
                                int static_mode, cudaStream_t s) {
   const unsigned grid = static_cast<unsigned>((g.num_items + 7) / 8);
   if (!static_mode && g.C % 64 == 0) {  // fast path: every lane owns two real channels
-#define LANCE_K1_FAST(BKV, NKV)                                                       \
-  if (g.a_bk == BKV && g.a_nk == NKV) {                                               \
-    input_quant_fast_kernel<BKV, NKV><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g); \
-    return cudaGetLastError();                                                        \
+    static const int depth = [] {
+      const char* e = std::getenv("LANCE_K1_DEPTH");
+      return e ? std::atoi(e) : 1;
+    }();
+#define LANCE_K1_FAST(BKV, NKV)                                                          \
+  if (g.a_bk == BKV && g.a_nk == NKV) {                                                  \
+    if (depth == 2)                                                                      \
+      input_quant_fast2_kernel<BKV, NKV>                                                 \
+          <<<static_cast<unsigned>((g.num_items + 5) / 6), 192, 0, s>>>(x, codes, rowsum, st, g); \
+    else                                                                                 \
+      input_quant_fast_kernel<BKV, NKV><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);  \
+    return cudaGetLastError();                                                           \
   }
     LANCE_K1_FAST(64, 1)
     LANCE_K1_FAST(128, 1)
