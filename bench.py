@@ -330,18 +330,29 @@ def main():
         gbs = stage_bytes_tot[i] / (stage_ms[i] * 1e-3) / 1e9 if stage_ms[i] > 0 else 0.0
         stages[nm] = {"ms_per_step": stage_ms[i] / args.steps, "achieved_gbs": gbs,
                       "frac_hbm": gbs / hbm}
-    dom = int(np.argmax(stage_ms))
+    # Roofline of the dominant kernel on its dominant layer shape: algorithmic
+    # bytes of one launch / its average launch time (CUDA events
+    # on the launch stream), traffic = ncu DRAM bytes of that same launch.
+    shape_ms = {}
+    for (spec, conv, *_), pl in zip(state, per_layer):
+        for si in range(3):
+            key = (si, spec.c, spec.k, spec.h)
+            shape_ms.setdefault(key, []).append(pl["us_per_forward"][si])
+    (dsi, dc, dk, dh), dus = max(shape_ms.items(), key=lambda kv: sum(kv[1]))
+    dom = dsi
+    launch_us = float(np.mean(dus))
+    launch_bytes = stage_bytes(dc, dk, dh, N)[dsi]
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            tj = json.load(f)
-        traffic = tj.get(names[dom])
+            traffic = json.load(f).get(names[dsi], {}).get(f"c{dc}_h{dh}")
     except Exception:
         pass
-    roofline = {"bound": "hbm", "kernel": names[dom], "achieved": stages[names[dom]]["achieved_gbs"],
-                "peak": hbm, "peak_source": hbm_src, "unit": "GB/s",
-                "frac": stages[names[dom]]["achieved_gbs"] / hbm, "traffic": traffic,
-                "algorithmic_bytes_per_step": float(stage_bytes_tot[dom] / args.steps),
+    achieved = launch_bytes / (launch_us * 1e-6) / 1e9
+    roofline = {"bound": "hbm", "kernel": names[dsi], "layer": {"c": dc, "k": dk, "h": dh, "n": N},
+                "achieved": achieved, "peak": hbm, "peak_source": hbm_src, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic,
+                "algorithmic_bytes_per_launch": float(launch_bytes), "launch_us": launch_us,
                 "stages": stages}
     i8 = int8_peak_tops(dev) if rank == 0 else None
     t3 = stage_ms[2] * 1e-3 / args.steps
