@@ -45,7 +45,8 @@
 namespace lance_dev {
 
 constexpr int kEpiWarps = 16;                      // warps 0..15: epilogue (4 warpgroups)
-constexpr int kProducerWarp = 16, kMmaWarp = 17;  // warpgroup 4: producer, MMA, 2 idle
+constexpr int kProducerWarp = 16, kMmaWarp = 17;  // warpgroup 4: producer, MMA,
+constexpr int kRowSumWarp0 = 18;                  // and two warps summing the A rows
 constexpr int kGemmThreadsP = 32 * 20;            // 640
 // Register split (setmaxnreg): the control warpgroup gives its registers to
 // the epilogue warpgroups (S partials of 64-filter tiles live in registers).
@@ -67,7 +68,7 @@ struct GemmCfg {
   // Output staging: per lane quadrant 32 tiles x 2 pixels x BN filters fp32.
   static constexpr uint32_t kOutBytes = 4 * 32 * 2 * BN * 4;
   static constexpr size_t kFixed =
-      1024 /*align*/ + 2 * kRsBytes + kOutBytes + 16 * 8 /*barriers, holder*/;
+      1024 /*align*/ + 2 * kRsBytes + kOutBytes + 32 * 8 /*barriers, holder*/;
 };
 
 // b_res: the whole B operand of the (single) filter tile stays resident in
@@ -139,7 +140,7 @@ template <int BK, int BN, bool SMALL, bool DUMP>
 __global__ void __launch_bounds__(kGemmThreadsP, 1)
     gemm_epilogue_kernel(const uint8_t* __restrict__ codes_a,
                          const uint8_t* __restrict__ codes_w,
-                         const __grid_constant__ CUtensorMap tmR,
+                         int32_t* __restrict__ rowsum_out,
                          const int32_t* __restrict__ colsum,
                          const LanceDevState* __restrict__ st, float* __restrict__ y,
                          int32_t* __restrict__ acc_dump, const float* __restrict__ bias,
@@ -170,8 +171,8 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   uint64_t* empty_bar = full_bar + stages;
   uint64_t* acc_full = empty_bar + stages;  // [4]
   uint64_t* acc_empty = acc_full + 4;       // [4]
-  uint64_t* rs_full = acc_empty + 4;        // [2]
-  uint64_t* rs_empty = rs_full + 2;         // [2]
+  uint64_t* rs_ready = acc_empty + 4;       // [2 tile buffers][4 j-groups]
+  uint64_t* rs_empty = rs_ready + 8;        // [2]
   uint64_t* b_full = rs_empty + 2;          // [1]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(b_full + 2);
   float* s_cterm = reinterpret_cast<float*>(tmem_holder + 4);  // [16][K_pad]: k3[p]*colsum[p][k]
@@ -184,16 +185,14 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], 3);  // MMA commit + the two row-sum warps
     }
     for (int b = 0; b < 4; ++b) {
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], kEpiWarps);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&rs_full[b], 1);
-      mbar_init(&rs_empty[b], kEpiWarps);
-    }
+    for (int b = 0; b < 8; ++b) mbar_init(&rs_ready[b], 2);
+    for (int b = 0; b < 2; ++b) mbar_init(&rs_empty[b], kEpiWarps);
     mbar_init(b_full, 1);
     fence_barrier_init();
   }
@@ -223,7 +222,6 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     setmaxnreg_dec<kCtrlRegs>();
     if (warp == kProducerWarp && lane == 0) {
       // ---------------- TMA producer ----------------
-      tma_prefetch_desc(&tmR);
       if (b_res) {  // the single filter tile's B images, once
         mbar_arrive_expect_tx(b_full, 16 * nk * Cfg::kBBytes);
         bulk_load(b_base, codes_w, 16 * nk * Cfg::kBBytes, b_full);
@@ -237,11 +235,6 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         // Operand images of this tile (lance_kernels.cuh umma_image_offset).
         const uint8_t* a_tile = codes_a + static_cast<long long>(mt) * 16 * nk * Cfg::kABytes;
         const uint8_t* b_tile = codes_w + static_cast<long long>(ntile) * 16 * nk * Cfg::kBBytes;
-        // Row sums of the tile's 128 rows for all 16 positions (OOB rows read 0).
-        const uint32_t rb = lt & 1u;
-        mbar_wait(&rs_empty[rb], ((lt >> 1) & 1u) ^ 1u);
-        mbar_arrive_expect_tx(&rs_full[rb], Cfg::kRsBytes);
-        tma_load_2d(s_rs + rb * 16 * kBM, &tmR, m0, 0, &rs_full[rb]);
         for (int j = 0; j < 4; ++j)
           for (int a = 0; a < 4; ++a) {
             const int u0 = image_plane(4 * a + j) * nk;
@@ -308,6 +301,57 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         }
       }
       __syncwarp();
+    } else if (warp >= kRowSumWarp0) {
+      // ---------------- row sums (lowpgemm.hpp:121-123) ----------------
+      // sum_c A[p][m][c] straight from every A stage: thread t owns rows t and
+      // t + 64; 16-byte chunks are visited in a lane-rotated order (a row's
+      // chunk order does not matter), which keeps the shared loads
+      // conflict-free.  Ready per (tile, j-group) for the epilogue.
+      constexpr int CPR = BK / 16;
+      const int t = (warp - kRowSumWarp0) * 32 + lane;
+      int s = 0;
+      uint32_t ph = 0;
+      uint32_t lt = 0;
+      for (int t_i = blockIdx.x; t_i < num_tiles; t_i += gridDim.x, ++lt) {
+        const int m0 = (t_i / nt) * kBM;
+        const uint32_t tb = lt & 1u;
+        mbar_wait(&rs_empty[tb], ((lt >> 1) & 1u) ^ 1u);  // epilogue done with this buffer
+        int32_t* rs_t = s_rs + tb * 16 * kBM;
+        for (int j = 0; j < 4; ++j) {
+          for (int a = 0; a < 4; ++a) {
+            const int p = 4 * a + j;
+            uint32_t s0 = 0, s1 = 0;
+            for (int kc = 0; kc < nk; ++kc) {
+              mbar_wait(&full_bar[s], ph);
+              const uint8_t* img = stage_base + static_cast<size_t>(s) * stage_bytes;
+              const uint4* r0 = reinterpret_cast<const uint4*>(img + t * BK);
+              const uint4* r1 = reinterpret_cast<const uint4*>(img + (t + 64) * BK);
+#pragma unroll
+              for (int c = 0; c < CPR; ++c) {
+                const int cc = (c + lane) & (CPR - 1);
+                const uint4 u = r0[cc], w = r1[cc];
+                s0 = __dp4a(u.x, 0x01010101u, __dp4a(u.y, 0x01010101u, __dp4a(u.z, 0x01010101u, __dp4a(u.w, 0x01010101u, s0))));
+                s1 = __dp4a(w.x, 0x01010101u, __dp4a(w.y, 0x01010101u, __dp4a(w.z, 0x01010101u, __dp4a(w.w, 0x01010101u, s1))));
+              }
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&empty_bar[s]);
+              if (++s == stages) {
+                s = 0;
+                ph ^= 1u;
+              }
+            }
+            rs_t[p * kBM + t] = static_cast<int32_t>(s0);
+            rs_t[p * kBM + t + 64] = static_cast<int32_t>(s1);
+            if (DUMP) {
+              if (m0 + t < g.M) rowsum_out[static_cast<long long>(p) * g.rs_pitch + m0 + t] = static_cast<int32_t>(s0);
+              if (m0 + t + 64 < g.M)
+                rowsum_out[static_cast<long long>(p) * g.rs_pitch + m0 + t + 64] = static_cast<int32_t>(s1);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&rs_ready[tb * 4 + j]);
+        }
+      }
     }
   } else {
     // ---------------- epilogue ----------------
@@ -405,12 +449,12 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       };
       const uint32_t rb = lt & 1u;
       const int32_t* rs_tile = s_rs + rb * 16 * kBM + row;
-      mbar_wait(&rs_full[rb], (lt >> 1) & 1u);
       float2 S[4][FPT / 2];  // running S_ab partials, filter pairs
 #pragma unroll
       for (int j = 0; j < 4; ++j, ++grp) {
         const uint32_t buf = grp % NB;
         float rterm[4], k1s[4], k4[4];  // per position 4a + j of this j-group
+        mbar_wait(&rs_ready[rb * 4 + j], (lt >> 1) & 1u);
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
           // k2[p] * float(sum_a): second term of affine_term
@@ -494,7 +538,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
 
 template <int BK, int BN, bool SMALL, bool DUMP>
 static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
-                                 const CUtensorMap* tmR, const int32_t* colsum,
+                                 int32_t* rowsum_out, const int32_t* colsum,
                                  const LanceDevState* st, float* y, int32_t* acc_dump,
                                  const float* bias, int relu, const GemmGeom& g0, cudaStream_t s) {
   GemmGeom g = g0;
@@ -528,34 +572,34 @@ static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
   const long long tiles = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * g.num_n_tiles;
   const int grid = static_cast<int>(tiles < sms ? tiles : sms);
   gemm_epilogue_kernel<BK, BN, SMALL, DUMP><<<grid, kGemmThreadsP, smem, s>>>(
-      codes_a, codes_w, *tmR, colsum, st, y, acc_dump, bias, relu, g);
+      codes_a, codes_w, rowsum_out, colsum, st, y, acc_dump, bias, relu, g);
   return cudaGetLastError();
 }
 
 template <int BK, int BN>
 static cudaError_t launch_gemm_bk(const uint8_t* codes_a, const uint8_t* codes_w, int small_acc,
-                                  const CUtensorMap* tmR, const int32_t* colsum,
+                                  int32_t* rowsum_out, const int32_t* colsum,
                                   const LanceDevState* st, float* y, int32_t* acc_dump,
                                   const float* bias, int relu, const GemmGeom& g, cudaStream_t s) {
   const bool dump = acc_dump != nullptr;
   if (small_acc)
-    return dump ? launch_gemm_t<BK, BN, true, true>(codes_a, codes_w, tmR, colsum, st, y, acc_dump,
+    return dump ? launch_gemm_t<BK, BN, true, true>(codes_a, codes_w, rowsum_out, colsum, st, y, acc_dump,
                                                     bias, relu, g, s)
-                : launch_gemm_t<BK, BN, true, false>(codes_a, codes_w, tmR, colsum, st, y, acc_dump,
+                : launch_gemm_t<BK, BN, true, false>(codes_a, codes_w, rowsum_out, colsum, st, y, acc_dump,
                                                      bias, relu, g, s);
-  return dump ? launch_gemm_t<BK, BN, false, true>(codes_a, codes_w, tmR, colsum, st, y, acc_dump,
+  return dump ? launch_gemm_t<BK, BN, false, true>(codes_a, codes_w, rowsum_out, colsum, st, y, acc_dump,
                                                    bias, relu, g, s)
-              : launch_gemm_t<BK, BN, false, false>(codes_a, codes_w, tmR, colsum, st, y, acc_dump,
+              : launch_gemm_t<BK, BN, false, false>(codes_a, codes_w, rowsum_out, colsum, st, y, acc_dump,
                                                     bias, relu, g, s);
 }
 
-cudaError_t launch_gemm(const uint8_t* codes_a, const uint8_t* codes_w, const CUtensorMap* tmR,
+cudaError_t launch_gemm(const uint8_t* codes_a, const uint8_t* codes_w, int32_t* rowsum_out,
                         int bk, int bn, int small_acc, const int32_t* colsum,
                         const LanceDevState* st, float* y, int32_t* acc_dump, const float* bias,
                         int relu, const GemmGeom& g, cudaStream_t s) {
 #define LANCE_GEMM_CASE(BKV, BNV)                                                            \
   if (bk == BKV && bn == BNV)                                                                \
-    return launch_gemm_bk<BKV, BNV>(codes_a, codes_w, small_acc, tmR, colsum, st, y, acc_dump, \
+    return launch_gemm_bk<BKV, BNV>(codes_a, codes_w, small_acc, rowsum_out, colsum, st, y, acc_dump, \
                                     bias, relu, g, s);
   LANCE_GEMM_CASE(128, 64)
   LANCE_GEMM_CASE(64, 64)

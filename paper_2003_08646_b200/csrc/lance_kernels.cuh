@@ -81,6 +81,7 @@ struct GemmGeom {
   int num_n_tiles;  // K_pad / BN
   int stages;       // shared-memory ring depth (set by the launcher)
   int b_resident;   // B operand resident in shared memory (set by the launcher)
+  int rs_pitch;     // row-sum plane pitch (acc-dump builds write the GEMM's row sums)
   int exp;          // experiment switches (LANCE_GEMM_EXP, profiling only; 0 = normal)
   unsigned long long* trace;  // CTA-0 event timestamps (LANCE_GEMM_TRACE, profiling only)
 };
@@ -135,7 +136,7 @@ cudaError_t launch_filter_prepare(const float* w, float* u_tmp, float* partials,
                                   uint8_t* codes_w, int32_t* colsum, LanceDevState* st,
                                   const FilterGeom& g, cudaStream_t s);
 // bn: filters per GEMM tile (16, 32 or 64); TMEM holds two j-groups of 4 x bn columns.
-cudaError_t launch_gemm(const uint8_t* codes_a, const uint8_t* codes_w, const CUtensorMap* tmR,
+cudaError_t launch_gemm(const uint8_t* codes_a, const uint8_t* codes_w, int32_t* rowsum_out,
                         int bk, int bn, int small_acc, const int32_t* colsum,
                         const LanceDevState* st, float* y, int32_t* acc_dump, const float* bias,
                         int relu, const GemmGeom& g, cudaStream_t s);
