@@ -420,6 +420,12 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   gg.trace = nullptr;
   gg.b_resident = 0;
   gg.rs_pitch = static_cast<int>(p->rs_pitch);
+  // Row sums: in the GEMM's spare warps when its stages are 64-byte K chunks
+  // (their shared-memory reads then cost the SS-UMMA little), else in K1.
+  // LANCE_RS_GEMM overrides.
+  gg.rs_warps = (p->BK <= 64) ? 1 : 0;
+  if (const char* e = std::getenv("LANCE_RS_GEMM")) gg.rs_warps = std::atoi(e) ? 1 : 0;
+  p->in_geom.rowsums = gg.rs_warps ? 0 : 1;
 
   // Operand images cover whole 128-row blocks; rows >= M stay code 0.
   const size_t codes_a_bytes = static_cast<size_t>(16) * ((p->M + kBM - 1) / kBM * kBM) * p->C_pad;
@@ -545,7 +551,7 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
   }
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[2], s));
-  LANCE_CUDA(launch_gemm(p->codes_a, p->codes_w, p->rowsum, p->BK, p->BN, p->small_acc, p->colsum, p->state, y_dev,
+  LANCE_CUDA(launch_gemm(p->codes_a, p->codes_w, &p->tmR, p->rowsum, p->BK, p->BN, p->small_acc, p->colsum, p->state, y_dev,
                          p->acc_dump, p->bias, p->relu, p->gemm_geom, s));
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[3], s));

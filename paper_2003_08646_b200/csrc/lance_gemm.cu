@@ -140,6 +140,7 @@ template <int BK, int BN, bool SMALL, bool DUMP>
 __global__ void __launch_bounds__(kGemmThreadsP, 1)
     gemm_epilogue_kernel(const uint8_t* __restrict__ codes_a,
                          const uint8_t* __restrict__ codes_w,
+                         const __grid_constant__ CUtensorMap tmR,
                          int32_t* __restrict__ rowsum_out,
                          const int32_t* __restrict__ colsum,
                          const LanceDevState* __restrict__ st, float* __restrict__ y,
@@ -185,13 +186,15 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 3);  // MMA commit + the two row-sum warps
+      mbar_init(&empty_bar[s], g.rs_warps ? 3 : 1);  // MMA commit (+ the two row-sum warps)
     }
     for (int b = 0; b < 4; ++b) {
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], kEpiWarps);
     }
-    for (int b = 0; b < 8; ++b) mbar_init(&rs_ready[b], 2);
+    // rs_warps: per (tile buffer, j-group), arrived by the two row-sum warps;
+    // else one TMA of the tile's row sums (written by K1) completes [tb][0].
+    for (int b = 0; b < 8; ++b) mbar_init(&rs_ready[b], g.rs_warps ? 2 : 1);
     for (int b = 0; b < 2; ++b) mbar_init(&rs_empty[b], kEpiWarps);
     mbar_init(b_full, 1);
     fence_barrier_init();
@@ -235,6 +238,12 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         // Operand images of this tile (lance_kernels.cuh umma_image_offset).
         const uint8_t* a_tile = codes_a + static_cast<long long>(mt) * 16 * nk * Cfg::kABytes;
         const uint8_t* b_tile = codes_w + static_cast<long long>(ntile) * 16 * nk * Cfg::kBBytes;
+        if (!g.rs_warps) {  // row sums of the tile's 128 rows, all 16 positions (OOB rows read 0)
+          const uint32_t rb = lt & 1u;
+          mbar_wait(&rs_empty[rb], ((lt >> 1) & 1u) ^ 1u);
+          mbar_arrive_expect_tx(&rs_ready[rb * 4], Cfg::kRsBytes);
+          tma_load_2d(s_rs + rb * 16 * kBM, &tmR, m0, 0, &rs_ready[rb * 4]);
+        }
         for (int j = 0; j < 4; ++j)
           for (int a = 0; a < 4; ++a) {
             const int u0 = image_plane(4 * a + j) * nk;
@@ -301,7 +310,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         }
       }
       __syncwarp();
-    } else if (warp >= kRowSumWarp0) {
+    } else if (warp >= kRowSumWarp0 && g.rs_warps) {
       // ---------------- row sums (lowpgemm.hpp:121-123) ----------------
       // sum_c A[p][m][c] straight from every A stage: thread t owns rows t and
       // t + 64; 16-byte chunks are visited in a lane-rotated order (a row's
@@ -454,7 +463,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       for (int j = 0; j < 4; ++j, ++grp) {
         const uint32_t buf = grp % NB;
         float rterm[4], k1s[4], k4[4];  // per position 4a + j of this j-group
-        mbar_wait(&rs_ready[rb * 4 + j], (lt >> 1) & 1u);
+        if (g.rs_warps || j == 0) mbar_wait(&rs_ready[rb * 4 + (g.rs_warps ? j : 0)], (lt >> 1) & 1u);
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
           // k2[p] * float(sum_a): second term of affine_term
@@ -538,7 +547,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
 
 template <int BK, int BN, bool SMALL, bool DUMP>
 static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
-                                 int32_t* rowsum_out, const int32_t* colsum,
+                                 const CUtensorMap* tmR, int32_t* rowsum_out, const int32_t* colsum,
                                  const LanceDevState* st, float* y, int32_t* acc_dump,
                                  const float* bias, int relu, const GemmGeom& g0, cudaStream_t s) {
   GemmGeom g = g0;
@@ -572,34 +581,35 @@ static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
   const long long tiles = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * g.num_n_tiles;
   const int grid = static_cast<int>(tiles < sms ? tiles : sms);
   gemm_epilogue_kernel<BK, BN, SMALL, DUMP><<<grid, kGemmThreadsP, smem, s>>>(
-      codes_a, codes_w, rowsum_out, colsum, st, y, acc_dump, bias, relu, g);
+      codes_a, codes_w, *tmR, rowsum_out, colsum, st, y, acc_dump, bias, relu, g);
   return cudaGetLastError();
 }
 
 template <int BK, int BN>
 static cudaError_t launch_gemm_bk(const uint8_t* codes_a, const uint8_t* codes_w, int small_acc,
-                                  int32_t* rowsum_out, const int32_t* colsum,
+                                  const CUtensorMap* tmR, int32_t* rowsum_out, const int32_t* colsum,
                                   const LanceDevState* st, float* y, int32_t* acc_dump,
                                   const float* bias, int relu, const GemmGeom& g, cudaStream_t s) {
   const bool dump = acc_dump != nullptr;
   if (small_acc)
-    return dump ? launch_gemm_t<BK, BN, true, true>(codes_a, codes_w, rowsum_out, colsum, st, y, acc_dump,
+    return dump ? launch_gemm_t<BK, BN, true, true>(codes_a, codes_w, tmR, rowsum_out, colsum, st, y, acc_dump,
                                                     bias, relu, g, s)
-                : launch_gemm_t<BK, BN, true, false>(codes_a, codes_w, rowsum_out, colsum, st, y, acc_dump,
+                : launch_gemm_t<BK, BN, true, false>(codes_a, codes_w, tmR, rowsum_out, colsum, st, y, acc_dump,
                                                      bias, relu, g, s);
-  return dump ? launch_gemm_t<BK, BN, false, true>(codes_a, codes_w, rowsum_out, colsum, st, y, acc_dump,
+  return dump ? launch_gemm_t<BK, BN, false, true>(codes_a, codes_w, tmR, rowsum_out, colsum, st, y, acc_dump,
                                                    bias, relu, g, s)
-              : launch_gemm_t<BK, BN, false, false>(codes_a, codes_w, rowsum_out, colsum, st, y, acc_dump,
+              : launch_gemm_t<BK, BN, false, false>(codes_a, codes_w, tmR, rowsum_out, colsum, st, y, acc_dump,
                                                     bias, relu, g, s);
 }
 
-cudaError_t launch_gemm(const uint8_t* codes_a, const uint8_t* codes_w, int32_t* rowsum_out,
+cudaError_t launch_gemm(const uint8_t* codes_a, const uint8_t* codes_w, const CUtensorMap* tmR,
+                        int32_t* rowsum_out,
                         int bk, int bn, int small_acc, const int32_t* colsum,
                         const LanceDevState* st, float* y, int32_t* acc_dump, const float* bias,
                         int relu, const GemmGeom& g, cudaStream_t s) {
 #define LANCE_GEMM_CASE(BKV, BNV)                                                            \
   if (bk == BKV && bn == BNV)                                                                \
-    return launch_gemm_bk<BKV, BNV>(codes_a, codes_w, small_acc, rowsum_out, colsum, st, y, acc_dump, \
+    return launch_gemm_bk<BKV, BNV>(codes_a, codes_w, small_acc, tmR, rowsum_out, colsum, st, y, acc_dump, \
                                     bias, relu, g, s);
   LANCE_GEMM_CASE(128, 64)
   LANCE_GEMM_CASE(64, 64)

@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(256, 2) input_quant_kernel(const float* __rest
 // per-lane validity branches; BK is a template parameter so the UMMA-image
 // address is a handful of shifts per tile, and the tie fix-up is one
 // warp-uniform branch per position pair.
-template <int BK, int NK>
+template <int BK, int NK, bool RS>
 __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* __restrict__ x,
                                                                   uint8_t* __restrict__ codes,
                                                                   int32_t* __restrict__ rowsum,
@@ -452,6 +452,7 @@ __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* _
     }
     const uint32_t lin = static_cast<uint32_t>((m & (kBM - 1)) * BK + cb);
     uint8_t* dst = cbase + (m >> 7) * blkstride + (lin ^ (((lin >> 7) & kMask) << 4));
+    uint32_t mine = 0u;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       float2 dd[2], gq[2], r[2];
@@ -486,6 +487,20 @@ __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* _
       }
       *reinterpret_cast<uint16_t*>(dst + image_plane(2 * k) * pstride) = static_cast<uint16_t>(pk0);
       *reinterpret_cast<uint16_t*>(dst + image_plane(2 * k + 1) * pstride) = static_cast<uint16_t>(pk1);
+      // Row sums (lowpgemm.hpp:121-123): positions (2k, 2k+1) as 16-bit halves
+      // (RS = false: the GEMM sums the A rows from its stages instead).
+      if (!RS) continue;
+      const uint32_t a = (pk0 & 0xFFFFu) | (pk1 << 16);                  // [p.c0, p.c1, q.c0, q.c1]
+      const uint32_t w = (a & 0x00FF00FFu) + ((a >> 8) & 0x00FF00FFu);  // [p sum | q sum]
+      const uint32_t tot = __reduce_add_sync(0xffffffffu, w);
+      if ((lane >> 1) == k) mine = (lane & 1) ? (tot >> 16) : (tot & 0xFFFFu);
+    }
+    if (RS && lane < 16) {
+      int32_t* rs = rowsum + static_cast<long long>(lane) * g.rs_pitch + m;
+      if (g.nchunks == 1)
+        *rs = static_cast<int32_t>(mine);
+      else  // channel chunks of one tile run in different warps (rowsum pre-zeroed)
+        atomicAdd(rs, static_cast<int32_t>(mine));
     }
   }
 }
@@ -646,8 +661,10 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
     if (depth == 2)                                                                      \
       input_quant_fast2_kernel<BKV, NKV>                                                 \
           <<<static_cast<unsigned>((g.num_items + 5) / 6), 192, 0, s>>>(x, codes, rowsum, st, g); \
+    else if (g.rowsums)                                                                  \
+      input_quant_fast_kernel<BKV, NKV, true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g); \
     else                                                                                 \
-      input_quant_fast_kernel<BKV, NKV><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);  \
+      input_quant_fast_kernel<BKV, NKV, false><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g); \
     return cudaGetLastError();                                                           \
   }
     LANCE_K1_FAST(64, 1)

@@ -40,6 +40,7 @@ struct InGeom {
   int rs_pitch;   // row-sum plane pitch (M rounded up to 4: 16-byte TMA strides)
   int a_bk;       // GEMM K chunk (32, 64 or 128 channels): codes are stored as UMMA images
   int a_nk;       // C_pad / a_bk
+  int rowsums;    // K1 fast path writes row sums (0 when the GEMM computes them)
   int pad;
   int nchunks;    // ceil(C_pad / kChunk)
   int seg_len;    // tiles per warp strip (a tile row is split into nseg strips)
@@ -82,6 +83,7 @@ struct GemmGeom {
   int stages;       // shared-memory ring depth (set by the launcher)
   int b_resident;   // B operand resident in shared memory (set by the launcher)
   int rs_pitch;     // row-sum plane pitch (acc-dump builds write the GEMM's row sums)
+  int rs_warps;     // 1: the GEMM sums the A rows itself; 0: K1's row sums via TMA
   int exp;          // experiment switches (LANCE_GEMM_EXP, profiling only; 0 = normal)
   unsigned long long* trace;  // CTA-0 event timestamps (LANCE_GEMM_TRACE, profiling only)
 };
@@ -136,7 +138,8 @@ cudaError_t launch_filter_prepare(const float* w, float* u_tmp, float* partials,
                                   uint8_t* codes_w, int32_t* colsum, LanceDevState* st,
                                   const FilterGeom& g, cudaStream_t s);
 // bn: filters per GEMM tile (16, 32 or 64); TMEM holds two j-groups of 4 x bn columns.
-cudaError_t launch_gemm(const uint8_t* codes_a, const uint8_t* codes_w, int32_t* rowsum_out,
+cudaError_t launch_gemm(const uint8_t* codes_a, const uint8_t* codes_w, const CUtensorMap* tmR,
+                        int32_t* rowsum_out,
                         int bk, int bn, int small_acc, const int32_t* colsum,
                         const LanceDevState* st, float* y, int32_t* acc_dump, const float* bias,
                         int relu, const GemmGeom& g, cudaStream_t s);
