@@ -426,6 +426,8 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   gg.rs_warps = (p->BK <= 64) ? 1 : 0;
   if (const char* e = std::getenv("LANCE_RS_GEMM")) gg.rs_warps = std::atoi(e) ? 1 : 0;
   p->in_geom.rowsums = gg.rs_warps ? 0 : 1;
+  p->in_geom.rev_items = 1;
+  if (const char* e = std::getenv("LANCE_K1_REVERSE")) p->in_geom.rev_items = std::atoi(e) ? 1 : 0;
 
   // Operand images cover whole 128-row blocks; rows >= M stay code 0.
   const size_t codes_a_bytes = static_cast<size_t>(16) * ((p->M + kBM - 1) / kBM * kBM) * p->C_pad;

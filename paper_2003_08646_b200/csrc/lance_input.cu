@@ -292,8 +292,12 @@ __global__ void __launch_bounds__(256, 2) input_quant_kernel(const float* __rest
   }
   const float top = static_cast<float>((1 << st->bits_i) - 1);
   __syncthreads();
-  const long long item = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
-  if (item >= g.num_items) return;
+  // Reverse order: the range pass (K0) just streamed x front to back, so the
+  // tail of x is still in L2 when this kernel starts; and the GEMM, which
+  // reads the codes front to back, then finds the last-written rows in L2.
+  const long long wi = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
+  if (wi >= g.num_items) return;
+  const long long item = g.rev_items ? g.num_items - 1 - wi : wi;
   const StripItem it = strip_item(g, item, lane);
   const bool lane_on = it.ch < g.C;
   const bool two = it.ch + 1 < g.C;
@@ -419,8 +423,12 @@ __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* _
   }
   const float top = static_cast<float>((1 << st->bits_i) - 1);
   __syncthreads();
-  const long long item = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
-  if (item >= g.num_items) return;
+  // Reverse order: the range pass (K0) just streamed x front to back, so the
+  // tail of x is still in L2 when this kernel starts; and the GEMM, which
+  // reads the codes front to back, then finds the last-written rows in L2.
+  const long long wi = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
+  if (wi >= g.num_items) return;
+  const long long item = g.rev_items ? g.num_items - 1 - wi : wi;
   const StripItem it = strip_item(g, item, lane);
   const Strip<true> sp(x, g, it);
   constexpr int kImg = kBM * BK;                       // bytes of one image
@@ -520,8 +528,12 @@ __global__ void __launch_bounds__(192, 2) input_quant_fast2_kernel(const float* 
   }
   const float top = static_cast<float>((1 << st->bits_i) - 1);
   __syncthreads();
-  const long long item = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
-  if (item >= g.num_items) return;
+  // Reverse order: the range pass (K0) just streamed x front to back, so the
+  // tail of x is still in L2 when this kernel starts; and the GEMM, which
+  // reads the codes front to back, then finds the last-written rows in L2.
+  const long long wi = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
+  if (wi >= g.num_items) return;
+  const long long item = g.rev_items ? g.num_items - 1 - wi : wi;
   const StripItem it = strip_item(g, item, lane);
   const Strip<true> sp(x, g, it);
   constexpr int kImg = kBM * BK;                       // bytes of one image

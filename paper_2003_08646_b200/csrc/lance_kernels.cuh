@@ -41,6 +41,7 @@ struct InGeom {
   int a_bk;       // GEMM K chunk (32, 64 or 128 channels): codes are stored as UMMA images
   int a_nk;       // C_pad / a_bk
   int rowsums;    // K1 fast path writes row sums (0 when the GEMM computes them)
+  int rev_items;  // K1 walks its work items back to front (L2 reuse, LANCE_K1_REVERSE)
   int pad;
   int nchunks;    // ceil(C_pad / kChunk)
   int seg_len;    // tiles per warp strip (a tile row is split into nseg strips)
