@@ -196,3 +196,26 @@ def test_global_params_across_shards(lo):
     got = np.concatenate(ys)
     ref = lo.lance_gemm(spec, x, w)
     assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), mismatch_report(got, ref)
+
+
+@pytest.mark.parametrize("env", [{"LANCE_BAND_K0": "1"}, {"LANCE_BAND_K1": "1"},
+                                 {"LANCE_BAND_K0": "1", "LANCE_BAND_K1": "1"},
+                                 {"LANCE_RS_GEMM": "0"}, {"LANCE_RS_GEMM": "1"},
+                                 {"LANCE_K1_REVERSE": "0"}, {"LANCE_K1_DEPTH": "2"}],
+                         ids=lambda e: "+".join(f"{k}={v}" for k, v in e.items()))
+def test_alternate_kernel_paths_bitexact(lo, env, monkeypatch):
+    # The non-default input / row-sum kernels (TMA band kernels, row sums in
+    # K1 vs the GEMM, item order, deeper K1 lookahead) are selected at plan
+    # creation; each must reproduce the reference bitwise like the defaults.
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for spec, dist, seed in [(Spec(2, 64, 17, 17, 64, 1), "relu", 3),
+                             (Spec(1, 128, 14, 14, 64, 1), "uniform", 4),
+                             (Spec(1, 256, 9, 9, 128, 0), "relu", 5)]:
+        x, w = make_inputs(lo.uniform, spec, dist, seed)
+        got = run_gpu(spec, x, w, gemm_cfg())
+        y, ref = lo.lance_gemm(spec, x, w, dump=True)
+        ref["y"] = y
+        for k in ("codes_a", "rowsum", "acc", "params_a", "y"):
+            assert np.array_equal(np.asarray(got[k]).view(np.uint8), np.asarray(ref[k]).view(np.uint8)), \
+                f"{env} {spec}: {k}: {mismatch_report(got[k], ref[k])}"
