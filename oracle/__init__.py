@@ -84,6 +84,13 @@ class Spec:
     def rows(self):
         return self.n * self.tiles
 
+    def tiles_m(self, m: int) -> int:
+        """extract_tiles grid for tile side m (tensor.hpp:130-131)."""
+        return ((self.out_h + m - 1) // m) * ((self.out_w + m - 1) // m)
+
+    def rows_m(self, m: int) -> int:
+        return self.n * self.tiles_m(m)
+
 
 def _ptr(a):
     return a.ctypes.data_as(ct.c_void_p) if a is not None else None
@@ -115,8 +122,12 @@ class Oracle:
         lib.lo_affine_term.argtypes = [ct.c_int32, ct.c_int32, ct.c_int32, ct.c_int,
                                        ct.POINTER(_QP), ct.POINTER(_QP)]
         lib.lo_affine_term.restype = ct.c_float
-        for fn in ("lo_transform_input", "lo_transform_filter", "lo_transform_output"):
+        for fn in ("lo_transform_input", "lo_transform_filter", "lo_transform_output",
+                   "lo_transform_input4", "lo_transform_filter4", "lo_transform_output4"):
             getattr(lib, fn).argtypes = [ct.c_void_p, ct.c_void_p]
+        lib.lo_lance_gemm_tiled.argtypes = [ct.POINTER(_Spec), ct.c_int, ct.c_int, ct.c_int,
+                                            ct.c_int, ct.c_void_p, ct.c_void_p, ct.c_void_p,
+                                            ct.POINTER(_QP), ct.POINTER(_Dump)]
         lib.lo_validate.argtypes = [ct.POINTER(_Spec), ct.c_int, ct.c_int, ct.c_int, ct.c_int]
         lib.lo_lance_gemm.argtypes = [ct.POINTER(_Spec), ct.c_int, ct.c_int, ct.c_int,
                                       ct.c_void_p, ct.c_void_p, ct.c_void_p,
@@ -161,6 +172,25 @@ class Oracle:
         self.lib.lo_transform_output(_ptr(m), _ptr(s))
         return s.reshape(2, 2)
 
+    # F(4x4,3x3) extension (Appendix D basis; not in the reference)
+    def transform_input4(self, d):
+        d = _f32(d).reshape(36)
+        v = np.empty(36, np.float32)
+        self.lib.lo_transform_input4(_ptr(d), _ptr(v))
+        return v.reshape(6, 6)
+
+    def transform_filter4(self, g):
+        g = _f32(g).reshape(9)
+        u = np.empty(36, np.float32)
+        self.lib.lo_transform_filter4(_ptr(g), _ptr(u))
+        return u.reshape(6, 6)
+
+    def transform_output4(self, m):
+        m = _f32(m).reshape(36)
+        s = np.empty(16, np.float32)
+        self.lib.lo_transform_output4(_ptr(m), _ptr(s))
+        return s.reshape(4, 4)
+
     def fit_params(self, values, bits):
         v = _f32(values).ravel()
         qp = _QP()
@@ -186,30 +216,34 @@ class Oracle:
 
     # -- the path ---------------------------------------------------------
     def lance_gemm(self, spec: Spec, x, w, bits_w=8, bits_i=8, gran=PER_POSITION,
-                   in_params=None, dump=False):
+                   in_params=None, dump=False, tile_m=2):
+        """lance_gemm (engines.hpp:492-536); tile_m=4 is the F(4x4,3x3)
+        extension (36 positions in every dump)."""
         x = _f32(x)
         w = _f32(w)
         s = _Spec(spec.n, spec.c, spec.h, spec.w, spec.k, spec.pad)
         y = np.empty((spec.n, spec.out_h, spec.out_w, spec.k), np.float32)
-        M, C, K = spec.rows, spec.c, spec.k
+        M, C, K = spec.rows_m(tile_m), spec.c, spec.k
+        NP = (tile_m + 2) ** 2
         d = None
         bufs = {}
         if dump:
             bufs = dict(
-                v=np.empty((16, M, C), np.float32), u=np.empty((16, C, K), np.float32),
-                codes_a=np.empty((16, M, C), np.uint8), codes_w=np.empty((16, C, K), np.uint8),
-                rowsum=np.empty((16, M), np.int32), colsum=np.empty((16, K), np.int32),
-                acc=np.empty((16, M, K), np.int32))
-            pa = (_QP * 16)()
-            pw = (_QP * 16)()
+                v=np.empty((NP, M, C), np.float32), u=np.empty((NP, C, K), np.float32),
+                codes_a=np.empty((NP, M, C), np.uint8), codes_w=np.empty((NP, C, K), np.uint8),
+                rowsum=np.empty((NP, M), np.int32), colsum=np.empty((NP, K), np.int32),
+                acc=np.empty((NP, M, K), np.int32))
+            pa = (_QP * NP)()
+            pw = (_QP * NP)()
             d = _Dump(*(_ptr(bufs[k]) for k in ("v", "u", "codes_a", "codes_w", "rowsum",
                                                  "colsum", "acc")),
                       ct.cast(pa, ct.c_void_p), ct.cast(pw, ct.c_void_p))
         ip = None
         if in_params is not None:
-            ip = (_QP * 16)(*[_QP(int(r[0]), r[1], r[2], r[3]) for r in np.asarray(in_params)])
-        rc = self.lib.lo_lance_gemm(ct.byref(s), bits_w, bits_i, gran, _ptr(x), _ptr(w), _ptr(y),
-                                    ip, ct.byref(d) if d is not None else None)
+            ip = (_QP * NP)(*[_QP(int(r[0]), r[1], r[2], r[3]) for r in np.asarray(in_params)])
+        rc = self.lib.lo_lance_gemm_tiled(ct.byref(s), tile_m, bits_w, bits_i, gran, _ptr(x),
+                                          _ptr(w), _ptr(y), ip,
+                                          ct.byref(d) if d is not None else None)
         self._err(rc)
         if not dump:
             return y

@@ -78,6 +78,9 @@ int lo_out_h(const lo_spec* s) { return s->h + 2 * s->pad - 3 + 1; }
 int lo_out_w(const lo_spec* s) { return s->w + 2 * s->pad - 3 + 1; }
 int lo_tiles_h(const lo_spec* s) { return (lo_out_h(s) + 1) / 2; }
 int lo_tiles_w(const lo_spec* s) { return (lo_out_w(s) + 1) / 2; }
+/* extract_tiles grid for tile side m (tensor.hpp:130-131). */
+int lo_tiles_h_m(const lo_spec* s, int m) { return (lo_out_h(s) + m - 1) / m; }
+int lo_tiles_w_m(const lo_spec* s, int m) { return (lo_out_w(s) + m - 1) / m; }
 
 /* ------------------------------------------------------------------------ */
 /* winograd.hpp:40-54: F(2x2,3x3) basis. */
@@ -91,6 +94,45 @@ static const float kBt[4][4] = {{1.0f, 0.0f, -1.0f, 0.0f},
                                 {0.0f, 1.0f, 0.0f, -1.0f}};
 static const float kAt[2][4] = {{1.0f, 1.0f, 1.0f, 0.0f},
                                 {0.0f, 1.0f, -1.0f, -1.0f}};
+
+/* F(4x4,3x3): not in the reference (winograd.hpp:27 "Only F(2x2, 3x3) is
+ * provided").  Builder-defined basis (Lavin & Gray),
+ * evaluated through the same matmul/two_sided conventions as the reference's
+ * F(2x2) basis; every entry is the fp32 value of the literal (1/6, 1/12, 1/24
+ * rounded to nearest).  Parity of this extension is self-pinned (correlation
+ * identity vs direct_conv, tests/test_f4.py). */
+static const float kG4[6][3] = {{0.25f, 0.0f, 0.0f},
+                                {-1.0f / 6.0f, -1.0f / 6.0f, -1.0f / 6.0f},
+                                {-1.0f / 6.0f, 1.0f / 6.0f, -1.0f / 6.0f},
+                                {1.0f / 24.0f, 1.0f / 12.0f, 1.0f / 6.0f},
+                                {1.0f / 24.0f, -1.0f / 12.0f, 1.0f / 6.0f},
+                                {0.0f, 0.0f, 1.0f}};
+static const float kBt4[6][6] = {{4.0f, 0.0f, -5.0f, 0.0f, 1.0f, 0.0f},
+                                 {0.0f, -4.0f, -4.0f, 1.0f, 1.0f, 0.0f},
+                                 {0.0f, 4.0f, -4.0f, -1.0f, 1.0f, 0.0f},
+                                 {0.0f, -2.0f, -1.0f, 2.0f, 1.0f, 0.0f},
+                                 {0.0f, 2.0f, -1.0f, -2.0f, 1.0f, 0.0f},
+                                 {0.0f, 4.0f, 0.0f, -5.0f, 0.0f, 1.0f}};
+static const float kAt4[4][6] = {{1.0f, 1.0f, 1.0f, 1.0f, 1.0f, 0.0f},
+                                 {0.0f, 1.0f, -1.0f, 2.0f, -2.0f, 0.0f},
+                                 {0.0f, 1.0f, 1.0f, 4.0f, 4.0f, 0.0f},
+                                 {0.0f, 1.0f, -1.0f, 8.0f, -8.0f, 1.0f}};
+
+/* WinogradBasis (winograd.hpp:30-37) for m = 2 or 4. */
+typedef struct {
+  int m, alpha;
+  const float *g, *bt, *at;
+} lo_basis;
+
+static lo_basis basis_for(int m) {
+  lo_basis b;
+  b.m = m;
+  b.alpha = m + 2;
+  b.g = (m == 4) ? &kG4[0][0] : &kG[0][0];
+  b.bt = (m == 4) ? &kBt4[0][0] : &kBt[0][0];
+  b.at = (m == 4) ? &kAt4[0][0] : &kAt[0][0];
+  return b;
+}
 
 /* matrix.hpp:75-84: out = a*b, i-k-j order, accumulate from +0.0f. */
 static void matmul(const float* a, int ar, int ac, const float* b, int bc, float* out) {
@@ -110,7 +152,7 @@ static void transpose(const float* a, int r, int c, float* out) {
 
 /* winograd.hpp:59-61: two_sided(t, x) = (t x) t^T. t is tr x tc, x tc x tc. */
 static void two_sided(const float* t, int tr, int tc, const float* x, float* out) {
-  float tx[16], tt[16];
+  float tx[36], tt[36];
   matmul(t, tr, tc, x, tc, tx);
   transpose(t, tr, tc, tt);
   matmul(tx, tr, tc, tt, tr, out);
@@ -122,6 +164,10 @@ void lo_transform_input(const float d[16], float v[16]) { two_sided(&kBt[0][0], 
 void lo_transform_filter(const float g[9], float u[16]) { two_sided(&kG[0][0], 4, 3, g, u); }
 /* winograd.hpp:80-84 */
 void lo_transform_output(const float m[16], float s[4]) { two_sided(&kAt[0][0], 2, 4, m, s); }
+/* The same three transforms for F(4x4,3x3) (Appendix D basis). */
+void lo_transform_input4(const float d[36], float v[36]) { two_sided(&kBt4[0][0], 6, 6, d, v); }
+void lo_transform_filter4(const float g[9], float u[36]) { two_sided(&kG4[0][0], 6, 3, g, u); }
+void lo_transform_output4(const float m[36], float s[16]) { two_sided(&kAt4[0][0], 4, 6, m, s); }
 
 /* ------------------------------------------------------------------------ */
 /* quant.hpp:54-72 */
@@ -194,17 +240,17 @@ int lo_validate(const lo_spec* s, int bits_w, int bits_i, int gran, int mode_gem
 /* ------------------------------------------------------------------------ */
 /* quantize_domain (engines.hpp:140-183) for the PerPosition / PerTensor
  * cases lance_gemm admits.  values = [16][slice]. */
-static int quantize_domain(const float* values, size_t slice, int bits, int gran,
-                           uint8_t* codes, lo_qparams params[16]) {
+static int quantize_domain(const float* values, size_t slice, int np, int bits, int gran,
+                           uint8_t* codes, lo_qparams* params) {
   int rc;
   if (gran == LO_PER_TENSOR) {
-    rc = lo_fit_params(values, 16 * slice, bits, &params[0]);
+    rc = lo_fit_params(values, np * slice, bits, &params[0]);
     if (rc) return rc;
-    for (int p = 1; p < 16; ++p) params[p] = params[0]; /* param_at -> params[0] (:135) */
-    for (size_t i = 0; i < 16 * slice; ++i) codes[i] = lo_quantize(values[i], &params[0]);
+    for (int p = 1; p < np; ++p) params[p] = params[0]; /* param_at -> params[0] (:135) */
+    for (size_t i = 0; i < np * slice; ++i) codes[i] = lo_quantize(values[i], &params[0]);
     return LO_OK;
   }
-  for (int p = 0; p < 16; ++p) {
+  for (int p = 0; p < np; ++p) {
     rc = lo_fit_params(values + (size_t)p * slice, slice, bits, &params[p]);
     if (rc) return rc;
     for (size_t i = 0; i < slice; ++i)
@@ -213,76 +259,84 @@ static int quantize_domain(const float* values, size_t slice, int bits, int gran
   return LO_OK;
 }
 
-/* lance_gemm (engines.hpp:492-536). */
-int lo_lance_gemm(const lo_spec* s, int bits_w, int bits_i, int gran, const float* x,
-                  const float* w, float* y, const lo_qparams* in_params, lo_dump* dump) {
+/* lance_gemm (engines.hpp:492-536) for tile side m (2: the reference path;
+ * 4: the F(4x4,3x3) extension, same algorithm with alpha = 6, 36 positions).
+ * Every "16" / "2" / "4" literal of engines.hpp:240-255,510,531-532 and
+ * extract_tiles (tensor.hpp:116-152) becomes np = alpha^2 / m / alpha. */
+int lo_lance_gemm_tiled(const lo_spec* s, int tile_m, int bits_w, int bits_i, int gran,
+                        const float* x, const float* w, float* y, const lo_qparams* in_params,
+                        lo_dump* dump) {
+  if (tile_m != 2 && tile_m != 4) return fail(LO_EINVAL, "lance_gemm: tile side must be 2 or 4");
   int rc = lo_validate(s, bits_w, bits_i, gran, 1);
   if (rc) return rc;
+  const lo_basis bs = basis_for(tile_m);
+  const int tm = bs.m, al = bs.alpha, np = al * al;
   const int N = s->n, C = s->c, H = s->h, W = s->w, K = s->k, pad = s->pad;
-  const int OH = lo_out_h(s), OW = lo_out_w(s), PH = lo_tiles_h(s), PW = lo_tiles_w(s);
+  const int OH = lo_out_h(s), OW = lo_out_w(s), PH = lo_tiles_h_m(s, tm), PW = lo_tiles_w_m(s, tm);
   const size_t P = (size_t)PH * PW, M = (size_t)N * P;
 
-  float* v = (float*)malloc(sizeof(float) * 16 * M * C);
-  float* u = (float*)malloc(sizeof(float) * 16 * (size_t)C * K);
-  uint8_t* va = (uint8_t*)malloc(16 * M * C);
-  uint8_t* ub = (uint8_t*)malloc(16 * (size_t)C * K);
+  float* v = (float*)malloc(sizeof(float) * np * M * C);
+  float* u = (float*)malloc(sizeof(float) * np * (size_t)C * K);
+  uint8_t* va = (uint8_t*)malloc(np * M * C);
+  uint8_t* ub = (uint8_t*)malloc(np * (size_t)C * K);
   int32_t* acc = (int32_t*)malloc(sizeof(int32_t) * M * K);
-  float* mdom = (float*)malloc(sizeof(float) * 16 * M * K);
-  int32_t* rsum = (int32_t*)malloc(sizeof(int32_t) * 16 * M);
-  int32_t* csum = (int32_t*)malloc(sizeof(int32_t) * 16 * (size_t)K);
-  lo_qparams pa[16], pb[16];
+  float* mdom = (float*)malloc(sizeof(float) * np * M * K);
+  int32_t* rsum = (int32_t*)malloc(sizeof(int32_t) * np * M);
+  int32_t* csum = (int32_t*)malloc(sizeof(int32_t) * np * (size_t)K);
+  lo_qparams pa[36], pb[36];
   if (!v || !u || !va || !ub || !acc || !mdom || !rsum || !csum) {
     rc = fail(LO_EINVAL, "oracle: out of memory");
     goto done;
   }
 
   /* extract_tiles (tensor.hpp:116-152) + domain_from_tiles (engines.hpp:189-211):
-   * tile t = ti*PW + tj, row = img*P + t, zero padding, v[p][row][ch]. */
+   * tile t = ti*PW + tj, row = img*P + t, origin (m*ti - pad, m*tj - pad), zero
+   * padding, v[p][row][ch] with p = alpha*a + b. */
   for (int img = 0; img < N; ++img)
     for (int ti = 0; ti < PH; ++ti)
       for (int tj = 0; tj < PW; ++tj) {
         const size_t row = (size_t)img * P + (size_t)ti * PW + tj;
         for (int ch = 0; ch < C; ++ch) {
-          float d[16], vv[16];
-          for (int a = 0; a < 4; ++a)
-            for (int b = 0; b < 4; ++b) {
-              const int si = ti * 2 - pad + a, sj = tj * 2 - pad + b;
-              d[a * 4 + b] = (si >= 0 && si < H && sj >= 0 && sj < W)
-                                 ? x[(((size_t)img * H + si) * W + sj) * C + ch]
-                                 : 0.0f;
+          float d[36], vv[36];
+          for (int a = 0; a < al; ++a)
+            for (int b = 0; b < al; ++b) {
+              const int si = ti * tm - pad + a, sj = tj * tm - pad + b;
+              d[a * al + b] = (si >= 0 && si < H && sj >= 0 && sj < W)
+                                  ? x[(((size_t)img * H + si) * W + sj) * C + ch]
+                                  : 0.0f;
             }
-          lo_transform_input(d, vv);
-          for (int p = 0; p < 16; ++p) v[((size_t)p * M + row) * C + ch] = vv[p];
+          two_sided(bs.bt, al, al, d, vv);
+          for (int p = 0; p < np; ++p) v[((size_t)p * M + row) * C + ch] = vv[p];
         }
       }
 
   /* domain_from_filters (engines.hpp:215-233): g[a][b] = w.at(k,a,b,c), u[p][c][k]. */
   for (int ki = 0; ki < K; ++ki)
     for (int ci = 0; ci < C; ++ci) {
-      float g[9], uu[16];
+      float g[9], uu[36];
       for (int a = 0; a < 3; ++a)
         for (int b = 0; b < 3; ++b) g[a * 3 + b] = w[(((size_t)ki * 3 + a) * 3 + b) * C + ci];
-      lo_transform_filter(g, uu);
-      for (int p = 0; p < 16; ++p) u[((size_t)p * C + ci) * K + ki] = uu[p];
+      two_sided(bs.g, al, 3, g, uu);
+      for (int p = 0; p < np; ++p) u[((size_t)p * C + ci) * K + ki] = uu[p];
     }
 
   /* quantize_domain for v and u (engines.hpp:505-506). */
   if (in_params) {
-    for (int p = 0; p < 16; ++p) pa[p] = in_params[p];
-    for (int p = 0; p < 16; ++p)
+    for (int p = 0; p < np; ++p) pa[p] = in_params[p];
+    for (int p = 0; p < np; ++p)
       for (size_t i = 0; i < M * C; ++i) {
         const size_t idx = (size_t)p * M * C + i;
         va[idx] = lo_quantize(v[idx], &pa[p]);
       }
   } else {
-    rc = quantize_domain(v, M * C, bits_i, gran, va, pa);
+    rc = quantize_domain(v, M * C, np, bits_i, gran, va, pa);
     if (rc) goto done;
   }
-  rc = quantize_domain(u, (size_t)C * K, bits_w, gran, ub, pb);
+  rc = quantize_domain(u, (size_t)C * K, np, bits_w, gran, ub, pb);
   if (rc) goto done;
 
-  /* 16 x affine_gemm (engines.hpp:510-525; lowpgemm.hpp:118-134). */
-  for (int p = 0; p < 16; ++p) {
+  /* np x affine_gemm (engines.hpp:510-525; lowpgemm.hpp:118-134). */
+  for (int p = 0; p < np; ++p) {
     const uint8_t* A = va + (size_t)p * M * C;
     const uint8_t* B = ub + (size_t)p * C * K;
     memset(acc, 0, sizeof(int32_t) * M * K);
@@ -316,30 +370,30 @@ int lo_lance_gemm(const lo_spec* s, int bits_w, int bits_i, int gran, const floa
   for (size_t row = 0; row < M; ++row) {
     const int img = (int)(row / P), t = (int)(row % P), ti = t / PW, tj = t % PW;
     for (int ki = 0; ki < K; ++ki) {
-      float m[16], s2[4];
-      for (int p = 0; p < 16; ++p) m[p] = mdom[((size_t)p * M + row) * K + ki];
-      lo_transform_output(m, s2);
-      for (int a = 0; a < 2; ++a) {
-        const int oi = ti * 2 + a;
+      float m[36], s2[16];
+      for (int p = 0; p < np; ++p) m[p] = mdom[((size_t)p * M + row) * K + ki];
+      two_sided(bs.at, tm, al, m, s2);
+      for (int a = 0; a < tm; ++a) {
+        const int oi = ti * tm + a;
         if (oi >= OH) break;
-        for (int b = 0; b < 2; ++b) {
-          const int oj = tj * 2 + b;
+        for (int b = 0; b < tm; ++b) {
+          const int oj = tj * tm + b;
           if (oj >= OW) break;
-          y[(((size_t)img * OH + oi) * OW + oj) * K + ki] = s2[a * 2 + b];
+          y[(((size_t)img * OH + oi) * OW + oj) * K + ki] = s2[a * tm + b];
         }
       }
     }
   }
 
   if (dump) {
-    if (dump->v) memcpy(dump->v, v, sizeof(float) * 16 * M * C);
-    if (dump->u) memcpy(dump->u, u, sizeof(float) * 16 * (size_t)C * K);
-    if (dump->codes_a) memcpy(dump->codes_a, va, 16 * M * C);
-    if (dump->codes_w) memcpy(dump->codes_w, ub, 16 * (size_t)C * K);
-    if (dump->rowsum) memcpy(dump->rowsum, rsum, sizeof(int32_t) * 16 * M);
-    if (dump->colsum) memcpy(dump->colsum, csum, sizeof(int32_t) * 16 * (size_t)K);
-    if (dump->params_a) memcpy(dump->params_a, pa, sizeof pa);
-    if (dump->params_w) memcpy(dump->params_w, pb, sizeof pb);
+    if (dump->v) memcpy(dump->v, v, sizeof(float) * np * M * C);
+    if (dump->u) memcpy(dump->u, u, sizeof(float) * np * (size_t)C * K);
+    if (dump->codes_a) memcpy(dump->codes_a, va, np * M * C);
+    if (dump->codes_w) memcpy(dump->codes_w, ub, np * (size_t)C * K);
+    if (dump->rowsum) memcpy(dump->rowsum, rsum, sizeof(int32_t) * np * M);
+    if (dump->colsum) memcpy(dump->colsum, csum, sizeof(int32_t) * np * (size_t)K);
+    if (dump->params_a) memcpy(dump->params_a, pa, sizeof(lo_qparams) * np);
+    if (dump->params_w) memcpy(dump->params_w, pb, sizeof(lo_qparams) * np);
   }
   rc = LO_OK;
 done:
@@ -352,6 +406,11 @@ done:
   free(rsum);
   free(csum);
   return rc;
+}
+
+int lo_lance_gemm(const lo_spec* s, int bits_w, int bits_i, int gran, const float* x,
+                  const float* w, float* y, const lo_qparams* in_params, lo_dump* dump) {
+  return lo_lance_gemm_tiled(s, 2, bits_w, bits_i, gran, x, w, y, in_params, dump);
 }
 
 /* direct_conv (engines.hpp:266-295): channels ascending, fp32 accumulation. */

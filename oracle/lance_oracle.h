@@ -54,7 +54,7 @@ typedef struct {
   int32_t* rowsum;
   int32_t* colsum;
   int32_t* acc;
-  lo_qparams* params_a; /* [16] */
+  lo_qparams* params_a; /* [16] ([36] for F(4x4)) */
   lo_qparams* params_w; /* [16] */
 } lo_dump;
 
@@ -74,6 +74,14 @@ void lo_transform_input(const float d[16], float v[16]);
 void lo_transform_filter(const float g[9], float u[16]);
 void lo_transform_output(const float m[16], float s[4]);
 
+/* F(4x4,3x3) extension (SURVEY.md Appendix D basis, not in the reference):
+ * same matmul conventions, alpha = 6, 36 positions. */
+void lo_transform_input4(const float d[36], float v[36]);
+void lo_transform_filter4(const float g[9], float u[36]);
+void lo_transform_output4(const float m[36], float s[16]);
+int lo_tiles_h_m(const lo_spec* s, int m);
+int lo_tiles_w_m(const lo_spec* s, int m);
+
 /* quant.hpp:54-72 and 77-84. */
 int lo_fit_params(const float* values, size_t count, int bits, lo_qparams* out);
 uint8_t lo_quantize(float x, const lo_qparams* p);
@@ -91,6 +99,12 @@ int lo_validate(const lo_spec* s, int bits_w, int bits_i, int granularity, int m
 int lo_lance_gemm(const lo_spec* s, int bits_w, int bits_i, int granularity,
                   const float* x, const float* w, float* y,
                   const lo_qparams* in_params, lo_dump* dump);
+
+/* lance_gemm for tile side m = 2 (== lo_lance_gemm) or 4 (F(4x4,3x3)
+ * extension; dumps and in_params then hold 36 positions). */
+int lo_lance_gemm_tiled(const lo_spec* s, int tile_m, int bits_w, int bits_i, int granularity,
+                        const float* x, const float* w, float* y,
+                        const lo_qparams* in_params, lo_dump* dump);
 
 /* direct_conv (engines.hpp:266-295): fp32 reference used for error bounds. */
 int lo_direct_conv(const lo_spec* s, const float* x, const float* w, float* y);

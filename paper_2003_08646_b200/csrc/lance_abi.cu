@@ -426,6 +426,15 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   gg.rs_warps = (p->BK <= 64) ? 1 : 0;
   if (const char* e = std::getenv("LANCE_RS_GEMM")) gg.rs_warps = std::atoi(e) ? 1 : 0;
   p->in_geom.rowsums = gg.rs_warps ? 0 : 1;
+  // One thread sustains ~1 bulk copy per ~460 SM cycles from L2 whatever its
+  // size (scratch/l2_ingress_bench.cu), so each stage's copies are split over
+  // several producer lanes (LANCE_GEMM_LANES).  Measured in the GEMM, more
+  // lanes are slower (SS-UMMA already saturates shared-memory bandwidth), so 1.
+  gg.ld_lanes = 1;
+  if (const char* e = std::getenv("LANCE_GEMM_LANES")) {
+    const int v = std::atoi(e);
+    gg.ld_lanes = (v == 1 || v == 2 || v == 4 || v == 8) ? v : 4;
+  }
   p->in_geom.rev_items = 1;
   if (const char* e = std::getenv("LANCE_K1_REVERSE")) p->in_geom.rev_items = std::atoi(e) ? 1 : 0;
 

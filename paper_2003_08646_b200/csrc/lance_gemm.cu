@@ -223,9 +223,14 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
 
   if (warp >= kEpiWarps) {
     setmaxnreg_dec<kCtrlRegs>();
-    if (warp == kProducerWarp && lane == 0) {
+    if (warp == kProducerWarp && lane < g.ld_lanes) {
       // ---------------- TMA producer ----------------
-      if (b_res) {  // the single filter tile's B images, once
+      // Lanes 0..ld_lanes-1 each copy a 1/ld_lanes slice of every stage (the
+      // images are contiguous bytes); lane 0 alone posts the expected bytes,
+      // before the slices in program order, so the phase cannot complete early.
+      const int nl = g.ld_lanes;
+      const uint32_t a_part = Cfg::kABytes / nl, b_part = Cfg::kBBytes / nl;
+      if (b_res && lane == 0) {  // the single filter tile's B images, once
         mbar_arrive_expect_tx(b_full, 16 * nk * Cfg::kBBytes);
         bulk_load(b_base, codes_w, 16 * nk * Cfg::kBBytes, b_full);
       }
@@ -236,9 +241,9 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         const int mt = t / nt, ntile = t % nt;
         const int m0 = mt * kBM;
         // Operand images of this tile (lance_kernels.cuh umma_image_offset).
-        const uint8_t* a_tile = codes_a + static_cast<long long>(mt) * 16 * nk * Cfg::kABytes;
-        const uint8_t* b_tile = codes_w + static_cast<long long>(ntile) * 16 * nk * Cfg::kBBytes;
-        if (!g.rs_warps) {  // row sums of the tile's 128 rows, all 16 positions (OOB rows read 0)
+        const uint8_t* a_tile = codes_a + static_cast<long long>(mt) * 16 * nk * Cfg::kABytes + lane * a_part;
+        const uint8_t* b_tile = codes_w + static_cast<long long>(ntile) * 16 * nk * Cfg::kBBytes + lane * b_part;
+        if (!g.rs_warps && lane == 0) {  // row sums of the tile's 128 rows, all 16 positions (OOB rows read 0)
           const uint32_t rb = lt & 1u;
           mbar_wait(&rs_empty[rb], ((lt >> 1) & 1u) ^ 1u);
           mbar_arrive_expect_tx(&rs_ready[rb * 4], Cfg::kRsBytes);
@@ -250,10 +255,11 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
             for (int kc = 0; kc < nk; ++kc) {
               mbar_wait(&empty_bar[s], ph ^ 1u);
               uint8_t* sa = stage_base + static_cast<size_t>(s) * stage_bytes;
-              mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
-              bulk_load(sa, a_tile + (u0 + kc) * Cfg::kABytes, Cfg::kABytes, &full_bar[s]);
+              if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
+              __syncwarp((1u << nl) - 1u);
+              bulk_load(sa + lane * a_part, a_tile + (u0 + kc) * Cfg::kABytes, a_part, &full_bar[s]);
               if (!b_res)
-                bulk_load(sa + Cfg::kABytes, b_tile + (u0 + kc) * Cfg::kBBytes, Cfg::kBBytes,
+                bulk_load(sa + Cfg::kABytes + lane * b_part, b_tile + (u0 + kc) * Cfg::kBBytes, b_part,
                           &full_bar[s]);
               if (++s == stages) {
                 s = 0;

@@ -85,6 +85,7 @@ struct GemmGeom {
   int b_resident;   // B operand resident in shared memory (set by the launcher)
   int rs_pitch;     // row-sum plane pitch (acc-dump builds write the GEMM's row sums)
   int rs_warps;     // 1: the GEMM sums the A rows itself; 0: K1's row sums via TMA
+  int ld_lanes;     // producer lanes issuing each stage's bulk copies (1, 2, 4 or 8)
   int exp;          // experiment switches (LANCE_GEMM_EXP, profiling only; 0 = normal)
   unsigned long long* trace;  // CTA-0 event timestamps (LANCE_GEMM_TRACE, profiling only)
 };
