@@ -114,8 +114,9 @@ lance_config c_cfg(const Cfg& c) {
 // lance_gemm for any types with the reference's members (this namespace's or
 // the reference's own lance::Tensor4 / FilterBank / ConvSpec / LanceConfig).
 // check_layer (engines.hpp:84-91) is reproduced before the ABI call.
+// tile_m = 4 selects the F(4x4,3x3) extension (lance_gemm_host_tiled).
 template <class T4, class FB, class Spec, class Cfg>
-T4 lance_gemm_any(const T4& x, const FB& w, const Spec& spec, const Cfg& cfg) {
+T4 lance_gemm_any(const T4& x, const FB& w, const Spec& spec, const Cfg& cfg, int tile_m = 2) {
   const lance_conv_spec cs = detail::c_spec(spec);
   const lance_config cc = detail::c_cfg(cfg);
   // ConvSpec::validate first, exactly as check_layer does.
@@ -129,13 +130,21 @@ T4 lance_gemm_any(const T4& x, const FB& w, const Spec& spec, const Cfg& cfg) {
     throw std::invalid_argument("filter dims do not match spec");
   detail::throw_status(lance_validate(&cs, &cc));
   T4 y(spec.n, spec.out_h(), spec.out_w(), spec.k);
-  detail::throw_status(lance_gemm_host(&cs, &cc, x.data.data(), w.data.data(), y.data.data()));
+  detail::throw_status(
+      lance_gemm_host_tiled(&cs, &cc, tile_m, x.data.data(), w.data.data(), y.data.data()));
   return y;
 }
 
 inline Tensor4 lance_gemm(const Tensor4& x, const FilterBank& w, const ConvSpec& spec,
                           const LanceConfig& cfg) {
   return lance_gemm_any(x, w, spec, cfg);
+}
+
+// F(4x4,3x3) extension: the same algorithm with 6x6 tiles at stride 4 and 36
+// Winograd positions (not in the reference; SURVEY.md Appendix D basis).
+inline Tensor4 lance_gemm_f4(const Tensor4& x, const FilterBank& w, const ConvSpec& spec,
+                             const LanceConfig& cfg) {
+  return lance_gemm_any(x, w, spec, cfg, 4);
 }
 
 // Device-resident layer: filters prepared once (K2), forward per batch.

@@ -157,6 +157,25 @@ LANCE_API int lance_plan_read_stage_times(lance_plan_t plan, double* sum_ms3, in
 /* Kernel launches issued by the most recent forward on this plan. */
 LANCE_API int lance_plan_last_launch_count(lance_plan_t plan);
 
+/* ---------------------------------------------------------------------------
+ * F(4x4,3x3) extension (not in the reference,
+ * whose extract_tiles rejects m != 2, tensor.hpp:117-118).  tile_m = 2 is
+ * exactly lance_plan_create / lance_gemm_host; tile_m = 4 runs the same
+ * algorithm with 6x6 tiles at stride 4 and 36 Winograd positions (SURVEY.md
+ * Appendix D basis, reference matmul order).  On a tile_m = 4 plan every
+ * per-position array of the API holds 36 entries instead of 16:
+ * lance_plan_forward_static / lance_plan_get_params take 36 lance_qparams,
+ * the debug buffers are [36][...] and the acc dump is [36][M][K], with
+ * M = N * ceil(OH/4) * ceil(OW/4). */
+LANCE_API int lance_plan_create_tiled(const lance_conv_spec* spec, const lance_config* cfg,
+                                      int tile_m, int device, lance_plan_t* plan);
+/* Winograd positions of the plan: 16 (tile_m 2) or 36 (tile_m 4). */
+LANCE_API int lance_plan_positions(lance_plan_t plan);
+LANCE_API int lance_gemm_host_tiled(const lance_conv_spec* spec, const lance_config* cfg,
+                                    int tile_m, const float* x, const float* w, float* y);
+/* (m+2)^2 * tiles * N * C * K for tile side m (engines.hpp:573-575 generalised). */
+LANCE_API uint64_t lance_winograd_multiply_count_tiled(const lance_conv_spec* spec, int tile_m);
+
 /* Synthetic-input fixture: lance::UniformSource(seed) stream (rng.hpp:27-47),
  * mt19937_64 top-24-bit -> U(-1,1).  Host memory. */
 LANCE_API void lance_uniform_fill(uint64_t seed, float* out, size_t count);

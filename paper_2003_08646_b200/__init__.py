@@ -7,9 +7,9 @@ reference's operator API mirrored here and in include/lance/b200.hpp.
 from .api import (ConvSpec, Granularity, LanceConfig, LanceConv, LanceDeviceError,
                   LanceError, LanceMode, LanceNaNError, QuantParams, direct_multiply_count,
                   lance_gemm, params_array, uniform_floats, validate,
-                  winograd_multiply_count)
+                  winograd_multiply_count, winograd_multiply_count_tiled)
 
 __all__ = ["ConvSpec", "Granularity", "LanceConfig", "LanceConv", "LanceDeviceError",
            "LanceError", "LanceMode", "LanceNaNError", "QuantParams",
            "direct_multiply_count", "lance_gemm", "params_array", "uniform_floats",
-           "validate", "winograd_multiply_count"]
+           "validate", "winograd_multiply_count", "winograd_multiply_count_tiled"]

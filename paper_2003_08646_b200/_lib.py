@@ -79,6 +79,13 @@ def lib():
         L.lance_plan_stage_timing.argtypes = [P, ct.c_int]
         L.lance_plan_read_stage_times.argtypes = [P, ct.POINTER(ct.c_double),
                                                   ct.POINTER(ct.c_int)]
+        L.lance_plan_create_tiled.argtypes = [ct.POINTER(CSpec), ct.POINTER(CConfig), ct.c_int,
+                                              ct.c_int, ct.POINTER(P)]
+        L.lance_plan_positions.argtypes = [P]
+        L.lance_gemm_host_tiled.argtypes = [ct.POINTER(CSpec), ct.POINTER(CConfig), ct.c_int,
+                                            P, P, P]
+        L.lance_winograd_multiply_count_tiled.argtypes = [ct.POINTER(CSpec), ct.c_int]
+        L.lance_winograd_multiply_count_tiled.restype = ct.c_uint64
         L.lance_uniform_fill.argtypes = [ct.c_uint64, P, ct.c_size_t]
         L.lance_uniform_fill.restype = None
         _lib = L
@@ -93,5 +100,7 @@ EXPORTED = [
     "lance_plan_set_epilogue", "lance_plan_sync", "lance_plan_get_params",
     "lance_plan_debug_read", "lance_plan_set_acc_dump", "lance_plan_last_launch_count",
     "lance_plan_stage_timing", "lance_plan_read_stage_times",
+    "lance_plan_create_tiled", "lance_plan_positions", "lance_gemm_host_tiled",
+    "lance_winograd_multiply_count_tiled",
     "lance_uniform_fill",
 ]

@@ -126,6 +126,11 @@ def winograd_multiply_count(spec: ConvSpec) -> int:
     return int(_lib.lib().lance_winograd_multiply_count(ct.byref(spec._c())))
 
 
+def winograd_multiply_count_tiled(spec: ConvSpec, tile_m: int) -> int:
+    """(m+2)^2 * tiles * N * C * K for tile side m (2 or 4)."""
+    return int(_lib.lib().lance_winograd_multiply_count_tiled(ct.byref(spec._c()), int(tile_m)))
+
+
 def direct_multiply_count(spec: ConvSpec) -> int:
     return int(_lib.lib().lance_direct_multiply_count(ct.byref(spec._c())))
 
@@ -144,11 +149,13 @@ def _host_f32(a, shape, name):
     return a
 
 
-def lance_gemm(x, w, spec: ConvSpec, cfg: LanceConfig, out: np.ndarray | None = None):
+def lance_gemm(x, w, spec: ConvSpec, cfg: LanceConfig, out: np.ndarray | None = None,
+               tile_m: int = 2):
     """lance::lance_gemm (engines.hpp:492-536) on host arrays.
 
     x: [N][H][W][C] float32 (NHWC), w: [K][3][3][C] float32 (KRSC).
     Returns y: [N][OH][OW][K] float32.  Runs on the current CUDA device.
+    tile_m=4 selects the F(4x4,3x3) extension (not in the reference).
     """
     L = _lib.lib()
     cs, cc = spec._c(), cfg._c()
@@ -159,8 +166,8 @@ def lance_gemm(x, w, spec: ConvSpec, cfg: LanceConfig, out: np.ndarray | None = 
     y = out if out is not None else np.empty(shape, np.float32)
     if y.dtype != np.float32 or not y.flags.c_contiguous or y.size != int(np.prod(shape)):
         raise LanceError("output buffer does not match spec")
-    _check(L.lance_gemm_host(ct.byref(cs), ct.byref(cc), x.ctypes.data, w.ctypes.data,
-                             y.ctypes.data))
+    _check(L.lance_gemm_host_tiled(ct.byref(cs), ct.byref(cc), int(tile_m), x.ctypes.data,
+                                   w.ctypes.data, y.ctypes.data))
     return y.reshape(shape)
 
 
@@ -181,14 +188,18 @@ class LanceConv:
     streams); every kernel is the in-tree sm_100a library.
     """
 
-    def __init__(self, spec: ConvSpec, cfg: LanceConfig, device: int = 0):
+    def __init__(self, spec: ConvSpec, cfg: LanceConfig, device: int = 0, tile_m: int = 2):
+        """tile_m=2: the reference F(2x2,3x3) path; tile_m=4: the F(4x4,3x3)
+        extension (36 positions in params / dumps)."""
         self.spec = spec
         self.cfg = cfg
         self.device = device
+        self.tile_m = int(tile_m)
         self._plan = ct.c_void_p()
         L = _lib.lib()
-        _check(L.lance_plan_create(ct.byref(spec._c()), ct.byref(cfg._c()), device,
-                                   ct.byref(self._plan)))
+        _check(L.lance_plan_create_tiled(ct.byref(spec._c()), ct.byref(cfg._c()), self.tile_m,
+                                         device, ct.byref(self._plan)))
+        self.positions = int(L.lance_plan_positions(self._plan))
         self._acc = None
         self._bias = None
 
@@ -205,7 +216,9 @@ class LanceConv:
 
     @property
     def rows(self) -> int:
-        return self.spec.n * self.spec.tiles_per_image()
+        m = self.tile_m
+        s = self.spec
+        return s.n * ((s.out_h() + m - 1) // m) * ((s.out_w() + m - 1) // m)
 
     @property
     def device_bytes(self) -> int:
@@ -233,12 +246,12 @@ class LanceConv:
             self._plan, ct.c_void_p(bias.data_ptr()) if bias is not None else None, int(relu)))
 
     def set_acc_dump(self, acc):
-        """Also write the raw int32 accumulators [16][M][K] on later forwards."""
+        """Also write the raw int32 accumulators [positions][M][K] on later forwards."""
         import torch
         if acc is not None:
             if not (acc.is_cuda and acc.dtype == torch.int32 and acc.is_contiguous()
-                    and acc.numel() == 16 * self.rows * self.spec.k):
-                raise LanceError("acc dump must be int32 CUDA [16][M][K]")
+                    and acc.numel() == self.positions * self.rows * self.spec.k):
+                raise LanceError("acc dump must be int32 CUDA [positions][M][K]")
         self._acc = acc
         _check(_lib.lib().lance_plan_set_acc_dump(
             self._plan, ct.c_void_p(acc.data_ptr()) if acc is not None else None))
@@ -259,8 +272,10 @@ class LanceConv:
             _check(L.lance_plan_forward(self._plan, ct.c_void_p(x.data_ptr()),
                                         ct.c_void_p(y.data_ptr()), _stream_ptr(stream)))
         else:
-            arr = (_lib.CQParams * 16)(*[_lib.CQParams(q.bits, q.t_min, q.t_max, q.scale)
-                                         for q in params])
+            if len(params) != self.positions:
+                raise LanceError(f"static params: expected {self.positions} QuantParams")
+            arr = (_lib.CQParams * self.positions)(
+                *[_lib.CQParams(q.bits, q.t_min, q.t_max, q.scale) for q in params])
             _check(L.lance_plan_forward_static(self._plan, arr, ct.c_void_p(x.data_ptr()),
                                                ct.c_void_p(y.data_ptr()), _stream_ptr(stream)))
         return y
@@ -284,18 +299,18 @@ class LanceConv:
         return [arr[0], arr[1], arr[2]], n.value
 
     def params(self):
-        a = (_lib.CQParams * 16)()
-        b = (_lib.CQParams * 16)()
+        a = (_lib.CQParams * self.positions)()
+        b = (_lib.CQParams * self.positions)()
         _check(_lib.lib().lance_plan_get_params(self._plan, a, b))
         conv = lambda arr: [QuantParams(q.bits, q.t_min, q.t_max, q.scale) for q in arr]
         return conv(a), conv(b)
 
     def debug_read(self, what: str) -> np.ndarray:
-        s, M = self.spec, self.rows
-        table = {"codes_a": (_lib.DBG_CODES_A, (16, M, s.c), np.uint8),
-                 "rowsum": (_lib.DBG_ROWSUM, (16, M), np.int32),
-                 "codes_w": (_lib.DBG_CODES_W, (16, s.c, s.k), np.uint8),
-                 "colsum": (_lib.DBG_COLSUM, (16, s.k), np.int32)}
+        s, M, P = self.spec, self.rows, self.positions
+        table = {"codes_a": (_lib.DBG_CODES_A, (P, M, s.c), np.uint8),
+                 "rowsum": (_lib.DBG_ROWSUM, (P, M), np.int32),
+                 "codes_w": (_lib.DBG_CODES_W, (P, s.c, s.k), np.uint8),
+                 "colsum": (_lib.DBG_COLSUM, (P, s.k), np.int32)}
         code, shape, dt = table[what]
         out = np.empty(shape, dt)
         _check(_lib.lib().lance_plan_debug_read(self._plan, code, out.ctypes.data, out.nbytes))
@@ -303,5 +318,5 @@ class LanceConv:
 
 
 def params_array(qps) -> np.ndarray:
-    """[16] QuantParams -> float32 [16, 4] (bits, t_min, t_max, scale)."""
+    """[P] QuantParams -> float32 [P, 4] (bits, t_min, t_max, scale)."""
     return np.array([[q.bits, q.t_min, q.t_max, q.scale] for q in qps], dtype=np.float32)

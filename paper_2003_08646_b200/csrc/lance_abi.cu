@@ -136,6 +136,9 @@ int make_input_map(CUtensorMap* map, const float* x, const lance_conv_spec& s, c
 
 struct lance_plan_s {
   int device = 0;
+  int tm = 2;   // Winograd output tile side: 2 (reference F(2x2,3x3)) or 4 (F(4x4,3x3))
+  int np = 16;  // positions (tm + 2)^2
+  F4Geom f4{};
   lance_conv_spec spec{};
   lance_config cfg{};
   int OH = 0, OW = 0, TH = 0, TW = 0, P = 0;
@@ -260,10 +263,19 @@ void lance_uniform_fill(uint64_t seed, float* out, size_t count) {
   }
 }
 
+static int create_f4(lance_plan_s* p, const lance_conv_spec* spec, const lance_config* cfg);
+
 int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int device,
                       lance_plan_t* out) {
+  return lance_plan_create_tiled(spec, cfg, 2, device, out);
+}
+
+int lance_plan_create_tiled(const lance_conv_spec* spec, const lance_config* cfg, int tile_m,
+                            int device, lance_plan_t* out) {
   if (!out) return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_create: null output");
   *out = nullptr;
+  if (tile_m != 2 && tile_m != 4)
+    return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_create: tile_m must be 2 or 4");
   int rc = validate(spec, cfg);
   if (rc) return rc;
   int ndev = 0;
@@ -285,6 +297,15 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   p->spec = *spec;
   p->cfg = *cfg;
   p->sm_count = prop.multiProcessorCount;
+  if (tile_m == 4) {
+    if ((rc = create_f4(p, spec, cfg))) {
+      free_plan(p);
+      delete p;
+      return rc;
+    }
+    *out = p;
+    return LANCE_OK;
+  }
   p->OH = out_h(*spec);
   p->OW = out_w(*spec);
   p->TH = (p->OH + 1) / 2;
@@ -482,6 +503,81 @@ int lance_plan_create(const lance_conv_spec* spec, const lance_config* cfg, int 
   return LANCE_OK;
 }
 
+// F(4x4,3x3) plan (lance_f4.cu): 36 positions, BN = 16, B operand images
+// of 16 filters, row sums written by the quantiser.
+static int create_f4(lance_plan_s* p, const lance_conv_spec* spec, const lance_config* cfg) {
+  p->tm = 4;
+  p->np = 36;
+  p->OH = out_h(*spec);
+  p->OW = out_w(*spec);
+  p->TH = (p->OH + 3) / 4;
+  p->TW = (p->OW + 3) / 4;
+  p->P = p->TH * p->TW;
+  p->M = static_cast<long long>(spec->n) * p->P;
+  if (static_cast<long long>(spec->n) * p->OH * p->OW >= (1LL << 27))
+    return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_gemm: N * OH * OW exceeds 2^27 output pixels");
+  p->C_pad = round_up(spec->c, 32);
+  p->BK = (p->C_pad % 128 == 0) ? 128 : (p->C_pad % 64 == 0 ? 64 : 32);
+  p->BN = 16;
+  p->K_pad = round_up(spec->k, 16);
+  p->rs_pitch = p->M;
+  p->small_acc = static_cast<double>(spec->c) * ((1 << cfg->bits_i) - 1) *
+                     ((1 << cfg->bits_w) - 1) < 16777216.0;
+  F4Geom& g = p->f4;
+  g.N = spec->n;
+  g.H = spec->h;
+  g.W = spec->w;
+  g.C = spec->c;
+  g.K = spec->k;
+  g.pad = spec->pad;
+  g.OH = p->OH;
+  g.OW = p->OW;
+  g.TH = p->TH;
+  g.TW = p->TW;
+  g.P = p->P;
+  g.M = static_cast<int>(p->M);
+  g.C_pad = p->C_pad;
+  g.K_pad = p->K_pad;
+  g.bk = p->BK;
+  g.nk = p->C_pad / p->BK;
+  g.rs_pitch = static_cast<int>(p->rs_pitch);
+  g.granularity = cfg->granularity;
+  g.num_n_tiles = p->K_pad / 16;
+  g.stages = 0;
+  p->range_grid = f4_range_grid(g, p->sm_count);
+  const long long kc = static_cast<long long>(spec->k) * spec->c;
+  p->filter_grid = static_cast<int>(std::min<long long>((kc + 255) / 256, 2LL * p->sm_count));
+  const size_t codes_a_bytes = static_cast<size_t>(36) * ((p->M + kBM - 1) / kBM * kBM) * p->C_pad;
+  const size_t codes_w_bytes = static_cast<size_t>(36) * p->K_pad * p->C_pad;
+  const int part_rows = std::max(p->range_grid, p->filter_grid);
+  int rc;
+  if ((rc = dev_alloc(p, &p->codes_a, codes_a_bytes)) ||
+      (rc = dev_alloc(p, &p->rowsum, sizeof(int32_t) * 36 * p->rs_pitch)) ||
+      (rc = dev_alloc(p, &p->codes_w, codes_w_bytes)) ||
+      (rc = dev_alloc(p, &p->colsum, sizeof(int32_t) * 36 * p->K_pad)) ||
+      (rc = dev_alloc(p, &p->u_tmp, sizeof(float) * 36 * kc)) ||
+      (rc = dev_alloc(p, &p->partials, sizeof(float) * 72 * part_rows)) ||
+      (rc = dev_alloc(p, &p->state, sizeof(LanceDevState))))
+    return rc;
+  cudaError_t e = cudaMemset(p->codes_a, 0, codes_a_bytes);
+  if (e == cudaSuccess) e = cudaMemset(p->codes_w, 0, codes_w_bytes);
+  if (e == cudaSuccess) e = cudaMemset(p->colsum, 0, sizeof(int32_t) * 36 * p->K_pad);
+  LanceDevState init{};
+  init.bits_i = cfg->bits_i;
+  init.bits_w = cfg->bits_w;
+  if (e == cudaSuccess) e = cudaMemcpy(p->state, &init, sizeof init, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "plan init");
+  return LANCE_OK;
+}
+
+int lance_plan_positions(lance_plan_t p) { return p ? p->np : 0; }
+
+uint64_t lance_winograd_multiply_count_tiled(const lance_conv_spec* s, int tile_m) {
+  if (tile_m != 2 && tile_m != 4) return 0;
+  const uint64_t tiles = uint64_t((out_h(*s) + tile_m - 1) / tile_m) * ((out_w(*s) + tile_m - 1) / tile_m);
+  return uint64_t(tile_m + 2) * (tile_m + 2) * tiles * s->n * s->c * uint64_t(s->k);
+}
+
 int lance_plan_destroy(lance_plan_t p) {
   if (!p) return LANCE_OK;
   DeviceGuard guard(p->device);
@@ -496,8 +592,12 @@ int lance_plan_set_filters(lance_plan_t p, const float* w_dev, void* stream) {
   if (!p || !w_dev) return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_set_filters: null argument");
   DeviceGuard guard(p->device);
   auto s = static_cast<cudaStream_t>(stream);
-  LANCE_CUDA(launch_filter_prepare(w_dev, p->u_tmp, p->partials, p->filter_grid, p->codes_w,
-                                   p->colsum, p->state, p->f_geom, s));
+  if (p->tm == 4)
+    LANCE_CUDA(launch_f4_filter_prepare(w_dev, p->u_tmp, p->partials, p->filter_grid, p->codes_w,
+                                        p->colsum, p->state, p->f4, s));
+  else
+    LANCE_CUDA(launch_filter_prepare(w_dev, p->u_tmp, p->partials, p->filter_grid, p->codes_w,
+                                     p->colsum, p->state, p->f_geom, s));
   p->filters_ready = true;
   return LANCE_OK;
 }
@@ -520,8 +620,34 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
     ++p->recorded;
     LANCE_CUDA(cudaEventRecord(ev[0], s));
   }
+  if (p->tm == 4) {
+    if (static_params) {
+      StaticParams prm{};
+      prm.np = 36;
+      for (int i = 0; i < 36; ++i) {
+        if (static_params[i].bits != p->cfg.bits_i)
+          return fail(LANCE_ERR_INVALID_ARGUMENT, "static params: bits differ from cfg.bits_i");
+        prm.tmin[i] = static_params[i].t_min;
+        prm.tmax[i] = static_params[i].t_max;
+        prm.scale[i] = static_params[i].scale;
+      }
+      LANCE_CUDA(launch_static_params(p->state, prm, p->spec.c, s));
+    } else {
+      LANCE_CUDA(launch_f4_range(x_dev, p->partials, p->range_grid, p->state, p->f4, s));
+    }
+    if (ev) LANCE_CUDA(cudaEventRecord(ev[1], s));
+    LANCE_CUDA(launch_f4_quant(x_dev, p->codes_a, p->rowsum, p->state, p->f4, static_params != nullptr,
+                               p->sm_count, s));
+    if (ev) LANCE_CUDA(cudaEventRecord(ev[2], s));
+    LANCE_CUDA(launch_f4_gemm(p->codes_a, p->codes_w, p->rowsum, p->colsum, p->small_acc, p->state, y_dev,
+                              p->acc_dump, p->bias, p->relu, p->f4, s));
+    if (ev) LANCE_CUDA(cudaEventRecord(ev[3], s));
+    p->last_launches = 3;
+    return LANCE_OK;
+  }
   if (static_params) {
     StaticParams prm{};
+    prm.np = 16;
     for (int i = 0; i < 16; ++i) {
       if (static_params[i].bits != p->cfg.bits_i)
         return fail(LANCE_ERR_INVALID_ARGUMENT, "static params: bits differ from cfg.bits_i");
@@ -636,7 +762,7 @@ int lance_plan_get_params(lance_plan_t p, lance_qparams* in16, lance_qparams* w1
   LanceDevState st;
   LANCE_CUDA(cudaDeviceSynchronize());
   LANCE_CUDA(cudaMemcpy(&st, p->state, sizeof st, cudaMemcpyDeviceToHost));
-  for (int i = 0; i < 16; ++i) {
+  for (int i = 0; i < p->np; ++i) {
     if (in16) in16[i] = {p->cfg.bits_i, st.a_tmin[i], st.a_tmax[i], st.a_scale[i]};
     if (w16) w16[i] = {p->cfg.bits_w, st.w_tmin[i], st.w_tmax[i], st.w_scale[i]};
   }
@@ -648,44 +774,46 @@ int lance_plan_debug_read(lance_plan_t p, int what, void* dst, size_t bytes) {
   DeviceGuard guard(p->device);
   LANCE_CUDA(cudaDeviceSynchronize());
   const long long M = p->M;
-  const int C = p->spec.c, K = p->spec.k;
+  const int C = p->spec.c, K = p->spec.k, np = p->np;
   switch (what) {
-    case LANCE_DBG_CODES_A: {  // device UMMA images -> reference [16][M][C]
-      if (bytes != size_t(16) * M * C) return fail(LANCE_ERR_INVALID_ARGUMENT, "bad size");
-      std::string tmp(size_t(16) * ((M + kBM - 1) / kBM * kBM) * p->C_pad, '\0');
+    case LANCE_DBG_CODES_A: {  // device UMMA images -> reference [np][M][C]
+      if (bytes != size_t(np) * M * C) return fail(LANCE_ERR_INVALID_ARGUMENT, "bad size");
+      std::string tmp(size_t(np) * ((M + kBM - 1) / kBM * kBM) * p->C_pad, '\0');
       LANCE_CUDA(cudaMemcpy(tmp.data(), p->codes_a, tmp.size(), cudaMemcpyDeviceToHost));
       auto* out = static_cast<uint8_t*>(dst);
       const int nk = p->C_pad / p->BK;
-      for (int q = 0; q < 16; ++q)
+      for (int q = 0; q < np; ++q)
         for (long long m = 0; m < M; ++m)
           for (int c = 0; c < C; ++c)
-            out[(size_t(q) * M + m) * C + c] =
-                static_cast<uint8_t>(tmp[umma_image_offset(m, c, q, kBM, p->BK, nk)]);
+            out[(size_t(q) * M + m) * C + c] = static_cast<uint8_t>(
+                tmp[np == 16 ? umma_image_offset(m, c, q, kBM, p->BK, nk)
+                             : umma_image_offset_np(m, c, q, kBM, p->BK, nk, np)]);
       return LANCE_OK;
     }
     case LANCE_DBG_ROWSUM: {
-      if (bytes != sizeof(int32_t) * 16 * M) return fail(LANCE_ERR_INVALID_ARGUMENT, "bad size");
+      if (bytes != sizeof(int32_t) * np * M) return fail(LANCE_ERR_INVALID_ARGUMENT, "bad size");
       LANCE_CUDA(cudaMemcpy2D(dst, sizeof(int32_t) * M, p->rowsum, sizeof(int32_t) * p->rs_pitch,
-                              sizeof(int32_t) * M, 16, cudaMemcpyDeviceToHost));
+                              sizeof(int32_t) * M, np, cudaMemcpyDeviceToHost));
       return LANCE_OK;
     }
-    case LANCE_DBG_CODES_W: {  // device UMMA images -> reference [16][C][K]
-      if (bytes != size_t(16) * C * K) return fail(LANCE_ERR_INVALID_ARGUMENT, "bad size");
-      std::string tmp(size_t(16) * p->K_pad * p->C_pad, '\0');
+    case LANCE_DBG_CODES_W: {  // device UMMA images -> reference [np][C][K]
+      if (bytes != size_t(np) * C * K) return fail(LANCE_ERR_INVALID_ARGUMENT, "bad size");
+      std::string tmp(size_t(np) * p->K_pad * p->C_pad, '\0');
       LANCE_CUDA(cudaMemcpy(tmp.data(), p->codes_w, tmp.size(), cudaMemcpyDeviceToHost));
       auto* out = static_cast<uint8_t*>(dst);
       const int nk = p->C_pad / p->BK;
-      for (int q = 0; q < 16; ++q)
+      for (int q = 0; q < np; ++q)
         for (int c = 0; c < C; ++c)
           for (int k = 0; k < K; ++k)
-            out[(size_t(q) * C + c) * K + k] =
-                static_cast<uint8_t>(tmp[umma_image_offset(k, c, q, p->BN, p->BK, nk)]);
+            out[(size_t(q) * C + c) * K + k] = static_cast<uint8_t>(
+                tmp[np == 16 ? umma_image_offset(k, c, q, p->BN, p->BK, nk)
+                             : umma_image_offset_np(k, c, q, p->BN, p->BK, nk, np)]);
       return LANCE_OK;
     }
     case LANCE_DBG_COLSUM: {
-      if (bytes != sizeof(int32_t) * 16 * K) return fail(LANCE_ERR_INVALID_ARGUMENT, "bad size");
+      if (bytes != sizeof(int32_t) * np * K) return fail(LANCE_ERR_INVALID_ARGUMENT, "bad size");
       LANCE_CUDA(cudaMemcpy2D(dst, sizeof(int32_t) * K, p->colsum, sizeof(int32_t) * p->K_pad,
-                              sizeof(int32_t) * K, 16, cudaMemcpyDeviceToHost));
+                              sizeof(int32_t) * K, np, cudaMemcpyDeviceToHost));
       return LANCE_OK;
     }
     default:
@@ -702,12 +830,19 @@ struct HostCtx {
   float *x = nullptr, *w = nullptr, *y = nullptr;
   cudaStream_t stream = nullptr;
 };
-using Key = std::tuple<int, int, int, int, int, int, int, int, int, int>;
+using Key = std::tuple<int, int, int, int, int, int, int, int, int, int, int>;
 thread_local std::map<Key, HostCtx> g_host_ctx;
 }  // namespace
 
 int lance_gemm_host(const lance_conv_spec* spec, const lance_config* cfg, const float* x,
                     const float* w, float* y) {
+  return lance_gemm_host_tiled(spec, cfg, 2, x, w, y);
+}
+
+int lance_gemm_host_tiled(const lance_conv_spec* spec, const lance_config* cfg, int tile_m,
+                          const float* x, const float* w, float* y) {
+  if (tile_m != 2 && tile_m != 4)
+    return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_gemm: tile_m must be 2 or 4");
   int rc = validate(spec, cfg);
   if (rc) return rc;
   if (!x || !w || !y) return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_gemm: null buffer");
@@ -717,13 +852,13 @@ int lance_gemm_host(const lance_conv_spec* spec, const lance_config* cfg, const 
     return fail(LANCE_ERR_NO_DEVICE, "no CUDA device: the B200 lance_gemm path has no CPU fallback");
   }
   const Key key{dev, spec->n, spec->c, spec->h, spec->w, spec->k, spec->pad, cfg->bits_w,
-                cfg->bits_i, cfg->granularity};
+                cfg->bits_i, cfg->granularity, tile_m};
   HostCtx& ctx = g_host_ctx[key];
   const size_t xb = sizeof(float) * size_t(spec->n) * spec->h * spec->w * spec->c;
   const size_t wb = sizeof(float) * size_t(spec->k) * 9 * spec->c;
   const size_t yb = sizeof(float) * size_t(spec->n) * out_h(*spec) * out_w(*spec) * spec->k;
   if (!ctx.plan) {
-    if ((rc = lance_plan_create(spec, cfg, dev, &ctx.plan))) {
+    if ((rc = lance_plan_create_tiled(spec, cfg, tile_m, dev, &ctx.plan))) {
       g_host_ctx.erase(key);
       return rc;
     }

@@ -133,6 +133,27 @@ __device__ __forceinline__ uint32_t quantize_code(float v, float tmin, float sca
 constexpr float kMagic = 12582912.0f;            // 1.5 * 2^23
 constexpr float kTieGuard = 0.49993896484375f;   // 0.5 - 2^-14
 
+// Exact reference code for a value whose fast-path residual flagged it as
+// being near the rounding boundary h = n + 0.5*sign(r) (dynamic params: d >= 0,
+// scale > 0 normal).  roundf(RN(d/s)) crosses to the upper code iff
+// RN(d/s) >= h, i.e. iff d/s > mid(pred(h), h) (a float quotient is never a
+// midpoint, so there is no tie), i.e. iff d - s*h > -s*delta with
+// delta = (h - pred(h))/2.  d - s*h is exactly representable here
+// (|d - s*h| <= s*2^-13, granularity ulp(s)/2), so one FFMA decides it.
+__device__ __forceinline__ uint32_t exact_code_near_boundary(float d, float s, float gq, float r,
+                                                             float top) {
+  const float n = __fsub_rn(gq, kMagic);
+  const float h = (r > 0.0f) ? __fadd_rn(n, 0.5f) : __fsub_rn(n, 0.5f);
+  const float lower = (r > 0.0f) ? n : __fsub_rn(n, 1.0f);
+  const float upper = __fadd_rn(lower, 1.0f);
+  const float pred_h = __int_as_float(__float_as_int(h) - 1);
+  const float delta = __fmul_rn(__fsub_rn(h, pred_h), 0.5f);
+  const float e = __fmaf_rn(-s, h, d);
+  float c = (e > -__fmul_rn(s, delta)) ? upper : lower;
+  c = fminf(fmaxf(c, 0.0f), top);
+  return static_cast<uint32_t>(c);
+}
+
 // ---------------------------------------------------------------- ranges
 // Block-wide (min, max) partials -> the last block to finish folds all
 // partials; returns true in that block with the 32 results in s_red[0..31].
@@ -226,8 +247,8 @@ __device__ __forceinline__ void fit_from_ranges(const float* s_red, int gran, in
 
 // Hoisted constants of affine_term (lowpgemm.hpp:110-114), a = input,
 // b = weight:  m = ((k1*dot + k2*sum_a) + k3*sum_b) + k4.
-__device__ __forceinline__ void make_epilogue_consts(LanceDevState* st, int C) {
-  if (threadIdx.x < 16) {
+__device__ __forceinline__ void make_epilogue_consts(LanceDevState* st, int C, int np = 16) {
+  if (threadIdx.x < np) {
     const int p = threadIdx.x;
     const float sa = st->a_scale[p], oa = st->a_tmin[p];
     const float sb = st->w_scale[p], ob = st->w_tmin[p];

@@ -244,27 +244,6 @@ __global__ void __launch_bounds__(256, 2) input_range_fast_kernel(const float* _
   }
 }
 
-// Exact reference code for a value whose fast-path residual flagged it as
-// being near the rounding boundary h = n + 0.5*sign(r) (dynamic params: d >= 0,
-// scale > 0 normal).  roundf(RN(d/s)) crosses to the upper code iff
-// RN(d/s) >= h, i.e. iff d/s > mid(pred(h), h) (a float quotient is never a
-// midpoint, so there is no tie), i.e. iff d - s*h > -s*delta with
-// delta = (h - pred(h))/2.  d - s*h is exactly representable here
-// (|d - s*h| <= s*2^-13, granularity ulp(s)/2), so one FFMA decides it.
-__device__ __forceinline__ uint32_t exact_code_near_boundary(float d, float s, float gq, float r,
-                                                             float top) {
-  const float n = __fsub_rn(gq, kMagic);
-  const float h = (r > 0.0f) ? __fadd_rn(n, 0.5f) : __fsub_rn(n, 0.5f);
-  const float lower = (r > 0.0f) ? n : __fsub_rn(n, 1.0f);
-  const float upper = __fadd_rn(lower, 1.0f);
-  const float pred_h = __int_as_float(__float_as_int(h) - 1);
-  const float delta = __fmul_rn(__fsub_rn(h, pred_h), 0.5f);
-  const float e = __fmaf_rn(-s, h, d);
-  float c = (e > -__fmul_rn(s, delta)) ? upper : lower;
-  c = fminf(fmaxf(c, 0.0f), top);
-  return static_cast<uint32_t>(c);
-}
-
 // --------------------------------------------------------------------------
 // K1: codes + row sums, one strip per warp.
 //
@@ -628,7 +607,7 @@ __global__ void __launch_bounds__(192, 2) input_quant_fast2_kernel(const float* 
 
 // Static-params mode: caller-supplied input QuantParams[16].
 __global__ void static_params_kernel(LanceDevState* st, StaticParams prm, int C) {
-  if (threadIdx.x < 16) {
+  if (threadIdx.x < prm.np) {
     const int p = threadIdx.x;
     const float s = prm.scale[p];
     st->a_tmin[p] = prm.tmin[p];
@@ -637,8 +616,8 @@ __global__ void static_params_kernel(LanceDevState* st, StaticParams prm, int C)
     st->a_rcp[p] = (s == 0.0f) ? 0.0f : __frcp_rn(s);
     if (p == 0) st->nan_in = 0;
   }
-  __syncwarp();
-  make_epilogue_consts(st, C);
+  __syncthreads();
+  make_epilogue_consts(st, C, prm.np);
 }
 
 // --------------------------------------------------------------------------
@@ -704,7 +683,7 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
 
 cudaError_t launch_static_params(LanceDevState* st, const StaticParams& prm, int C,
                                  cudaStream_t s) {
-  static_params_kernel<<<1, 32, 0, s>>>(st, prm, C);
+  static_params_kernel<<<1, 64, 0, s>>>(st, prm, C);
   return cudaGetLastError();
 }
 

@@ -13,7 +13,8 @@
 
 namespace lance_dev {
 
-constexpr int kPositions = 16;  // (m + r - 1)^2 for F(2x2,3x3)
+constexpr int kPositions = 16;     // (m + r - 1)^2 for F(2x2,3x3)
+constexpr int kMaxPositions = 36;  // F(4x4,3x3) extension (lance_f4.cu)
 constexpr int kBM = 128;        // GEMM rows (Winograd tiles) per CTA = UMMA M
 constexpr int kChunk = 64;      // channels per K0/K1 warp item (32 lanes x 2)
 
@@ -22,9 +23,9 @@ constexpr int kChunk = 64;      // channels per K0/K1 warp item (32 lanes x 2)
 // for both operands plus the hoisted affine constants of affine_term
 // (lowpgemm.hpp:110-114): m = ((k1*dot + k2*sum_a) + k3*sum_b) + k4.
 struct LanceDevState {
-  float a_tmin[kPositions], a_tmax[kPositions], a_scale[kPositions], a_rcp[kPositions];
-  float w_tmin[kPositions], w_tmax[kPositions], w_scale[kPositions];
-  float k1[kPositions], k2[kPositions], k3[kPositions], k4[kPositions];
+  float a_tmin[kMaxPositions], a_tmax[kMaxPositions], a_scale[kMaxPositions], a_rcp[kMaxPositions];
+  float w_tmin[kMaxPositions], w_tmax[kMaxPositions], w_scale[kMaxPositions];
+  float k1[kMaxPositions], k2[kMaxPositions], k3[kMaxPositions], k4[kMaxPositions];
   int bits_i, bits_w;
   int nan_in, nan_w;
   unsigned int ticket_in, ticket_w;
@@ -119,8 +120,35 @@ __host__ __device__ __forceinline__ long long umma_image_offset(long long row, i
 }
 
 struct StaticParams {
-  float tmin[kPositions], tmax[kPositions], scale[kPositions];
+  float tmin[kMaxPositions], tmax[kMaxPositions], scale[kMaxPositions];
+  int np;  // positions in use (16, or 36 for F(4x4))
 };
+
+// F(4x4,3x3) geometry (lance_f4.cu): 6x6 input tiles at stride 4, 36
+// positions, BN = 16 filters per GEMM tile.
+struct F4Geom {
+  int N, H, W, C, K, pad;
+  int OH, OW, TH, TW, P;
+  int M;             // N * P GEMM rows
+  int C_pad, K_pad;  // C_pad = nk * bk, K_pad multiple of 16
+  int bk, nk;        // UMMA image K chunk (32 / 64 / 128 channels) and chunks
+  int rs_pitch;      // row-sum plane pitch
+  int granularity;   // 1 PerPosition, 2 PerTensor
+  int num_n_tiles;   // K_pad / 16
+  int stages;        // GEMM ring depth (set by the launcher)
+};
+
+// The operand image offset of umma_image_offset for np position planes in
+// natural order (F(4x4): np = 36, p = 6a + b).
+__host__ __device__ __forceinline__ long long umma_image_offset_np(long long row, int c, int p,
+                                                                    int rows_per_img, int bk,
+                                                                    int nk, int np) {
+  const long long blk = row / rows_per_img;
+  const int r = static_cast<int>(row - blk * rows_per_img);
+  const int kc = c / bk, cb = c - kc * bk;
+  return ((blk * np + p) * nk + kc) * static_cast<long long>(rows_per_img * bk) +
+         umma_swizzle(static_cast<uint32_t>(r * bk + cb), bk);
+}
 
 // Host-side launchers.  All stream-ordered.
 int input_range_grid(const InGeom& g, int sm_count);
@@ -145,5 +173,20 @@ cudaError_t launch_gemm(const uint8_t* codes_a, const uint8_t* codes_w, const CU
                         int bk, int bn, int small_acc, const int32_t* colsum,
                         const LanceDevState* st, float* y, int32_t* acc_dump, const float* bias,
                         int relu, const GemmGeom& g, cudaStream_t s);
+
+// F(4x4,3x3) launchers (lance_f4.cu).
+int f4_range_grid(const F4Geom& g, int sm_count);
+cudaError_t launch_f4_range(const float* x, float* partials, int grid, LanceDevState* st,
+                            const F4Geom& g, cudaStream_t s);
+cudaError_t launch_f4_quant(const float* x, uint8_t* codes, int32_t* rowsum,
+                            const LanceDevState* st, const F4Geom& g, int static_mode,
+                            int sm_count, cudaStream_t s);
+cudaError_t launch_f4_filter_prepare(const float* w, float* u_tmp, float* partials, int grid,
+                                     uint8_t* codes_w, int32_t* colsum, LanceDevState* st,
+                                     const F4Geom& g, cudaStream_t s);
+cudaError_t launch_f4_gemm(const uint8_t* codes_a, const uint8_t* codes_w, const int32_t* rowsum,
+                           const int32_t* colsum, int small_acc, const LanceDevState* st, float* y,
+                           int32_t* acc_dump, const float* bias, int relu, const F4Geom& g,
+                           cudaStream_t s);
 
 }  // namespace lance_dev

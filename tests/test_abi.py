@@ -67,6 +67,15 @@ def test_multiply_counts():
     assert lance.winograd_multiply_count(s) == 16 * 16 * 256 * 512 * 512
 
 
+def test_multiply_counts_tiled():
+    s = lance.ConvSpec(256, 64, 56, 56, 64, 1)
+    assert lance.winograd_multiply_count_tiled(s, 2) == lance.winograd_multiply_count(s)
+    assert lance.winograd_multiply_count_tiled(s, 4) == 36 * 14 * 14 * 256 * 64 * 64
+    s = lance.ConvSpec(1, 8, 7, 7, 8, 1)  # 7x7 -> 2x2 tiles of 4
+    assert lance.winograd_multiply_count_tiled(s, 4) == 36 * 4 * 8 * 8
+    assert lance.winograd_multiply_count_tiled(s, 3) == 0
+
+
 def test_uniform_fixture_matches_reference_stream():
     assert np.array_equal(lance.uniform_floats(4096, 42), Oracle().uniform(42, 4096))
 
@@ -80,3 +89,6 @@ def test_no_cpu_fallback_without_device():
     with pytest.raises(lance.LanceDeviceError):
         lance.lance_gemm(np.zeros((1, 8, 8, 4), np.float32), np.zeros((4, 3, 3, 4), np.float32),
                          s, cfg)
+    with pytest.raises(lance.LanceDeviceError):
+        lance.lance_gemm(np.zeros((1, 8, 8, 4), np.float32), np.zeros((4, 3, 3, 4), np.float32),
+                         s, cfg, tile_m=4)
