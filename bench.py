@@ -45,21 +45,23 @@ def peaks():
         return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
 
 
-def layer_dims(c, k, h, n, pad=1):
+def layer_dims(c, k, h, n, pad=1, tm=2):
     oh = h + 2 * pad - 2
-    th = (oh + 1) // 2
+    th = (oh + tm - 1) // tm
     p = th * th
     m = n * p
     return oh, p, m
 
 
-def stage_bytes(c, k, h, n):
-    """Algorithmic HBM bytes per launch."""
-    oh, _, m = layer_dims(c, k, h, n)
+def stage_bytes(c, k, h, n, tm=2):
+    """Algorithmic HBM bytes per launch; np = (tm+2)^2
+    Winograd positions (16 for F(2x2), 36 for F(4x4))."""
+    oh, _, m = layer_dims(c, k, h, n, tm=tm)
+    npos = (tm + 2) ** 2
     x = 4 * n * h * h * c
     k0 = x
-    k1 = x + 16 * m * c + 4 * 16 * m
-    k3 = 16 * m * c + 16 * c * k + 4 * 16 * m + 4 * 16 * k + 4 * n * oh * oh * k
+    k1 = x + npos * m * c + 4 * npos * m
+    k3 = npos * m * c + npos * c * k + 4 * npos * m + 4 * npos * k + 4 * n * oh * oh * k
     return k0, k1, k3
 
 
@@ -68,9 +70,9 @@ def direct_macs(c, k, h, n):
     return n * k * c * oh * oh * 9
 
 
-def winograd_macs(c, k, h, n):
-    _, _, m = layer_dims(c, k, h, n)
-    return 16 * m * c * k
+def winograd_macs(c, k, h, n, tm=2):
+    _, _, m = layer_dims(c, k, h, n, tm=tm)
+    return (tm + 2) ** 2 * m * c * k
 
 
 class ClockSampler:
@@ -156,6 +158,22 @@ def cpu_reference_images_per_s(batch: int, reps: int, threads: int):
     return batch / total, total
 
 
+def cpu_port_f4_images_per_s(batch: int):
+    """F(4x4) has no reference implementation: the oracle port
+    (lo_lance_gemm_tiled, tile_m=4, one thread) on the 13 layer shapes."""
+    import oracle
+    lo = oracle.Oracle()
+    total = 0.0
+    for i, (c, k, h) in enumerate(RESNET18):
+        spec = oracle.Spec(batch, c, h, h, k, 1)
+        x = lo.uniform(42 + i, batch * h * h * c).reshape(batch, h, h, c)
+        w = lo.uniform(7 + i, k * 9 * c).reshape(k, 3, 3, c)
+        t0 = time.perf_counter()
+        lo.lance_gemm(spec, x, w, tile_m=4)
+        total += time.perf_counter() - t0
+    return batch / total, total
+
+
 def run_reference_arm(args, ws, rank):
     """--impl reference: the reference CPU implementation on the host cores."""
     if rank != 0:
@@ -227,6 +245,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--layers", type=str, default="", help="comma list of layer indices (debug)")
+    ap.add_argument("--tile-m", type=int, default=2, choices=[2, 4],
+                    help="Winograd output tile: 2 = F(2x2,3x3) (reference), 4 = F(4x4,3x3) (BASELINE config 4)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -251,6 +271,7 @@ def main():
     if args.layers:
         layers = [RESNET18[int(i)] for i in args.layers.split(",")]
     N = args.batch
+    TM = args.tile_m
     cfg = lance.LanceConfig(8, 8, lance.Granularity.PerPosition, lance.LanceMode.Gemm)
 
     # Synthetic inputs: UniformSource(seed) x then w (bench.hpp:129-133), per layer and rank.
@@ -261,7 +282,7 @@ def main():
         host = lance.uniform_floats(nx + nw, 42 + 1000 * rank + i)
         x = torch.from_numpy(host[:nx]).to(dev).view(N, h, h, c)
         w = torch.from_numpy(host[nx:]).to(dev).view(k, 3, 3, c)
-        conv = lance.LanceConv(spec, cfg, device=local)
+        conv = lance.LanceConv(spec, cfg, device=local, tile_m=TM)
         conv.set_filters(w)
         y = torch.empty((N, spec.out_h(), spec.out_w(), k), dtype=torch.float32, device=dev)
         state.append((spec, conv, x, w, y, host))
@@ -307,7 +328,7 @@ def main():
     for spec, conv, *_ in state:
         ms, nf = conv.read_stage_times()
         conv.stage_timing(False)
-        b = stage_bytes(spec.c, spec.k, spec.h, N)
+        b = stage_bytes(spec.c, spec.k, spec.h, N, TM)
         stage_ms += np.array(ms)
         stage_bytes_tot += np.array(b) * nf
         per_layer.append({"c": spec.c, "k": spec.k, "h": spec.h,
@@ -341,11 +362,11 @@ def main():
     (dsi, dc, dk, dh), dus = max(shape_ms.items(), key=lambda kv: sum(kv[1]))
     dom = dsi
     launch_us = float(np.mean(dus))
-    launch_bytes = stage_bytes(dc, dk, dh, N)[dsi]
+    launch_bytes = stage_bytes(dc, dk, dh, N, TM)[dsi]
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(names[dsi], {}).get(f"c{dc}_h{dh}")
+            traffic = json.load(f).get(names[dsi], {}).get(f"c{dc}_h{dh}" + ("_f4" if TM == 4 else ""))
     except Exception:
         pass
     achieved = launch_bytes / (launch_us * 1e-6) / 1e9
@@ -356,7 +377,7 @@ def main():
                 "stages": stages}
     i8 = int8_peak_tops(dev) if rank == 0 else None
     t3 = stage_ms[2] * 1e-3 / args.steps
-    wmacs = sum(winograd_macs(c, k, h, N) for c, k, h in layers)
+    wmacs = sum(winograd_macs(c, k, h, N, TM) for c, k, h in layers)
     roofline["gemm_stage_int8"] = {"achieved_tops": 2 * wmacs / t3 / 1e12 if t3 > 0 else None,
                                    "peak_tops": i8, "peak_source": "measured here: torch._int_mm 8192^3",
                                    "frac": (2 * wmacs / t3 / 1e12 / i8) if (i8 and t3 > 0) else None}
@@ -378,7 +399,7 @@ def main():
 
         def e2e_step():
             for spec, hx, hw, hy in pinned:
-                lance.lance_gemm(hx, hw, spec, cfg, out=hy)
+                lance.lance_gemm(hx, hw, spec, cfg, out=hy, tile_m=TM)
 
         e2e_step()
         if pg:
@@ -397,7 +418,12 @@ def main():
                "api": "lance_gemm(x, w, spec, cfg) host drop-in (K2 + K0 + K1 + K3/K4 per call, pinned host buffers)"}
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
+    if rank == 0 and ws == 1 and not args.no_cpu and TM == 4:
+        v, tot = cpu_port_f4_images_per_s(1)
+        cpu = {"value": v, "unit": "images/s", "cores": 1, "kind": "port",
+               "sample": f"13 ResNet-18 3x3 layers at batch 1, oracle lo_lance_gemm_tiled(tile_m=4) "
+                         f"single thread ({tot:.2f} s/pass); the reference has no F(4x4)"}
+    elif rank == 0 and ws == 1 and not args.no_cpu:
         try:
             threads = os.cpu_count() or 1
             v, tot = cpu_reference_images_per_s(args.cpu_batch, 3, threads)
@@ -414,8 +440,9 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (lance::UniformSource seed 42+layer, x then w; bench.hpp:129-133)",
-            "config": {"workload": WORKLOAD, "batch_per_gpu": N, "global_batch": N * ws,
-                       "layers": [list(l) for l in layers], "winograd": "F(2x2,3x3)",
+            "config": {"workload": WORKLOAD + ("_f4x4" if TM == 4 else ""), "batch_per_gpu": N,
+                       "global_batch": N * ws,
+                       "layers": [list(l) for l in layers], "winograd": f"F({TM}x{TM},3x3)",
                        "bits_w": 8, "bits_i": 8, "granularity": "PerPosition", "pad": 1,
                        "parallelism": f"batch-shard x{ws}, no collective",
                        "filters": "prepared once per layer (K2) outside the step",
