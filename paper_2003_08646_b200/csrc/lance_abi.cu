@@ -544,6 +544,22 @@ static int create_f4(lance_plan_s* p, const lance_conv_spec* spec, const lance_c
   g.granularity = cfg->granularity;
   g.num_n_tiles = p->K_pad / 16;
   g.stages = 0;
+  g.units = 0;
+  g.b_resident = 0;
+  g.ld_lanes = 2;
+  if (const char* e = std::getenv("LANCE_F4_LANES")) {
+    const int v = std::atoi(e);
+    g.ld_lanes = (v == 1 || v == 2 || v == 4) ? v : 2;
+  }
+  // Warp strips along tile rows: whole rows unless that leaves too few warps
+  // to fill the SMs; then shorter strips.
+  g.seg_len = p->TW;
+  for (;;) {
+    g.nseg = (p->TW + g.seg_len - 1) / g.seg_len;
+    g.num_items = static_cast<long long>(spec->n) * p->TH * g.nseg * ((spec->c + 31) / 32);
+    if (g.num_items >= 32LL * p->sm_count || g.seg_len <= 1) break;
+    g.seg_len = (g.seg_len + 1) / 2;
+  }
   p->range_grid = f4_range_grid(g, p->sm_count);
   const long long kc = static_cast<long long>(spec->k) * spec->c;
   p->filter_grid = static_cast<int>(std::min<long long>((kc + 255) / 256, 2LL * p->sm_count));
@@ -787,7 +803,7 @@ int lance_plan_debug_read(lance_plan_t p, int what, void* dst, size_t bytes) {
           for (int c = 0; c < C; ++c)
             out[(size_t(q) * M + m) * C + c] = static_cast<uint8_t>(
                 tmp[np == 16 ? umma_image_offset(m, c, q, kBM, p->BK, nk)
-                             : umma_image_offset_np(m, c, q, kBM, p->BK, nk, np)]);
+                             : umma_image_offset_np(m, c, f4_plane(q), kBM, p->BK, nk, np)]);
       return LANCE_OK;
     }
     case LANCE_DBG_ROWSUM: {
@@ -807,7 +823,7 @@ int lance_plan_debug_read(lance_plan_t p, int what, void* dst, size_t bytes) {
           for (int k = 0; k < K; ++k)
             out[(size_t(q) * C + c) * K + k] = static_cast<uint8_t>(
                 tmp[np == 16 ? umma_image_offset(k, c, q, p->BN, p->BK, nk)
-                             : umma_image_offset_np(k, c, q, p->BN, p->BK, nk, np)]);
+                             : umma_image_offset_np(k, c, f4_plane(q), p->BN, p->BK, nk, np)]);
       return LANCE_OK;
     }
     case LANCE_DBG_COLSUM: {

@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "lance_common.cuh"
 
@@ -45,6 +46,22 @@ __device__ __forceinline__ void bt6(const float (&x)[6], float (&y)[6]) {
   y[5] = __fadd_rn(__fsub_rn(x1_4, __fmul_rn(5.0f, x[3])), x[5]);
 }
 
+// bt6 on two independent vectors at once (packed f32x2): products by 2 and 4
+// by exact doubling, 5x as RN(4x + x) == RN(5x); negated leading terms are
+// folded as RN(-a - b) = -RN(a + b), RN(-s + c) = RN(c - s) (same IEEE results).
+__device__ __forceinline__ void bt6_2(const float2 (&x)[6], float2 (&y)[6]) {
+  const float2 x0_2 = add2(x[0], x[0]), x0_4 = add2(x0_2, x0_2);
+  const float2 x1_2 = add2(x[1], x[1]), x1_4 = add2(x1_2, x1_2);
+  const float2 x2_2 = add2(x[2], x[2]), x2_4 = add2(x2_2, x2_2), x2_5 = add2(x2_4, x[2]);
+  const float2 x3_2 = add2(x[3], x[3]), x3_4 = add2(x3_2, x3_2), x3_5 = add2(x3_4, x[3]);
+  y[0] = add2(sub2(x0_4, x2_5), x[4]);
+  y[1] = add2(sub2(x[3], add2(x1_4, x2_4)), x[4]);
+  y[2] = add2(sub2(sub2(x1_4, x2_4), x[3]), x[4]);
+  y[3] = add2(sub2(x3_2, add2(x1_2, x[2])), x[4]);
+  y[4] = add2(sub2(sub2(x1_2, x[2]), x3_2), x[4]);
+  y[5] = add2(sub2(x1_4, x3_5), x[5]);
+}
+
 // y = G x for a 3-vector, G = [1/4,0,0], [-1/6,-1/6,-1/6], [-1/6,1/6,-1/6],
 // [1/24,1/12,1/6], [1/24,-1/12,1/6], [0,0,1] (fp32 literals).
 __device__ __forceinline__ void g6(const float (&x)[3], float (&y)[6]) {
@@ -66,6 +83,18 @@ __device__ __forceinline__ void at6(const float (&m)[6], float (&t)[4]) {
   t[1] = __fsub_rn(__fadd_rn(d12, __fmul_rn(2.0f, m[3])), __fmul_rn(2.0f, m[4]));
   t[2] = __fadd_rn(__fadd_rn(s12, __fmul_rn(4.0f, m[3])), __fmul_rn(4.0f, m[4]));
   t[3] = __fadd_rn(__fsub_rn(__fadd_rn(d12, __fmul_rn(8.0f, m[3])), __fmul_rn(8.0f, m[4])), m[5]);
+}
+
+// at6 on two filters at once (packed f32x2 adds; x2 / x4 / x8 by exact doubling).
+__device__ __forceinline__ void at6_2(const float2 (&m)[6], float2 (&t)[4]) {
+  const float2 d12 = sub2(m[1], m[2]), s12 = add2(m[1], m[2]);
+  const float2 m3_2 = add2(m[3], m[3]), m4_2 = add2(m[4], m[4]);
+  const float2 m3_4 = add2(m3_2, m3_2), m4_4 = add2(m4_2, m4_2);
+  const float2 m3_8 = add2(m3_4, m3_4), m4_8 = add2(m4_4, m4_4);
+  t[0] = add2(add2(add2(add2(m[0], m[1]), m[2]), m[3]), m[4]);
+  t[1] = sub2(add2(d12, m3_2), m4_2);
+  t[2] = add2(add2(s12, m3_4), m4_4);
+  t[3] = add2(sub2(add2(d12, m3_8), m4_8), m[5]);
 }
 
 // First pass of the input transform, fused with the loads: t = B^T d for the
@@ -181,7 +210,58 @@ __device__ __forceinline__ void fit36(const float* s_fin, int gran, int bits, fl
 }
 
 // --------------------------------------------------------------------------
-// F0: ranges.  One warp per Winograd tile, lanes over channels.
+// F0 / F1 work decomposition: a warp walks a strip of tiles along one tile
+// row (img, ti, tj0 .. tj1) for 32 channels (one per lane).  Adjacent tiles
+// share two input columns, so each step loads the 4 new columns and carries
+// the first-pass (B^T d) columns 4, 5 of the previous tile as columns 0, 1.
+// The first pass is scalar per column; its outputs land directly in row-pair
+// registers tp[r][k] = (t[r][k], t[r+3][k]) for the packed second pass.
+struct F4Strip {
+  int img, ti, tj0, tj1, c;
+  bool cok;
+  uint32_t rowmask;  // bit a: input row 4ti - pad + a inside the image
+};
+
+__device__ __forceinline__ F4Strip f4_strip(const F4Geom& g, long long item, int lane) {
+  F4Strip st;
+  const int ncg = (g.C + 31) >> 5;
+  const int cg = static_cast<int>(item % ncg);
+  long long rest = item / ncg;
+  const int seg = static_cast<int>(rest % g.nseg);
+  rest /= g.nseg;
+  st.ti = static_cast<int>(rest % g.TH);
+  st.img = static_cast<int>(rest / g.TH);
+  st.tj0 = seg * g.seg_len;
+  st.tj1 = min(st.tj0 + g.seg_len, g.TW);
+  st.c = cg * 32 + lane;
+  st.cok = st.c < g.C;
+  const int y0 = 4 * st.ti - g.pad;
+  st.rowmask = 0;
+#pragma unroll
+  for (int a = 0; a < 6; ++a)
+    if (y0 + a >= 0 && y0 + a < g.H) st.rowmask |= 1u << a;
+  return st;
+}
+
+// First pass for input column xx of the strip's rows: t[.][b] into tp.
+__device__ __forceinline__ void f4_col(const float* __restrict__ rowbase, long long rowstride,
+                                       const F4Geom& g, const F4Strip& st, int xx, int b,
+                                       float2 (&tp)[3][6]) {
+  const bool colok = st.cok && xx >= 0 && xx < g.W;
+  const float* p = rowbase + static_cast<long long>(xx) * g.C;
+  float col[6], y6[6];
+#pragma unroll
+  for (int a = 0; a < 6; ++a)
+    col[a] = (colok && ((st.rowmask >> a) & 1u)) ? __ldg(p + a * rowstride) : 0.0f;
+  bt6(col, y6);
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    tp[r][b].x = y6[r];
+    tp[r][b].y = y6[r + 3];
+  }
+}
+
+// F0: ranges.
 __global__ void __launch_bounds__(256, 2) f4_range_kernel(const float* __restrict__ x,
                                                           float* __restrict__ partials,
                                                           LanceDevState* __restrict__ st,
@@ -195,23 +275,35 @@ __global__ void __launch_bounds__(256, 2) f4_range_kernel(const float* __restric
     hi[p] = __int_as_float(0xff800000);
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long ntiles = static_cast<long long>(g.M);
-  for (long long tile = static_cast<long long>(blockIdx.x) * 8 + warp; tile < ntiles;
-       tile += static_cast<long long>(gridDim.x) * 8) {
-    const int img = static_cast<int>(tile / g.P), t = static_cast<int>(tile - static_cast<long long>(img) * g.P);
-    const int ti = t / g.TW, tj = t - ti * g.TW;
-    for (int c = lane; c < g.C; c += 32) {
-      float tb[36];  // B^T d of this channel
-      load_bt_tile6(x, g, img, ti, tj, c, tb);
+  const long long rowstride = static_cast<long long>(g.W) * g.C;
+  for (long long item = static_cast<long long>(blockIdx.x) * 8 + warp; item < g.num_items;
+       item += static_cast<long long>(gridDim.x) * 8) {
+    const F4Strip sp = f4_strip(g, item, lane);
+    const float* rowbase = x + (static_cast<long long>(sp.img) * g.H + (4 * sp.ti - g.pad)) * rowstride + sp.c;
+    float2 tp[3][6];
+    f4_col(rowbase, rowstride, g, sp, 4 * sp.tj0 - g.pad, 0, tp);
+    f4_col(rowbase, rowstride, g, sp, 4 * sp.tj0 - g.pad + 1, 1, tp);
+    for (int tj = sp.tj0; tj < sp.tj1; ++tj) {
 #pragma unroll
-      for (int i = 0; i < 6; ++i) {
-        float v[6];
-        bt_row6(tb, i, v);
+      for (int b = 2; b < 6; ++b) f4_col(rowbase, rowstride, g, sp, 4 * tj - g.pad + b, b, tp);
+      if (sp.cok) {
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          lo[6 * i + k] = fmin_nan(lo[6 * i + k], v[k]);
-          hi[6 * i + k] = fmax_nan(hi[6 * i + k], v[k]);
+        for (int r = 0; r < 3; ++r) {
+          float2 v2[6];
+          bt6_2(tp[r], v2);
+#pragma unroll
+          for (int k = 0; k < 6; ++k) {
+            lo[6 * r + k] = fmin_nan(lo[6 * r + k], v2[k].x);
+            hi[6 * r + k] = fmax_nan(hi[6 * r + k], v2[k].x);
+            lo[6 * r + 18 + k] = fmin_nan(lo[6 * r + 18 + k], v2[k].y);
+            hi[6 * r + 18 + k] = fmax_nan(hi[6 * r + 18 + k], v2[k].y);
+          }
         }
+      }
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        tp[r][0] = tp[r][4];
+        tp[r][1] = tp[r][5];
       }
     }
   }
@@ -223,75 +315,91 @@ __global__ void __launch_bounds__(256, 2) f4_range_kernel(const float* __restric
   }
 }
 
-// F1: codes (A operand UMMA images) + row sums.  One warp per tile; lane l
-// handles channels l, l + 32, ...; the warp's row sums are butterfly-reduced
-// (no atomics, deterministic).
+// F1: codes (A operand UMMA images, j-major planes) + row sums.  Positions
+// (p, p + 18) are quantised as one packed pair; the warp's per-tile row sums
+// are one REDUX per position, added into rowsum (zeroed by the launcher).
 template <bool STATIC>
 __global__ void __launch_bounds__(256, 2) f4_quant_kernel(const float* __restrict__ x,
                                                           uint8_t* __restrict__ codes,
                                                           int32_t* __restrict__ rowsum,
                                                           const LanceDevState* __restrict__ st,
                                                           F4Geom g) {
-  __shared__ float s_tmin[kNP4], s_rcp[kNP4], s_scale[kNP4];
-  if (threadIdx.x < kNP4) {
-    s_tmin[threadIdx.x] = st->a_tmin[threadIdx.x];
-    s_rcp[threadIdx.x] = st->a_rcp[threadIdx.x];
-    s_scale[threadIdx.x] = st->a_scale[threadIdx.x];
+  __shared__ float2 s_tmin2[18], s_rcp2[18], s_scale2[18];
+  if (threadIdx.x < 18) {
+    const int p = threadIdx.x;
+    s_tmin2[p] = make_float2(st->a_tmin[p], st->a_tmin[p + 18]);
+    s_rcp2[p] = make_float2(st->a_rcp[p], st->a_rcp[p + 18]);
+    s_scale2[p] = make_float2(st->a_scale[p], st->a_scale[p + 18]);
   }
   __syncthreads();
   const float top = static_cast<float>((1 << st->bits_i) - 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long plane = static_cast<long long>(kBM) * g.bk;  // bytes of one image
-  for (long long tile = static_cast<long long>(blockIdx.x) * 8 + warp; tile < g.M;
-       tile += static_cast<long long>(gridDim.x) * 8) {
-    const int img = static_cast<int>(tile / g.P), t = static_cast<int>(tile - static_cast<long long>(img) * g.P);
-    const int ti = t / g.TW, tj = t - ti * g.TW;
-    int rs[kNP4];
+  const long long rowstride = static_cast<long long>(g.W) * g.C;
+  const long long img_bytes = static_cast<long long>(kBM) * g.bk;  // one UMMA image
+  const long long pstride = g.nk * img_bytes;                       // one position plane
+  for (long long item = static_cast<long long>(blockIdx.x) * 8 + warp; item < g.num_items;
+       item += static_cast<long long>(gridDim.x) * 8) {
+    const F4Strip sp = f4_strip(g, item, lane);
+    const float* rowbase = x + (static_cast<long long>(sp.img) * g.H + (4 * sp.ti - g.pad)) * rowstride + sp.c;
+    const int kc = sp.c / g.bk, cb = sp.c - kc * g.bk;
+    float2 tp[3][6];
+    f4_col(rowbase, rowstride, g, sp, 4 * sp.tj0 - g.pad, 0, tp);
+    f4_col(rowbase, rowstride, g, sp, 4 * sp.tj0 - g.pad + 1, 1, tp);
+    for (int tj = sp.tj0; tj < sp.tj1; ++tj) {
 #pragma unroll
-    for (int p = 0; p < kNP4; ++p) rs[p] = 0;
-    const long long blk = tile / kBM;
-    const int r = static_cast<int>(tile - blk * kBM);
-    for (int c = lane; c < g.C; c += 32) {
-      float tb[36];  // B^T d of this channel
-      load_bt_tile6(x, g, img, ti, tj, c, tb);
-      const int kc = c / g.bk, cb = c - kc * g.bk;
-      uint8_t* dst = codes + ((blk * kNP4) * g.nk + kc) * plane +
+      for (int b = 2; b < 6; ++b) f4_col(rowbase, rowstride, g, sp, 4 * tj - g.pad + b, b, tp);
+      const long long tile = (static_cast<long long>(sp.img) * g.TH + sp.ti) * g.TW + tj;
+      const long long blk = tile / kBM;
+      const int r = static_cast<int>(tile - blk * kBM);
+      uint8_t* dst = codes + (blk * kNP4) * pstride + kc * img_bytes +
                      umma_swizzle(static_cast<uint32_t>(r * g.bk + cb), g.bk);
+      uint32_t mine0 = 0, mine1 = 0;  // row sums of positions lane, lane + 32
 #pragma unroll
-      for (int i = 0; i < 6; ++i) {
-        float v6[6];
-        bt_row6(tb, i, v6);
+      for (int rr = 0; rr < 3; ++rr) {
+        float2 v2[6];
+        bt6_2(tp[rr], v2);
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
-          const int p = 6 * i + k;
-          uint32_t code;
+          const int p = 6 * rr + k;  // and p + 18 in .y
+          uint32_t c0, c1;
           if (STATIC) {
-            code = quantize_code(v6[k], s_tmin[p], s_scale[p], top);
+            c0 = quantize_code(v2[k].x, s_tmin2[p].x, s_scale2[p].x, top);
+            c1 = quantize_code(v2[k].y, s_tmin2[p].y, s_scale2[p].y, top);
           } else {
-            const float dd = __fsub_rn(v6[k], s_tmin[p]);
-            const float gq = __fmaf_rn(dd, s_rcp[p], kMagic);
-            const float rr = __fmaf_rn(dd, s_rcp[p], __fsub_rn(kMagic, gq));
-            code = (fabsf(rr) < kTieGuard) ? (__float_as_uint(gq) & 0xFFu)
-                                           : exact_code_near_boundary(dd, s_scale[p], gq, rr, top);
+            const float2 dd = sub2(v2[k], s_tmin2[p]);
+            const float2 gq = fma2(dd, s_rcp2[p], bcast2(kMagic));
+            const float2 rr2 = fma2(dd, s_rcp2[p], sub2(bcast2(kMagic), gq));
+            c0 = __float_as_uint(gq.x) & 0xFFu;
+            c1 = __float_as_uint(gq.y) & 0xFFu;
+            if (__builtin_expect(!(fmaxf(fabsf(rr2.x), fabsf(rr2.y)) < kTieGuard), 0)) {
+              if (!(fabsf(rr2.x) < kTieGuard)) c0 = exact_code_near_boundary(dd.x, s_scale2[p].x, gq.x, rr2.x, top);
+              if (!(fabsf(rr2.y) < kTieGuard)) c1 = exact_code_near_boundary(dd.y, s_scale2[p].y, gq.y, rr2.y, top);
+            }
           }
-          dst[static_cast<long long>(p) * g.nk * plane] = static_cast<uint8_t>(code);
-          rs[p] += static_cast<int>(code);
+          if (!sp.cok) c0 = c1 = 0u;
+          else {
+            dst[f4_plane(p) * pstride] = static_cast<uint8_t>(c0);
+            dst[f4_plane(p + 18) * pstride] = static_cast<uint8_t>(c1);
+          }
+          const uint32_t s0 = __reduce_add_sync(0xffffffffu, c0);
+          const uint32_t s1 = __reduce_add_sync(0xffffffffu, c1);
+          if (lane == (p & 31)) {
+            if (p < 32) mine0 = s0; else mine1 = s0;
+          }
+          if (lane == ((p + 18) & 31)) {
+            if (p + 18 < 32) mine0 = s1; else mine1 = s1;
+          }
         }
       }
-    }
+      atomicAdd(rowsum + static_cast<long long>(lane) * g.rs_pitch + tile, static_cast<int>(mine0));
+      if (lane + 32 < kNP4)
+        atomicAdd(rowsum + static_cast<long long>(lane + 32) * g.rs_pitch + tile, static_cast<int>(mine1));
 #pragma unroll
-    for (int p = 0; p < kNP4; ++p) {
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) rs[p] += __shfl_xor_sync(0xffffffffu, rs[p], off);
+      for (int q = 0; q < 3; ++q) {
+        tp[q][0] = tp[q][4];
+        tp[q][1] = tp[q][5];
+      }
     }
-    int mine0 = 0, mine1 = 0;
-#pragma unroll
-    for (int p = 0; p < kNP4; ++p) {
-      if (p == lane) mine0 = rs[p];
-      if (p == lane + 32) mine1 = rs[p];
-    }
-    rowsum[static_cast<long long>(lane) * g.rs_pitch + tile] = mine0;
-    if (lane + 32 < kNP4) rowsum[static_cast<long long>(lane + 32) * g.rs_pitch + tile] = mine1;
   }
 }
 
@@ -360,7 +468,7 @@ __global__ void __launch_bounds__(128) f4_filter_quant_kernel(const float* __res
     int sum = 0;
     for (int c = threadIdx.x; c < g.C; c += blockDim.x) {
       const uint32_t code = quantize_code(u_tmp[p * total + static_cast<long long>(k) * g.C + c], tmin, scale, top);
-      codes_w[umma_image_offset_np(k, c, p, 16, g.bk, g.nk, kNP4)] = static_cast<uint8_t>(code);
+      codes_w[umma_image_offset_np(k, c, f4_plane(p), 16, g.bk, g.nk, kNP4)] = static_cast<uint8_t>(code);
       sum += static_cast<int>(code);
     }
 #pragma unroll
@@ -406,20 +514,27 @@ __global__ void __launch_bounds__(kF4Threads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ float s_k1[kNP4], s_k2[kNP4], s_k4[kNP4];
   __shared__ float s_ct[2][kNP4 * kF4BN];
-  __shared__ uint64_t s_bars[2 * 16 + 2 * kF4AccBufs];
+  __shared__ uint64_t s_bars[2 * 16 + 2 * kF4AccBufs + 1];
   __shared__ uint32_t s_tmem;
   __shared__ int s_fast;
 
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stages = g.stages;
   const int nk = g.nk;
+  const int U = g.units;  // (plane, k chunk) units per stage; divides 6 * nk
+  const bool b_res = g.b_resident != 0;
+  const uint32_t a_bytes = U * Cfg::kABytes, b_bytes = b_res ? 0u : U * Cfg::kBBytes;
+  const uint32_t stage_bytes = a_bytes + b_bytes;
+  uint8_t* b_base = smem + static_cast<size_t>(stages) * stage_bytes;  // resident B (b_res)
   uint64_t* full_bar = s_bars;
   uint64_t* empty_bar = s_bars + 16;
   uint64_t* acc_full = s_bars + 32;
   uint64_t* acc_empty = acc_full + kF4AccBufs;
+  uint64_t* b_full = acc_empty + kF4AccBufs;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = g.num_n_tiles;
   const int num_tiles = ((g.M + kBM - 1) / kBM) * nt;
+  const int grp_units = 6 * nk;  // units of one j-group (contiguous, j-major planes)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -430,6 +545,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], kF4EpiWarps);
     }
+    mbar_init(b_full, 1);
     fence_barrier_init();
   }
   if (threadIdx.x < kNP4) {
@@ -452,30 +568,38 @@ __global__ void __launch_bounds__(kF4Threads, 1)
 
   if (warp >= kF4EpiWarps) {
     setmaxnreg_dec<32>();
-    if (warp == kF4EpiWarps && lane == 0) {
+    if (warp == kF4EpiWarps && lane < g.ld_lanes) {
       // ---------------- bulk-copy producer ----------------
+      // A stage is U consecutive (plane, k chunk) units of the tile's j-major
+      // operand images: one contiguous run, copied as ld_lanes slices (a single
+      // thread issues ~1 bulk copy per ~460 cycles from L2, whatever its size).
+      const int nl = g.ld_lanes;
+      const uint32_t a_part = a_bytes / nl, b_part = b_bytes / nl;
+      if (b_res && lane == 0) {  // the CTA's fixed filter tile (grid % nt == 0)
+        const uint32_t bb = kNP4 * nk * Cfg::kBBytes;
+        mbar_arrive_expect_tx(b_full, bb);
+        bulk_load(b_base, codes_w + static_cast<long long>(blockIdx.x % nt) * bb, bb, b_full);
+      }
       int s = 0;
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         const int mt = t / nt, ntile = t - (t / nt) * nt;
-        const uint8_t* a_tile = codes_a + static_cast<long long>(mt) * kNP4 * nk * Cfg::kABytes;
-        const uint8_t* b_tile = codes_w + static_cast<long long>(ntile) * kNP4 * nk * Cfg::kBBytes;
-        for (int j = 0; j < 6; ++j)
-          for (int a = 0; a < 6; ++a) {
-            const int u0 = (6 * a + j) * nk;
-            for (int kc = 0; kc < nk; ++kc) {
-              mbar_wait(&empty_bar[s], ph ^ 1u);
-              uint8_t* sa = smem + static_cast<size_t>(s) * Cfg::kStageBytes;
-              mbar_arrive_expect_tx(&full_bar[s], Cfg::kStageBytes);
-              bulk_load(sa, a_tile + static_cast<long long>(u0 + kc) * Cfg::kABytes, Cfg::kABytes, &full_bar[s]);
-              bulk_load(sa + Cfg::kABytes, b_tile + static_cast<long long>(u0 + kc) * Cfg::kBBytes,
-                        Cfg::kBBytes, &full_bar[s]);
-              if (++s == stages) {
-                s = 0;
-                ph ^= 1u;
-              }
-            }
+        const uint8_t* a_tile = codes_a + static_cast<long long>(mt) * kNP4 * nk * Cfg::kABytes + lane * a_part;
+        const uint8_t* b_tile = codes_w + static_cast<long long>(ntile) * kNP4 * nk * Cfg::kBBytes + lane * b_part;
+        for (int u = 0; u < kNP4 * nk; u += U) {
+          mbar_wait(&empty_bar[s], ph ^ 1u);
+          uint8_t* sa = smem + static_cast<size_t>(s) * stage_bytes;
+          if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
+          __syncwarp((1u << nl) - 1u);
+          bulk_load(sa + lane * a_part, a_tile + static_cast<long long>(u) * Cfg::kABytes, a_part, &full_bar[s]);
+          if (!b_res)
+            bulk_load(sa + a_bytes + lane * b_part, b_tile + static_cast<long long>(u) * Cfg::kBBytes, b_part,
+                      &full_bar[s]);
+          if (++s == stages) {
+            s = 0;
+            ph ^= 1u;
           }
+        }
       }
     } else if (warp == kF4EpiWarps + 1) {
       // ---------------- TMEM + UMMA issuer ----------------
@@ -486,6 +610,8 @@ __global__ void __launch_bounds__(kF4Threads, 1)
       tc_fence_after();
       const uint32_t tmem_base = s_tmem;
       if (lane == 0) {
+        if (b_res) mbar_wait(b_full, 0);
+        const uint32_t b_res_base = smem_u32(b_base);
         int s = 0;
         uint32_t ph = 0;
         uint32_t grp = 0;
@@ -495,24 +621,28 @@ __global__ void __launch_bounds__(kF4Threads, 1)
             mbar_wait(&acc_empty[buf], (grp / kF4AccBufs) & 1u);
             tc_fence_after();
             const uint32_t d_base = tmem_base + buf * kF4GroupCols;
-            for (int a = 0; a < 6; ++a) {
-              for (int kc = 0; kc < nk; ++kc) {
-                mbar_wait(&full_bar[s], ph);
-                tc_fence_after();
-                const uint32_t sa = smem_u32(smem + static_cast<size_t>(s) * Cfg::kStageBytes);
-                const uint32_t sb = sa + Cfg::kABytes;
+            for (int lu0 = 0; lu0 < grp_units; lu0 += U) {
+              mbar_wait(&full_bar[s], ph);
+              tc_fence_after();
+              const uint32_t sa = smem_u32(smem + static_cast<size_t>(s) * stage_bytes);
+              for (int uu = 0; uu < U; ++uu) {
+                const int lu = lu0 + uu;          // unit within the j-group
+                const int a = lu / nk, kc = lu - (lu / nk) * nk;
+                const uint32_t ua = sa + uu * Cfg::kABytes;
+                const uint32_t ub = b_res ? b_res_base + (j * grp_units + lu) * Cfg::kBBytes
+                                          : sa + a_bytes + uu * Cfg::kBBytes;
 #pragma unroll
                 for (int kk = 0; kk < BK / 32; ++kk) {
-                  const uint64_t adesc = umma_smem_desc(sa + kk * 32, 8 * BK, Cfg::kLayout);
-                  const uint64_t bdesc = umma_smem_desc(sb + kk * 32, 8 * BK, Cfg::kLayout);
+                  const uint64_t adesc = umma_smem_desc(ua + kk * 32, 8 * BK, Cfg::kLayout);
+                  const uint64_t bdesc = umma_smem_desc(ub + kk * 32, 8 * BK, Cfg::kLayout);
                   umma_i8(d_base + static_cast<uint32_t>(a * kF4BN), adesc, bdesc, kIdesc,
                           (kc > 0 || kk > 0) ? 1u : 0u);
                 }
-                umma_commit(&empty_bar[s]);
-                if (++s == stages) {
-                  s = 0;
-                  ph ^= 1u;
-                }
+              }
+              umma_commit(&empty_bar[s]);
+              if (++s == stages) {
+                s = 0;
+                ph ^= 1u;
               }
             }
             umma_commit(&acc_full[buf]);
@@ -548,81 +678,94 @@ __global__ void __launch_bounds__(kF4Threads, 1)
         ct[i] = (kk < g.K) ? __fmul_rn(st->k3[p], static_cast<float>(colsum[p * g.K_pad + kk])) : 0.0f;
       }
       named_bar_sync(2, 32 * kF4EpiWarps);
-      float S[16][4];  // S[4i + b][filter]
+      float2 S[16][2];  // S[4i + b][filter pair]
+      int rs_cur[6];
+#pragma unroll
+      for (int a = 0; a < 6; ++a)
+        rs_cur[a] = row_ok ? __ldg(rowsum + static_cast<long long>(6 * a) * g.rs_pitch + m) : 0;
 #pragma unroll
       for (int j = 0; j < 6; ++j, ++grp) {
         float rterm[6];
 #pragma unroll
-        for (int a = 0; a < 6; ++a) {
-          const int p = 6 * a + j;
-          const int rs = row_ok ? __ldg(rowsum + static_cast<long long>(p) * g.rs_pitch + m) : 0;
-          rterm[a] = __fmul_rn(s_k2[p], static_cast<float>(rs));
+        for (int a = 0; a < 6; ++a) rterm[a] = __fmul_rn(s_k2[6 * a + j], static_cast<float>(rs_cur[a]));
+        if (j < 5) {  // prefetch the next j-group's row sums (hides the load behind this group)
+#pragma unroll
+          for (int a = 0; a < 6; ++a)
+            rs_cur[a] = row_ok ? __ldg(rowsum + static_cast<long long>(6 * a + j + 1) * g.rs_pitch + m) : 0;
         }
         const uint32_t buf = grp % kF4AccBufs;
         mbar_wait(&acc_full[buf], (grp / kF4AccBufs) & 1u);
         tc_fence_after();
-        uint32_t ac[6][4];
+        // Two filters at a time (x2 loads keep 12 accumulators live, not 24);
+        // the buffer is released once both halves are in registers.
 #pragma unroll
-        for (int a = 0; a < 6; ++a) tmem_ld_x4(lane_base + buf * kF4GroupCols + a * kF4BN + f0, ac[a]);
-        tmem_ld_wait();
-#pragma unroll
-        for (int a = 0; a < 6; ++a) reg_fence(ac[a]);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[buf]);
-        if (DUMP && row_ok) {
+        for (int fh = 0; fh < 2; ++fh) {
+          uint32_t ac[6][2];
 #pragma unroll
           for (int a = 0; a < 6; ++a)
+            tmem_ld_x2(lane_base + buf * kF4GroupCols + a * kF4BN + f0 + 2 * fh, ac[a]);
+          tmem_ld_wait();
 #pragma unroll
-            for (int f = 0; f < 4; ++f)
-              if (kf0 + f < g.K)
-                acc_dump[(static_cast<long long>(6 * a + j) * g.M + m) * g.K + kf0 + f] =
-                    static_cast<int32_t>(ac[a][f]);
-        }
+          for (int a = 0; a < 6; ++a) reg_fence(ac[a]);
+          if (fh == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[buf]);
+          }
+          if (DUMP && row_ok) {
 #pragma unroll
-        for (int f = 0; f < 4; ++f) {
-          float mm[6];
+            for (int a = 0; a < 6; ++a)
+#pragma unroll
+              for (int f = 0; f < 2; ++f)
+                if (kf0 + 2 * fh + f < g.K)
+                  acc_dump[(static_cast<long long>(6 * a + j) * g.M + m) * g.K + kf0 + 2 * fh + f] =
+                      static_cast<int32_t>(ac[a][f]);
+          }
+          float2 mm[6];
 #pragma unroll
           for (int a = 0; a < 6; ++a) {
             const int p = 6 * a + j;
-            float v;  // RN(RN(k1 * dot) + RN(k2 * sum_a))
-            if (fast)
-              v = __fmaf_rn(__fmul_rn(s_k1[p], __uint_as_float(ac[a][f])), 8388608.0f /*2^23*/, rterm[a]);
-            else
-              v = __fadd_rn(__fmul_rn(s_k1[p], __int2float_rn(static_cast<int>(ac[a][f]))), rterm[a]);
+            float2 v;  // RN(RN(k1 * dot) + RN(k2 * sum_a)), two filters
+            if (fast) {
+              const float2 u = fma2(bcast2(s_k1[p]),
+                                    make_float2(__uint_as_float(ac[a][0]), __uint_as_float(ac[a][1])),
+                                    bcast2(0.0f));
+              v = fma2(u, bcast2(8388608.0f /*2^23*/), bcast2(rterm[a]));
+            } else {
+              v = add2(make_float2(__fmul_rn(s_k1[p], __int2float_rn(static_cast<int>(ac[a][0]))),
+                                   __fmul_rn(s_k1[p], __int2float_rn(static_cast<int>(ac[a][1])))),
+                       bcast2(rterm[a]));
+            }
             // ((k1*dot + k2*sum_a) + k3*sum_b) + k4 (lowpgemm.hpp:110-114)
-            mm[a] = __fadd_rn(__fadd_rn(v, ct[p * kF4BN + f0 + f]), s_k4[p]);
+            const float2 c2 = *reinterpret_cast<const float2*>(ct + p * kF4BN + f0 + 2 * fh);
+            mm[a] = add2(add2(v, c2), bcast2(s_k4[p]));
           }
-          float T[4];
-          at6(mm, T);
+          float2 T[4];
+          at6_2(mm, T);
           // S_ib = sum_j T_ij * A^T[b][j], left fold over j (matrix.hpp:80-82).
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const float tv = T[i];
+            const float2 tv = T[i];
             if (j == 0) {
-              S[4 * i + 0][f] = tv;
+              S[4 * i + 0][fh] = tv;
             } else if (j == 1) {
-              S[4 * i + 0][f] = __fadd_rn(S[4 * i + 0][f], tv);
-              S[4 * i + 1][f] = tv;
-              S[4 * i + 2][f] = tv;
-              S[4 * i + 3][f] = tv;
+              S[4 * i + 0][fh] = add2(S[4 * i + 0][fh], tv);
+              S[4 * i + 1][fh] = tv;
+              S[4 * i + 2][fh] = tv;
+              S[4 * i + 3][fh] = tv;
             } else if (j == 2) {
-              S[4 * i + 0][f] = __fadd_rn(S[4 * i + 0][f], tv);
-              S[4 * i + 1][f] = __fsub_rn(S[4 * i + 1][f], tv);
-              S[4 * i + 2][f] = __fadd_rn(S[4 * i + 2][f], tv);
-              S[4 * i + 3][f] = __fsub_rn(S[4 * i + 3][f], tv);
-            } else if (j == 3) {
-              S[4 * i + 0][f] = __fadd_rn(S[4 * i + 0][f], tv);
-              S[4 * i + 1][f] = __fadd_rn(S[4 * i + 1][f], __fmul_rn(2.0f, tv));
-              S[4 * i + 2][f] = __fadd_rn(S[4 * i + 2][f], __fmul_rn(4.0f, tv));
-              S[4 * i + 3][f] = __fadd_rn(S[4 * i + 3][f], __fmul_rn(8.0f, tv));
-            } else if (j == 4) {
-              S[4 * i + 0][f] = __fadd_rn(S[4 * i + 0][f], tv);
-              S[4 * i + 1][f] = __fsub_rn(S[4 * i + 1][f], __fmul_rn(2.0f, tv));
-              S[4 * i + 2][f] = __fadd_rn(S[4 * i + 2][f], __fmul_rn(4.0f, tv));
-              S[4 * i + 3][f] = __fsub_rn(S[4 * i + 3][f], __fmul_rn(8.0f, tv));
+              S[4 * i + 0][fh] = add2(S[4 * i + 0][fh], tv);
+              S[4 * i + 1][fh] = sub2(S[4 * i + 1][fh], tv);
+              S[4 * i + 2][fh] = add2(S[4 * i + 2][fh], tv);
+              S[4 * i + 3][fh] = sub2(S[4 * i + 3][fh], tv);
+            } else if (j == 3 || j == 4) {
+              const float2 t2 = add2(tv, tv), t4 = add2(t2, t2), t8 = add2(t4, t4);
+              S[4 * i + 0][fh] = add2(S[4 * i + 0][fh], tv);
+              S[4 * i + 1][fh] = (j == 3) ? add2(S[4 * i + 1][fh], t2) : sub2(S[4 * i + 1][fh], t2);
+              S[4 * i + 2][fh] = add2(S[4 * i + 2][fh], t4);
+              S[4 * i + 3][fh] = (j == 3) ? add2(S[4 * i + 3][fh], t8) : sub2(S[4 * i + 3][fh], t8);
             } else {
-              S[4 * i + 3][f] = __fadd_rn(S[4 * i + 3][f], tv);
+              S[4 * i + 3][fh] = add2(S[4 * i + 3][fh], tv);
             }
           }
         }
@@ -647,7 +790,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
             float o[4];
 #pragma unroll
             for (int f = 0; f < 4; ++f) {
-              float v = S[4 * i + b][f];
+              float v = (f & 1) ? S[4 * i + b][f >> 1].y : S[4 * i + b][f >> 1].x;
               if (bias != nullptr) v = __fadd_rn(v, bv[f]);
               if (relu) v = fmaxf(v, 0.0f);
               o[f] = __fadd_rn(v, 0.0f);
@@ -674,7 +817,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
 
 // --------------------------------------------------------------------------
 int f4_range_grid(const F4Geom& g, int sm_count) {
-  const long long blocks = (static_cast<long long>(g.M) + 7) / 8;
+  const long long blocks = (g.num_items + 7) / 8;
   const long long cap = 2LL * sm_count;
   return static_cast<int>(blocks < cap ? blocks : cap);
 }
@@ -688,8 +831,10 @@ cudaError_t launch_f4_range(const float* x, float* partials, int grid, LanceDevS
 cudaError_t launch_f4_quant(const float* x, uint8_t* codes, int32_t* rowsum,
                             const LanceDevState* st, const F4Geom& g, int static_mode,
                             int sm_count, cudaStream_t s) {
-  const long long blocks = (static_cast<long long>(g.M) + 7) / 8;
+  const long long blocks = (g.num_items + 7) / 8;
   const int grid = static_cast<int>(blocks < 4LL * sm_count ? blocks : 4LL * sm_count);
+  cudaError_t e = cudaMemsetAsync(rowsum, 0, sizeof(int32_t) * kNP4 * static_cast<size_t>(g.rs_pitch), s);
+  if (e != cudaSuccess) return e;
   if (static_mode)
     f4_quant_kernel<true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
   else
@@ -712,15 +857,40 @@ static cudaError_t launch_f4_gemm_t(const uint8_t* codes_a, const uint8_t* codes
                                     const int32_t* rowsum, const int32_t* colsum,
                                     const LanceDevState* st, float* y, int32_t* acc_dump,
                                     const float* bias, int relu, const F4Geom& g0, cudaStream_t s) {
+  using Cfg = F4Cfg<BK>;
   F4Geom g = g0;
-  int stages = 16;
   const size_t kLimit = 200 * 1024;
-  while (stages > 2 && 1024 + static_cast<size_t>(stages) * F4Cfg<BK>::kStageBytes > kLimit) --stages;
-  g.stages = stages;
-  const size_t smem = 1024 + static_cast<size_t>(stages) * F4Cfg<BK>::kStageBytes;
-  static bool configured[64] = {};
+  int sms = 148;
   int dev = 0;
   cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int nt = g.num_n_tiles;
+  const long long tiles = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * nt;
+  // Units per stage: the largest divisor of a j-group's 6 * nk units whose A
+  // run stays within 32 KB (fewer, larger bulk copies).
+  int U = 1;
+  for (int u = 1; u <= 6 * g.nk; ++u)
+    if ((6 * g.nk) % u == 0 && u * Cfg::kABytes <= 32 * 1024) U = u;
+  if (const char* e = std::getenv("LANCE_F4_UNITS")) {
+    const int v = std::atoi(e);
+    if (v >= 1 && (6 * g.nk) % v == 0) U = v;
+  }
+  g.units = U;
+  // Resident B: the CTA keeps one filter tile (36 planes x nk chunks x 16 x BK)
+  // when it fits beside a few stages; the grid is then a multiple of nt so each
+  // CTA's tiles share one filter tile.
+  const size_t b_bytes = static_cast<size_t>(kNP4) * g.nk * Cfg::kBBytes;
+  const int res_grid = (sms / nt) * nt;
+  g.b_resident = (b_bytes <= 80 * 1024 && res_grid >= 1) ? 1 : 0;
+  if (const char* e = std::getenv("LANCE_F4_BRES")) g.b_resident = g.b_resident && std::atoi(e) != 0;
+  const size_t stage_bytes = static_cast<size_t>(U) * (Cfg::kABytes + (g.b_resident ? 0 : Cfg::kBBytes));
+  const size_t fixed = 1024 + (g.b_resident ? b_bytes : 0);
+  int stages = 16;
+  while (stages > 2 && fixed + stages * stage_bytes > kLimit) --stages;
+  g.stages = stages;
+  const size_t smem = fixed + stages * stage_bytes;
+  if (smem > kLimit) return cudaErrorInvalidValue;
+  static bool configured[64] = {};
   if (dev < 0 || dev >= 64 || !configured[dev]) {
     cudaError_t e = cudaFuncSetAttribute(f4_gemm_kernel<BK, SMALL, DUMP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -728,10 +898,8 @@ static cudaError_t launch_f4_gemm_t(const uint8_t* codes_a, const uint8_t* codes
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) configured[dev] = true;
   }
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long tiles = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * g.num_n_tiles;
-  const int grid = static_cast<int>(tiles < sms ? tiles : sms);
+  const int cap = g.b_resident ? res_grid : sms;
+  const int grid = static_cast<int>(tiles < cap ? tiles : cap);
   f4_gemm_kernel<BK, SMALL, DUMP><<<grid, kF4Threads, smem, s>>>(codes_a, codes_w, rowsum, colsum,
                                                                   st, y, acc_dump, bias, relu, g);
   return cudaGetLastError();

@@ -136,10 +136,20 @@ struct F4Geom {
   int granularity;   // 1 PerPosition, 2 PerTensor
   int num_n_tiles;   // K_pad / 16
   int stages;        // GEMM ring depth (set by the launcher)
+  int units;         // (position, k chunk) units per GEMM stage (divides 6 * nk; launcher)
+  int b_resident;    // the CTA's filter tile stays in shared memory (launcher)
+  int ld_lanes;      // producer lanes splitting each stage's copies
+  int seg_len, nseg; // F0 / F1 strips: tiles per warp strip, strips per tile row
+  long long num_items;  // N * TH * nseg * ceil(C / 32) warp strips
 };
 
-// The operand image offset of umma_image_offset for np position planes in
-// natural order (F(4x4): np = 36, p = 6a + b).
+// F(4x4) operand planes are j-major: position p = 6a + j is plane 6j + a, so
+// the 6 positions of a GEMM j-group {6a + j} (and their k chunks) are one
+// contiguous run and a stage can copy several units at once.
+__host__ __device__ __forceinline__ constexpr int f4_plane(int p) { return (p % 6) * 6 + p / 6; }
+
+// The operand image offset of umma_image_offset for np position planes; `p`
+// is the PLANE index (F(4x4): f4_plane(position)).
 __host__ __device__ __forceinline__ long long umma_image_offset_np(long long row, int c, int p,
                                                                     int rows_per_img, int bk,
                                                                     int nk, int np) {

@@ -9,7 +9,7 @@ mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
 for L in "$@"; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$K -s $SKIP -c 1 \
-    -o $OUT/${K}_L$L python bench.py --layers $L --steps 1 --warmup 3 --no-cpu --no-e2e \
+    -o $OUT/${K}_L$L python bench.py --layers $L --steps 1 --warmup 3 --no-cpu --no-e2e ${BENCH_ARGS:-} \
     > $OUT/ncu_${K}_L$L.log 2>&1
 done
 echo done
