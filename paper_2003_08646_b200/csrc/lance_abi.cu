@@ -546,6 +546,8 @@ static int create_f4(lance_plan_s* p, const lance_conv_spec* spec, const lance_c
   g.stages = 0;
   g.units = 0;
   g.b_resident = 0;
+  g.exp = 0;
+  if (const char* e = std::getenv("LANCE_F4_EXP")) g.exp = std::atoi(e);
   g.ld_lanes = 2;
   if (const char* e = std::getenv("LANCE_F4_LANES")) {
     const int v = std::atoi(e);

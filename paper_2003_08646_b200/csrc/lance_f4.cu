@@ -526,6 +526,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
   const uint32_t a_bytes = U * Cfg::kABytes, b_bytes = b_res ? 0u : U * Cfg::kBBytes;
   const uint32_t stage_bytes = a_bytes + b_bytes;
   uint8_t* b_base = smem + static_cast<size_t>(stages) * stage_bytes;  // resident B (b_res)
+  float* s_out = reinterpret_cast<float*>(b_base + (b_res ? kNP4 * g.nk * Cfg::kBBytes : 0));  // [4][32][64]
   uint64_t* full_bar = s_bars;
   uint64_t* empty_bar = s_bars + 16;
   uint64_t* acc_full = s_bars + 32;
@@ -633,6 +634,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
                                           : sa + a_bytes + uu * Cfg::kBBytes;
 #pragma unroll
                 for (int kk = 0; kk < BK / 32; ++kk) {
+                  if (g.exp & 2) break;
                   const uint64_t adesc = umma_smem_desc(ua + kk * 32, 8 * BK, Cfg::kLayout);
                   const uint64_t bdesc = umma_smem_desc(ub + kk * 32, 8 * BK, Cfg::kLayout);
                   umma_i8(d_base + static_cast<uint32_t>(a * kF4BN), adesc, bdesc, kIdesc,
@@ -721,6 +723,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
                   acc_dump[(static_cast<long long>(6 * a + j) * g.M + m) * g.K + kf0 + 2 * fh + f] =
                       static_cast<int32_t>(ac[a][f]);
           }
+          if (g.exp & 1) continue;
           float2 mm[6];
 #pragma unroll
           for (int a = 0; a < 6; ++a) {
@@ -771,40 +774,71 @@ __global__ void __launch_bounds__(kF4Threads, 1)
         }
       }
       // merge_tiles (tensor.hpp:157-182): output (4ti + i, 4tj + b), overhang
-      // discarded; optional bias / ReLU; +0 canonicalisation.
-      if (row_ok && kf0 < g.K) {
+      // discarded; optional bias / ReLU; +0 canonicalisation.  One output row
+      // i at a time, each lane quadrant stages its 32 tiles x 4 pixels x 16
+      // filters in shared memory (16-byte chunk c of a tile's 64-float row at
+      // c ^ (tile & 7): conflict-free both ways), then its 4 warps write whole
+      // 64-byte pixel segments (4 lanes per pixel) instead of one scattered
+      // 16-byte piece per lane.
+      if (g.exp & 4) continue;
+      int pix0 = 0, vmask = 0;  // first output pixel of this lane's tile; bit 4i + b valid
+      if (row_ok) {
         const int img = m / g.P, tt = m - (m / g.P) * g.P;
         const int ti = tt / g.TW, tj = tt - ti * g.TW;
-        float bv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-        if (bias != nullptr)
+        pix0 = (img * g.OH + 4 * ti) * g.OW + 4 * tj;
 #pragma unroll
-          for (int f = 0; f < 4; ++f) bv[f] = (kf0 + f < g.K) ? __ldg(bias + kf0 + f) : 0.0f;
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int oh = 4 * ti + i;
-          if (oh >= g.OH) break;
+          for (int b = 0; b < 4; ++b)
+            if (4 * ti + i < g.OH && 4 * tj + b < g.OW) vmask |= 1 << (4 * i + b);
+      }
+      float2 bv[2] = {bcast2(0.0f), bcast2(0.0f)};
+      if (bias != nullptr)
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int ow = 4 * tj + b;
-            if (ow >= g.OW) break;
-            float o[4];
+        for (int h = 0; h < 2; ++h)
+          bv[h] = make_float2(kf0 + 2 * h < g.K ? __ldg(bias + kf0 + 2 * h) : 0.0f,
+                              kf0 + 2 * h + 1 < g.K ? __ldg(bias + kf0 + 2 * h + 1) : 0.0f);
+      float* stg = s_out + q * (32 * 64);
+      const int wq = warp >> 2;
 #pragma unroll
-            for (int f = 0; f < 4; ++f) {
-              float v = (f & 1) ? S[4 * i + b][f >> 1].y : S[4 * i + b][f >> 1].x;
-              if (bias != nullptr) v = __fadd_rn(v, bv[f]);
-              if (relu) v = fmaxf(v, 0.0f);
-              o[f] = __fadd_rn(v, 0.0f);
+      for (int i = 0; i < 4; ++i) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          float2 o[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float2 v = S[4 * i + b][h];
+            if (bias != nullptr) v = add2(v, bv[h]);
+            if (relu) {
+              v.x = fmaxf(v.x, 0.0f);
+              v.y = fmaxf(v.y, 0.0f);
             }
-            float* d = y + (static_cast<long long>(img * g.OH + oh) * g.OW + ow) * g.K + kf0;
-            if (k4ok) {
-              *reinterpret_cast<float4*>(d) = make_float4(o[0], o[1], o[2], o[3]);
-            } else {
+            o[h] = add2(v, bcast2(0.0f));  // the reference never yields -0
+          }
+          const int chunk = (b * 4 + wq) ^ (lane & 7);
+          *reinterpret_cast<float4*>(stg + lane * 64 + chunk * 4) = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
+        }
+        named_bar_sync(3 + q, 128);
 #pragma unroll
-              for (int f = 0; f < 4; ++f)
-                if (kf0 + f < g.K) d[f] = o[f];
-            }
+        for (int it = 0; it < 4; ++it) {
+          const int k = wq * 32 + lane + 128 * it;  // chunk id: fq fastest, then b, then tile
+          const int fq = k & 3, b = (k >> 2) & 3, tile = k >> 4;
+          const int tpix = __shfl_sync(0xffffffffu, pix0, tile);
+          const int tmask = __shfl_sync(0xffffffffu, vmask, tile);
+          const float4 val = *reinterpret_cast<const float4*>(stg + tile * 64 + (((b * 4 + fq) ^ (tile & 7)) * 4));
+          const int kf = n0 + 4 * fq;
+          if (!((tmask >> (4 * i + b)) & 1) || kf >= g.K) continue;
+          float* d = y + (static_cast<long long>(tpix) + i * g.OW + b) * g.K + kf;
+          if (k4ok) {
+            *reinterpret_cast<float4*>(d) = val;
+          } else {
+            const float e4[4] = {val.x, val.y, val.z, val.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (kf + e < g.K) d[e] = e4[e];
           }
         }
+        named_bar_sync(3 + q, 128);  // staging buffer free again
       }
     }
   }
@@ -859,7 +893,7 @@ static cudaError_t launch_f4_gemm_t(const uint8_t* codes_a, const uint8_t* codes
                                     const float* bias, int relu, const F4Geom& g0, cudaStream_t s) {
   using Cfg = F4Cfg<BK>;
   F4Geom g = g0;
-  const size_t kLimit = 200 * 1024;
+  const size_t kLimit = 220 * 1024;
   int sms = 148;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -884,7 +918,7 @@ static cudaError_t launch_f4_gemm_t(const uint8_t* codes_a, const uint8_t* codes
   g.b_resident = (b_bytes <= 80 * 1024 && res_grid >= 1) ? 1 : 0;
   if (const char* e = std::getenv("LANCE_F4_BRES")) g.b_resident = g.b_resident && std::atoi(e) != 0;
   const size_t stage_bytes = static_cast<size_t>(U) * (Cfg::kABytes + (g.b_resident ? 0 : Cfg::kBBytes));
-  const size_t fixed = 1024 + (g.b_resident ? b_bytes : 0);
+  const size_t fixed = 1024 + (g.b_resident ? b_bytes : 0) + 4 * 32 * 64 * sizeof(float);
   int stages = 16;
   while (stages > 2 && fixed + stages * stage_bytes > kLimit) --stages;
   g.stages = stages;
