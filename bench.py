@@ -31,8 +31,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 RESNET18 = [(64, 64, 56)] * 4 + [(128, 128, 28)] * 3 + [(256, 256, 14)] * 3 + [(512, 512, 7)] * 3
+# BASELINE.json configs[1] / SURVEY.md 8(d) config 2: VGG-16-CIFAR 13-conv stack, N = 128.
+VGG16_CIFAR = [(3, 64, 32), (64, 64, 32), (64, 128, 16), (128, 128, 16), (128, 256, 8),
+               (256, 256, 8), (256, 256, 8), (256, 512, 4), (512, 512, 4), (512, 512, 4),
+               (512, 512, 2), (512, 512, 2), (512, 512, 2)]
+WORKLOADS = {"resnet18": (RESNET18, 256, "resnet18_3x3_stride1_convs_x13"),
+             "vgg16_cifar": (VGG16_CIFAR, 128, "vgg16_cifar_3x3_convs_x13")}
 METRIC = "int8 Winograd conv TOPS-equivalent & images/sec vs roofline, 1/2/4/8 B200 vs CPU ref"
-WORKLOAD = "resnet18_3x3_stride1_convs_x13"
 HBM_FALLBACK = 6650.0
 
 
@@ -145,26 +150,26 @@ def dist_setup():
     return ws, rank, local
 
 
-def cpu_reference_images_per_s(batch: int, reps: int, threads: int):
+def cpu_reference_images_per_s(batch: int, reps: int, threads: int, layers=None):
     """The reference's own lance_gemm (oracle/_ref, compiled from the reference
     headers) on the 13 layer shapes at `batch` images, median of `reps`
     steady_clock repeats each (bench.hpp:157-167)."""
     import oracle
     ref = oracle.Reference()
     total = 0.0
-    for i, (c, k, h) in enumerate(RESNET18):
+    for i, (c, k, h) in enumerate(layers or RESNET18):
         med_ns, _ = ref.time_lance_gemm(oracle.Spec(batch, c, h, h, k, 1), threads, 42 + i, reps)
         total += med_ns * 1e-9
     return batch / total, total
 
 
-def cpu_port_f4_images_per_s(batch: int):
+def cpu_port_f4_images_per_s(batch: int, layers=None):
     """F(4x4) has no reference implementation: the oracle port
     (lo_lance_gemm_tiled, tile_m=4, one thread) on the 13 layer shapes."""
     import oracle
     lo = oracle.Oracle()
     total = 0.0
-    for i, (c, k, h) in enumerate(RESNET18):
+    for i, (c, k, h) in enumerate(layers or RESNET18):
         spec = oracle.Spec(batch, c, h, h, k, 1)
         x = lo.uniform(42 + i, batch * h * h * c).reshape(batch, h, h, c)
         w = lo.uniform(7 + i, k * 9 * c).reshape(k, 3, 3, c)
@@ -181,28 +186,29 @@ def run_reference_arm(args, ws, rank):
     import oracle
     threads = os.cpu_count() or 1
     batch = args.ref_batch
+    wl_layers, wl_batch, wl_name = WORKLOADS[args.workload]
     ref = oracle.Reference()
     times = []
     for step in range(args.warmup + args.steps):
         t = 0.0
-        for i, (c, k, h) in enumerate(RESNET18):
+        for i, (c, k, h) in enumerate(wl_layers):
             med_ns, _ = ref.time_lance_gemm(oracle.Spec(batch, c, h, h, k, 1), threads, 42 + i, 1)
             t += med_ns * 1e-9
         if step >= args.warmup:
             times.append(t)
     mean_t = sum(times) / len(times)
     value = batch / mean_t
-    tops = 2 * sum(direct_macs(c, k, h, batch) for c, k, h in RESNET18) / mean_t / 1e12
+    tops = 2 * sum(direct_macs(c, k, h, batch) for c, k, h in wl_layers) / mean_t / 1e12
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": mean_t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (reference UniformSource, seed 42+layer)",
-        "config": {"workload": WORKLOAD, "batch_per_step": batch,
-                   "note": f"bounded CPU sample: {batch} images per step of the batch-256 workload"},
+        "config": {"workload": wl_name, "batch_per_step": batch,
+                   "note": f"bounded CPU sample: {batch} images per step of the batch-{wl_batch} workload"},
         "tops_equivalent": tops,
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "reference",
-                         "sample": f"13 ResNet-18 3x3 layers at batch {batch}, one lance_gemm call each per step"},
+                         "sample": f"{len(wl_layers)} {wl_name} layers at batch {batch}, one lance_gemm call each per step"},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -232,13 +238,75 @@ def int8_peak_tops(device):
         return None
 
 
+def run_stack(args, ws, rank, local, N):
+    """The layer-stack driver on VGG-16-CIFAR (paper_2003_08646_b200/stack.py):
+    13 chained convs with bias + ReLU and 4 max-pools, one CUDA-graph replay per
+    step, inputs resident; images/s over the whole stack."""
+    import numpy as np
+    import torch
+    import paper_2003_08646_b200 as lance
+    from paper_2003_08646_b200.stack import VGG16_CIFAR as STACK, LanceStack
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    cfg = lance.LanceConfig(8, 8, lance.Granularity.PerPosition, lance.LanceMode.Gemm)
+    stack = LanceStack(STACK, N, 32, 32, cfg, device=local, tile_m=args.tile_m)
+    ws_, bs_ = [], []
+    for i, st in enumerate(stack.convs):
+        w = lance.uniform_floats(st.k * 9 * st.c, 7 + i) * np.float32(np.sqrt(2.0 / (9 * st.c)))
+        ws_.append(torch.from_numpy(w.astype(np.float32)).to(dev).view(st.k, 3, 3, st.c))
+        bs_.append(torch.zeros(st.k, dtype=torch.float32, device=dev))
+    stack.set_weights(ws_, bs_)
+    x = torch.from_numpy(lance.uniform_floats(N * 32 * 32 * 3, 42 + rank)).to(dev).view(N, 32, 32, 3)
+    stack.capture(x)
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(args.warmup):
+        stack.replay()
+    torch.cuda.synchronize(dev)
+    stream = torch.cuda.current_stream(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    clocks.mark()
+    e0.record(stream)
+    for _ in range(args.steps):
+        stack.replay()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks.mark()
+    clk = clocks.stop()
+    stack.sync()
+    elapsed = e0.elapsed_time(e1) * 1e-3
+    if rank == 0:
+        convs = [(s.c, s.k, s.h) for s in stack.convs]
+        print(json.dumps({
+            "metric": METRIC, "value": N * args.steps * ws / elapsed, "unit": "images/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (UniformSource); He-scaled random weights, zero bias",
+            "config": {"workload": "vgg16_cifar_stack_chained" + ("_f4x4" if args.tile_m == 4 else ""),
+                       "batch_per_gpu": N, "convs": convs, "pools": 4,
+                       "epilogue": "bias + ReLU fused", "launch": "one CUDA graph per step",
+                       "winograd": f"F({args.tile_m}x{args.tile_m},3x3)"},
+            "tops_equivalent": 2 * sum(direct_macs(c, k, h, N) for c, k, h in convs) * args.steps * ws / elapsed / 1e12,
+            "gpu_launches": stack.launches_per_forward() * args.steps,
+            "clocks": clk}), flush=True)
+    stack.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--batch", type=int, default=0, help="images per GPU (default: the workload's)")
+    ap.add_argument("--workload", default="resnet18", choices=sorted(WORKLOADS),
+                    help="resnet18 = BASELINE config 3 (default), vgg16_cifar = config 2")
+    ap.add_argument("--stack", action="store_true",
+                    help="vgg16_cifar only: run the chained layer-stack driver (bias + ReLU + "
+                         "2x2 max-pools, one CUDA graph per step) instead of independent layers")
     ap.add_argument("--ref-batch", type=int, default=2)
     ap.add_argument("--cpu-batch", type=int, default=4)
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -267,10 +335,14 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
         pg = dist
 
-    layers = RESNET18
+    wl_layers, wl_batch, wl_name = WORKLOADS[args.workload]
+    layers = wl_layers
     if args.layers:
-        layers = [RESNET18[int(i)] for i in args.layers.split(",")]
-    N = args.batch
+        layers = [wl_layers[int(i)] for i in args.layers.split(",")]
+    N = args.batch or wl_batch
+    if args.stack:
+        run_stack(args, ws, rank, local, N)
+        return
     TM = args.tile_m
     cfg = lance.LanceConfig(8, 8, lance.Granularity.PerPosition, lance.LanceMode.Gemm)
 
@@ -419,16 +491,16 @@ def main():
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu and TM == 4:
-        v, tot = cpu_port_f4_images_per_s(1)
+        v, tot = cpu_port_f4_images_per_s(1, layers)
         cpu = {"value": v, "unit": "images/s", "cores": 1, "kind": "port",
                "sample": f"13 ResNet-18 3x3 layers at batch 1, oracle lo_lance_gemm_tiled(tile_m=4) "
                          f"single thread ({tot:.2f} s/pass); the reference has no F(4x4)"}
     elif rank == 0 and ws == 1 and not args.no_cpu:
         try:
             threads = os.cpu_count() or 1
-            v, tot = cpu_reference_images_per_s(args.cpu_batch, 3, threads)
+            v, tot = cpu_reference_images_per_s(args.cpu_batch, 3, threads, layers)
             cpu = {"value": v, "unit": "images/s", "cores": threads, "kind": "reference",
-                   "sample": f"13 ResNet-18 3x3 layers at batch {args.cpu_batch} (of 256), reference "
+                   "sample": f"{len(layers)} {wl_name} layers at batch {args.cpu_batch} (of {N}), reference "
                              f"lance_gemm median of 3 steady_clock repeats per layer ({tot:.2f} s/pass)"}
         except Exception as e:  # reference shim absent
             cpu = {"value": None, "unit": "images/s", "cores": 0, "kind": "reference",
@@ -440,7 +512,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (lance::UniformSource seed 42+layer, x then w; bench.hpp:129-133)",
-            "config": {"workload": WORKLOAD + ("_f4x4" if TM == 4 else ""), "batch_per_gpu": N,
+            "config": {"workload": wl_name + ("_f4x4" if TM == 4 else ""), "batch_per_gpu": N,
                        "global_batch": N * ws,
                        "layers": [list(l) for l in layers], "winograd": f"F({TM}x{TM},3x3)",
                        "bits_w": 8, "bits_i": 8, "granularity": "PerPosition", "pad": 1,

@@ -176,6 +176,12 @@ LANCE_API int lance_gemm_host_tiled(const lance_conv_spec* spec, const lance_con
 /* (m+2)^2 * tiles * N * C * K for tile side m (engines.hpp:573-575 generalised). */
 LANCE_API uint64_t lance_winograd_multiply_count_tiled(const lance_conv_spec* spec, int tile_m);
 
+/* Layer-stack glue (not part of lance_gemm):
+ * 2x2 / stride-2 max-pool of a device NHWC tensor, y [n][h/2][w/2][c], on
+ * `stream` -- the pooling between VGG-16-CIFAR conv stages (BASELINE config 2). */
+LANCE_API int lance_maxpool2x2_nhwc(const float* x_dev, float* y_dev, int n, int h, int w, int c,
+                                    void* stream);
+
 /* Synthetic-input fixture: lance::UniformSource(seed) stream (rng.hpp:27-47),
  * mt19937_64 top-24-bit -> U(-1,1).  Host memory. */
 LANCE_API void lance_uniform_fill(uint64_t seed, float* out, size_t count);

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_build")
 LIB = os.path.join(OUT_DIR, "liblance_b200.so")
-SOURCES = ["lance_input.cu", "lance_band.cu", "lance_filter.cu", "lance_gemm.cu", "lance_f4.cu", "lance_abi.cu"]
+SOURCES = ["lance_input.cu", "lance_band.cu", "lance_filter.cu", "lance_gemm.cu", "lance_f4.cu", "lance_stack.cu", "lance_abi.cu"]
 HEADERS = ["lance_common.cuh", "lance_kernels.cuh", "lance_ptx.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-DLANCE_JMAJOR=" + os.environ.get("LANCE_JMAJOR", "0"), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",

@@ -590,6 +590,20 @@ static int create_f4(lance_plan_s* p, const lance_conv_spec* spec, const lance_c
 
 int lance_plan_positions(lance_plan_t p) { return p ? p->np : 0; }
 
+int lance_maxpool2x2_nhwc(const float* x_dev, float* y_dev, int n, int h, int w, int c,
+                          void* stream) {
+  if (!x_dev || !y_dev) return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_maxpool2x2: null buffer");
+  if (n < 1 || h < 2 || w < 2 || c < 1) return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_maxpool2x2: bad dims");
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(LANCE_ERR_NO_DEVICE, "no CUDA device");
+  }
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  LANCE_CUDA(launch_maxpool2x2(x_dev, y_dev, n, h, w, c, sms, static_cast<cudaStream_t>(stream)));
+  return LANCE_OK;
+}
+
 uint64_t lance_winograd_multiply_count_tiled(const lance_conv_spec* s, int tile_m) {
   if (tile_m != 2 && tile_m != 4) return 0;
   const uint64_t tiles = uint64_t((out_h(*s) + tile_m - 1) / tile_m) * ((out_w(*s) + tile_m - 1) / tile_m);

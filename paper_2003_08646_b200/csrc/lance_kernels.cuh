@@ -185,6 +185,10 @@ cudaError_t launch_gemm(const uint8_t* codes_a, const uint8_t* codes_w, const CU
                         const LanceDevState* st, float* y, int32_t* acc_dump, const float* bias,
                         int relu, const GemmGeom& g, cudaStream_t s);
 
+// Layer-stack glue (lance_stack.cu).
+cudaError_t launch_maxpool2x2(const float* x, float* y, int N, int H, int W, int C, int sm_count,
+                              cudaStream_t s);
+
 // F(4x4,3x3) launchers (lance_f4.cu).
 int f4_range_grid(const F4Geom& g, int sm_count);
 cudaError_t launch_f4_range(const float* x, float* partials, int grid, LanceDevState* st,
