@@ -194,9 +194,18 @@ __device__ __forceinline__ bool block_minmax_and_ticket(float (&lo)[16], float (
   __threadfence();
   const int col = threadIdx.x & 31;
   float r = (col < 16) ? __int_as_float(0x7f800000) : __int_as_float(0xff800000);
-  for (int b = warp; b < static_cast<int>(gridDim.x); b += nw) {
-    const float v = __ldcg(partials + static_cast<long long>(b) * 32 + col);
-    r = (col < 16) ? fmin_nan(r, v) : fmax_nan(r, v);
+  // Eight independent partial loads in flight per thread (a serial chain of
+  // dependent L2 round trips here cost tens of microseconds on small layers).
+  const int nb = static_cast<int>(gridDim.x);
+  for (int b0 = warp; b0 < nb; b0 += 8 * nw) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int b = b0 + u * nw;
+      v[u] = (b < nb) ? __ldcg(partials + static_cast<long long>(b) * 32 + col) : r;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) r = (col < 16) ? fmin_nan(r, v[u]) : fmax_nan(r, v[u]);
   }
   __syncthreads();
   s_red[threadIdx.x] = r;

@@ -166,14 +166,34 @@ __device__ __forceinline__ bool block_minmax36(float (&lo)[kNP4], float (&hi)[kN
   __syncthreads();
   if (!s_last) return false;
   __threadfence();
-  if (threadIdx.x < 72) {
-    const int i = threadIdx.x;
+  {
+    // Column i = threadIdx.x % 72 over the blocks b = threadIdx.x / 72 + k * (nthreads / 72),
+    // eight independent loads in flight, then a shared-memory fold of the rows.
+    const int rows = static_cast<int>(blockDim.x) / 72;
+    const int i = threadIdx.x % 72, row0 = threadIdx.x / 72;
     float r = (i < 36) ? __int_as_float(0x7f800000) : __int_as_float(0xff800000);
-    for (int b = 0; b < static_cast<int>(gridDim.x); ++b) {
-      const float v = __ldcg(partials + static_cast<long long>(b) * 72 + i);
-      r = (i < 36) ? fmin_nan(r, v) : fmax_nan(r, v);
+    const int nb = static_cast<int>(gridDim.x);
+    if (row0 < rows) {
+      for (int b0 = row0; b0 < nb; b0 += 8 * rows) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int b = b0 + u * rows;
+          v[u] = (b < nb) ? __ldcg(partials + static_cast<long long>(b) * 72 + i) : r;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) r = (i < 36) ? fmin_nan(r, v[u]) : fmax_nan(r, v[u]);
+      }
     }
-    s_fin[i] = r;
+    __syncthreads();
+    if (row0 < rows) s_red[row0 * 72 + i] = r;
+    __syncthreads();
+    if (threadIdx.x < 72) {
+      float q = s_red[threadIdx.x];
+      for (int w = 1; w < rows; ++w)
+        q = (threadIdx.x < 36) ? fmin_nan(q, s_red[w * 72 + threadIdx.x]) : fmax_nan(q, s_red[w * 72 + threadIdx.x]);
+      s_fin[threadIdx.x] = q;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) *ticket = 0u;
