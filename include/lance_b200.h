@@ -182,6 +182,10 @@ LANCE_API uint64_t lance_winograd_multiply_count_tiled(const lance_conv_spec* sp
 LANCE_API int lance_maxpool2x2_nhwc(const float* x_dev, float* y_dev, int n, int h, int w, int c,
                                     void* stream);
 
+/* The CLI's output checksum (lance_main.cpp:41-51): FNV-1a 64 over the
+ * little-endian bytes of `count` floats.  Host memory, no device needed. */
+LANCE_API uint64_t lance_fnv1a64(const float* data, size_t count);
+
 /* Synthetic-input fixture: lance::UniformSource(seed) stream (rng.hpp:27-47),
  * mt19937_64 top-24-bit -> U(-1,1).  Host memory. */
 LANCE_API void lance_uniform_fill(uint64_t seed, float* out, size_t count);

@@ -280,6 +280,8 @@ class Reference:
                                                    ct.POINTER(ct.c_double)]
         lib.ref_run_verify.argtypes = [ct.c_char_p, ct.c_size_t]
         lib.ref_set_threads.argtypes = [ct.c_int]
+        lib.ref_write_lten.argtypes = [ct.c_char_p] + [ct.c_int] * 4 + [ct.c_void_p]
+        lib.ref_read_lten.argtypes = [ct.c_char_p, ct.c_void_p, ct.c_void_p, ct.c_size_t]
         self.lib = lib
 
     def _err(self, rc):
@@ -339,6 +341,18 @@ class Reference:
                                           threads, seed, reps, ct.byref(med), ct.byref(mn))
         self._err(rc)
         return med.value, mn.value
+
+    def write_lten(self, path: str, t):
+        t = _f32(t)
+        n, h, w, c = t.shape
+        self._err(self.lib.ref_write_lten(path.encode(), n, h, w, c, _ptr(t)))
+
+    def read_lten(self, path: str):
+        dims = np.zeros(4, np.int32)
+        self._err(self.lib.ref_read_lten(path.encode(), _ptr(dims), None, 0))
+        out = np.empty(tuple(int(d) for d in dims), np.float32)
+        self._err(self.lib.ref_read_lten(path.encode(), _ptr(dims), _ptr(out), out.size))
+        return out
 
     def run_verify(self):
         buf = ct.create_string_buffer(1 << 16)

@@ -20,6 +20,7 @@
 
 #include "lance/engines.hpp"
 #include "lance/rng.hpp"
+#include "lance/tensor_io.hpp"
 #include "lance/verify.hpp"
 
 namespace {
@@ -216,6 +217,36 @@ int ref_run_verify(char* report, size_t cap) {
     report[nb] = 0;
   }
   return ok ? 0 : 1;
+}
+
+// tensor_io.hpp:94-150: the reference's own LTEN writer / reader (format pins
+// for paper_2003_08646_b200/tensor_io.py).  ref_read_lten returns 0 and fills
+// dims[4] (+ data when non-NULL and cap is enough), 2 on FormatError.
+int ref_write_lten(const char* path, int n, int h, int w, int c, const float* data) {
+  try {
+    lance::Tensor4 t(n, h, w, c);
+    std::memcpy(t.data.data(), data, sizeof(float) * t.data.size());
+    lance::write_tensor_file(t, path);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+int ref_read_lten(const char* path, int* dims, float* data, size_t cap) {
+  try {
+    const lance::Tensor4 t = lance::read_tensor_file(path);
+    dims[0] = t.n;
+    dims[1] = t.h;
+    dims[2] = t.w;
+    dims[3] = t.c;
+    if (data && cap >= t.data.size()) std::memcpy(data, t.data.data(), sizeof(float) * t.data.size());
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
 }
 
 }  // extern "C"

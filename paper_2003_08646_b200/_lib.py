@@ -87,6 +87,8 @@ def lib():
         L.lance_winograd_multiply_count_tiled.argtypes = [ct.POINTER(CSpec), ct.c_int]
         L.lance_winograd_multiply_count_tiled.restype = ct.c_uint64
         L.lance_maxpool2x2_nhwc.argtypes = [P, P, ct.c_int, ct.c_int, ct.c_int, ct.c_int, P]
+        L.lance_fnv1a64.argtypes = [P, ct.c_size_t]
+        L.lance_fnv1a64.restype = ct.c_uint64
         L.lance_uniform_fill.argtypes = [ct.c_uint64, P, ct.c_size_t]
         L.lance_uniform_fill.restype = None
         _lib = L
@@ -102,6 +104,6 @@ EXPORTED = [
     "lance_plan_debug_read", "lance_plan_set_acc_dump", "lance_plan_last_launch_count",
     "lance_plan_stage_timing", "lance_plan_read_stage_times",
     "lance_plan_create_tiled", "lance_plan_positions", "lance_gemm_host_tiled",
-    "lance_winograd_multiply_count_tiled", "lance_maxpool2x2_nhwc",
+    "lance_winograd_multiply_count_tiled", "lance_maxpool2x2_nhwc", "lance_fnv1a64",
     "lance_uniform_fill",
 ]

@@ -255,6 +255,19 @@ uint64_t lance_winograd_multiply_count(const lance_conv_spec* s) {
   return 16u * tiles * s->n * s->c * uint64_t(s->k);
 }
 
+uint64_t lance_fnv1a64(const float* data, size_t count) {
+  uint64_t h = 1469598103934665603ull;
+  for (size_t i = 0; i < count; ++i) {
+    uint32_t bits;
+    std::memcpy(&bits, data + i, 4);
+    for (int b = 0; b < 4; ++b) {
+      h ^= (bits >> (8 * b)) & 0xffu;
+      h *= 1099511628211ull;
+    }
+  }
+  return h;
+}
+
 void lance_uniform_fill(uint64_t seed, float* out, size_t count) {
   std::mt19937_64 rng(seed);  // UniformSource (rng.hpp:27-47)
   for (size_t i = 0; i < count; ++i) {
