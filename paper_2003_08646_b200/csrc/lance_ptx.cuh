@@ -33,8 +33,24 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// LANCE_WAIT_HINT > 0: try_wait with a suspend-time hint (ns), so a waiting
+// thread sleeps in hardware until the phase completes (or the hint elapses)
+// instead of re-issuing the poll loop -- spinning control warps otherwise take
+// issue slots from the epilogue warps sharing their SM sub-partition.
+#ifndef LANCE_WAIT_HINT
+#define LANCE_WAIT_HINT 0
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
+#if LANCE_WAIT_HINT > 0
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "n"(LANCE_WAIT_HINT)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -42,6 +58,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "=r"(ok)
       : "r"(addr), "r"(parity)
       : "memory");
+#endif
   return ok != 0;
 }
 
