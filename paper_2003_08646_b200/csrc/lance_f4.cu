@@ -338,7 +338,11 @@ __global__ void __launch_bounds__(256, 2) f4_range_kernel(const float* __restric
 // F1: codes (A operand UMMA images, j-major planes) + row sums.  Positions
 // (p, p + 18) are quantised as one packed pair; the warp's per-tile row sums
 // are one REDUX per position, added into rowsum (zeroed by the launcher).
-template <bool STATIC>
+// BK / NK > 0: compile-time image geometry, so the 36 per-position store
+// offsets are immediates; NK = 0: runtime geometry (any shape).  The tie
+// check is one branch per row pair (12 codes), the rare fix-up recomputes
+// that row's flagged codes exactly before they are stored.
+template <bool STATIC, int BK, int NK>
 __global__ void __launch_bounds__(256, 2) f4_quant_kernel(const float* __restrict__ x,
                                                           uint8_t* __restrict__ codes,
                                                           int32_t* __restrict__ rowsum,
@@ -355,13 +359,14 @@ __global__ void __launch_bounds__(256, 2) f4_quant_kernel(const float* __restric
   const float top = static_cast<float>((1 << st->bits_i) - 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long rowstride = static_cast<long long>(g.W) * g.C;
-  const long long img_bytes = static_cast<long long>(kBM) * g.bk;  // one UMMA image
-  const long long pstride = g.nk * img_bytes;                       // one position plane
+  const int bk = NK > 0 ? BK : g.bk;
+  const int img_bytes = kBM * bk;                              // one UMMA image
+  const int pstride = (NK > 0 ? NK : g.nk) * img_bytes;        // one position plane
   for (long long item = static_cast<long long>(blockIdx.x) * 8 + warp; item < g.num_items;
        item += static_cast<long long>(gridDim.x) * 8) {
     const F4Strip sp = f4_strip(g, item, lane);
     const float* rowbase = x + (static_cast<long long>(sp.img) * g.H + (4 * sp.ti - g.pad)) * rowstride + sp.c;
-    const int kc = sp.c / g.bk, cb = sp.c - kc * g.bk;
+    const int kc = sp.c / bk, cb = sp.c - kc * bk;
     float2 tp[3][6];
     f4_col(rowbase, rowstride, g, sp, 4 * sp.tj0 - g.pad, 0, tp);
     f4_col(rowbase, rowstride, g, sp, 4 * sp.tj0 - g.pad + 1, 1, tp);
@@ -371,38 +376,56 @@ __global__ void __launch_bounds__(256, 2) f4_quant_kernel(const float* __restric
       const long long tile = (static_cast<long long>(sp.img) * g.TH + sp.ti) * g.TW + tj;
       const long long blk = tile / kBM;
       const int r = static_cast<int>(tile - blk * kBM);
-      uint8_t* dst = codes + (blk * kNP4) * pstride + kc * img_bytes +
-                     umma_swizzle(static_cast<uint32_t>(r * g.bk + cb), g.bk);
+      uint8_t* dst = codes + (blk * kNP4) * static_cast<long long>(pstride) + kc * img_bytes +
+                     umma_swizzle(static_cast<uint32_t>(r * bk + cb), bk);
       uint32_t mine0 = 0, mine1 = 0;  // row sums of positions lane, lane + 32
 #pragma unroll
       for (int rr = 0; rr < 3; ++rr) {
         float2 v2[6];
         bt6_2(tp[rr], v2);
+        uint32_t c0[6], c1[6];  // positions 6rr + k (.x) and 6rr + 18 + k (.y)
+        if (STATIC) {
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          const int p = 6 * rr + k;  // and p + 18 in .y
-          uint32_t c0, c1;
-          if (STATIC) {
-            c0 = quantize_code(v2[k].x, s_tmin2[p].x, s_scale2[p].x, top);
-            c1 = quantize_code(v2[k].y, s_tmin2[p].y, s_scale2[p].y, top);
-          } else {
+          for (int k = 0; k < 6; ++k) {
+            const int p = 6 * rr + k;
+            c0[k] = quantize_code(v2[k].x, s_tmin2[p].x, s_scale2[p].x, top);
+            c1[k] = quantize_code(v2[k].y, s_tmin2[p].y, s_scale2[p].y, top);
+          }
+        } else {
+          float rmax = 0.0f;
+#pragma unroll
+          for (int k = 0; k < 6; ++k) {
+            const int p = 6 * rr + k;
             const float2 dd = sub2(v2[k], s_tmin2[p]);
             const float2 gq = fma2(dd, s_rcp2[p], bcast2(kMagic));
             const float2 rr2 = fma2(dd, s_rcp2[p], sub2(bcast2(kMagic), gq));
-            c0 = __float_as_uint(gq.x) & 0xFFu;
-            c1 = __float_as_uint(gq.y) & 0xFFu;
-            if (__builtin_expect(!(fmaxf(fabsf(rr2.x), fabsf(rr2.y)) < kTieGuard), 0)) {
-              if (!(fabsf(rr2.x) < kTieGuard)) c0 = exact_code_near_boundary(dd.x, s_scale2[p].x, gq.x, rr2.x, top);
-              if (!(fabsf(rr2.y) < kTieGuard)) c1 = exact_code_near_boundary(dd.y, s_scale2[p].y, gq.y, rr2.y, top);
+            c0[k] = __float_as_uint(gq.x) & 0xFFu;
+            c1[k] = __float_as_uint(gq.y) & 0xFFu;
+            rmax = fmax3_nan(rmax, fabsf(rr2.x), fabsf(rr2.y));
+          }
+          if (__builtin_expect(!(rmax < kTieGuard), 0)) {
+            // Rare (~1e-4 per value): re-derive this row's flagged codes exactly.
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+              const int p = 6 * rr + k;
+              const float2 dd = sub2(v2[k], s_tmin2[p]);
+              const float2 gq = fma2(dd, s_rcp2[p], bcast2(kMagic));
+              const float2 rr2 = fma2(dd, s_rcp2[p], sub2(bcast2(kMagic), gq));
+              if (!(fabsf(rr2.x) < kTieGuard)) c0[k] = exact_code_near_boundary(dd.x, s_scale2[p].x, gq.x, rr2.x, top);
+              if (!(fabsf(rr2.y) < kTieGuard)) c1[k] = exact_code_near_boundary(dd.y, s_scale2[p].y, gq.y, rr2.y, top);
             }
           }
-          if (!sp.cok) c0 = c1 = 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          const int p = 6 * rr + k;
+          if (!sp.cok) c0[k] = c1[k] = 0u;
           else {
-            dst[f4_plane(p) * pstride] = static_cast<uint8_t>(c0);
-            dst[f4_plane(p + 18) * pstride] = static_cast<uint8_t>(c1);
+            dst[f4_plane(p) * pstride] = static_cast<uint8_t>(c0[k]);
+            dst[f4_plane(p + 18) * pstride] = static_cast<uint8_t>(c1[k]);
           }
-          const uint32_t s0 = __reduce_add_sync(0xffffffffu, c0);
-          const uint32_t s1 = __reduce_add_sync(0xffffffffu, c1);
+          const uint32_t s0 = __reduce_add_sync(0xffffffffu, c0[k]);
+          const uint32_t s1 = __reduce_add_sync(0xffffffffu, c1[k]);
           if (lane == (p & 31)) {
             if (p < 32) mine0 = s0; else mine1 = s0;
           }
@@ -889,10 +912,21 @@ cudaError_t launch_f4_quant(const float* x, uint8_t* codes, int32_t* rowsum,
   const int grid = static_cast<int>(blocks < 4LL * sm_count ? blocks : 4LL * sm_count);
   cudaError_t e = cudaMemsetAsync(rowsum, 0, sizeof(int32_t) * kNP4 * static_cast<size_t>(g.rs_pitch), s);
   if (e != cudaSuccess) return e;
-  if (static_mode)
-    f4_quant_kernel<true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
-  else
-    f4_quant_kernel<false><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
+#define LANCE_F4Q(BKV, NKV)                                                                   \
+  if ((NKV == 0) || (g.bk == BKV && g.nk == NKV)) {                                           \
+    if (static_mode)                                                                          \
+      f4_quant_kernel<true, BKV, NKV><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);          \
+    else                                                                                      \
+      f4_quant_kernel<false, BKV, NKV><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);         \
+    return cudaGetLastError();                                                                \
+  }
+  LANCE_F4Q(64, 1)
+  LANCE_F4Q(128, 1)
+  LANCE_F4Q(128, 2)
+  LANCE_F4Q(128, 4)
+  LANCE_F4Q(32, 1)
+  LANCE_F4Q(0, 0)
+#undef LANCE_F4Q
   return cudaGetLastError();
 }
 
