@@ -453,6 +453,22 @@ def main():
     roofline["gemm_stage_int8"] = {"achieved_tops": 2 * wmacs / t3 / 1e12 if t3 > 0 else None,
                                    "peak_tops": i8, "peak_source": "measured here: torch._int_mm 8192^3",
                                    "frac": (2 * wmacs / t3 / 1e12 / i8) if (i8 and t3 > 0) else None}
+    # The GEMM stage's own roofline: min(INT8 peak, HBM x arithmetic intensity)
+    # per layer (its operands + y must cross HBM at least once), summed as times.
+    if i8:
+        att_s, ach_s, rows = 0.0, 0.0, []
+        for (spec, *_), pl in zip(state, per_layer):
+            ops = 2 * winograd_macs(spec.c, spec.k, spec.h, N, TM)
+            byt = stage_bytes(spec.c, spec.k, spec.h, N, TM)[2]
+            t_floor = max(ops / (i8 * 1e12), byt / (hbm * 1e9))
+            t_meas = pl["us_per_forward"][2] * 1e-6
+            att_s += t_floor
+            ach_s += t_meas
+            rows.append({"c": spec.c, "h": spec.h, "ops_per_byte": round(ops / byt, 1),
+                         "bound": "tensor" if ops / (i8 * 1e12) > byt / (hbm * 1e9) else "hbm",
+                         "frac_of_attainable": round(t_floor / t_meas, 3) if t_meas > 0 else None})
+        roofline["gemm_stage_int8"]["frac_of_attainable"] = att_s / ach_s if ach_s > 0 else None
+        roofline["gemm_stage_int8"]["per_layer_attainable"] = rows
     roofline["per_layer"] = per_layer
 
     # ---- e2e through the public host API (reference-facing lance_gemm) ----
