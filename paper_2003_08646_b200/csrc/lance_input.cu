@@ -621,6 +621,117 @@ __global__ void static_params_kernel(LanceDevState* st, StaticParams prm, int C)
 }
 
 // --------------------------------------------------------------------------
+// Small-C path (C < 32, e.g. the RGB first layer of VGG, C = 3): the strip
+// kernels put channels on lanes, which would leave most lanes idle; here one
+// thread owns one (tile, channel) and walks a grid-stride loop.  Same
+// arithmetic as input_transform2 / the quantisers above, scalar.
+__device__ __forceinline__ void smallc_tile(const float* __restrict__ x, const InGeom& g,
+                                            long long i, float (&v)[16], long long& tile, int& c) {
+  tile = i / g.C;
+  c = static_cast<int>(i - tile * g.C);
+  const int img = static_cast<int>(tile / g.P), t = static_cast<int>(tile - static_cast<long long>(img) * g.P);
+  const int ti = t / g.TW, tj = t - ti * g.TW;
+  const int y0 = 2 * ti - g.pad, x0 = 2 * tj - g.pad;
+  const float* base = x + static_cast<long long>(img) * g.H * g.W * g.C + c;
+  float d[16];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int yy = y0 + a, xx = x0 + b;
+      d[a * 4 + b] = (yy >= 0 && yy < g.H && xx >= 0 && xx < g.W)
+                         ? __ldg(base + (static_cast<long long>(yy) * g.W + xx) * g.C)
+                         : 0.0f;
+    }
+  float t4[16];  // column pass first (B^T d), then rows
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    t4[0 * 4 + b] = __fsub_rn(d[0 * 4 + b], d[2 * 4 + b]);
+    t4[1 * 4 + b] = __fadd_rn(d[1 * 4 + b], d[2 * 4 + b]);
+    t4[2 * 4 + b] = __fsub_rn(d[2 * 4 + b], d[1 * 4 + b]);
+    t4[3 * 4 + b] = __fsub_rn(d[1 * 4 + b], d[3 * 4 + b]);
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    v[a * 4 + 0] = __fsub_rn(t4[a * 4 + 0], t4[a * 4 + 2]);
+    v[a * 4 + 1] = __fadd_rn(t4[a * 4 + 1], t4[a * 4 + 2]);
+    v[a * 4 + 2] = __fsub_rn(t4[a * 4 + 2], t4[a * 4 + 1]);
+    v[a * 4 + 3] = __fsub_rn(t4[a * 4 + 1], t4[a * 4 + 3]);
+  }
+}
+
+__global__ void __launch_bounds__(256) input_range_smallc_kernel(const float* __restrict__ x,
+                                                                 float* __restrict__ partials,
+                                                                 LanceDevState* __restrict__ st,
+                                                                 InGeom g) {
+  __shared__ float s_red[256];
+  float lo[16], hi[16];
+#pragma unroll
+  for (int p = 0; p < 16; ++p) {
+    lo[p] = __int_as_float(0x7f800000);
+    hi[p] = __int_as_float(0xff800000);
+  }
+  const long long total = static_cast<long long>(g.M) * g.C;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float v[16];
+    long long tile;
+    int c;
+    smallc_tile(x, g, i, v, tile, c);
+#pragma unroll
+    for (int p = 0; p < 16; ++p) {
+      lo[p] = fmin_nan(lo[p], v[p]);
+      hi[p] = fmax_nan(hi[p], v[p]);
+    }
+  }
+  if (block_minmax_and_ticket(lo, hi, partials, &st->ticket_in, s_red)) {
+    fit_from_ranges(s_red, g.granularity, st->bits_i, st->a_tmin, st->a_tmax, st->a_scale,
+                    st->a_rcp, &st->nan_in);
+    __syncthreads();
+    make_epilogue_consts(st, g.C);
+  }
+}
+
+template <bool STATIC>
+__global__ void __launch_bounds__(256) input_quant_smallc_kernel(const float* __restrict__ x,
+                                                                 uint8_t* __restrict__ codes,
+                                                                 int32_t* __restrict__ rowsum,
+                                                                 const LanceDevState* __restrict__ st,
+                                                                 InGeom g) {
+  __shared__ float s_tmin[16], s_scale[16], s_rcp[16];
+  if (threadIdx.x < 16) {
+    s_tmin[threadIdx.x] = st->a_tmin[threadIdx.x];
+    s_scale[threadIdx.x] = st->a_scale[threadIdx.x];
+    s_rcp[threadIdx.x] = st->a_rcp[threadIdx.x];
+  }
+  __syncthreads();
+  const float top = static_cast<float>((1 << st->bits_i) - 1);
+  const long long total = static_cast<long long>(g.M) * g.C;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float v[16];
+    long long tile;
+    int c;
+    smallc_tile(x, g, i, v, tile, c);
+#pragma unroll
+    for (int p = 0; p < 16; ++p) {
+      uint32_t code;
+      if (STATIC) {
+        code = quantize_code(v[p], s_tmin[p], s_scale[p], top);
+      } else {
+        const float dd = __fsub_rn(v[p], s_tmin[p]);
+        const float gq = __fmaf_rn(dd, s_rcp[p], kMagic);
+        const float rr = __fmaf_rn(dd, s_rcp[p], __fsub_rn(kMagic, gq));
+        code = (fabsf(rr) < kTieGuard) ? (__float_as_uint(gq) & 0xFFu)
+                                       : exact_code_near_boundary(dd, s_scale[p], gq, rr, top);
+      }
+      codes[umma_image_offset(tile, c, p, kBM, g.a_bk, g.a_nk)] = static_cast<uint8_t>(code);
+      if (g.rowsums) atomicAdd(rowsum + static_cast<long long>(p) * g.rs_pitch + tile, static_cast<int>(code));
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
 int input_range_grid(const InGeom& g, int sm_count) {
   const long long blocks = (g.num_items + 7) / 8;
   const long long cap = 2LL * sm_count;  // 2 resident 256-thread blocks per SM
@@ -629,7 +740,9 @@ int input_range_grid(const InGeom& g, int sm_count) {
 
 cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceDevState* st,
                                const InGeom& g, int vec2, cudaStream_t s) {
-  if (g.C % 64 == 0)
+  if (g.C < 32)
+    input_range_smallc_kernel<<<grid, 256, 0, s>>>(x, partials, st, g);
+  else if (g.C % 64 == 0)
     input_range_fast_kernel<<<grid, 256, 0, s>>>(x, partials, st, g);
   else if (vec2)
     input_range_kernel<true><<<grid, 256, 0, s>>>(x, partials, st, g);
@@ -642,6 +755,19 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
                                const LanceDevState* st, const InGeom& g, int vec2,
                                int static_mode, cudaStream_t s) {
   const unsigned grid = static_cast<unsigned>((g.num_items + 7) / 8);
+  if (g.C < 32) {
+    const long long total = static_cast<long long>(g.M) * g.C;
+    const unsigned sgrid = static_cast<unsigned>((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+    if (g.rowsums) {  // atomically accumulated here (normally the GEMM sums the rows at BK = 32)
+      cudaError_t e = cudaMemsetAsync(rowsum, 0, sizeof(int32_t) * 16 * static_cast<size_t>(g.rs_pitch), s);
+      if (e != cudaSuccess) return e;
+    }
+    if (static_mode)
+      input_quant_smallc_kernel<true><<<sgrid, 256, 0, s>>>(x, codes, rowsum, st, g);
+    else
+      input_quant_smallc_kernel<false><<<sgrid, 256, 0, s>>>(x, codes, rowsum, st, g);
+    return cudaGetLastError();
+  }
   if (!static_mode && g.C % 64 == 0) {  // fast path: every lane owns two real channels
     static const int depth = [] {
       const char* e = std::getenv("LANCE_K1_DEPTH");

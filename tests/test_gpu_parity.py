@@ -211,7 +211,8 @@ def test_alternate_kernel_paths_bitexact(lo, env, monkeypatch):
         monkeypatch.setenv(k, v)
     for spec, dist, seed in [(Spec(2, 64, 17, 17, 64, 1), "relu", 3),
                              (Spec(1, 128, 14, 14, 64, 1), "uniform", 4),
-                             (Spec(1, 256, 9, 9, 128, 0), "relu", 5)]:
+                             (Spec(1, 256, 9, 9, 128, 0), "relu", 5),
+                             (Spec(3, 3, 15, 13, 20, 1), "relu", 6)]:  # small-C kernels
         x, w = make_inputs(lo.uniform, spec, dist, seed)
         got = run_gpu(spec, x, w, gemm_cfg())
         y, ref = lo.lance_gemm(spec, x, w, dump=True)
