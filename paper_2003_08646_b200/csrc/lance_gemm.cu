@@ -467,7 +467,11 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       float2 S[4][FPT / 2];  // running S_ab partials, filter pairs
 #pragma unroll
       for (int j = 0; j < 4; ++j, ++grp) {
-        const uint32_t buf = grp % NB;
+        // Every tile has 4 j-groups and 4 % NB == 0, so the buffer is j % NB:
+        // a compile-time constant once j is unrolled (TMEM / constant addresses
+        // fold into immediates).  The phase parity still follows grp.
+        static_assert(4 % NB == 0, "j-group buffers must divide the 4 j-groups of a tile");
+        const uint32_t buf = static_cast<uint32_t>(j % NB);
         float rterm[4], k1s[4], k4[4];  // per position 4a + j of this j-group
         if (g.rs_warps || j == 0) mbar_wait(&rs_ready[rb * 4 + (g.rs_warps ? j : 0)], (lt >> 1) & 1u);
 #pragma unroll
