@@ -387,7 +387,12 @@ __global__ void __launch_bounds__(256, 2) input_quant_kernel(const float* __rest
 // per-lane validity branches; BK is a template parameter so the UMMA-image
 // address is a handful of shifts per tile, and the tie fix-up is one
 // warp-uniform branch per position pair.
-template <int BK, int NK, bool RS>
+// STATIC: caller-supplied params (values may lie outside [t_min, t_max]):
+// q = RN(d * rcp) is clamped to [-1, top + 1] before the magic-number rounding
+// and the code to [0, top]; far-out values then round to 0 / top exactly as the
+// reference's clamps do, and near-ties (|residual| >= 0.5 - 2^-14, which
+// includes the 0.5 and top + 0.5 boundaries) take the IEEE-division quantiser.
+template <int BK, int NK, bool RS, bool STATIC = false>
 __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* __restrict__ x,
                                                                   uint8_t* __restrict__ codes,
                                                                   int32_t* __restrict__ rowsum,
@@ -453,8 +458,16 @@ __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* _
       }
       uint32_t pk0 = __byte_perm(__float_as_uint(gq[0].x), __float_as_uint(gq[0].y), 0x0040);
       uint32_t pk1 = __byte_perm(__float_as_uint(gq[1].x), __float_as_uint(gq[1].y), 0x0040);
-      const float rmax = fmax3_nan(fmax3_nan(fabsf(r[0].x), fabsf(r[0].y), fabsf(r[1].x)),
-                                   fabsf(r[1].y), 0.0f);
+      float rmax = fmax3_nan(fmax3_nan(fabsf(r[0].x), fabsf(r[0].y), fabsf(r[1].x)),
+                             fabsf(r[1].y), 0.0f);
+      if (STATIC) {
+        // Caller params: a value whose rounded code falls outside [0, top]
+        // (or whose product is too large for the magic-number rounding) joins
+        // the exact path, which applies the reference's clamps.
+        const float glo = fmin3_nan(fmin3_nan(gq[0].x, gq[0].y, gq[1].x), gq[1].y, kMagic);
+        const float ghi = fmax3_nan(fmax3_nan(gq[0].x, gq[0].y, gq[1].x), gq[1].y, kMagic);
+        if (!(glo >= kMagic) || !(ghi <= __fadd_rn(kMagic, top))) rmax = 1.0f;
+      }
       if (__builtin_expect(__any_sync(0xffffffffu, !(rmax < kTieGuard)), 0)) {
         // Rare (~1e-4 per value): re-derive flagged codes exactly.
         if (!(rmax < kTieGuard)) {
@@ -465,8 +478,14 @@ __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* _
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float sc = s_scale[2 * k + (e >> 1)];
-            c[e] = (fabsf(rv[e]) < kTieGuard) ? (__float_as_uint(gv[e]) & 0xFFu)
-                                              : exact_code_near_boundary(dv[e], sc, gv[e], rv[e], top);
+            const float2 vv = v[2 * k + (e >> 1)];
+            if (STATIC)
+              c[e] = (fabsf(rv[e]) < kTieGuard && gv[e] >= kMagic && gv[e] <= __fadd_rn(kMagic, top))
+                         ? (__float_as_uint(gv[e]) & 0xFFu)
+                         : quantize_code((e & 1) ? vv.y : vv.x, s_tmin[2 * k + (e >> 1)], sc, top);
+            else
+              c[e] = (fabsf(rv[e]) < kTieGuard) ? (__float_as_uint(gv[e]) & 0xFFu)
+                                                : exact_code_near_boundary(dv[e], sc, gv[e], rv[e], top);
           }
           pk0 = c[0] | (c[1] << 8);
           pk1 = c[2] | (c[3] << 8);
@@ -498,6 +517,7 @@ __global__ void __launch_bounds__(192, 2) input_quant_fast2_kernel(const float* 
                                                                   int32_t* __restrict__ rowsum,
                                                                   const LanceDevState* __restrict__ st,
                                                                   InGeom g) {
+  constexpr bool STATIC = false;  // dynamic params only (LANCE_K1_DEPTH=2 experiment)
   __shared__ float s_tmin[16], s_scale[16], s_rcp[16];
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid < 16) {
@@ -564,8 +584,16 @@ __global__ void __launch_bounds__(192, 2) input_quant_fast2_kernel(const float* 
       }
       uint32_t pk0 = __byte_perm(__float_as_uint(gq[0].x), __float_as_uint(gq[0].y), 0x0040);
       uint32_t pk1 = __byte_perm(__float_as_uint(gq[1].x), __float_as_uint(gq[1].y), 0x0040);
-      const float rmax = fmax3_nan(fmax3_nan(fabsf(r[0].x), fabsf(r[0].y), fabsf(r[1].x)),
-                                   fabsf(r[1].y), 0.0f);
+      float rmax = fmax3_nan(fmax3_nan(fabsf(r[0].x), fabsf(r[0].y), fabsf(r[1].x)),
+                             fabsf(r[1].y), 0.0f);
+      if (STATIC) {
+        // Caller params: a value whose rounded code falls outside [0, top]
+        // (or whose product is too large for the magic-number rounding) joins
+        // the exact path, which applies the reference's clamps.
+        const float glo = fmin3_nan(fmin3_nan(gq[0].x, gq[0].y, gq[1].x), gq[1].y, kMagic);
+        const float ghi = fmax3_nan(fmax3_nan(gq[0].x, gq[0].y, gq[1].x), gq[1].y, kMagic);
+        if (!(glo >= kMagic) || !(ghi <= __fadd_rn(kMagic, top))) rmax = 1.0f;
+      }
       if (__builtin_expect(__any_sync(0xffffffffu, !(rmax < kTieGuard)), 0)) {
         // Rare (~1e-4 per value): re-derive flagged codes exactly.
         if (!(rmax < kTieGuard)) {
@@ -576,8 +604,14 @@ __global__ void __launch_bounds__(192, 2) input_quant_fast2_kernel(const float* 
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float sc = s_scale[2 * k + (e >> 1)];
-            c[e] = (fabsf(rv[e]) < kTieGuard) ? (__float_as_uint(gv[e]) & 0xFFu)
-                                              : exact_code_near_boundary(dv[e], sc, gv[e], rv[e], top);
+            const float2 vv = v[2 * k + (e >> 1)];
+            if (STATIC)
+              c[e] = (fabsf(rv[e]) < kTieGuard && gv[e] >= kMagic && gv[e] <= __fadd_rn(kMagic, top))
+                         ? (__float_as_uint(gv[e]) & 0xFFu)
+                         : quantize_code((e & 1) ? vv.y : vv.x, s_tmin[2 * k + (e >> 1)], sc, top);
+            else
+              c[e] = (fabsf(rv[e]) < kTieGuard) ? (__float_as_uint(gv[e]) & 0xFFu)
+                                                : exact_code_near_boundary(dv[e], sc, gv[e], rv[e], top);
           }
           pk0 = c[0] | (c[1] << 8);
           pk1 = c[2] | (c[3] << 8);
@@ -768,14 +802,18 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
       input_quant_smallc_kernel<false><<<sgrid, 256, 0, s>>>(x, codes, rowsum, st, g);
     return cudaGetLastError();
   }
-  if (!static_mode && g.C % 64 == 0) {  // fast path: every lane owns two real channels
+  if (g.C % 64 == 0) {  // fast path: every lane owns two real channels
     static const int depth = [] {
       const char* e = std::getenv("LANCE_K1_DEPTH");
       return e ? std::atoi(e) : 1;
     }();
 #define LANCE_K1_FAST(BKV, NKV)                                                          \
   if (g.a_bk == BKV && g.a_nk == NKV) {                                                  \
-    if (depth == 2)                                                                      \
+    if (static_mode && g.rowsums)                                                        \
+      input_quant_fast_kernel<BKV, NKV, true, true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g); \
+    else if (static_mode)                                                                \
+      input_quant_fast_kernel<BKV, NKV, false, true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g); \
+    else if (depth == 2)                                                                 \
       input_quant_fast2_kernel<BKV, NKV>                                                 \
           <<<static_cast<unsigned>((g.num_items + 5) / 6), 192, 0, s>>>(x, codes, rowsum, st, g); \
     else if (g.rowsums)                                                                  \

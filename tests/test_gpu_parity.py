@@ -220,3 +220,32 @@ def test_alternate_kernel_paths_bitexact(lo, env, monkeypatch):
         for k in ("codes_a", "rowsum", "acc", "params_a", "y"):
             assert np.array_equal(np.asarray(got[k]).view(np.uint8), np.asarray(ref[k]).view(np.uint8)), \
                 f"{env} {spec}: {k}: {mismatch_report(got[k], ref[k])}"
+
+
+@pytest.mark.parametrize("spec", [Spec(2, 64, 17, 17, 64, 1),    # fast K1, row sums in the GEMM
+                                  Spec(1, 128, 14, 14, 64, 1),   # fast K1, row sums in K1
+                                  Spec(1, 96, 9, 11, 24, 0)])    # generic K1
+def test_static_params_out_of_range_bitexact(lo, spec):
+    """Static (caller) params narrower than / shifted from the data: codes
+    saturate at 0 and top, one position has scale 0 -- the fast static
+    quantiser's clamps and tie fallback must reproduce quantize() exactly."""
+    x, w = make_inputs(lo.uniform, spec, "relu", 41)
+    _, d = lo.lance_gemm(spec, x, w, dump=True)
+    pa = d["params_a"].copy()
+    rng = np.random.default_rng(0)
+    for p in range(16):
+        lo_, hi_ = float(pa[p, 1]), float(pa[p, 2])
+        span = hi_ - lo_
+        a = np.float32(lo_ + span * rng.uniform(0.1, 0.4))
+        b = np.float32(hi_ - span * rng.uniform(0.1, 0.4))
+        pa[p, 1], pa[p, 2] = a, b
+        pa[p, 3] = np.float32(np.float32(b - a) / np.float32(255.0))
+    pa[5, 2] = pa[5, 1]
+    pa[5, 3] = np.float32(0.0)  # scale 0 -> every code 0
+    qps = [lance.QuantParams(8, float(r[1]), float(r[2]), float(r[3])) for r in pa]
+    got = run_gpu(spec, x, w, gemm_cfg(), params=qps)
+    y, ref = lo.lance_gemm(spec, x, w, in_params=pa, dump=True)
+    ref["y"] = y
+    for k in ("codes_a", "rowsum", "acc", "y"):
+        assert np.array_equal(np.asarray(got[k]).view(np.uint8), np.asarray(ref[k]).view(np.uint8)), \
+            f"{k}: {mismatch_report(got[k], ref[k])}"
