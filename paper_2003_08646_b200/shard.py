@@ -49,7 +49,7 @@ def params_from_minmax(lo: np.ndarray, hi: np.ndarray, bits: int) -> list[QuantP
 
 
 def allreduce_minmax(lo, hi, group=None):
-    """Global (min, max) per position across ranks: one all-reduce of 32 floats
+    """Global (min, max) per position across ranks: one all-reduce of 2 x P floats
     (MAX over [-lo, hi]; -(-x) is exact). Works with any torch.distributed
     backend (NCCL on GPUs, gloo on CPU)."""
     import torch
@@ -62,7 +62,35 @@ def allreduce_minmax(lo, hi, group=None):
         buf = buf.cuda()
     dist.all_reduce(buf, op=dist.ReduceOp.MAX, group=group)
     buf = buf.cpu().numpy()
-    return -buf[:16], buf[16:]
+    n = lo_t.numel()  # 16 positions, or 36 for F(4x4)
+    return -buf[:n], buf[n:]
+
+
+def scatter_batch(x_full, n_total: int, shape_tail, src: int = 0, group=None):
+    """Scatter of a full batch held by rank `src` into contiguous per-rank
+    slices (verification only, outside any timed region).  x_full: the
+    [N, ...] array on `src` (ignored elsewhere); returns this rank's slice.
+    NCCL over NVLink on GPUs, gloo on CPU."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    cuda = dist.get_backend(group) == "nccl"
+    dev = torch.device("cuda", torch.cuda.current_device()) if cuda else torch.device("cpu")
+    spans = [shard_range(n_total, world, r) for r in range(world)]
+    a, b = spans[rank]
+    out = torch.empty((b - a,) + tuple(shape_tail), dtype=torch.float32, device=dev)
+    if rank == src:
+        full = torch.as_tensor(np.ascontiguousarray(x_full, dtype=np.float32)).to(dev)
+        for r, (ra, rb) in enumerate(spans):
+            if r == src:
+                out.copy_(full[ra:rb])
+            else:
+                dist.send(full[ra:rb].contiguous(), dst=r, group=group)
+    else:
+        dist.recv(out, src=src, group=group)
+    return out
 
 
 def gather_batch(y_local, n_total: int, group=None):
@@ -73,11 +101,53 @@ def gather_batch(y_local, n_total: int, group=None):
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    t = torch.as_tensor(np.ascontiguousarray(y_local))
+    t = y_local if isinstance(y_local, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(y_local))
     if dist.get_backend(group) == "nccl":
         t = t.cuda()
+    else:
+        t = t.cpu()
     sizes = [shard_range(n_total, world, r) for r in range(world)]
     shape = tuple(t.shape[1:])
-    parts = [torch.empty((b - a,) + shape, dtype=t.dtype, device=t.device) for a, b in sizes]
-    dist.all_gather(parts, t, group=group)
-    return torch.cat(parts).cpu().numpy()
+    # Uneven shards: every rank contributes a slice padded to the largest one
+    # (all_gather needs equal sizes), trimmed again after the exchange.
+    mx = max(b - a for a, b in sizes)
+    if t.shape[0] < mx:
+        t = torch.cat([t, torch.zeros((mx - t.shape[0],) + shape, dtype=t.dtype, device=t.device)])
+    parts = [torch.empty((mx,) + shape, dtype=t.dtype, device=t.device) for _ in sizes]
+    dist.all_gather(parts, t.contiguous(), group=group)
+    return torch.cat([p[: b - a] for p, (a, b) in zip(parts, sizes)]).cpu().numpy()
+
+
+def verify_sharded(x_full, w, spec, cfg, group=None, tile_m: int = 2):
+    """Multi-GPU full-batch parity check of one layer (north star: NCCL only
+    scatters inputs and gathers outputs for verification).  Rank 0 holds x
+    [N,H,W,C] and w; x is scattered, every rank runs its slice in the
+    full-batch-parity mode (local range pass -> 128-byte MAX all-reduce ->
+    static-params forward), and the gathered output is returned on every rank.
+    It must equal one full-batch lance_gemm call bitwise.  w must be given on
+    every rank (with NCCL rank 0's copy is broadcast)."""
+    import torch
+    import torch.distributed as dist
+
+    from .api import ConvSpec, LanceConv
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    a, b = shard_range(spec.n, world, rank)
+    xs = scatter_batch(x_full, spec.n, (spec.h, spec.w, spec.c), group=group)
+    wt = torch.as_tensor(np.ascontiguousarray(w, dtype=np.float32)).cuda()
+    if dist.get_backend(group) == "nccl":  # rank 0's filters everywhere
+        dist.broadcast(wt, src=0, group=group)
+    conv = LanceConv(ConvSpec(b - a, spec.c, spec.h, spec.w, spec.k, spec.pad), cfg,
+                     device=torch.cuda.current_device(), tile_m=tile_m)
+    conv.set_filters(wt)
+    conv.forward(xs.cuda())            # local range pass
+    conv.sync()
+    local, _ = conv.params()
+    lo = np.array([q.t_min for q in local], np.float32)
+    hi = np.array([q.t_max for q in local], np.float32)
+    glo, ghi = allreduce_minmax(lo, hi, group)
+    y = conv.forward(xs.cuda(), params=params_from_minmax(glo, ghi, cfg.bits_i))
+    conv.sync()
+    out = gather_batch(y, spec.n, group)
+    conv.close()
+    return out

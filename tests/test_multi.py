@@ -102,3 +102,37 @@ def test_gloo_world2_per_shard_and_global_parity():
     assert np.array_equal(results["y_glob_all"].view(np.uint32), y_full.view(np.uint32))
     # and the per-shard mode really differs from the full batch (batch coupling)
     assert not np.array_equal(results["y_all"], y_full)
+
+
+def _scatter_worker(rank, world, port, results):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, tail = 7, (3, 4, 5)
+        full = np.arange(n * 60, dtype=np.float32).reshape((n,) + tail) if rank == 0 else None
+        part = shard.scatter_batch(full, n, tail)
+        a, b = shard.shard_range(n, world, rank)
+        ok = np.array_equal(part.numpy(), np.arange(n * 60, dtype=np.float32).reshape((n,) + tail)[a:b])
+        back = shard.gather_batch(part, n)
+        lo = np.linspace(-1, 0, 36).astype(np.float32) - rank
+        hi = np.linspace(0, 1, 36).astype(np.float32) + rank
+        glo, ghi = shard.allreduce_minmax(lo, hi)  # 36 positions (F(4x4))
+        if rank == 0:
+            results["ok"] = ok
+            results["back"] = back
+            results["glo"], results["ghi"] = glo, ghi
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world3_scatter_gather_and_36_position_allreduce():
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_scatter_worker, args=(3, _free_port(), results), nprocs=3, join=True)
+    assert results["ok"]
+    assert np.array_equal(results["back"], np.arange(7 * 60, dtype=np.float32).reshape(7, 3, 4, 5))
+    assert np.array_equal(results["glo"], np.linspace(-1, 0, 36).astype(np.float32) - 2)
+    assert np.array_equal(results["ghi"], np.linspace(0, 1, 36).astype(np.float32) + 2)
