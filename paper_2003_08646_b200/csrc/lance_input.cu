@@ -655,6 +655,100 @@ __global__ void static_params_kernel(LanceDevState* st, StaticParams prm, int C)
 }
 
 // --------------------------------------------------------------------------
+// K0 variant (LANCE_K0_ASYNC = D): the two new input columns of the next D
+// tiles are staged per lane with cp.async (8-byte copies, zero-fill outside
+// the image) in a shared-memory ring instead of registers, so the lookahead
+// is not limited by the register budget.  A lane only ever reads back the
+// slots it copied itself, so per-thread cp.async groups are the only ordering
+// needed.  Arithmetic identical to input_range_fast_kernel.
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int D>
+__global__ void __launch_bounds__(256, 2) input_range_async_kernel(const float* __restrict__ x,
+                                                                   float* __restrict__ partials,
+                                                                   LanceDevState* __restrict__ st,
+                                                                   InGeom g) {
+  extern __shared__ float2 s_ring[];  // [8 warps][D slots][2 columns][4 rows][32 lanes]
+  __shared__ float s_red[256];
+  float lo[16], hi[16];
+#pragma unroll
+  for (int p = 0; p < 16; ++p) {
+    lo[p] = __int_as_float(0x7f800000);
+    hi[p] = __int_as_float(0xff800000);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float2* ring = s_ring + static_cast<size_t>(warp) * D * 8 * 32;
+  const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+  for (long long item = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + warp;
+       item < g.num_items; item += stride) {
+    const StripItem it = strip_item(g, item, lane);
+    const Strip<true> sp(x, g, it);
+    auto issue = [&](int tj) {  // the 2 new columns of tile tj into slot tj % D
+      float2* slot = ring + (tj % D) * 8 * 32;
+      if (tj < it.tj1) {
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int xx = 2 * tj - g.pad + 2 + cc;
+          const bool cok = (xx >= 0) && (xx < g.W);
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            const bool ok = cok && sp.rok[a] && sp.c0ok;
+            const float* src = ok ? sp.row[a] + static_cast<long long>(xx) * g.C : x;
+            cp_async8(slot + (cc * 4 + a) * 32 + lane, src, ok);
+          }
+        }
+      }
+      cp_async_commit();  // one group per tile, empty past the strip end
+    };
+    float2 ta[4], tb[4], tc[4], td[4];
+    const int xx0 = 2 * it.tj0 - g.pad;
+    sp.column(xx0, ta);
+    sp.column(xx0 + 1, tb);
+#pragma unroll
+    for (int q = 0; q < D; ++q) issue(it.tj0 + q);
+    for (int tj = it.tj0; tj < it.tj1; ++tj) {
+      cp_async_wait<D - 1>();  // this tile's group has landed
+      const float2* slot = ring + (tj % D) * 8 * 32;
+      float2 pc[4], pd[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        pc[a] = slot[a * 32 + lane];
+        pd[a] = slot[(4 + a) * 32 + lane];
+      }
+      issue(tj + D);  // refill the slot just read (program order: reads first)
+      colpass(pc, tc);
+      colpass(pd, td);
+      float2 v[16];
+      row_pass(ta, tb, tc, td, v);
+#pragma unroll
+      for (int p = 0; p < 16; ++p) {
+        lo[p] = fmin3_nan(lo[p], v[p].x, v[p].y);
+        hi[p] = fmax3_nan(hi[p], v[p].x, v[p].y);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        ta[a] = tc[a];
+        tb[a] = td[a];
+      }
+    }
+    cp_async_wait<0>();
+  }
+  if (block_minmax_and_ticket(lo, hi, partials, &st->ticket_in, s_red)) {
+    fit_from_ranges(s_red, g.granularity, st->bits_i, st->a_tmin, st->a_tmax, st->a_scale,
+                    st->a_rcp, &st->nan_in);
+    __syncthreads();
+    make_epilogue_consts(st, g.C);
+  }
+}
+
+// --------------------------------------------------------------------------
 // Small-C path (C < 32, e.g. the RGB first layer of VGG, C = 3): the strip
 // kernels put channels on lanes, which would leave most lanes idle; here one
 // thread owns one (tile, channel) and walks a grid-stride loop.  Same
@@ -774,10 +868,34 @@ int input_range_grid(const InGeom& g, int sm_count) {
 
 cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceDevState* st,
                                const InGeom& g, int vec2, cudaStream_t s) {
-  if (g.C < 32)
+  // K0 input staging: cp.async ring of K0_DEPTH tiles (default 4; 0 = the
+  // register-lookahead kernel).  Measured: 4 is 7-8 % faster than registers on
+  // the 56x56 / 28x28 layers; 8 halves residency (128 KB per block) and loses.
+  static const int async_depth = [] {
+    const char* e = std::getenv("LANCE_K0_ASYNC");
+    return e ? std::atoi(e) : 4;
+  }();
+  if (g.C < 32) {
     input_range_smallc_kernel<<<grid, 256, 0, s>>>(x, partials, st, g);
-  else if (g.C % 64 == 0)
+  } else if (g.C % 64 == 0 && (async_depth == 4 || async_depth == 6 || async_depth == 8)) {
+    const size_t smem = static_cast<size_t>(8) * async_depth * 8 * 32 * sizeof(float2);
+#define LANCE_K0_ASYNC_CASE(DV)                                                                   \
+    if (async_depth == DV) {                                                                     \
+      static bool set = false;                                                                   \
+      if (!set) {                                                                                \
+        cudaFuncSetAttribute(input_range_async_kernel<DV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             static_cast<int>(smem));                                            \
+        set = true;                                                                              \
+      }                                                                                          \
+      input_range_async_kernel<DV><<<grid, 256, smem, s>>>(x, partials, st, g);                  \
+    }
+    LANCE_K0_ASYNC_CASE(4)
+    LANCE_K0_ASYNC_CASE(6)
+    LANCE_K0_ASYNC_CASE(8)
+#undef LANCE_K0_ASYNC_CASE
+  } else if (g.C % 64 == 0) {
     input_range_fast_kernel<<<grid, 256, 0, s>>>(x, partials, st, g);
+  }
   else if (vec2)
     input_range_kernel<true><<<grid, 256, 0, s>>>(x, partials, st, g);
   else
