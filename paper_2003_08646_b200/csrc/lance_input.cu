@@ -387,12 +387,21 @@ __global__ void __launch_bounds__(256, 2) input_quant_kernel(const float* __rest
 // per-lane validity branches; BK is a template parameter so the UMMA-image
 // address is a handful of shifts per tile, and the tie fix-up is one
 // warp-uniform branch per position pair.
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 // STATIC: caller-supplied params (values may lie outside [t_min, t_max]):
 // q = RN(d * rcp) is clamped to [-1, top + 1] before the magic-number rounding
 // and the code to [0, top]; far-out values then round to 0 / top exactly as the
 // reference's clamps do, and near-ties (|residual| >= 0.5 - 2^-14, which
 // includes the 0.5 and top + 0.5 boundaries) take the IEEE-division quantiser.
-template <int BK, int NK, bool RS, bool STATIC = false>
+template <int BK, int NK, bool RS, bool STATIC = false, int ASYNC = 0>
 __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* __restrict__ x,
                                                                   uint8_t* __restrict__ codes,
                                                                   int32_t* __restrict__ rowsum,
@@ -425,14 +434,51 @@ __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* _
   int xx = 2 * it.tj0 - g.pad;
   sp.column(xx, ta);
   sp.column(xx + 1, tb);
-  sp.load(xx + 2, pc);
-  sp.load(xx + 3, pd);
+  // ASYNC > 0: the next ASYNC tiles' two new columns are staged per lane with
+  // cp.async in a shared-memory ring (as input_range_async_kernel).
+  extern __shared__ float2 s_ring1[];
+  float2* ring = s_ring1 + static_cast<size_t>(tid >> 5) * (ASYNC > 0 ? ASYNC : 1) * 8 * 32;
+  auto issue = [&](int t) {
+    if (ASYNC > 0) {
+      float2* slot = ring + (t % (ASYNC > 0 ? ASYNC : 1)) * 8 * 32;
+      if (t < it.tj1) {
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int xc = 2 * t - g.pad + 2 + cc;
+          const bool cok = (xc >= 0) && (xc < g.W);
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            const bool ok = cok && sp.rok[a] && sp.c0ok;
+            cp_async8(slot + (cc * 4 + a) * 32 + lane, ok ? sp.row[a] + static_cast<long long>(xc) * g.C : x, ok);
+          }
+        }
+      }
+      cp_async_commit();
+    }
+  };
+  if (ASYNC > 0) {
+#pragma unroll
+    for (int q = 0; q < (ASYNC > 0 ? ASYNC : 1); ++q) issue(it.tj0 + q);
+  } else {
+    sp.load(xx + 2, pc);
+    sp.load(xx + 3, pd);
+  }
   int m = (it.img * g.TH + it.ti) * g.TW + it.tj0;
   for (int tj = it.tj0; tj < it.tj1; ++tj, xx += 2, ++m) {
     float2 v[16];
+    if (ASYNC > 0) {
+      cp_async_wait<(ASYNC > 0 ? ASYNC - 1 : 0)>();
+      const float2* slot = ring + (tj % (ASYNC > 0 ? ASYNC : 1)) * 8 * 32;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        pc[a] = slot[a * 32 + lane];
+        pd[a] = slot[(4 + a) * 32 + lane];
+      }
+      issue(tj + ASYNC);
+    }
     colpass(pc, tc);
     colpass(pd, td);
-    if (tj + 1 < it.tj1) {  // software prefetch of the next tile's two new columns
+    if (ASYNC == 0 && tj + 1 < it.tj1) {  // software prefetch of the next tile's two new columns
       sp.load(xx + 4, pc);
       sp.load(xx + 5, pd);
     }
@@ -661,15 +707,6 @@ __global__ void static_params_kernel(LanceDevState* st, StaticParams prm, int C)
 // is not limited by the register budget.  A lane only ever reads back the
 // slots it copied itself, so per-thread cp.async groups are the only ordering
 // needed.  Arithmetic identical to input_range_fast_kernel.
-__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc, bool valid) {
-  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(sdst));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(valid ? 8 : 0)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-
 template <int D>
 __global__ void __launch_bounds__(256, 2) input_range_async_kernel(const float* __restrict__ x,
                                                                    float* __restrict__ partials,
@@ -925,6 +962,23 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
       const char* e = std::getenv("LANCE_K1_DEPTH");
       return e ? std::atoi(e) : 1;
     }();
+    static const int k1_async = [] {
+      const char* e = std::getenv("LANCE_K1_ASYNC");
+      return e ? std::atoi(e) : 0;
+    }();
+    const size_t k1_smem = k1_async == 4 ? static_cast<size_t>(8) * 4 * 8 * 32 * sizeof(float2) : 0;
+    static bool k1_attr = false;
+    if (k1_async == 4 && !k1_attr) {  // 64 KB rings: opt every instantiation in once
+#define LANCE_K1_ATTR(BKV, NKV)                                                                   \
+      cudaFuncSetAttribute(input_quant_fast_kernel<BKV, NKV, true, false, 4>,                     \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k1_smem)); \
+      cudaFuncSetAttribute(input_quant_fast_kernel<BKV, NKV, false, false, 4>,                    \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k1_smem));
+      LANCE_K1_ATTR(64, 1) LANCE_K1_ATTR(128, 1) LANCE_K1_ATTR(128, 2) LANCE_K1_ATTR(128, 3)
+      LANCE_K1_ATTR(128, 4) LANCE_K1_ATTR(64, 3) LANCE_K1_ATTR(64, 5)
+#undef LANCE_K1_ATTR
+      k1_attr = true;
+    }
 #define LANCE_K1_FAST(BKV, NKV)                                                          \
   if (g.a_bk == BKV && g.a_nk == NKV) {                                                  \
     if (static_mode && g.rowsums)                                                        \
@@ -934,6 +988,10 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
     else if (depth == 2)                                                                 \
       input_quant_fast2_kernel<BKV, NKV>                                                 \
           <<<static_cast<unsigned>((g.num_items + 5) / 6), 192, 0, s>>>(x, codes, rowsum, st, g); \
+    else if (k1_async == 4 && g.rowsums)                                                 \
+      input_quant_fast_kernel<BKV, NKV, true, false, 4><<<grid, 256, k1_smem, s>>>(x, codes, rowsum, st, g); \
+    else if (k1_async == 4)                                                              \
+      input_quant_fast_kernel<BKV, NKV, false, false, 4><<<grid, 256, k1_smem, s>>>(x, codes, rowsum, st, g); \
     else if (g.rowsums)                                                                  \
       input_quant_fast_kernel<BKV, NKV, true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g); \
     else                                                                                 \
