@@ -281,7 +281,57 @@ __device__ __forceinline__ void f4_col(const float* __restrict__ rowbase, long l
   }
 }
 
+// Optional input staging (template D > 0): the 4 new input columns x 6 rows
+// of the next D tiles are copied per lane with 4-byte cp.async (zero-fill
+// outside the image) into a shared-memory ring; the first pass then reads them
+// from the slot.  A lane only reads what it copied itself.
+__device__ __forceinline__ void f4_cp_async4(float* sdst, const float* gsrc, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(gsrc), "r"(valid ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void f4_cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void f4_cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int D>
+__device__ __forceinline__ void f4_ring_issue(float* ring, int lane, const float* __restrict__ x,
+                                              const float* __restrict__ rowbase, long long rowstride,
+                                              const F4Geom& g, const F4Strip& sp, int t) {
+  float* slot = ring + (t % D) * 24 * 32;
+  if (t < sp.tj1) {
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      const int xx = 4 * t - g.pad + 2 + cc;
+      const bool colok = sp.cok && xx >= 0 && xx < g.W;
+      const float* p = rowbase + static_cast<long long>(xx) * g.C;
+#pragma unroll
+      for (int a = 0; a < 6; ++a) {
+        const bool ok = colok && ((sp.rowmask >> a) & 1u);
+        f4_cp_async4(slot + (cc * 6 + a) * 32 + lane, ok ? p + a * rowstride : x, ok);
+      }
+    }
+  }
+  f4_cp_commit();
+}
+
+// First pass for column b (2..5) of tile t from its staged slot.
+template <int D>
+__device__ __forceinline__ void f4_col_staged(const float* ring, int lane, int t, int b, float2 (&tp)[3][6]) {
+  const float* slot = ring + (t % D) * 24 * 32 + (b - 2) * 6 * 32 + lane;
+  float col[6], y6[6];
+#pragma unroll
+  for (int a = 0; a < 6; ++a) col[a] = slot[a * 32];
+  bt6(col, y6);
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    tp[r][b].x = y6[r];
+    tp[r][b].y = y6[r + 3];
+  }
+}
+
 // F0: ranges.
+template <int D>
 __global__ void __launch_bounds__(256, 2) f4_range_kernel(const float* __restrict__ x,
                                                           float* __restrict__ partials,
                                                           LanceDevState* __restrict__ st,
@@ -296,6 +346,8 @@ __global__ void __launch_bounds__(256, 2) f4_range_kernel(const float* __restric
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long rowstride = static_cast<long long>(g.W) * g.C;
+  extern __shared__ float f4ring_all[];  // D > 0: [8 warps][D][24][32]
+  float* f4ring = f4ring_all + static_cast<size_t>(warp) * (D > 0 ? D : 1) * 24 * 32;
   for (long long item = static_cast<long long>(blockIdx.x) * 8 + warp; item < g.num_items;
        item += static_cast<long long>(gridDim.x) * 8) {
     const F4Strip sp = f4_strip(g, item, lane);
@@ -303,9 +355,21 @@ __global__ void __launch_bounds__(256, 2) f4_range_kernel(const float* __restric
     float2 tp[3][6];
     f4_col(rowbase, rowstride, g, sp, 4 * sp.tj0 - g.pad, 0, tp);
     f4_col(rowbase, rowstride, g, sp, 4 * sp.tj0 - g.pad + 1, 1, tp);
-    for (int tj = sp.tj0; tj < sp.tj1; ++tj) {
+    if (D > 0) {
 #pragma unroll
-      for (int b = 2; b < 6; ++b) f4_col(rowbase, rowstride, g, sp, 4 * tj - g.pad + b, b, tp);
+      for (int q = 0; q < (D > 0 ? D : 1); ++q)
+        f4_ring_issue<(D > 0 ? D : 1)>(f4ring, lane, x, rowbase, rowstride, g, sp, sp.tj0 + q);
+    }
+    for (int tj = sp.tj0; tj < sp.tj1; ++tj) {
+      if (D > 0) {
+        f4_cp_wait<(D > 0 ? D - 1 : 0)>();
+#pragma unroll
+        for (int b = 2; b < 6; ++b) f4_col_staged<(D > 0 ? D : 1)>(f4ring, lane, tj, b, tp);
+        f4_ring_issue<(D > 0 ? D : 1)>(f4ring, lane, x, rowbase, rowstride, g, sp, tj + D);
+      } else {
+#pragma unroll
+        for (int b = 2; b < 6; ++b) f4_col(rowbase, rowstride, g, sp, 4 * tj - g.pad + b, b, tp);
+      }
       if (sp.cok) {
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
@@ -326,6 +390,7 @@ __global__ void __launch_bounds__(256, 2) f4_range_kernel(const float* __restric
         tp[r][1] = tp[r][5];
       }
     }
+    if (D > 0) f4_cp_wait<0>();
   }
   if (block_minmax36(lo, hi, partials, &st->ticket_in, s_red, s_fin)) {
     fit36(s_fin, g.granularity, st->bits_i, st->a_tmin, st->a_tmax, st->a_scale, st->a_rcp,
@@ -342,7 +407,7 @@ __global__ void __launch_bounds__(256, 2) f4_range_kernel(const float* __restric
 // offsets are immediates; NK = 0: runtime geometry (any shape).  The tie
 // check is one branch per row pair (12 codes), the rare fix-up recomputes
 // that row's flagged codes exactly before they are stored.
-template <bool STATIC, int BK, int NK>
+template <bool STATIC, int BK, int NK, int D = 0>
 __global__ void __launch_bounds__(256, 2) f4_quant_kernel(const float* __restrict__ x,
                                                           uint8_t* __restrict__ codes,
                                                           int32_t* __restrict__ rowsum,
@@ -362,6 +427,8 @@ __global__ void __launch_bounds__(256, 2) f4_quant_kernel(const float* __restric
   const int bk = NK > 0 ? BK : g.bk;
   const int img_bytes = kBM * bk;                              // one UMMA image
   const int pstride = (NK > 0 ? NK : g.nk) * img_bytes;        // one position plane
+  extern __shared__ float f4qring_all[];  // D > 0: [8 warps][D][24][32]
+  float* f4ring = f4qring_all + static_cast<size_t>(warp) * (D > 0 ? D : 1) * 24 * 32;
   for (long long item = static_cast<long long>(blockIdx.x) * 8 + warp; item < g.num_items;
        item += static_cast<long long>(gridDim.x) * 8) {
     const F4Strip sp = f4_strip(g, item, lane);
@@ -370,9 +437,21 @@ __global__ void __launch_bounds__(256, 2) f4_quant_kernel(const float* __restric
     float2 tp[3][6];
     f4_col(rowbase, rowstride, g, sp, 4 * sp.tj0 - g.pad, 0, tp);
     f4_col(rowbase, rowstride, g, sp, 4 * sp.tj0 - g.pad + 1, 1, tp);
-    for (int tj = sp.tj0; tj < sp.tj1; ++tj) {
+    if (D > 0) {
 #pragma unroll
-      for (int b = 2; b < 6; ++b) f4_col(rowbase, rowstride, g, sp, 4 * tj - g.pad + b, b, tp);
+      for (int q = 0; q < (D > 0 ? D : 1); ++q)
+        f4_ring_issue<(D > 0 ? D : 1)>(f4ring, lane, x, rowbase, rowstride, g, sp, sp.tj0 + q);
+    }
+    for (int tj = sp.tj0; tj < sp.tj1; ++tj) {
+      if (D > 0) {
+        f4_cp_wait<(D > 0 ? D - 1 : 0)>();
+#pragma unroll
+        for (int b = 2; b < 6; ++b) f4_col_staged<(D > 0 ? D : 1)>(f4ring, lane, tj, b, tp);
+        f4_ring_issue<(D > 0 ? D : 1)>(f4ring, lane, x, rowbase, rowstride, g, sp, tj + D);
+      } else {
+#pragma unroll
+        for (int b = 2; b < 6; ++b) f4_col(rowbase, rowstride, g, sp, 4 * tj - g.pad + b, b, tp);
+      }
       const long long tile = (static_cast<long long>(sp.img) * g.TH + sp.ti) * g.TW + tj;
       const long long blk = tile / kBM;
       const int r = static_cast<int>(tile - blk * kBM);
@@ -443,6 +522,7 @@ __global__ void __launch_bounds__(256, 2) f4_quant_kernel(const float* __restric
         tp[q][1] = tp[q][5];
       }
     }
+    if (D > 0) f4_cp_wait<0>();
   }
 }
 
@@ -899,9 +979,40 @@ int f4_range_grid(const F4Geom& g, int sm_count) {
   return static_cast<int>(blocks < cap ? blocks : cap);
 }
 
+static int f4_async_depth() {
+  static const int d = [] {
+    const char* e = std::getenv("LANCE_F4_ASYNC");
+    return e ? std::atoi(e) : 2;  // measured: 2 beats 0 (no lookahead) and 4
+  }();
+  return d;
+}
+
+static int f4_quant_depth() {
+  static const int d = [] {
+    const char* e = std::getenv("LANCE_F4Q_ASYNC");
+    return e ? std::atoi(e) : 2;  // measured: -5 % on the 56x56 layer
+  }();
+  return d;
+}
+
 cudaError_t launch_f4_range(const float* x, float* partials, int grid, LanceDevState* st,
                             const F4Geom& g, cudaStream_t s) {
-  f4_range_kernel<<<grid, 256, 0, s>>>(x, partials, st, g);
+  const int d = f4_async_depth();
+  if (d == 2 || d == 4) {
+    const size_t smem = static_cast<size_t>(8) * d * 24 * 32 * sizeof(float);
+    static bool set = false;
+    if (!set) {
+      cudaFuncSetAttribute(f4_range_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 2 * 24 * 32 * 4);
+      cudaFuncSetAttribute(f4_range_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4 * 24 * 32 * 4);
+      set = true;
+    }
+    if (d == 2)
+      f4_range_kernel<2><<<grid, 256, smem, s>>>(x, partials, st, g);
+    else
+      f4_range_kernel<4><<<grid, 256, smem, s>>>(x, partials, st, g);
+  } else {
+    f4_range_kernel<0><<<grid, 256, 0, s>>>(x, partials, st, g);
+  }
   return cudaGetLastError();
 }
 
@@ -912,12 +1023,28 @@ cudaError_t launch_f4_quant(const float* x, uint8_t* codes, int32_t* rowsum,
   const int grid = static_cast<int>(blocks < 4LL * sm_count ? blocks : 4LL * sm_count);
   cudaError_t e = cudaMemsetAsync(rowsum, 0, sizeof(int32_t) * kNP4 * static_cast<size_t>(g.rs_pitch), s);
   if (e != cudaSuccess) return e;
+  const int qd = f4_quant_depth();
+  const size_t qsmem = static_cast<size_t>(8) * 2 * 24 * 32 * sizeof(float);
 #define LANCE_F4Q(BKV, NKV)                                                                   \
   if ((NKV == 0) || (g.bk == BKV && g.nk == NKV)) {                                           \
-    if (static_mode)                                                                          \
+    if (qd == 2) {                                                                            \
+      static bool set = false;                                                                \
+      if (!set) {                                                                             \
+        cudaFuncSetAttribute(f4_quant_kernel<true, BKV, NKV, 2>,                              \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qsmem)); \
+        cudaFuncSetAttribute(f4_quant_kernel<false, BKV, NKV, 2>,                             \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qsmem)); \
+        set = true;                                                                           \
+      }                                                                                       \
+      if (static_mode)                                                                        \
+        f4_quant_kernel<true, BKV, NKV, 2><<<grid, 256, qsmem, s>>>(x, codes, rowsum, st, g); \
+      else                                                                                    \
+        f4_quant_kernel<false, BKV, NKV, 2><<<grid, 256, qsmem, s>>>(x, codes, rowsum, st, g); \
+    } else if (static_mode) {                                                                 \
       f4_quant_kernel<true, BKV, NKV><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);          \
-    else                                                                                      \
+    } else {                                                                                  \
       f4_quant_kernel<false, BKV, NKV><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);         \
+    }                                                                                         \
     return cudaGetLastError();                                                                \
   }
   LANCE_F4Q(64, 1)
