@@ -789,25 +789,40 @@ __global__ void __launch_bounds__(kF4Threads, 1)
       for (int b = 0; b < kF4AccBufs; ++b) mbar_arrive(&acc_empty[b]);
     const bool fast = s_fast != 0;
     const bool k4ok = (g.K & 3) == 0;
+    // k3[p] * float(colsum[p][k]) of a tile's 16 filters into s_ct[buf]; the
+    // next tile's constants and first row sums are fetched one tile ahead so
+    // their global-load latency hides behind the current tile.
+    auto fill_ct = [&](int tt, uint32_t b) {
+      if (tt >= num_tiles) return;
+      const int nn0 = (tt - (tt / nt) * nt) * kF4BN;
+      float* c = s_ct[b];
+      for (int i = threadIdx.x; i < kNP4 * kF4BN; i += 32 * kF4EpiWarps) {
+        const int p = i >> 4, kk = nn0 + (i & 15);
+        c[i] = (kk < g.K) ? __fmul_rn(st->k3[p], static_cast<float>(colsum[p * g.K_pad + kk])) : 0.0f;
+      }
+    };
+    auto row_sums_j0 = [&](int tt, int (&rs)[6]) {
+      const int mm = (tt / nt) * kBM + row;
+      const bool ok = tt < num_tiles && mm < g.M;
+#pragma unroll
+      for (int a = 0; a < 6; ++a) rs[a] = ok ? __ldg(rowsum + static_cast<long long>(6 * a) * g.rs_pitch + mm) : 0;
+    };
+    int rs_cur[6];
+    fill_ct(blockIdx.x, 0);
+    row_sums_j0(blockIdx.x, rs_cur);
     uint32_t grp = 0, lt = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
       const int m0 = (t / nt) * kBM, n0 = (t - (t / nt) * nt) * kF4BN;
       const int m = m0 + row;
       const bool row_ok = m < g.M;
       const int kf0 = n0 + f0;
-      // k3[p] * float(colsum[p][k]) of the tile's 16 filters (double-buffered
-      // by tile parity; one barrier per tile orders it against the readers).
-      float* ct = s_ct[lt & 1u];
-      for (int i = threadIdx.x; i < kNP4 * kF4BN; i += 32 * kF4EpiWarps) {
-        const int p = i >> 4, kk = n0 + (i & 15);
-        ct[i] = (kk < g.K) ? __fmul_rn(st->k3[p], static_cast<float>(colsum[p * g.K_pad + kk])) : 0.0f;
-      }
+      // s_ct[lt & 1] was written during the previous tile (or the prologue);
+      // after this barrier every thread is done with tile lt - 1, so the other
+      // buffer can take the next tile's constants.
       named_bar_sync(2, 32 * kF4EpiWarps);
+      float* ct = s_ct[lt & 1u];
+      fill_ct(t + gridDim.x, (lt + 1) & 1u);
       float2 S[16][2];  // S[4i + b][filter pair]
-      int rs_cur[6];
-#pragma unroll
-      for (int a = 0; a < 6; ++a)
-        rs_cur[a] = row_ok ? __ldg(rowsum + static_cast<long long>(6 * a) * g.rs_pitch + m) : 0;
 #pragma unroll
       for (int j = 0; j < 6; ++j, ++grp) {
         float rterm[6];
@@ -817,6 +832,8 @@ __global__ void __launch_bounds__(kF4Threads, 1)
 #pragma unroll
           for (int a = 0; a < 6; ++a)
             rs_cur[a] = row_ok ? __ldg(rowsum + static_cast<long long>(6 * a + j + 1) * g.rs_pitch + m) : 0;
+        } else {  // ... and across the tile boundary: the next tile's first j-group
+          row_sums_j0(t + gridDim.x, rs_cur);
         }
         const uint32_t buf = grp % kF4AccBufs;
         mbar_wait(&acc_full[buf], (grp / kF4AccBufs) & 1u);
