@@ -28,6 +28,17 @@
 
 namespace lance_dev {
 
+// Dynamic shared-memory opt-in is per device: remember it per device ordinal.
+static inline bool lance_attr_once(bool (&done)[64]) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return true;  // always (re)apply outside the table
+  if (done[dev]) return false;
+  done[dev] = true;
+  return true;
+}
+
+
 constexpr int kNP4 = 36;
 constexpr float kC6 = 1.0f / 6.0f, kC12 = 1.0f / 12.0f, kC24 = 1.0f / 24.0f;
 
@@ -1017,11 +1028,11 @@ cudaError_t launch_f4_range(const float* x, float* partials, int grid, LanceDevS
   const int d = f4_async_depth();
   if (d == 2 || d == 4) {
     const size_t smem = static_cast<size_t>(8) * d * 24 * 32 * sizeof(float);
-    static bool set = false;
-    if (!set) {
+    static bool set_dev[64] = {};
+    if (lance_attr_once(set_dev)) {
       cudaFuncSetAttribute(f4_range_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 2 * 24 * 32 * 4);
       cudaFuncSetAttribute(f4_range_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4 * 24 * 32 * 4);
-      set = true;
+
     }
     if (d == 2)
       f4_range_kernel<2><<<grid, 256, smem, s>>>(x, partials, st, g);
@@ -1045,13 +1056,13 @@ cudaError_t launch_f4_quant(const float* x, uint8_t* codes, int32_t* rowsum,
 #define LANCE_F4Q(BKV, NKV)                                                                   \
   if ((NKV == 0) || (g.bk == BKV && g.nk == NKV)) {                                           \
     if (qd == 2) {                                                                            \
-      static bool set = false;                                                                \
-      if (!set) {                                                                             \
+      static bool set_dev[64] = {};                                                           \
+      if (lance_attr_once(set_dev)) {                                                         \
         cudaFuncSetAttribute(f4_quant_kernel<true, BKV, NKV, 2>,                              \
                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qsmem)); \
         cudaFuncSetAttribute(f4_quant_kernel<false, BKV, NKV, 2>,                             \
                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qsmem)); \
-        set = true;                                                                           \
+                                                                                          \
       }                                                                                       \
       if (static_mode)                                                                        \
         f4_quant_kernel<true, BKV, NKV, 2><<<grid, 256, qsmem, s>>>(x, codes, rowsum, st, g); \

@@ -27,6 +27,17 @@
 
 namespace lance_dev {
 
+// Dynamic shared-memory opt-in is per device: remember it per device ordinal.
+static inline bool lance_attr_once(bool (&done)[64]) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return true;  // always (re)apply outside the table
+  if (done[dev]) return false;
+  done[dev] = true;
+  return true;
+}
+
+
 // Warp work item: (img, ti, tile segment, channel chunk).
 struct StripItem {
   int img, ti, tj0, tj1, ch;
@@ -918,11 +929,11 @@ cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceD
     const size_t smem = static_cast<size_t>(8) * async_depth * 8 * 32 * sizeof(float2);
 #define LANCE_K0_ASYNC_CASE(DV)                                                                   \
     if (async_depth == DV) {                                                                     \
-      static bool set = false;                                                                   \
-      if (!set) {                                                                                \
+      static bool set_dev[64] = {};                                                              \
+      if (lance_attr_once(set_dev)) {                                                            \
         cudaFuncSetAttribute(input_range_async_kernel<DV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                              static_cast<int>(smem));                                            \
-        set = true;                                                                              \
+                                                                                          \
       }                                                                                          \
       input_range_async_kernel<DV><<<grid, 256, smem, s>>>(x, partials, st, g);                  \
     }
@@ -967,8 +978,8 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
       return e ? std::atoi(e) : 0;
     }();
     const size_t k1_smem = k1_async == 4 ? static_cast<size_t>(8) * 4 * 8 * 32 * sizeof(float2) : 0;
-    static bool k1_attr = false;
-    if (k1_async == 4 && !k1_attr) {  // 64 KB rings: opt every instantiation in once
+    static bool k1_attr_dev[64] = {};
+    if (k1_async == 4 && lance_attr_once(k1_attr_dev)) {  // 64 KB rings: opt every instantiation in once
 #define LANCE_K1_ATTR(BKV, NKV)                                                                   \
       cudaFuncSetAttribute(input_quant_fast_kernel<BKV, NKV, true, false, 4>,                     \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k1_smem)); \
@@ -977,7 +988,7 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
       LANCE_K1_ATTR(64, 1) LANCE_K1_ATTR(128, 1) LANCE_K1_ATTR(128, 2) LANCE_K1_ATTR(128, 3)
       LANCE_K1_ATTR(128, 4) LANCE_K1_ATTR(64, 3) LANCE_K1_ATTR(64, 5)
 #undef LANCE_K1_ATTR
-      k1_attr = true;
+
     }
 #define LANCE_K1_FAST(BKV, NKV)                                                          \
   if (g.a_bk == BKV && g.a_nk == NKV) {                                                  \
