@@ -301,6 +301,10 @@ __device__ __forceinline__ void f4_cp_async4(float* sdst, const float* gsrc, boo
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(gsrc), "r"(valid ? 4 : 0)
                : "memory");
 }
+__device__ __forceinline__ void f4_cp_async4_sz(float* sdst, const float* gsrc, uint32_t src_bytes) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(gsrc), "r"(src_bytes) : "memory");
+}
 __device__ __forceinline__ void f4_cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void f4_cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -311,16 +315,17 @@ __device__ __forceinline__ void f4_ring_issue(float* ring, int lane, const float
                                               const F4Geom& g, const F4Strip& sp, int t) {
   float* slot = ring + (t % D) * 24 * 32;
   if (t < sp.tj1) {
+    // Zero-fill copies read nothing at size 0: the address is passed as is
+    // and only the size is predicated (no pointer selects on the hot path).
 #pragma unroll
     for (int cc = 0; cc < 4; ++cc) {
       const int xx = 4 * t - g.pad + 2 + cc;
-      const bool colok = sp.cok && xx >= 0 && xx < g.W;
+      const uint32_t colsz = (sp.cok && static_cast<unsigned>(xx) < static_cast<unsigned>(g.W)) ? 4u : 0u;
       const float* p = rowbase + static_cast<long long>(xx) * g.C;
 #pragma unroll
-      for (int a = 0; a < 6; ++a) {
-        const bool ok = colok && ((sp.rowmask >> a) & 1u);
-        f4_cp_async4(slot + (cc * 6 + a) * 32 + lane, ok ? p + a * rowstride : x, ok);
-      }
+      for (int a = 0; a < 6; ++a)
+        f4_cp_async4_sz(slot + (cc * 6 + a) * 32 + lane, p + a * rowstride,
+                        ((sp.rowmask >> a) & 1u) ? colsz : 0u);
     }
   }
   f4_cp_commit();

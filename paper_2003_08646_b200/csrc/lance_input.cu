@@ -403,6 +403,10 @@ __device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc, bool val
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(valid ? 8 : 0)
                : "memory");
 }
+__device__ __forceinline__ void cp_async8_sz(void* sdst, const void* gsrc, uint32_t src_bytes) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(src_bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -738,19 +742,23 @@ __global__ void __launch_bounds__(256, 2) input_range_async_kernel(const float* 
        item < g.num_items; item += stride) {
     const StripItem it = strip_item(g, item, lane);
     const Strip<true> sp(x, g, it);
+    // Zero-fill copies read nothing when their size is 0, so the (possibly
+    // out-of-image) address is passed unconditionally and only the size is
+    // predicated: per-row sizes once per strip, one AND per copy.
+    uint32_t rsz[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) rsz[a] = (sp.rok[a] && sp.c0ok) ? 8u : 0u;
     auto issue = [&](int tj) {  // the 2 new columns of tile tj into slot tj % D
       float2* slot = ring + (tj % D) * 8 * 32;
       if (tj < it.tj1) {
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const int xx = 2 * tj - g.pad + 2 + cc;
-          const bool cok = (xx >= 0) && (xx < g.W);
+          const uint32_t cz = (static_cast<unsigned>(xx) < static_cast<unsigned>(g.W)) ? 0xFFFFFFFFu : 0u;
+          const long long co = static_cast<long long>(xx) * g.C;
 #pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            const bool ok = cok && sp.rok[a] && sp.c0ok;
-            const float* src = ok ? sp.row[a] + static_cast<long long>(xx) * g.C : x;
-            cp_async8(slot + (cc * 4 + a) * 32 + lane, src, ok);
-          }
+          for (int a = 0; a < 4; ++a)
+            cp_async8_sz(slot + (cc * 4 + a) * 32 + lane, sp.row[a] + co, rsz[a] & cz);
         }
       }
       cp_async_commit();  // one group per tile, empty past the strip end
