@@ -89,10 +89,15 @@ LANCE_API uint64_t lance_direct_multiply_count(const lance_conv_spec* spec);
 /* ---------------------------------------------------------------------------
  * Drop-in for lance::lance_gemm(x, w, spec, cfg) -> y (engines.hpp:492-536):
  * HOST buffers in and out, synchronous.  x [N][H][W][C], w [K][3][3][C],
- * y [N][OH][OW][K].  Internally caches one plan per (spec, cfg) per thread.
+ * y [N][OH][OW][K].  Internally caches one plan per (spec, cfg) per thread
+ * (bounded LRU, see lance_host_cache_clear).
  * Pinned (page-locked) host buffers give full-bandwidth copies. */
 LANCE_API int lance_gemm_host(const lance_conv_spec* spec, const lance_config* cfg, const float* x,
                     const float* w, float* y);
+/* The host drop-in keeps a per-thread LRU of layer contexts (at most 16
+ * layers / 8 GiB of device memory; freed at thread exit).  This releases the
+ * calling thread's contexts now. */
+LANCE_API int lance_host_cache_clear(void);
 
 /* ---------------------------------------------------------------------------
  * Device API.  A plan owns the per-layer state: prepared filter codes (K2),

@@ -62,6 +62,7 @@ def lib():
         L.lance_direct_multiply_count.argtypes = [ct.POINTER(CSpec)]
         L.lance_direct_multiply_count.restype = ct.c_uint64
         L.lance_gemm_host.argtypes = [ct.POINTER(CSpec), ct.POINTER(CConfig), P, P, P]
+        L.lance_host_cache_clear.argtypes = []
         L.lance_plan_create.argtypes = [ct.POINTER(CSpec), ct.POINTER(CConfig), ct.c_int,
                                         ct.POINTER(P)]
         L.lance_plan_destroy.argtypes = [P]
@@ -98,6 +99,7 @@ def lib():
 EXPORTED = [
     "lance_abi_version", "lance_status_string", "lance_last_error", "lance_validate",
     "lance_winograd_multiply_count", "lance_direct_multiply_count", "lance_gemm_host",
+    "lance_host_cache_clear",
     "lance_plan_create", "lance_plan_destroy", "lance_plan_device_bytes",
     "lance_plan_set_filters", "lance_plan_forward", "lance_plan_forward_static",
     "lance_plan_set_epilogue", "lance_plan_sync", "lance_plan_get_params",

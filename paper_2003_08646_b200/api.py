@@ -143,8 +143,14 @@ def uniform_floats(count: int, seed: int) -> np.ndarray:
 
 
 def _host_f32(a, shape, name):
+    """check_layer's dims check (engines.hpp:84-91): a 4-D array must have
+    exactly the spec's shape (an NCHW array or a [K,C,3,3] filter bank with the
+    right element count is rejected); a flat 1-D array of the right size is
+    accepted as raw NHWC / KRSC storage."""
     a = np.ascontiguousarray(a, dtype=np.float32)
-    if a.size != int(np.prod(shape)):
+    if a.ndim == 1 and a.size == int(np.prod(shape)):
+        return a
+    if tuple(a.shape) != tuple(shape):
         raise LanceError(f"{name} dims do not match spec")
     return a
 
@@ -227,8 +233,11 @@ class LanceConv:
     def _check_tensor(self, t, shape, name):
         import torch
         if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32
-                and t.is_contiguous() and t.numel() == int(np.prod(shape))):
+                and t.is_contiguous()):
             raise LanceError(f"{name} must be a contiguous float32 CUDA tensor of shape {shape}")
+        # exact shape (engines.hpp:84-91); a flat 1-D tensor is raw NHWC / KRSC storage
+        if not (tuple(t.shape) == tuple(shape) or (t.dim() == 1 and t.numel() == int(np.prod(shape)))):
+            raise LanceError(f"{name} dims do not match spec: got {tuple(t.shape)}, expected {tuple(shape)}")
 
     def set_filters(self, w, stream=None):
         """K2: G g G^T + per-position quantisation (engines.hpp:215-233)."""

@@ -18,12 +18,16 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_build")
 LIB = os.path.join(OUT_DIR, "liblance_b200.so")
-SOURCES = ["lance_input.cu", "lance_band.cu", "lance_filter.cu", "lance_gemm.cu", "lance_f4.cu", "lance_stack.cu", "lance_abi.cu"]
+SOURCES = ["lance_input.cu", "lance_filter.cu", "lance_gemm.cu", "lance_f4.cu", "lance_stack.cu", "lance_abi.cu"]
 HEADERS = ["lance_common.cuh", "lance_kernels.cuh", "lance_ptx.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-DLANCE_JMAJOR=" + os.environ.get("LANCE_JMAJOR", "0"), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
          "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "-I" + os.path.join(ROOT, "include")]
+# LANCE_PROFILING=1: honour the experiment / A-B environment switches
+# (lance_knob) -- tools/*.sh only; release builds ignore the environment.
+if os.environ.get("LANCE_PROFILING"):
+    FLAGS.append("-DLANCE_PROFILING")
 
 
 def _stale() -> bool:
@@ -39,15 +43,19 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     os.makedirs(OUT_DIR, exist_ok=True)
-    objs = []
-    for src in SOURCES:
-        obj = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
+    objs = [os.path.join(OUT_DIR, src.replace(".cu", ".o")) for src in SOURCES]
+
+    def compile_one(src_obj):
+        src, obj = src_obj
         cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
-        objs.append(obj)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        list(ex.map(compile_one, zip(SOURCES, objs)))
     tmp = LIB + ".tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
     subprocess.run(cmd, check=True)

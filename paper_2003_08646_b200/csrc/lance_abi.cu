@@ -10,6 +10,8 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
+#include <list>
 #include <map>
 #include <mutex>
 #include <random>
@@ -40,6 +42,51 @@ int cuda_fail(cudaError_t e, const char* where) {
     cudaError_t e_ = (call);                                     \
     if (e_ != cudaSuccess) return cuda_fail(e_, #call);          \
   } while (0)
+
+}  // namespace
+
+// Experiment / A-B switches (tools/*.sh): honoured only by LANCE_PROFILING
+// builds; a release library ignores the environment and uses the defaults.
+namespace lance_dev {
+int lance_knob(const char* name, int def) {
+#ifdef LANCE_PROFILING
+  if (const char* e = std::getenv(name)) return std::atoi(e);
+#else
+  (void)name;
+#endif
+  return def;
+}
+
+cudaError_t ensure_smem_attr(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{dev, fn}];
+  if (have >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
+int current_sm_count() {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int sms = 148;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+  cache[dev] = sms;
+  return sms;
+}
+}  // namespace lance_dev
+
+namespace {
 
 int out_h(const lance_conv_spec& s) { return s.h + 2 * s.pad - 3 + 1; }
 int out_w(const lance_conv_spec& s) { return s.w + 2 * s.pad - 3 + 1; }
@@ -113,25 +160,6 @@ int make_rowsum_map(CUtensorMap* map, void* base, long long rows, long long pitc
   return LANCE_OK;
 }
 
-// x viewed as [N][H][W][C] fp32; box = chb channels x box_w pixels x 1 row x
-// 1 image.  Out-of-bounds pixels / rows read as 0 (the reference's zero pad).
-int make_input_map(CUtensorMap* map, const float* x, const lance_conv_spec& s, const BandGeom& b) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn) return fail(LANCE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(s.c), static_cast<cuuint64_t>(s.w),
-                              static_cast<cuuint64_t>(s.h), static_cast<cuuint64_t>(s.n)};
-  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(s.c) * 4,
-                                 static_cast<cuuint64_t>(s.c) * 4 * s.w,
-                                 static_cast<cuuint64_t>(s.c) * 4 * s.w * s.h};
-  const cuuint32_t box[4] = {static_cast<cuuint32_t>(b.chb), static_cast<cuuint32_t>(b.box_w), 1, 1};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims, strides,
-                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(LANCE_ERR_CUDA, "cuTensorMapEncodeTiled (input) failed: " + std::to_string(r));
-  return LANCE_OK;
-}
-
 }  // namespace
 
 struct lance_plan_s {
@@ -147,10 +175,6 @@ struct lance_plan_s {
   int sm_count = 148;
   int range_grid = 1, filter_grid = 1;
   InGeom in_geom{};
-  BandGeom band{};
-  bool band_k0 = false, band_k1 = false;  // which stages use the band kernels (LANCE_BAND_K0/K1)
-  CUtensorMap tmX{};
-  const float* tmX_ptr = nullptr;
   FilterGeom f_geom{};
   GemmGeom gemm_geom{};
   bool vec2 = false;
@@ -190,6 +214,7 @@ struct DeviceGuard {
 };
 
 void free_plan(lance_plan_s* p) {
+#ifdef LANCE_PROFILING
   if (p->gemm_geom.trace != nullptr) {
     if (const char* path = std::getenv("LANCE_GEMM_TRACE")) {
       std::vector<unsigned long long> h(500000);
@@ -202,8 +227,9 @@ void free_plan(lance_plan_s* p) {
         }
       }
     }
-    cudaFree(p->gemm_geom.trace);
   }
+#endif
+  cudaFree(p->gemm_geom.trace);
   for (cudaEvent_t e : p->events) cudaEventDestroy(e);
   p->events.clear();
   cudaFree(p->codes_a);
@@ -337,8 +363,8 @@ int lance_plan_create_tiled(const lance_conv_spec* spec, const lance_config* cfg
                                       ((out_w(*spec) + 1) / 2) + kBM - 1) / kBM;
     if (p->BN == 64 && row_blocks * ((spec->k + 63) / 64) < p->sm_count) p->BN = 32;
   }
-  if (const char* e = std::getenv("LANCE_GEMM_BN")) {
-    const int v = std::atoi(e);
+  {
+    const int v = lance_knob("LANCE_GEMM_BN", 0);
     if (v == 16 || v == 32 || v == 64) p->BN = v;
   }
   p->K_pad = round_up(spec->k, p->BN);
@@ -379,57 +405,6 @@ int lance_plan_create_tiled(const lance_conv_spec* spec, const lance_config* cfg
   }
   g.granularity = cfg->granularity;
   p->range_grid = input_range_grid(g, p->sm_count);
-  {
-    // v4 band kernels: C % 4 == 0 (16-byte TMA strides), a box row of 2 TW + 2
-    // pixels (<= 256), a channel band of 64/128/256 (a multiple of BK that
-    // divides C_pad) with TW * chb / 4 <= 512 threads, and the ring + staging
-    // within shared memory.
-    BandGeom& b = p->band;
-    b.enabled = 0;
-    const char* off = std::getenv("LANCE_BAND_OFF");
-    if (!(off && std::atoi(off)) && spec->c % 4 == 0) {
-      for (int chb : {256, 128, 64}) {
-        if (p->C_pad % chb || chb % p->BK) continue;
-        const int qpt = chb / 4;
-        if (qpt > 256) continue;
-        b.chb = chb;
-        b.nbc = p->C_pad / chb;
-        b.nkb = chb / p->BK;
-        // Column slices of <= 256 / qpt tiles (one thread per tile x channel quad).
-        const int maxt = 256 / qpt;
-        b.ncs = (p->TW + maxt - 1) / maxt;
-        b.tws = (p->TW + b.ncs - 1) / b.ncs;
-        b.box_w = 2 * b.tws + 2;
-        if (b.box_w > 256) continue;
-        b.slot_bytes = b.box_w * chb * 4;
-        b.run_bytes = b.tws * p->BK;
-        b.stg_bytes = 16 * b.nkb * b.run_bytes;
-        // Ring depth: as many row slots as two CTAs per SM can hold (the
-        // loader runs ring - 4 rows ahead of the compute warps), <= 16.
-        b.ring = 16;  // even: slots are used in row pairs
-        while (b.ring > 6 &&
-               2 * (size_t(b.ring) * b.slot_bytes + 2 * size_t(b.stg_bytes) + 2048) > 225 * 1024)
-          b.ring -= 2;
-        if (2 * (size_t(b.ring) * b.slot_bytes + 2 * size_t(b.stg_bytes) + 2048) > 225 * 1024) continue;
-        // Tile rows per item: enough items for ~4 waves of 2 CTAs per SM.
-        const long long per = static_cast<long long>(spec->n) * b.nbc * b.ncs;
-        b.nseg = 1;
-        while (per * b.nseg < 8LL * p->sm_count && b.nseg < p->TH) ++b.nseg;
-        b.trs = (p->TH + b.nseg - 1) / b.nseg;
-        b.nseg = (p->TH + b.trs - 1) / b.trs;
-        b.items = per * b.nseg;
-        const size_t smem = size_t(b.ring) * b.slot_bytes + 2 * size_t(b.stg_bytes) + 128;
-        const int per_sm = 2;  // ~120 registers x 256 threads
-        (void)smem;
-        b.grid = static_cast<int>(std::min<long long>(b.items, static_cast<long long>(per_sm) * p->sm_count));
-        b.enabled = 1;
-        break;
-      }
-    }
-    if (b.enabled) p->range_grid = std::max(p->range_grid, b.grid);
-    if (const char* e = std::getenv("LANCE_BAND_K0")) p->band_k0 = std::atoi(e) != 0;
-    if (const char* e = std::getenv("LANCE_BAND_K1")) p->band_k1 = std::atoi(e) != 0;
-  }
   p->small_acc = static_cast<double>(spec->c) * ((1 << cfg->bits_i) - 1) *
                      ((1 << cfg->bits_w) - 1) < 16777216.0;  // every accumulator < 2^24 (exact fp32 bit trick)
 
@@ -456,28 +431,24 @@ int lance_plan_create_tiled(const lance_conv_spec* spec, const lance_config* cfg
   gg.num_kchunks = p->C_pad / p->BK;
   gg.num_n_tiles = p->K_pad / p->BN;
   gg.stages = 0;  // chosen by the launcher
-  gg.exp = 0;
-  if (const char* e = std::getenv("LANCE_GEMM_EXP")) gg.exp = std::atoi(e);
+  gg.exp = lance_knob("LANCE_GEMM_EXP", 0);
   gg.trace = nullptr;
   gg.b_resident = 0;
   gg.rs_pitch = static_cast<int>(p->rs_pitch);
   // Row sums: in the GEMM's spare warps when its stages are 64-byte K chunks
   // (their shared-memory reads then cost the SS-UMMA little), else in K1.
   // LANCE_RS_GEMM overrides.
-  gg.rs_warps = (p->BK <= 64) ? 1 : 0;
-  if (const char* e = std::getenv("LANCE_RS_GEMM")) gg.rs_warps = std::atoi(e) ? 1 : 0;
+  gg.rs_warps = lance_knob("LANCE_RS_GEMM", p->BK <= 64 ? 1 : 0) ? 1 : 0;
   p->in_geom.rowsums = gg.rs_warps ? 0 : 1;
   // One thread sustains ~1 bulk copy per ~460 SM cycles from L2 whatever its
   // size (scratch/l2_ingress_bench.cu), so each stage's copies are split over
   // several producer lanes (LANCE_GEMM_LANES).  Measured in the GEMM, more
   // lanes are slower (SS-UMMA already saturates shared-memory bandwidth), so 1.
-  gg.ld_lanes = 1;
-  if (const char* e = std::getenv("LANCE_GEMM_LANES")) {
-    const int v = std::atoi(e);
-    gg.ld_lanes = (v == 1 || v == 2 || v == 4 || v == 8) ? v : 4;
+  {
+    const int v = lance_knob("LANCE_GEMM_LANES", 1);
+    gg.ld_lanes = (v == 1 || v == 2 || v == 4 || v == 8) ? v : 1;
   }
-  p->in_geom.rev_items = 1;
-  if (const char* e = std::getenv("LANCE_K1_REVERSE")) p->in_geom.rev_items = std::atoi(e) ? 1 : 0;
+  p->in_geom.rev_items = lance_knob("LANCE_K1_REVERSE", 1) ? 1 : 0;
 
   // Operand images cover whole 128-row blocks; rows >= M stay code 0.
   const size_t codes_a_bytes = static_cast<size_t>(16) * ((p->M + kBM - 1) / kBM * kBM) * p->C_pad;
@@ -508,7 +479,7 @@ int lance_plan_create_tiled(const lance_conv_spec* spec, const lance_config* cfg
     delete p;
     return cuda_fail(e, "plan init");
   }
-  if (std::getenv("LANCE_GEMM_TRACE") != nullptr &&
+  if (lance_knob("LANCE_GEMM_TRACE", 0) != 0 &&
       (rc = dev_alloc(p, &p->gemm_geom.trace, sizeof(unsigned long long) * 500000))) {
     free_plan(p);
     delete p;
@@ -566,11 +537,9 @@ static int create_f4(lance_plan_s* p, const lance_conv_spec* spec, const lance_c
   g.stages = 0;
   g.units = 0;
   g.b_resident = 0;
-  g.exp = 0;
-  if (const char* e = std::getenv("LANCE_F4_EXP")) g.exp = std::atoi(e);
-  g.ld_lanes = 2;
-  if (const char* e = std::getenv("LANCE_F4_LANES")) {
-    const int v = std::atoi(e);
+  g.exp = lance_knob("LANCE_F4_EXP", 0);
+  {
+    const int v = lance_knob("LANCE_F4_LANES", 2);
     g.ld_lanes = (v == 1 || v == 2 || v == 4) ? v : 2;
   }
   // Warp strips along tile rows: whole rows unless that leaves too few warps
@@ -708,36 +677,16 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
       prm.scale[i] = static_params[i].scale;
     }
     LANCE_CUDA(launch_static_params(p->state, prm, p->spec.c, s));
-  } else if (p->band.enabled && p->band_k0) {
-    if (p->tmX_ptr != x_dev) {
-      int rc = make_input_map(&p->tmX, x_dev, p->spec, p->band);
-      if (rc) return rc;
-      p->tmX_ptr = x_dev;
-    }
-    LANCE_CUDA(launch_band(&p->tmX, p->codes_a, p->rowsum, p->partials, p->state, p->in_geom,
-                           p->band, 0, 0, s));
   } else {
     LANCE_CUDA(launch_input_range(x_dev, p->partials, p->range_grid, p->state, p->in_geom,
                                   p->vec2, s));
   }
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[1], s));
-  if (p->band.enabled && p->band_k1) {
-    if (p->tmX_ptr != x_dev) {
-      int rc = make_input_map(&p->tmX, x_dev, p->spec, p->band);
-      if (rc) return rc;
-      p->tmX_ptr = x_dev;
-    }
-    if (p->band.nbc > 1 || p->band.chb == 256)  // row sums accumulate atomically
-      LANCE_CUDA(cudaMemsetAsync(p->rowsum, 0, sizeof(int32_t) * 16 * p->rs_pitch, s));
-    LANCE_CUDA(launch_band(&p->tmX, p->codes_a, p->rowsum, p->partials, p->state, p->in_geom,
-                           p->band, 1, static_params != nullptr, s));
-  } else {
-    if (p->in_geom.nchunks > 1)
-      LANCE_CUDA(cudaMemsetAsync(p->rowsum, 0, sizeof(int32_t) * 16 * p->rs_pitch, s));
-    LANCE_CUDA(launch_input_quant(x_dev, p->codes_a, p->rowsum, p->state, p->in_geom, p->vec2,
-                                  static_params != nullptr, s));
-  }
+  if (p->in_geom.nchunks > 1 && p->in_geom.rowsums)
+    LANCE_CUDA(cudaMemsetAsync(p->rowsum, 0, sizeof(int32_t) * 16 * p->rs_pitch, s));
+  LANCE_CUDA(launch_input_quant(x_dev, p->codes_a, p->rowsum, p->state, p->in_geom, p->vec2,
+                                static_params != nullptr, s));
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[2], s));
   LANCE_CUDA(launch_gemm(p->codes_a, p->codes_w, &p->tmR, p->rowsum, p->BK, p->BN, p->small_acc, p->colsum, p->state, y_dev,
@@ -881,10 +830,60 @@ struct HostCtx {
   lance_plan_t plan = nullptr;
   float *x = nullptr, *w = nullptr, *y = nullptr;
   cudaStream_t stream = nullptr;
+  size_t bytes = 0;  // plan + staging device bytes
 };
+
+void release(HostCtx& c) {
+  if (c.stream) cudaStreamSynchronize(c.stream);
+  lance_plan_destroy(c.plan);
+  cudaFree(c.x);
+  cudaFree(c.w);
+  cudaFree(c.y);
+  if (c.stream) cudaStreamDestroy(c.stream);
+  c = HostCtx{};
+}
+
 using Key = std::tuple<int, int, int, int, int, int, int, int, int, int, int>;
-thread_local std::map<Key, HostCtx> g_host_ctx;
+
+// Per-thread LRU of host drop-in contexts (plan + staging buffers), bounded in
+// entries and device bytes; the least recently used layers are released
+// first and everything is freed when the thread exits.
+struct HostCache {
+  static constexpr size_t kMaxEntries = 16;
+  static constexpr size_t kMaxBytes = size_t(8) << 30;
+  std::list<std::pair<Key, HostCtx>> lru;  // front = most recent
+  size_t bytes = 0;
+  ~HostCache() { clear(); }
+  void clear() {
+    for (auto& kv : lru) release(kv.second);
+    lru.clear();
+    bytes = 0;
+  }
+  HostCtx* find(const Key& k) {
+    for (auto it = lru.begin(); it != lru.end(); ++it)
+      if (it->first == k) {
+        lru.splice(lru.begin(), lru, it);
+        return &lru.front().second;
+      }
+    return nullptr;
+  }
+  // Make room for an entry of `need` bytes.
+  void evict_for(size_t need) {
+    while (!lru.empty() && (lru.size() >= kMaxEntries || bytes + need > kMaxBytes)) {
+      HostCtx& c = lru.back().second;
+      bytes -= std::min(bytes, c.bytes);
+      release(c);
+      lru.pop_back();
+    }
+  }
+};
+thread_local HostCache g_host_cache;
 }  // namespace
+
+int lance_host_cache_clear(void) {
+  g_host_cache.clear();
+  return LANCE_OK;
+}
 
 int lance_gemm_host(const lance_conv_spec* spec, const lance_config* cfg, const float* x,
                     const float* w, float* y) {
@@ -905,28 +904,28 @@ int lance_gemm_host_tiled(const lance_conv_spec* spec, const lance_config* cfg, 
   }
   const Key key{dev, spec->n, spec->c, spec->h, spec->w, spec->k, spec->pad, cfg->bits_w,
                 cfg->bits_i, cfg->granularity, tile_m};
-  HostCtx& ctx = g_host_ctx[key];
   const size_t xb = sizeof(float) * size_t(spec->n) * spec->h * spec->w * spec->c;
   const size_t wb = sizeof(float) * size_t(spec->k) * 9 * spec->c;
   const size_t yb = sizeof(float) * size_t(spec->n) * out_h(*spec) * out_w(*spec) * spec->k;
-  if (!ctx.plan) {
-    if ((rc = lance_plan_create_tiled(spec, cfg, tile_m, dev, &ctx.plan))) {
-      g_host_ctx.erase(key);
-      return rc;
-    }
-    cudaError_t e = cudaMalloc(&ctx.x, xb);
-    if (e == cudaSuccess) e = cudaMalloc(&ctx.w, wb);
-    if (e == cudaSuccess) e = cudaMalloc(&ctx.y, yb);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx.stream, cudaStreamNonBlocking);
+  HostCtx* cp = g_host_cache.find(key);
+  if (!cp) {
+    g_host_cache.evict_for(xb + wb + yb);
+    HostCtx c;
+    if ((rc = lance_plan_create_tiled(spec, cfg, tile_m, dev, &c.plan))) return rc;
+    cudaError_t e = cudaMalloc(&c.x, xb);
+    if (e == cudaSuccess) e = cudaMalloc(&c.w, wb);
+    if (e == cudaSuccess) e = cudaMalloc(&c.y, yb);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
-      lance_plan_destroy(ctx.plan);
-      cudaFree(ctx.x);
-      cudaFree(ctx.w);
-      cudaFree(ctx.y);
-      g_host_ctx.erase(key);
+      release(c);
       return cuda_fail(e, "lance_gemm host staging");
     }
+    c.bytes = lance_plan_device_bytes(c.plan) + xb + wb + yb;
+    g_host_cache.lru.emplace_front(key, c);
+    g_host_cache.bytes += c.bytes;
+    cp = &g_host_cache.lru.front().second;
   }
+  HostCtx& ctx = *cp;
   LANCE_CUDA(cudaMemcpyAsync(ctx.w, w, wb, cudaMemcpyHostToDevice, ctx.stream));
   LANCE_CUDA(cudaMemcpyAsync(ctx.x, x, xb, cudaMemcpyHostToDevice, ctx.stream));
   if ((rc = lance_plan_set_filters(ctx.plan, ctx.w, ctx.stream))) return rc;

@@ -28,17 +28,6 @@
 
 namespace lance_dev {
 
-// Dynamic shared-memory opt-in is per device: remember it per device ordinal.
-static inline bool lance_attr_once(bool (&done)[64]) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return true;  // always (re)apply outside the table
-  if (done[dev]) return false;
-  done[dev] = true;
-  return true;
-}
-
-
 constexpr int kNP4 = 36;
 constexpr float kC6 = 1.0f / 6.0f, kC12 = 1.0f / 12.0f, kC24 = 1.0f / 24.0f;
 
@@ -1013,18 +1002,12 @@ int f4_range_grid(const F4Geom& g, int sm_count) {
 }
 
 static int f4_async_depth() {
-  static const int d = [] {
-    const char* e = std::getenv("LANCE_F4_ASYNC");
-    return e ? std::atoi(e) : 2;  // measured: 2 beats 0 (no lookahead) and 4
-  }();
+  static const int d = lance_knob("LANCE_F4_ASYNC", 2);  // measured: 2 beats 0 (no lookahead) and 4
   return d;
 }
 
 static int f4_quant_depth() {
-  static const int d = [] {
-    const char* e = std::getenv("LANCE_F4Q_ASYNC");
-    return e ? std::atoi(e) : 2;  // measured: -5 % on the 56x56 layer
-  }();
+  static const int d = lance_knob("LANCE_F4Q_ASYNC", 2);  // measured: -5 % on the 56x56 layer
   return d;
 }
 
@@ -1033,12 +1016,9 @@ cudaError_t launch_f4_range(const float* x, float* partials, int grid, LanceDevS
   const int d = f4_async_depth();
   if (d == 2 || d == 4) {
     const size_t smem = static_cast<size_t>(8) * d * 24 * 32 * sizeof(float);
-    static bool set_dev[64] = {};
-    if (lance_attr_once(set_dev)) {
-      cudaFuncSetAttribute(f4_range_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 2 * 24 * 32 * 4);
-      cudaFuncSetAttribute(f4_range_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4 * 24 * 32 * 4);
-
-    }
+    const cudaError_t e = d == 2 ? ensure_smem_attr(reinterpret_cast<const void*>(f4_range_kernel<2>), smem)
+                                 : ensure_smem_attr(reinterpret_cast<const void*>(f4_range_kernel<4>), smem);
+    if (e != cudaSuccess) return e;
     if (d == 2)
       f4_range_kernel<2><<<grid, 256, smem, s>>>(x, partials, st, g);
     else
@@ -1061,14 +1041,10 @@ cudaError_t launch_f4_quant(const float* x, uint8_t* codes, int32_t* rowsum,
 #define LANCE_F4Q(BKV, NKV)                                                                   \
   if ((NKV == 0) || (g.bk == BKV && g.nk == NKV)) {                                           \
     if (qd == 2) {                                                                            \
-      static bool set_dev[64] = {};                                                           \
-      if (lance_attr_once(set_dev)) {                                                         \
-        cudaFuncSetAttribute(f4_quant_kernel<true, BKV, NKV, 2>,                              \
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qsmem)); \
-        cudaFuncSetAttribute(f4_quant_kernel<false, BKV, NKV, 2>,                             \
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qsmem)); \
-                                                                                          \
-      }                                                                                       \
+      const cudaError_t ea = static_mode                                                      \
+          ? ensure_smem_attr(reinterpret_cast<const void*>(f4_quant_kernel<true, BKV, NKV, 2>), qsmem)  \
+          : ensure_smem_attr(reinterpret_cast<const void*>(f4_quant_kernel<false, BKV, NKV, 2>), qsmem); \
+      if (ea != cudaSuccess) return ea;                                                       \
       if (static_mode)                                                                        \
         f4_quant_kernel<true, BKV, NKV, 2><<<grid, 256, qsmem, s>>>(x, codes, rowsum, st, g); \
       else                                                                                    \
@@ -1108,10 +1084,7 @@ static cudaError_t launch_f4_gemm_t(const uint8_t* codes_a, const uint8_t* codes
   using Cfg = F4Cfg<BK>;
   F4Geom g = g0;
   const size_t kLimit = 220 * 1024;
-  int sms = 148;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = current_sm_count();
   const int nt = g.num_n_tiles;
   const long long tiles = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * nt;
   // Units per stage: the largest divisor of a j-group's 6 * nk units whose A
@@ -1119,8 +1092,8 @@ static cudaError_t launch_f4_gemm_t(const uint8_t* codes_a, const uint8_t* codes
   int U = 1;
   for (int u = 1; u <= 6 * g.nk; ++u)
     if ((6 * g.nk) % u == 0 && u * Cfg::kABytes <= 32 * 1024) U = u;
-  if (const char* e = std::getenv("LANCE_F4_UNITS")) {
-    const int v = std::atoi(e);
+  {
+    const int v = lance_knob("LANCE_F4_UNITS", 0);
     if (v >= 1 && (6 * g.nk) % v == 0) U = v;
   }
   g.units = U;
@@ -1130,7 +1103,7 @@ static cudaError_t launch_f4_gemm_t(const uint8_t* codes_a, const uint8_t* codes
   const size_t b_bytes = static_cast<size_t>(kNP4) * g.nk * Cfg::kBBytes;
   const int res_grid = (sms / nt) * nt;
   g.b_resident = (b_bytes <= 80 * 1024 && res_grid >= 1) ? 1 : 0;
-  if (const char* e = std::getenv("LANCE_F4_BRES")) g.b_resident = g.b_resident && std::atoi(e) != 0;
+  g.b_resident = g.b_resident && lance_knob("LANCE_F4_BRES", 1) != 0;
   const size_t stage_bytes = static_cast<size_t>(U) * (Cfg::kABytes + (g.b_resident ? 0 : Cfg::kBBytes));
   const size_t fixed = 1024 + (g.b_resident ? b_bytes : 0) + 4 * 32 * 64 * sizeof(float);
   int stages = 16;
@@ -1138,13 +1111,9 @@ static cudaError_t launch_f4_gemm_t(const uint8_t* codes_a, const uint8_t* codes
   g.stages = stages;
   const size_t smem = fixed + stages * stage_bytes;
   if (smem > kLimit) return cudaErrorInvalidValue;
-  static bool configured[64] = {};
-  if (dev < 0 || dev >= 64 || !configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(f4_gemm_kernel<BK, SMALL, DUMP>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kLimit));
+  {
+    const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(f4_gemm_kernel<BK, SMALL, DUMP>), kLimit);
     if (e != cudaSuccess) return e;
-    if (dev >= 0 && dev < 64) configured[dev] = true;
   }
   const int cap = g.b_resident ? res_grid : sms;
   const int grid = static_cast<int>(tiles < cap ? tiles : cap);

@@ -67,32 +67,36 @@ struct GemmCfg {
   static constexpr uint32_t kRsBytes = 16 * kBM * 4;  // row sums of one tile [16][128] i32
   // Output staging: per lane quadrant 32 tiles x 2 pixels x BN filters fp32.
   static constexpr uint32_t kOutBytes = 4 * 32 * 2 * BN * 4;
+  // Third affine term k3[p] * colsum[p][k] of the tile's filters, two tile buffers.
+  static constexpr uint32_t kCtBytes = 2 * 16 * BN * 4;
   static constexpr size_t kFixed =
-      1024 /*align*/ + 2 * kRsBytes + kOutBytes + 32 * 8 /*barriers, holder*/;
+      1024 /*align*/ + 2 * kRsBytes + kOutBytes + kCtBytes + 32 * 8 /*barriers, holder*/;
 };
 
 // b_res: the whole B operand of the (single) filter tile stays resident in
 // shared memory and stages carry only A.
 template <int BK, int BN>
-__host__ __device__ constexpr size_t gemm_smem_bytes(int stages, int nk, int b_res, int k_pad) {
+__host__ __device__ constexpr size_t gemm_smem_bytes(int stages, int nk, int b_res) {
   return GemmCfg<BK, BN>::kFixed +
          static_cast<size_t>(stages) *
              (b_res ? GemmCfg<BK, BN>::kABytes : GemmCfg<BK, BN>::kStageBytes) +
          (b_res ? static_cast<size_t>(16) * nk * GemmCfg<BK, BN>::kBBytes : 0) +
-         static_cast<size_t>(stages) * 16 + static_cast<size_t>(16) * k_pad * 4;
+         static_cast<size_t>(stages) * 16;
 }
 
 // Epilogue of one j-group for 4 filters (one TMEM x4 load per position).
 // acc[a][i]: accumulator of position p = 4a + j, filter f0 + 4c + i;
-// k1s[a] = k1[p] * 2^126 (fast) or k1[p]; ct_j: cterm row of position j.
+// k1s[a] = k1[p] * 2^126 (fast) or k1[p]; ct_j: the tile's cterm row of
+// position j at this thread's 4 filters (rows of positions 4a + j are 4 * BN apart).
+template <int BN>
 __device__ __forceinline__ void affine_group4(const uint32_t (&acc)[4][4], bool fast,
                                               const float (&k1s)[4], const float (&k4)[4],
                                               const float (&rterm)[4], const float* ct_j,
-                                              int K_pad, float2 (&T0)[2], float2 (&T1)[2]) {
+                                              float2 (&T0)[2], float2 (&T1)[2]) {
   float2 m[4][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
-    const float4 ct = *reinterpret_cast<const float4*>(ct_j + a * 4 * K_pad);
+    const float4 ct = *reinterpret_cast<const float4*>(ct_j + a * 4 * BN);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint32_t d0 = acc[a][2 * h], d1 = acc[a][2 * h + 1];
@@ -153,7 +157,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   constexpr uint32_t kIdesc = umma_idesc_u8(kBM, BN);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ float s_k1[16], s_k2[16], s_k4[16];
+  __shared__ float s_k1[16], s_k2[16], s_k3[16], s_k4[16];
   __shared__ int s_fast;
 
   // 1024-byte aligned base (SWIZZLE_128B atoms), derived by offsetting the
@@ -176,7 +180,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   uint64_t* rs_empty = rs_ready + 8;        // [2]
   uint64_t* b_full = rs_empty + 2;          // [1]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(b_full + 2);
-  float* s_cterm = reinterpret_cast<float*>(tmem_holder + 4);  // [16][K_pad]: k3[p]*colsum[p][k]
+  float* s_cterm = reinterpret_cast<float*>(tmem_holder + 4);  // [2 tiles][16][BN]: k3[p]*colsum[p][k]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = g.num_n_tiles;
@@ -200,12 +204,6 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     fence_barrier_init();
   }
   if (warp < kEpiWarps) {
-    // Third term of affine_term for every filter of the layer.
-    for (int i = threadIdx.x; i < 16 * K_pad; i += 32 * kEpiWarps) {
-      const int p = i / K_pad, kf = i - p * K_pad;
-      const float csum = (kf < g.K) ? static_cast<float>(colsum[i]) : 0.0f;
-      s_cterm[i] = __fmul_rn(st->k3[p], csum);
-    }
     const int e = threadIdx.x;
     if (e < 32) {
       const float k1 = e < 16 ? st->k1[e] : 0.0f;
@@ -214,6 +212,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       if (e < 16) {
         s_k1[e] = fast ? __fmul_rn(k1, kTwo126) : k1;
         s_k2[e] = st->k2[e];
+        s_k3[e] = st->k3[e];
         s_k4[e] = st->k4[e];
       }
       if (e == 0) s_fast = fast ? 1 : 0;
@@ -384,9 +383,25 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     if (lane == 0)
       for (int b = 0; b < NB; ++b) mbar_arrive(&acc_empty[b]);
     const bool fast = s_fast != 0;
+    // Third affine term of a tile's filters, k3[p] * colsum[p][n0 + f]
+    // (lowpgemm.hpp:110-114), into tile buffer b: 16 x BN values, 2 per thread.
+    auto cterm_slice = [&](int t, uint32_t b) {
+      const int n0 = (t % nt) * BN;
+      for (int i = threadIdx.x; i < 16 * BN; i += 32 * kEpiWarps) {
+        const int p = i / BN, kf = n0 + (i - p * BN);
+        const float csum = (kf < g.K) ? static_cast<float>(__ldg(colsum + p * K_pad + kf)) : 0.0f;
+        s_cterm[b * 16 * BN + i] = __fmul_rn(s_k3[p], csum);
+      }
+    };
+    if (static_cast<int>(blockIdx.x) < num_tiles) cterm_slice(blockIdx.x, 0);
     uint32_t grp = 0;
     uint32_t lt = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+      // Slice lt is visible to every epilogue warp after this barrier, and
+      // every warp is done with tile lt - 1, so its buffer takes tile lt + 1.
+      named_bar_sync(6, 32 * kEpiWarps);
+      if (t + static_cast<int>(gridDim.x) < num_tiles) cterm_slice(t + gridDim.x, (lt + 1) & 1u);
+      const float* ct_tile = s_cterm + (lt & 1u) * 16 * BN;
       const int m0 = (t / nt) * kBM, n0 = (t % nt) * BN;
       const int m = m0 + row;
       const bool row_ok = m < g.M;
@@ -514,7 +529,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
           }
           if (g.exp & 1) continue;
           float2 T0[2], T1[2];
-          affine_group4(ac, fast, k1s, k4, rterm, s_cterm + j * K_pad + kf0 + 4 * c, K_pad, T0, T1);
+          affine_group4<BN>(ac, fast, k1s, k4, rterm, ct_tile + j * BN + f0 + 4 * c, T0, T1);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             float2& s00 = S[0][2 * c + h];
@@ -561,33 +576,19 @@ static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
                                  const LanceDevState* st, float* y, int32_t* acc_dump,
                                  const float* bias, int relu, const GemmGeom& g0, cudaStream_t s) {
   GemmGeom g = g0;
-  const int k_pad = g.num_n_tiles * BN;
   const int nk = g.num_kchunks;
   // Resident B: one filter tile whose 16 positions x C_pad images fit in 64 KB.
   const int b_res = (g.num_n_tiles == 1 && 16 * nk * GemmCfg<BK, BN>::kBBytes <= 64 * 1024) ? 1 : 0;
   int stages = 16;
-  while (stages > 2 && gemm_smem_bytes<BK, BN>(stages, nk, b_res, k_pad) > kSmemLimit) --stages;
-  const size_t smem = gemm_smem_bytes<BK, BN>(stages, nk, b_res, k_pad);
+  while (stages > 2 && gemm_smem_bytes<BK, BN>(stages, nk, b_res) > kSmemLimit) --stages;
+  const size_t smem = gemm_smem_bytes<BK, BN>(stages, nk, b_res);
   if (smem > kSmemLimit) return cudaErrorInvalidValue;
   g.b_resident = b_res;
   g.stages = stages;
-  static size_t configured[64] = {};  // dynamic-smem attribute set so far, per device
-  static int sm_count[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64 || configured[dev] < smem) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_epilogue_kernel<BK, BN, SMALL, DUMP>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (dev >= 0 && dev < 64) {
-      configured[dev] = smem;
-      sm_count[dev] = sms;
-    }
-  }
-  const int sms = (dev >= 0 && dev < 64) ? sm_count[dev] : 148;
+  const cudaError_t e =
+      ensure_smem_attr(reinterpret_cast<const void*>(gemm_epilogue_kernel<BK, BN, SMALL, DUMP>), smem);
+  if (e != cudaSuccess) return e;
+  const int sms = current_sm_count();
   const long long tiles = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * g.num_n_tiles;
   const int grid = static_cast<int>(tiles < sms ? tiles : sms);
   gemm_epilogue_kernel<BK, BN, SMALL, DUMP><<<grid, kGemmThreadsP, smem, s>>>(

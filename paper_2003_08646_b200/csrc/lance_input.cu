@@ -32,17 +32,6 @@ namespace lance_dev {
 #endif
 constexpr bool K1_INTERIOR = LANCE_K1_INTERIOR != 0;
 
-// Dynamic shared-memory opt-in is per device: remember it per device ordinal.
-static inline bool lance_attr_once(bool (&done)[64]) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return true;  // always (re)apply outside the table
-  if (done[dev]) return false;
-  done[dev] = true;
-  return true;
-}
-
-
 // Warp work item: (img, ti, tile segment, channel chunk).
 struct StripItem {
   int img, ti, tj0, tj1, ch;
@@ -203,70 +192,6 @@ __global__ void __launch_bounds__(256, 2) input_range_kernel(const float* __rest
   }
 }
 
-// K0 fast path (C % 64 == 0: every lane owns two real channels): the range
-// pass without per-lane validity branches.
-__global__ void __launch_bounds__(256, 2) input_range_fast_kernel(const float* __restrict__ x,
-                                                                  float* __restrict__ partials,
-                                                                  LanceDevState* __restrict__ st,
-                                                                  InGeom g) {
-  __shared__ float s_red[256];
-  float lo[16], hi[16];
-#pragma unroll
-  for (int p = 0; p < 16; ++p) {
-    lo[p] = __int_as_float(0x7f800000);
-    hi[p] = __int_as_float(0xff800000);
-  }
-  const int lane = threadIdx.x & 31;
-  const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
-  for (long long item = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-       item < g.num_items; item += stride) {
-    const StripItem it = strip_item(g, item, lane);
-    const Strip<true> sp(x, g, it);
-    // Two tiles of new columns in flight (pc/pd slot 0 and 1): the loads for
-    // tile tj + 2 are issued while tile tj computes.
-    float2 ta[4], tb[4], tc[4], td[4], pc[2][4], pd[2][4];
-    int xx = 2 * it.tj0 - g.pad;
-    sp.column(xx, ta);
-    sp.column(xx + 1, tb);
-    sp.load(xx + 2, pc[0]);
-    sp.load(xx + 3, pd[0]);
-    if (it.tj0 + 1 < it.tj1) {
-      sp.load(xx + 4, pc[1]);
-      sp.load(xx + 5, pd[1]);
-    }
-    auto tile = [&](int sl, int tj, int xb) {
-      colpass(pc[sl], tc);
-      colpass(pd[sl], td);
-      if (tj + 2 < it.tj1) {  // prefetch two tiles ahead
-        sp.load(xb + 6, pc[sl]);
-        sp.load(xb + 7, pd[sl]);
-      }
-      float2 v[16];
-      row_pass(ta, tb, tc, td, v);
-#pragma unroll
-      for (int p = 0; p < 16; ++p) {
-        lo[p] = fmin3_nan(lo[p], v[p].x, v[p].y);
-        hi[p] = fmax3_nan(hi[p], v[p].x, v[p].y);
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        ta[a] = tc[a];
-        tb[a] = td[a];
-      }
-    };
-    for (int tj = it.tj0; tj < it.tj1; tj += 2, xx += 4) {
-      tile(0, tj, xx);
-      if (tj + 1 < it.tj1) tile(1, tj + 1, xx + 2);
-    }
-  }
-  if (block_minmax_and_ticket(lo, hi, partials, &st->ticket_in, s_red)) {
-    fit_from_ranges(s_red, g.granularity, st->bits_i, st->a_tmin, st->a_tmax, st->a_scale,
-                    st->a_rcp, &st->nan_in);
-    __syncthreads();
-    make_epilogue_consts(st, g.C);
-  }
-}
-
 // --------------------------------------------------------------------------
 // K1: codes + row sums, one strip per warp.
 //
@@ -395,7 +320,7 @@ __global__ void __launch_bounds__(256, 2) input_quant_kernel(const float* __rest
       const uint32_t tot = __reduce_add_sync(0xffffffffu, w);
       if ((lane >> 1) == k) mine = (lane & 1) ? (tot >> 16) : (tot & 0xFFFFu);
     }
-    if (lane < 16) {
+    if (g.rowsums && lane < 16) {
       int32_t* rs = rowsum + static_cast<long long>(lane) * g.rs_pitch + m;
       if (g.nchunks == 1)
         *rs = static_cast<int32_t>(mine);
@@ -428,7 +353,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // and the code to [0, top]; far-out values then round to 0 / top exactly as the
 // reference's clamps do, and near-ties (|residual| >= 0.5 - 2^-14, which
 // includes the 0.5 and top + 0.5 boundaries) take the IEEE-division quantiser.
-template <int BK, int NK, bool RS, bool STATIC = false, int ASYNC = 0>
+template <int BK, int NK, bool RS, bool STATIC = false>
 __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* __restrict__ x,
                                                                   uint8_t* __restrict__ codes,
                                                                   int32_t* __restrict__ rowsum,
@@ -462,51 +387,14 @@ __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* _
   int xx = 2 * it.tj0 - g.pad;
   sp.column(xx, ta);
   sp.column(xx + 1, tb);
-  // ASYNC > 0: the next ASYNC tiles' two new columns are staged per lane with
-  // cp.async in a shared-memory ring (as input_range_async_kernel).
-  extern __shared__ float2 s_ring1[];
-  float2* ring = s_ring1 + static_cast<size_t>(tid >> 5) * (ASYNC > 0 ? ASYNC : 1) * 8 * 32;
-  auto issue = [&](int t) {
-    if (ASYNC > 0) {
-      float2* slot = ring + (t % (ASYNC > 0 ? ASYNC : 1)) * 8 * 32;
-      if (t < it.tj1) {
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          const int xc = 2 * t - g.pad + 2 + cc;
-          const bool cok = (xc >= 0) && (xc < g.W);
-#pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            const bool ok = cok && sp.rok[a] && sp.c0ok;
-            cp_async8(slot + (cc * 4 + a) * 32 + lane, ok ? sp.row[a] + static_cast<long long>(xc) * g.C : x, ok);
-          }
-        }
-      }
-      cp_async_commit();
-    }
-  };
-  if (ASYNC > 0) {
-#pragma unroll
-    for (int q = 0; q < (ASYNC > 0 ? ASYNC : 1); ++q) issue(it.tj0 + q);
-  } else {
-    sp.load(xx + 2, pc);
-    sp.load(xx + 3, pd);
-  }
+  sp.load(xx + 2, pc);
+  sp.load(xx + 3, pd);
   int m = (it.img * g.TH + it.ti) * g.TW + it.tj0;
   for (int tj = it.tj0; tj < it.tj1; ++tj, xx += 2, ++m) {
     float2 v[16];
-    if (ASYNC > 0) {
-      cp_async_wait<(ASYNC > 0 ? ASYNC - 1 : 0)>();
-      const float2* slot = ring + (tj % (ASYNC > 0 ? ASYNC : 1)) * 8 * 32;
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        pc[a] = slot[a * 32 + lane];
-        pd[a] = slot[(4 + a) * 32 + lane];
-      }
-      issue(tj + ASYNC);
-    }
     colpass(pc, tc);
     colpass(pd, td);
-    if (ASYNC == 0 && tj + 1 < it.tj1) {  // software prefetch of the next tile's two new columns
+    if (tj + 1 < it.tj1) {  // software prefetch of the next tile's two new columns
       if (K1_INTERIOR && !RS && rows_in && xx + 4 >= 0 && xx + 5 < g.W) {  // warp-uniform; measured -3 % (RS variant: +1.5 %, so off there)
         sp.load_in(xx + 4, pc);
         sp.load_in(xx + 5, pd);
@@ -590,134 +478,6 @@ __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* _
   }
 }
 
-template <int BK, int NK>
-__global__ void __launch_bounds__(192, 2) input_quant_fast2_kernel(const float* __restrict__ x,
-                                                                  uint8_t* __restrict__ codes,
-                                                                  int32_t* __restrict__ rowsum,
-                                                                  const LanceDevState* __restrict__ st,
-                                                                  InGeom g) {
-  constexpr bool STATIC = false;  // dynamic params only (LANCE_K1_DEPTH=2 experiment)
-  __shared__ float s_tmin[16], s_scale[16], s_rcp[16];
-  const int tid = threadIdx.x, lane = tid & 31;
-  if (tid < 16) {
-    s_tmin[tid] = st->a_tmin[tid];
-    s_scale[tid] = st->a_scale[tid];
-    s_rcp[tid] = st->a_rcp[tid];
-  }
-  const float top = static_cast<float>((1 << st->bits_i) - 1);
-  __syncthreads();
-  // Reverse order: the range pass (K0) just streamed x front to back, so the
-  // tail of x is still in L2 when this kernel starts; and the GEMM, which
-  // reads the codes front to back, then finds the last-written rows in L2.
-  const long long wi = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
-  if (wi >= g.num_items) return;
-  const long long item = g.rev_items ? g.num_items - 1 - wi : wi;
-  const StripItem it = strip_item(g, item, lane);
-  const Strip<true> sp(x, g, it);
-  constexpr int kImg = kBM * BK;                       // bytes of one image
-  constexpr uint32_t kMask = BK == 128 ? 7u : (BK == 64 ? 3u : 1u);
-  const int kc = it.ch / BK, cb = it.ch % BK;
-  constexpr int pstride = NK * kImg;           // one position plane (compile-time: immediate offsets)
-  constexpr long long blkstride = 16LL * pstride;  // one 128-row block
-  uint8_t* const cbase = codes + static_cast<long long>(kc) * kImg;
-  // Two tiles of new columns in flight (pc/pd slots 0 and 1): the loads for
-  // tile tj + 2 are issued while tile tj computes.
-  float2 ta[4], tb[4], tc[4], td[4], pc[2][4], pd[2][4];
-  int xx = 2 * it.tj0 - g.pad;
-  sp.column(xx, ta);
-  sp.column(xx + 1, tb);
-  sp.load(xx + 2, pc[0]);
-  sp.load(xx + 3, pd[0]);
-  if (it.tj0 + 1 < it.tj1) {
-    sp.load(xx + 4, pc[1]);
-    sp.load(xx + 5, pd[1]);
-  }
-  const int m_first = (it.img * g.TH + it.ti) * g.TW + it.tj0;
-  auto tile = [&](int sl, int tj, int xb, int m) {
-    float2 v[16];
-    colpass(pc[sl], tc);
-    colpass(pd[sl], td);
-    if (tj + 2 < it.tj1) {  // prefetch two tiles ahead
-      sp.load(xb + 6, pc[sl]);
-      sp.load(xb + 7, pd[sl]);
-    }
-    row_pass(ta, tb, tc, td, v);
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      ta[a] = tc[a];
-      tb[a] = td[a];
-    }
-    const uint32_t lin = static_cast<uint32_t>((m & (kBM - 1)) * BK + cb);
-    uint8_t* dst = cbase + (m >> 7) * blkstride + (lin ^ (((lin >> 7) & kMask) << 4));
-    uint32_t mine = 0u;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      float2 dd[2], gq[2], r[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int p = 2 * k + h;
-        const float rcp = s_rcp[p];
-        dd[h] = sub2(v[p], bcast2(s_tmin[p]));
-        gq[h] = fma2(dd[h], bcast2(rcp), bcast2(kMagic));
-        r[h] = fma2(dd[h], bcast2(rcp), sub2(bcast2(kMagic), gq[h]));
-      }
-      uint32_t pk0 = __byte_perm(__float_as_uint(gq[0].x), __float_as_uint(gq[0].y), 0x0040);
-      uint32_t pk1 = __byte_perm(__float_as_uint(gq[1].x), __float_as_uint(gq[1].y), 0x0040);
-      float rmax = fmax3_nan(fmax3_nan(fabsf(r[0].x), fabsf(r[0].y), fabsf(r[1].x)),
-                             fabsf(r[1].y), 0.0f);
-      if (STATIC) {
-        // Caller params: a value whose rounded code falls outside [0, top]
-        // (or whose product is too large for the magic-number rounding) joins
-        // the exact path, which applies the reference's clamps.
-        const float glo = fmin3_nan(fmin3_nan(gq[0].x, gq[0].y, gq[1].x), gq[1].y, kMagic);
-        const float ghi = fmax3_nan(fmax3_nan(gq[0].x, gq[0].y, gq[1].x), gq[1].y, kMagic);
-        if (!(glo >= kMagic) || !(ghi <= __fadd_rn(kMagic, top))) rmax = 1.0f;
-      }
-      if (__builtin_expect(__any_sync(0xffffffffu, !(rmax < kTieGuard)), 0)) {
-        // Rare (~1e-4 per value): re-derive flagged codes exactly.
-        if (!(rmax < kTieGuard)) {
-          uint32_t c[4];
-          const float dv[4] = {dd[0].x, dd[0].y, dd[1].x, dd[1].y};
-          const float gv[4] = {gq[0].x, gq[0].y, gq[1].x, gq[1].y};
-          const float rv[4] = {r[0].x, r[0].y, r[1].x, r[1].y};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float sc = s_scale[2 * k + (e >> 1)];
-            const float2 vv = v[2 * k + (e >> 1)];
-            if (STATIC)
-              c[e] = (fabsf(rv[e]) < kTieGuard && gv[e] >= kMagic && gv[e] <= __fadd_rn(kMagic, top))
-                         ? (__float_as_uint(gv[e]) & 0xFFu)
-                         : quantize_code((e & 1) ? vv.y : vv.x, s_tmin[2 * k + (e >> 1)], sc, top);
-            else
-              c[e] = (fabsf(rv[e]) < kTieGuard) ? (__float_as_uint(gv[e]) & 0xFFu)
-                                                : exact_code_near_boundary(dv[e], sc, gv[e], rv[e], top);
-          }
-          pk0 = c[0] | (c[1] << 8);
-          pk1 = c[2] | (c[3] << 8);
-        }
-      }
-      *reinterpret_cast<uint16_t*>(dst + image_plane(2 * k) * pstride) = static_cast<uint16_t>(pk0);
-      *reinterpret_cast<uint16_t*>(dst + image_plane(2 * k + 1) * pstride) = static_cast<uint16_t>(pk1);
-      // Row sums (lowpgemm.hpp:121-123): positions (2k, 2k+1) as 16-bit halves.
-      const uint32_t a = (pk0 & 0xFFFFu) | (pk1 << 16);                  // [p.c0, p.c1, q.c0, q.c1]
-      const uint32_t w = (a & 0x00FF00FFu) + ((a >> 8) & 0x00FF00FFu);  // [p sum | q sum]
-      const uint32_t tot = __reduce_add_sync(0xffffffffu, w);
-      if ((lane >> 1) == k) mine = (lane & 1) ? (tot >> 16) : (tot & 0xFFFFu);
-    }
-    if (lane < 16) {
-      int32_t* rs = rowsum + static_cast<long long>(lane) * g.rs_pitch + m;
-      if (g.nchunks == 1)
-        *rs = static_cast<int32_t>(mine);
-      else  // channel chunks of one tile run in different warps (rowsum pre-zeroed)
-        atomicAdd(rs, static_cast<int32_t>(mine));
-    }
-  };
-  for (int tj = it.tj0; tj < it.tj1; tj += 2, xx += 4) {
-    tile(0, tj, xx, m_first + (tj - it.tj0));
-    if (tj + 1 < it.tj1) tile(1, tj + 1, xx + 2, m_first + (tj + 1 - it.tj0));
-  }
-}
-
 // Static-params mode: caller-supplied input QuantParams[16].
 __global__ void static_params_kernel(LanceDevState* st, StaticParams prm, int C) {
   if (threadIdx.x < prm.np) {
@@ -734,12 +494,12 @@ __global__ void static_params_kernel(LanceDevState* st, StaticParams prm, int C)
 }
 
 // --------------------------------------------------------------------------
-// K0 variant (LANCE_K0_ASYNC = D): the two new input columns of the next D
+// K0 (C % 64 == 0): the two new input columns of the next D
 // tiles are staged per lane with cp.async (8-byte copies, zero-fill outside
 // the image) in a shared-memory ring instead of registers, so the lookahead
 // is not limited by the register budget.  A lane only ever reads back the
 // slots it copied itself, so per-thread cp.async groups are the only ordering
-// needed.  Arithmetic identical to input_range_fast_kernel.
+// needed.  Arithmetic as input_range_kernel.
 template <int D>
 __global__ void __launch_bounds__(256, 2) input_range_async_kernel(const float* __restrict__ x,
                                                                    float* __restrict__ partials,
@@ -942,38 +702,22 @@ int input_range_grid(const InGeom& g, int sm_count) {
 
 cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceDevState* st,
                                const InGeom& g, int vec2, cudaStream_t s) {
-  // K0 input staging: cp.async ring of K0_DEPTH tiles (default 4; 0 = the
-  // register-lookahead kernel).  Measured: 4 is 7-8 % faster than registers on
-  // the 56x56 / 28x28 layers; 8 halves residency (128 KB per block) and loses.
-  static const int async_depth = [] {
-    const char* e = std::getenv("LANCE_K0_ASYNC");
-    return e ? std::atoi(e) : 4;
-  }();
+  // K0 input staging: cp.async ring of 4 tiles per warp (measured: 7-8 % faster
+  // than register lookahead on the 56x56 / 28x28 layers; 8 halves residency).
+  constexpr int kDepth = 4;
   if (g.C < 32) {
     input_range_smallc_kernel<<<grid, 256, 0, s>>>(x, partials, st, g);
-  } else if (g.C % 64 == 0 && (async_depth == 4 || async_depth == 6 || async_depth == 8)) {
-    const size_t smem = static_cast<size_t>(8) * async_depth * 8 * 32 * sizeof(float2);
-#define LANCE_K0_ASYNC_CASE(DV)                                                                   \
-    if (async_depth == DV) {                                                                     \
-      static bool set_dev[64] = {};                                                              \
-      if (lance_attr_once(set_dev)) {                                                            \
-        cudaFuncSetAttribute(input_range_async_kernel<DV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             static_cast<int>(smem));                                            \
-                                                                                          \
-      }                                                                                          \
-      input_range_async_kernel<DV><<<grid, 256, smem, s>>>(x, partials, st, g);                  \
-    }
-    LANCE_K0_ASYNC_CASE(4)
-    LANCE_K0_ASYNC_CASE(6)
-    LANCE_K0_ASYNC_CASE(8)
-#undef LANCE_K0_ASYNC_CASE
   } else if (g.C % 64 == 0) {
-    input_range_fast_kernel<<<grid, 256, 0, s>>>(x, partials, st, g);
-  }
-  else if (vec2)
+    const size_t smem = static_cast<size_t>(8) * kDepth * 8 * 32 * sizeof(float2);
+    const cudaError_t attr =
+        ensure_smem_attr(reinterpret_cast<const void*>(input_range_async_kernel<kDepth>), smem);
+    if (attr != cudaSuccess) return attr;
+    input_range_async_kernel<kDepth><<<grid, 256, smem, s>>>(x, partials, st, g);
+  } else if (vec2) {
     input_range_kernel<true><<<grid, 256, 0, s>>>(x, partials, st, g);
-  else
+  } else {
     input_range_kernel<false><<<grid, 256, 0, s>>>(x, partials, st, g);
+  }
   return cudaGetLastError();
 }
 
@@ -995,40 +739,12 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
     return cudaGetLastError();
   }
   if (g.C % 64 == 0) {  // fast path: every lane owns two real channels
-    static const int depth = [] {
-      const char* e = std::getenv("LANCE_K1_DEPTH");
-      return e ? std::atoi(e) : 1;
-    }();
-    static const int k1_async = [] {
-      const char* e = std::getenv("LANCE_K1_ASYNC");
-      return e ? std::atoi(e) : 0;
-    }();
-    const size_t k1_smem = k1_async == 4 ? static_cast<size_t>(8) * 4 * 8 * 32 * sizeof(float2) : 0;
-    static bool k1_attr_dev[64] = {};
-    if (k1_async == 4 && lance_attr_once(k1_attr_dev)) {  // 64 KB rings: opt every instantiation in once
-#define LANCE_K1_ATTR(BKV, NKV)                                                                   \
-      cudaFuncSetAttribute(input_quant_fast_kernel<BKV, NKV, true, false, 4>,                     \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k1_smem)); \
-      cudaFuncSetAttribute(input_quant_fast_kernel<BKV, NKV, false, false, 4>,                    \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k1_smem));
-      LANCE_K1_ATTR(64, 1) LANCE_K1_ATTR(128, 1) LANCE_K1_ATTR(128, 2) LANCE_K1_ATTR(128, 3)
-      LANCE_K1_ATTR(128, 4) LANCE_K1_ATTR(64, 3) LANCE_K1_ATTR(64, 5)
-#undef LANCE_K1_ATTR
-
-    }
 #define LANCE_K1_FAST(BKV, NKV)                                                          \
   if (g.a_bk == BKV && g.a_nk == NKV) {                                                  \
     if (static_mode && g.rowsums)                                                        \
       input_quant_fast_kernel<BKV, NKV, true, true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g); \
     else if (static_mode)                                                                \
       input_quant_fast_kernel<BKV, NKV, false, true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g); \
-    else if (depth == 2)                                                                 \
-      input_quant_fast2_kernel<BKV, NKV>                                                 \
-          <<<static_cast<unsigned>((g.num_items + 5) / 6), 192, 0, s>>>(x, codes, rowsum, st, g); \
-    else if (k1_async == 4 && g.rowsums)                                                 \
-      input_quant_fast_kernel<BKV, NKV, true, false, 4><<<grid, 256, k1_smem, s>>>(x, codes, rowsum, st, g); \
-    else if (k1_async == 4)                                                              \
-      input_quant_fast_kernel<BKV, NKV, false, false, 4><<<grid, 256, k1_smem, s>>>(x, codes, rowsum, st, g); \
     else if (g.rowsums)                                                                  \
       input_quant_fast_kernel<BKV, NKV, true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g); \
     else                                                                                 \

@@ -29,7 +29,6 @@ struct LanceDevState {
   int bits_i, bits_w;
   int nan_in, nan_w;
   unsigned int ticket_in, ticket_w;
-  unsigned int band_ctr[2], band_done[2];  // dynamic work counters of the band kernels
 };
 
 // Input-side geometry shared by the range pass (K0) and the quantiser (K1).
@@ -49,25 +48,6 @@ struct InGeom {
   int nseg;
   long long num_items;  // N * TH * nseg * nchunks warp items
   int granularity;  // 1 = PerPosition, 2 = PerTensor
-};
-
-// v4 input kernels (lance_band.cu): bands of tile rows fed by 4-D TMA.
-struct BandGeom {
-  int enabled;     // shape supported (C % 4 == 0, chb | C_pad, chb % BK == 0, ...)
-  int chb;         // channels per band (64, 128 or 256; a multiple of the GEMM's BK)
-  int nbc;         // channel bands per image (C_pad / chb)
-  int nkb;         // GEMM k chunks per band (chb / BK)
-  int trs;         // tile rows per work item
-  int nseg;        // tile-row segments per image = ceil(TH / trs)
-  int tws;         // tiles per column slice (a CTA handles tws tiles of a tile row)
-  int ncs;         // column slices = ceil(TW / tws)
-  long long items; // N * nbc * ncs * nseg
-  int box_w;       // pixels per loaded row: 2 * tws + 2 from x = 2 * tj0 - pad
-  int slot_bytes;  // box_w * chb * 4
-  int ring;        // shared-memory row slots (<= 16)
-  int run_bytes;   // tws * BK: one staged (position, k chunk) run of image rows
-  int stg_bytes;   // 16 * nkb * run_bytes
-  int grid;
 };
 
 struct FilterGeom {
@@ -161,6 +141,17 @@ __host__ __device__ __forceinline__ long long umma_image_offset_np(long long row
          umma_swizzle(static_cast<uint32_t>(r * bk + cb), bk);
 }
 
+// Experiment switches: the environment value in LANCE_PROFILING builds, else def.
+int lance_knob(const char* name, int def);
+
+// Thread-safe, per-device dynamic shared-memory opt-in: raises the attribute
+// of kernel `fn` on the current device to at least `bytes` (cached per
+// (device, kernel) behind a mutex; plans may be created from several host
+// threads, one per GPU).
+cudaError_t ensure_smem_attr(const void* fn, size_t bytes);
+// Multiprocessor count of the current device (cached, thread-safe).
+int current_sm_count();
+
 // Host-side launchers.  All stream-ordered.
 int input_range_grid(const InGeom& g, int sm_count);
 cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceDevState* st,
@@ -168,11 +159,6 @@ cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceD
 cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
                                const LanceDevState* st, const InGeom& g, int vec2,
                                int static_mode, cudaStream_t s);
-size_t band_smem_bytes(const BandGeom& b, int mode);
-// mode 0: K0 range pass, 1: K1 quantise (static_mode: caller params).
-cudaError_t launch_band(const CUtensorMap* tmX, uint8_t* codes, int32_t* rowsum, float* partials,
-                        LanceDevState* st, const InGeom& g, const BandGeom& b, int mode,
-                        int static_mode, cudaStream_t s);
 cudaError_t launch_static_params(LanceDevState* st, const StaticParams& prm, int C,
                                  cudaStream_t s);
 cudaError_t launch_filter_prepare(const float* w, float* u_tmp, float* partials, int grid,

@@ -43,7 +43,7 @@ def read_tensor(path: str) -> np.ndarray:
         with open(path, "rb") as f:
             data = f.read()
     except OSError:
-        raise FormatError("cannot open for reading: " + path) from None
+        raise FormatError("cannot open: " + path) from None  # tensor_io.hpp:146
     if len(data) < 4:
         raise FormatError("tensor stream: truncated header")
     if data[:4] != MAGIC:

@@ -198,28 +198,43 @@ def test_global_params_across_shards(lo):
     assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), mismatch_report(got, ref)
 
 
-@pytest.mark.parametrize("env", [{"LANCE_BAND_K0": "1"}, {"LANCE_BAND_K1": "1"},
-                                 {"LANCE_BAND_K0": "1", "LANCE_BAND_K1": "1"},
-                                 {"LANCE_RS_GEMM": "0"}, {"LANCE_RS_GEMM": "1"},
-                                 {"LANCE_K1_REVERSE": "0"}, {"LANCE_K1_DEPTH": "2"}],
-                         ids=lambda e: "+".join(f"{k}={v}" for k, v in e.items()))
-def test_alternate_kernel_paths_bitexact(lo, env, monkeypatch):
-    # The non-default input / row-sum kernels (TMA band kernels, row sums in
-    # K1 vs the GEMM, item order, deeper K1 lookahead) are selected at plan
-    # creation; each must reproduce the reference bitwise like the defaults.
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    for spec, dist, seed in [(Spec(2, 64, 17, 17, 64, 1), "relu", 3),
-                             (Spec(1, 128, 14, 14, 64, 1), "uniform", 4),
-                             (Spec(1, 256, 9, 9, 128, 0), "relu", 5),
-                             (Spec(3, 3, 15, 13, 20, 1), "relu", 6)]:  # small-C kernels
-        x, w = make_inputs(lo.uniform, spec, dist, seed)
-        got = run_gpu(spec, x, w, gemm_cfg())
-        y, ref = lo.lance_gemm(spec, x, w, dump=True)
-        ref["y"] = y
-        for k in ("codes_a", "rowsum", "acc", "params_a", "y"):
-            assert np.array_equal(np.asarray(got[k]).view(np.uint8), np.asarray(ref[k]).view(np.uint8)), \
-                f"{env} {spec}: {k}: {mismatch_report(got[k], ref[k])}"
+@pytest.mark.parametrize("spec,dist,seed", [(Spec(2, 64, 17, 17, 64, 1), "relu", 3),   # row sums in the GEMM
+                                            (Spec(1, 128, 14, 14, 64, 1), "uniform", 4),  # row sums in K1
+                                            (Spec(1, 256, 9, 9, 128, 0), "relu", 5),
+                                            (Spec(3, 3, 15, 13, 20, 1), "relu", 6)],      # small-C kernels
+                         ids=lambda v: str(v))
+def test_kernel_family_shapes_bitexact(lo, spec, dist, seed):
+    # One shape per input-kernel family / row-sum placement, every stage bitwise.
+    x, w = make_inputs(lo.uniform, spec, dist, seed)
+    got = run_gpu(spec, x, w, gemm_cfg())
+    y, ref = lo.lance_gemm(spec, x, w, dump=True)
+    ref["y"] = y
+    for k in ("codes_a", "rowsum", "acc", "params_a", "y"):
+        assert np.array_equal(np.asarray(got[k]).view(np.uint8), np.asarray(ref[k]).view(np.uint8)), \
+            f"{spec}: {k}: {mismatch_report(got[k], ref[k])}"
+
+
+def test_tensor_shape_checked():
+    # check_layer (engines.hpp:84-91): an NCHW input or a [K,C,3,3] filter bank
+    # with the right element count is rejected, like the reference.
+    spec = lance.ConvSpec(1, 4, 6, 6, 8, 1)
+    conv = lance.LanceConv(spec, gemm_cfg())
+    with pytest.raises(lance.LanceError, match="filter dims do not match spec"):
+        conv.set_filters(torch.zeros(8, 4, 3, 3, device="cuda"))
+    conv.set_filters(torch.zeros(8, 3, 3, 4, device="cuda"))
+    with pytest.raises(lance.LanceError, match="input tensor dims do not match spec"):
+        conv.forward(torch.zeros(1, 4, 6, 6, device="cuda"))
+    conv.close()
+
+
+def test_large_k_layer(lo):
+    # K = 2048 filters (32 n-tiles): the epilogue's third-term table is per
+    # tile, so shared memory no longer grows with K.
+    spec = Spec(1, 64, 6, 6, 2048, 1)
+    x, w = make_inputs(lo.uniform, spec, "relu", 12)
+    got = run_gpu(spec, x, w, gemm_cfg(), acc=False)
+    ref = lo.lance_gemm(spec, x, w)
+    assert np.array_equal(got["y"].view(np.uint32), ref.view(np.uint32)), mismatch_report(got["y"], ref)
 
 
 @pytest.mark.parametrize("spec", [Spec(2, 64, 17, 17, 64, 1),    # fast K1, row sums in the GEMM
