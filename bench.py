@@ -11,10 +11,20 @@ epilogue) on device-resident inputs; filters are prepared once per layer (K2)
 outside the step, as the north star specifies.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--scaling strong|weak] [--mode shard|global]
 
-N>1 is launched by torchrun (one rank per GPU, NCCL); every rank runs its own
-batch of 256 with no collective on the data path (weak scaling); the step time
-is the max over ranks.  Rank 0 prints one JSON line.
+N > 1: one rank per GPU (NCCL).  Under torchrun the ranks come from the
+environment; without it, ``--gpus N`` re-launches this script through
+``torch.distributed.run`` itself.  Default (north star): the global
+batch of 256 is partitioned into contiguous slices of 256/N images (strong
+scaling), each rank runs its slice with no collective on the data path
+(``--mode shard``: per-shard PerPosition fit); ``--mode global`` times the
+global-fit mode instead (K0 -> one 2P+1-float NCCL MAX all-reduce -> K1 ->
+GEMM, bitwise one full-batch call); ``--scaling weak`` gives every rank 256
+images.  Step time = max over ranks of the CUDA-event time.  Outside the timed
+region, N > 1 runs shard.verify_sharded (NCCL scatter / all-reduce / gather)
+on a config-3 layer and compares it with one full-batch forward.  Rank 0
+prints one JSON line.
 """
 from __future__ import annotations
 
@@ -148,6 +158,34 @@ def dist_setup():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def maybe_spawn(args) -> None:
+    """--gpus N > 1 without a torchrun environment: re-launch this script as N
+    ranks on this node (torch.distributed.run, rendezvous on 127.0.0.1) and
+    exit with its status."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def cpu_reference_images_per_s(batch: int, reps: int, threads: int, layers=None):

@@ -124,6 +124,22 @@ LANCE_API int lance_plan_forward(lance_plan_t plan, const float* x_dev, float* y
 LANCE_API int lance_plan_forward_static(lance_plan_t plan, const lance_qparams* in_params16,
                               const float* x_dev, float* y_dev, void* stream);
 
+/* Global-fit mode across batch shards (SURVEY.md section 8(e) mode 2): the
+ * reference fits the PerPosition ranges over the WHOLE batch
+ * (quantize_domain, engines.hpp:157-165; fit_params, quant.hpp:54-72), so a
+ * batch split over G GPUs reproduces one full-batch lance_gemm call by
+ *   1. lance_plan_ranges on every shard (K0 only): writes the shard's fitted
+ *      ranges to minmax_dev as 2*P+1 floats [-t_min[0..P), t_max[0..P), nan];
+ *   2. ONE element-wise MAX all-reduce of that buffer across ranks (e.g.
+ *      ncclAllReduce(..., ncclFloat, ncclMax), 2*P+1 floats, on the stream);
+ *   3. lance_plan_forward_ranges: re-fits the input QuantParams from the
+ *      reduced ranges on the device, then K1 -> K3/K4.
+ * Stream-ordered, no host synchronisation.  P = lance_plan_positions(plan).
+ * A NaN anywhere in the global batch is reported by lance_plan_sync. */
+LANCE_API int lance_plan_ranges(lance_plan_t plan, const float* x_dev, float* minmax_dev, void* stream);
+LANCE_API int lance_plan_forward_ranges(lance_plan_t plan, const float* minmax_dev,
+                                        const float* x_dev, float* y_dev, void* stream);
+
 /* Optional fused bias + ReLU epilogue for subsequent forwards (north-star
  * extension; no reference oracle: equals relu(lance_gemm(x, w) + bias)).
  * bias_dev may be NULL (no bias).  relu is 0 or 1. */

@@ -265,10 +265,29 @@ class LanceConv:
         _check(_lib.lib().lance_plan_set_acc_dump(
             self._plan, ct.c_void_p(acc.data_ptr()) if acc is not None else None))
 
-    def forward(self, x, y=None, stream=None, params=None):
+    def ranges(self, x, out=None, stream=None):
+        """K0 only: this batch's fitted per-position ranges as a float32 CUDA
+        tensor [2P + 1] = [-t_min, t_max, nan] -- the layout one element-wise
+        MAX all-reduce combines across batch shards (global-fit mode,
+        engines.hpp:157-165)."""
+        import torch
+        s = self.spec
+        self._check_tensor(x, (s.n, s.h, s.w, s.c), "input tensor")
+        n = 2 * self.positions + 1
+        if out is None:
+            out = torch.empty(n, dtype=torch.float32, device=x.device)
+        if not (out.is_cuda and out.dtype == torch.float32 and out.is_contiguous() and out.numel() == n):
+            raise LanceError(f"ranges buffer must be a float32 CUDA tensor of {n} elements")
+        _check(_lib.lib().lance_plan_ranges(self._plan, ct.c_void_p(x.data_ptr()),
+                                            ct.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        return out
+
+    def forward(self, x, y=None, stream=None, params=None, ranges=None):
         """K0 -> K1 -> K3/K4.  Asynchronous on `stream`; call ``sync`` to
         surface a NaN error.  ``params`` (16 QuantParams) selects the
-        static-params mode (no range pass)."""
+        static-params mode (no range pass); ``ranges`` (a reduced buffer from
+        ``ranges()`` + a MAX all-reduce) fits the input params on the device
+        from global ranges instead of this batch's (no host round trip)."""
         import torch
         s = self.spec
         self._check_tensor(x, (s.n, s.h, s.w, s.c), "input tensor")
@@ -277,7 +296,14 @@ class LanceConv:
                             device=x.device)
         self._check_tensor(y, (s.n, s.out_h(), s.out_w(), s.k), "output")
         L = _lib.lib()
-        if params is None:
+        if ranges is not None:
+            if not (ranges.is_cuda and ranges.dtype == torch.float32 and ranges.is_contiguous()
+                    and ranges.numel() == 2 * self.positions + 1):
+                raise LanceError(f"ranges must be a float32 CUDA tensor of {2 * self.positions + 1} elements")
+            _check(L.lance_plan_forward_ranges(self._plan, ct.c_void_p(ranges.data_ptr()),
+                                               ct.c_void_p(x.data_ptr()), ct.c_void_p(y.data_ptr()),
+                                               _stream_ptr(stream)))
+        elif params is None:
             _check(L.lance_plan_forward(self._plan, ct.c_void_p(x.data_ptr()),
                                         ct.c_void_p(y.data_ptr()), _stream_ptr(stream)))
         else:

@@ -623,8 +623,10 @@ int lance_plan_set_filters(lance_plan_t p, const float* w_dev, void* stream) {
   return LANCE_OK;
 }
 
+// Input-parameter source of a forward: the batch's own range pass (K0), the
+// caller's QuantParams, or device ranges already reduced across ranks.
 static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStream_t s,
-                       const lance_qparams* static_params) {
+                       const lance_qparams* static_params, const float* minmax_dev = nullptr) {
   if (!p || !x_dev || !y_dev) return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_forward: null argument");
   if (!p->filters_ready)
     return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_forward: filters not set");
@@ -653,6 +655,8 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
         prm.scale[i] = static_params[i].scale;
       }
       LANCE_CUDA(launch_static_params(p->state, prm, p->spec.c, s));
+    } else if (minmax_dev) {
+      LANCE_CUDA(launch_fit_minmax(p->state, minmax_dev, 36, p->cfg.granularity, p->spec.c, s));
     } else {
       LANCE_CUDA(launch_f4_range(x_dev, p->partials, p->range_grid, p->state, p->f4, s));
     }
@@ -677,6 +681,8 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
       prm.scale[i] = static_params[i].scale;
     }
     LANCE_CUDA(launch_static_params(p->state, prm, p->spec.c, s));
+  } else if (minmax_dev) {
+    LANCE_CUDA(launch_fit_minmax(p->state, minmax_dev, 16, p->cfg.granularity, p->spec.c, s));
   } else {
     LANCE_CUDA(launch_input_range(x_dev, p->partials, p->range_grid, p->state, p->in_geom,
                                   p->vec2, s));
@@ -705,6 +711,24 @@ int lance_plan_forward_static(lance_plan_t p, const lance_qparams* in_params16,
                               const float* x_dev, float* y_dev, void* stream) {
   if (!in_params16) return fail(LANCE_ERR_INVALID_ARGUMENT, "static params: null");
   return run_forward(p, x_dev, y_dev, static_cast<cudaStream_t>(stream), in_params16);
+}
+
+int lance_plan_ranges(lance_plan_t p, const float* x_dev, float* minmax_dev, void* stream) {
+  if (!p || !x_dev || !minmax_dev) return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_ranges: null argument");
+  DeviceGuard guard(p->device);
+  auto s = static_cast<cudaStream_t>(stream);
+  if (p->tm == 4)
+    LANCE_CUDA(launch_f4_range(x_dev, p->partials, p->range_grid, p->state, p->f4, s));
+  else
+    LANCE_CUDA(launch_input_range(x_dev, p->partials, p->range_grid, p->state, p->in_geom, p->vec2, s));
+  LANCE_CUDA(launch_export_minmax(p->state, minmax_dev, p->np, s));
+  return LANCE_OK;
+}
+
+int lance_plan_forward_ranges(lance_plan_t p, const float* minmax_dev, const float* x_dev,
+                              float* y_dev, void* stream) {
+  if (!minmax_dev) return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_forward_ranges: null ranges");
+  return run_forward(p, x_dev, y_dev, static_cast<cudaStream_t>(stream), nullptr, minmax_dev);
 }
 
 int lance_plan_set_epilogue(lance_plan_t p, const float* bias_dev, int relu) {

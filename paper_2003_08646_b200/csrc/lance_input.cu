@@ -774,6 +774,61 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
   return cudaGetLastError();
 }
 
+// Global-fit mode (SURVEY 8(e) mode 2) on the device.  Export: the fitted
+// per-position ranges of the last range pass as [-t_min[0..np), t_max[0..np),
+// nan] -- the layout one element-wise MAX all-reduce combines across ranks
+// (-(-x) is exact; a NaN flag rides along as 1.0 because fmax drops NaNs).
+__global__ void export_minmax_kernel(const LanceDevState* st, float* minmax, int np) {
+  const int p = threadIdx.x;
+  if (p < np) {
+    minmax[p] = -st->a_tmin[p];
+    minmax[np + p] = st->a_tmax[p];
+  }
+  if (p == 0) minmax[2 * np] = st->nan_in ? 1.0f : 0.0f;
+}
+
+// Import: fit_params (quant.hpp:54-72) on the reduced ranges -> the input
+// QuantParams and affine constants of the plan (PerTensor folds, engines.hpp:151-156).
+__global__ void fit_minmax_kernel(LanceDevState* st, const float* __restrict__ minmax, int np,
+                                  int gran, int C) {
+  const int p = threadIdx.x;
+  bool bad = false;
+  if (p < np) {
+    float lo = -minmax[p], hi = minmax[np + p];
+    if (gran == 2) {
+      lo = -minmax[0];
+      hi = minmax[np];
+      for (int q = 1; q < np; ++q) {
+        lo = fmin_nan(lo, -minmax[q]);
+        hi = fmax_nan(hi, minmax[np + q]);
+      }
+    }
+    lo = __fadd_rn(lo, 0.0f);  // the reference never produces -0 (matrix.hpp:77-83)
+    hi = __fadd_rn(hi, 0.0f);
+    bad = isnan(lo) || isnan(hi) || isinf(lo) || isinf(hi);
+    const float s = __fdiv_rn(__fsub_rn(hi, lo), static_cast<float>((1 << st->bits_i) - 1));
+    st->a_tmin[p] = lo;
+    st->a_tmax[p] = hi;
+    st->a_scale[p] = s;
+    st->a_rcp[p] = (s == 0.0f) ? 0.0f : __frcp_rn(s);
+  }
+  const int any = __syncthreads_or(bad ? 1 : 0);
+  if (p == 0) st->nan_in = (any || minmax[2 * np] != 0.0f) ? 1 : 0;
+  __syncthreads();
+  make_epilogue_consts(st, C, np);
+}
+
+cudaError_t launch_export_minmax(const LanceDevState* st, float* minmax, int np, cudaStream_t s) {
+  export_minmax_kernel<<<1, 64, 0, s>>>(st, minmax, np);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fit_minmax(LanceDevState* st, const float* minmax, int np, int gran, int C,
+                              cudaStream_t s) {
+  fit_minmax_kernel<<<1, 64, 0, s>>>(st, minmax, np, gran, C);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_static_params(LanceDevState* st, const StaticParams& prm, int C,
                                  cudaStream_t s) {
   static_params_kernel<<<1, 64, 0, s>>>(st, prm, C);

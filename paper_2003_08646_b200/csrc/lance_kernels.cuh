@@ -161,6 +161,10 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
                                int static_mode, cudaStream_t s);
 cudaError_t launch_static_params(LanceDevState* st, const StaticParams& prm, int C,
                                  cudaStream_t s);
+// Global-fit mode: [-t_min[np], t_max[np], nan] export / re-fit on the device.
+cudaError_t launch_export_minmax(const LanceDevState* st, float* minmax, int np, cudaStream_t s);
+cudaError_t launch_fit_minmax(LanceDevState* st, const float* minmax, int np, int gran, int C,
+                              cudaStream_t s);
 cudaError_t launch_filter_prepare(const float* w, float* u_tmp, float* partials, int grid,
                                   uint8_t* codes_w, int32_t* colsum, LanceDevState* st,
                                   const FilterGeom& g, cudaStream_t s);

@@ -118,14 +118,42 @@ def gather_batch(y_local, n_total: int, group=None):
     return torch.cat([p[: b - a] for p, (a, b) in zip(parts, sizes)]).cpu().numpy()
 
 
+def allreduce_ranges(buf, group=None):
+    """Element-wise MAX all-reduce of a ``LanceConv.ranges`` buffer
+    [-t_min, t_max, nan] across the batch shards: the global PerPosition fit
+    of engines.hpp:157-165.  With NCCL the buffer stays on the device (one
+    2P+1-float ncclAllReduce on the current stream, no host round trip);
+    gloo reduces a host copy."""
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(buf, op=dist.ReduceOp.MAX, group=group)
+        return buf
+    host = buf.cpu()
+    dist.all_reduce(host, op=dist.ReduceOp.MAX, group=group)
+    buf.copy_(host)
+    return buf
+
+
+def global_forward(conv, x, y=None, group=None, stream=None):
+    """One shard's forward in the global-fit mode: K0 on the shard ->
+    all-reduce of the ranges -> on-device re-fit -> K1 -> K3/K4.  Every rank
+    of `group` must call it with its own slice; the result is bitwise the
+    shard's rows of one full-batch lance_gemm."""
+    r = conv.ranges(x, stream=stream)
+    allreduce_ranges(r, group)
+    return conv.forward(x, y, stream=stream, ranges=r)
+
+
 def verify_sharded(x_full, w, spec, cfg, group=None, tile_m: int = 2):
     """Multi-GPU full-batch parity check of one layer (north star: NCCL only
     scatters inputs and gathers outputs for verification).  Rank 0 holds x
     [N,H,W,C] and w; x is scattered, every rank runs its slice in the
-    full-batch-parity mode (local range pass -> 128-byte MAX all-reduce ->
-    static-params forward), and the gathered output is returned on every rank.
-    It must equal one full-batch lance_gemm call bitwise.  w must be given on
-    every rank (with NCCL rank 0's copy is broadcast)."""
+    global-fit mode (``global_forward``: K0 -> MAX all-reduce of the 2P+1
+    range floats on the device -> re-fit -> K1 -> GEMM), and the gathered
+    output is returned on every rank.  It must equal one full-batch
+    lance_gemm call bitwise.  w must be given on every rank (with NCCL rank
+    0's copy is broadcast)."""
     import torch
     import torch.distributed as dist
 
@@ -140,13 +168,7 @@ def verify_sharded(x_full, w, spec, cfg, group=None, tile_m: int = 2):
     conv = LanceConv(ConvSpec(b - a, spec.c, spec.h, spec.w, spec.k, spec.pad), cfg,
                      device=torch.cuda.current_device(), tile_m=tile_m)
     conv.set_filters(wt)
-    conv.forward(xs.cuda())            # local range pass
-    conv.sync()
-    local, _ = conv.params()
-    lo = np.array([q.t_min for q in local], np.float32)
-    hi = np.array([q.t_max for q in local], np.float32)
-    glo, ghi = allreduce_minmax(lo, hi, group)
-    y = conv.forward(xs.cuda(), params=params_from_minmax(glo, ghi, cfg.bits_i))
+    y = global_forward(conv, xs.cuda(), group=group)
     conv.sync()
     out = gather_batch(y, spec.n, group)
     conv.close()
