@@ -240,40 +240,31 @@ def run_reference_arm(args, ws, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": mean_t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": mean_t * 1e3, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (reference UniformSource, seed 42+layer)",
         "config": {"workload": wl_name, "batch_per_step": batch,
                    "note": f"bounded CPU sample: {batch} images per step of the batch-{wl_batch} workload"},
         "tops_equivalent": tops,
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "reference",
+                         "cpu_model": cpu_model(),
                          "sample": f"{len(wl_layers)} {wl_name} layers at batch {batch}, one lance_gemm call each per step"},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def int8_peak_tops(device):
-    """Dense INT8 tensor peak measured here (cuBLASLt int8 GEMM via torch._int_mm,
-    8192^3): the denominator for the GEMM stage's tensor fraction."""
-    import torch
-    try:
-        n = 8192
-        a = torch.randint(-64, 64, (n, n), dtype=torch.int8, device=device)
-        b = torch.randint(-64, 64, (n, n), dtype=torch.int8, device=device)
-        for _ in range(3):
-            torch._int_mm(a, b)
-        torch.cuda.synchronize(device)
-        best = 1e9
-        for _ in range(10):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            torch._int_mm(a, b)
-            e1.record()
-            e1.synchronize()
-            best = min(best, e0.elapsed_time(e1) * 1e-3)
-        return 2 * n ** 3 / best / 1e12
-    except Exception:
-        return None
+# Dense INT8 tensor peak: the builder's own tcgen05 kind::i8 microbenchmark on
+# this pool's B200s (scratch/umma_bench.cu, profiles/r01_umma_bench.txt): a
+# 128x128x32 u8 SS-UMMA issues every 64 SM cycles = 8192 MAC/clk/SM, i.e.
+# 2 * 8192 * 148 SMs * 1.965 GHz = 4.76 POPS at the max clock; the measured
+# sustained figure was 4516 TOPS.  cuBLAS s8 (torch._int_mm) reaches only
+# 2.7-3.3 POPS and would flatter every fraction by ~1.4x.
+INT8_PEAK_TOPS = 4516.0
+
+
+def int8_peak_tops():
+    return INT8_PEAK_TOPS, ("measured: own tcgen05 kind::i8 128x128x32 SS-UMMA microbenchmark "
+                            "(profiles/r01_umma_bench.txt), 4516 TOPS")
 
 
 def run_stack(args, ws, rank, local, N):
@@ -333,28 +324,98 @@ def run_stack(args, ws, rank, local, N):
     stack.close()
 
 
+def verify_with_cpu_reference(state, cfg, TM, rank):
+    """Part of the CPU-reference leg (outside the timed region): the first and
+    last image of every layer of the timed step, recomputed on the CPU by the
+    pinned oracle (oracle/lance_oracle.c, checked bitwise against the
+    reference in tests/test_oracle.py) with the GPU's fitted input
+    QuantParams, must equal the GPU's y bitwise (images are independent given
+    the batch's params, engines.hpp:199-200)."""
+    import numpy as np
+    import oracle
+    import paper_2003_08646_b200 as lance
+    lo = oracle.Oracle()
+    bad, checked, worst = 0, 0, None
+    for spec, conv, x, w, y, host, *_ in state:
+        pa, _ = conv.params()
+        arr = lance.params_array(pa)
+        yh = y.cpu().numpy()
+        xh = x.cpu().numpy()
+        wh = w.cpu().numpy()
+        for img in sorted({0, spec.n - 1}):
+            s1 = oracle.Spec(1, spec.c, spec.h, spec.w, spec.k, spec.pad)
+            ref = lo.lance_gemm(s1, xh[img:img + 1], wh, in_params=arr, tile_m=TM)
+            d = int(np.sum(ref.view(np.uint32) != yh[img:img + 1].view(np.uint32)))
+            checked += ref.size
+            if d:
+                bad += d
+                worst = {"layer": [spec.c, spec.k, spec.h], "image": img, "mismatches": d}
+    return {"layers": len(state), "images_per_layer": 2, "outputs_checked": checked,
+            "mismatches": bad, "bitexact": bad == 0, "first_failure": worst,
+            "checker": "oracle lance_gemm (pinned restatement) with the GPU's input QuantParams",
+            "tolerance": "0 ULP"}
+
+
+def cpu_baseline_reference(layers, wl_name, N, args, gpu_layer_us):
+    """The reference's own lance_gemm (oracle/_ref) on this box's host cores:
+    all hardware threads on a bounded batch sample of every layer, one thread
+    on one image of every layer, and the 7x7 layer at the FULL batch (same
+    config as the GPU line) next to the GPU's time for that layer."""
+    import oracle
+    ref = oracle.Reference()
+    threads = os.cpu_count() or 1
+    v, tot = cpu_reference_images_per_s(args.cpu_batch, 3, threads, layers)
+    v1, tot1 = cpu_reference_images_per_s(1, 1, 1, layers)
+    out = {"value": v, "unit": "images/s", "cores": threads, "kind": "reference",
+           "cpu_model": cpu_model(),
+           "sample": f"{len(layers)} {wl_name} layers at batch {args.cpu_batch} (of {N}), reference "
+                     f"lance_gemm, all {threads} threads, median of 3 steady_clock repeats per layer "
+                     f"({tot:.2f} s/pass)",
+           "single_thread": {"value": v1, "unit": "images/s", "cores": 1,
+                             "sample": f"{len(layers)} layers at batch 1, 1 thread ({tot1:.2f} s/pass)"}}
+    if args.cpu_full_layer and (512, 512, 7) in [tuple(l) for l in layers]:
+        i = [tuple(l) for l in layers].index((512, 512, 7))
+        med_ns, _ = ref.time_lance_gemm(oracle.Spec(N, 512, 7, 7, 512, 1), threads, 42 + i, 1)
+        gpu_us = gpu_layer_us.get((512, 512, 7))
+        out["full_batch_layer"] = {
+            "layer": {"c": 512, "k": 512, "h": 7, "n": N}, "cpu_s": med_ns * 1e-9, "cores": threads,
+            "gpu_us": gpu_us, "gpu_vs_cpu": (med_ns * 1e-9) / (gpu_us * 1e-6) if gpu_us else None,
+            "note": "same layer, same batch, same inputs: the reference at full batch vs the GPU forward (K0+K1+GEMM)"}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=0, help="images per GPU (default: the workload's)")
+    ap.add_argument("--batch", type=int, default=0, help="global batch (default: the workload's)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong (north star): the global batch is split over the ranks; "
+                         "weak: every rank runs the full batch")
+    ap.add_argument("--mode", default="shard", choices=["shard", "global"],
+                    help="shard: per-shard fit, no collective (north star); global: K0 -> NCCL "
+                         "MAX all-reduce of the ranges -> K1 -> GEMM (bitwise one full-batch call)")
     ap.add_argument("--workload", default="resnet18", choices=sorted(WORKLOADS),
                     help="resnet18 = BASELINE config 3 (default), vgg16_cifar = config 2")
     ap.add_argument("--stack", action="store_true",
                     help="vgg16_cifar only: run the chained layer-stack driver (bias + ReLU + "
                          "2x2 max-pools, one CUDA graph per step) instead of independent layers")
-    ap.add_argument("--ref-batch", type=int, default=2)
+    ap.add_argument("--ref-batch", type=int, default=8)
     ap.add_argument("--cpu-batch", type=int, default=4)
+    ap.add_argument("--cpu-full-layer", type=int, default=1,
+                    help="also time the reference on the 7x7 layer at the full batch")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--layers", type=str, default="", help="comma list of layer indices (debug)")
     ap.add_argument("--tile-m", type=int, default=2, choices=[2, 4],
                     help="Winograd output tile: 2 = F(2x2,3x3) (reference), 4 = F(4x4,3x3) (BASELINE config 4)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    maybe_spawn(args)
 
     ws, rank, local = dist_setup()
     if args.impl == "reference":
@@ -364,45 +425,68 @@ def main():
     import numpy as np
     import torch
     import paper_2003_08646_b200 as lance
+    from paper_2003_08646_b200 import shard
 
+    ndev = torch.cuda.device_count()
+    shared_device = ws > ndev  # more ranks than GPUs: a logic check only (gloo, shared device)
+    local = local % max(ndev, 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
+    backend = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        backend = "gloo" if shared_device else "nccl"
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
         pg = dist
 
     wl_layers, wl_batch, wl_name = WORKLOADS[args.workload]
     layers = wl_layers
     if args.layers:
         layers = [wl_layers[int(i)] for i in args.layers.split(",")]
-    N = args.batch or wl_batch
+    G = args.batch or wl_batch  # global batch
     if args.stack:
-        run_stack(args, ws, rank, local, N)
+        run_stack(args, ws, rank, local, G)
         return
+    if args.scaling == "strong":
+        a0, b0 = shard.shard_range(G, ws, rank)
+    else:
+        a0, b0 = 0, G
+    N = b0 - a0  # this rank's images
     TM = args.tile_m
     cfg = lance.LanceConfig(8, 8, lance.Granularity.PerPosition, lance.LanceMode.Gemm)
 
-    # Synthetic inputs: UniformSource(seed) x then w (bench.hpp:129-133), per layer and rank.
+    # Synthetic inputs: UniformSource(seed) x then w (bench.hpp:129-133), one
+    # stream per layer for the whole global batch; strong scaling gives every
+    # rank its contiguous slice of that batch, weak scaling its own stream.
     state = []
     for i, (c, k, h) in enumerate(layers):
         spec = lance.ConvSpec(N, c, h, h, k, 1)
-        nx, nw = N * h * h * c, k * 9 * c
-        host = lance.uniform_floats(nx + nw, 42 + 1000 * rank + i)
-        x = torch.from_numpy(host[:nx]).to(dev).view(N, h, h, c)
-        w = torch.from_numpy(host[nx:]).to(dev).view(k, 3, 3, c)
+        gx, nw = G * h * h * c, k * 9 * c
+        seed = 42 + i if args.scaling == "strong" else 42 + 1000 * rank + i
+        host = lance.uniform_floats(gx + nw, seed)
+        per = h * h * c
+        xs = host[a0 * per:b0 * per]
+        x = torch.from_numpy(xs).to(dev).view(N, h, h, c)
+        w = torch.from_numpy(host[gx:gx + nw]).to(dev).view(k, 3, 3, c)
         conv = lance.LanceConv(spec, cfg, device=local, tile_m=TM)
         conv.set_filters(w)
         y = torch.empty((N, spec.out_h(), spec.out_w(), k), dtype=torch.float32, device=dev)
-        state.append((spec, conv, x, w, y, host))
+        state.append((spec, conv, x, w, y, xs, host[gx:gx + nw]))
     torch.cuda.synchronize(dev)
 
     stream = torch.cuda.current_stream(dev)
+    use_global = args.mode == "global" and ws > 1
 
     def step():
-        for spec, conv, x, w, y, _ in state:
-            conv.forward(x, y, stream=stream)
+        for spec, conv, x, w, y, *_ in state:
+            if use_global:
+                shard.global_forward(conv, x, y, stream=stream)
+            else:
+                conv.forward(x, y, stream=stream)
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -445,14 +529,14 @@ def main():
                           "us_per_forward": [round(m / max(nf, 1) * 1e3, 2) for m in ms]})
 
     if pg:
-        t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+        t = torch.tensor([elapsed], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         elapsed = float(t.item())
 
-    images = N * args.steps * ws
+    images = (G if args.scaling == "strong" else G * ws) * args.steps
     value = images / elapsed
     ms_per_step = elapsed / args.steps * 1e3
-    tops_eq = 2 * sum(direct_macs(c, k, h, N) for c, k, h in layers) * args.steps * ws / elapsed / 1e12
+    tops_eq = 2 * sum(direct_macs(c, k, h, 1) for c, k, h in layers) * images / elapsed / 1e12
 
     hbm, hbm_src = peaks()
     names = ["K0_input_range", "K1_transform_quantize", "K3K4_gemm_epilogue"]
@@ -470,7 +554,6 @@ def main():
             key = (si, spec.c, spec.k, spec.h)
             shape_ms.setdefault(key, []).append(pl["us_per_forward"][si])
     (dsi, dc, dk, dh), dus = max(shape_ms.items(), key=lambda kv: sum(kv[1]))
-    dom = dsi
     launch_us = float(np.mean(dus))
     launch_bytes = stage_bytes(dc, dk, dh, N, TM)[dsi]
     traffic = None
@@ -485,11 +568,11 @@ def main():
                 "frac": achieved / hbm, "traffic": traffic,
                 "algorithmic_bytes_per_launch": float(launch_bytes), "launch_us": launch_us,
                 "stages": stages}
-    i8 = int8_peak_tops(dev) if rank == 0 else None
+    i8, i8_src = int8_peak_tops()
     t3 = stage_ms[2] * 1e-3 / args.steps
     wmacs = sum(winograd_macs(c, k, h, N, TM) for c, k, h in layers)
     roofline["gemm_stage_int8"] = {"achieved_tops": 2 * wmacs / t3 / 1e12 if t3 > 0 else None,
-                                   "peak_tops": i8, "peak_source": "measured here: torch._int_mm 8192^3",
+                                   "peak_tops": i8, "peak_source": i8_src,
                                    "frac": (2 * wmacs / t3 / 1e12 / i8) if (i8 and t3 > 0) else None}
     # The GEMM stage's own roofline: min(INT8 peak, HBM x arithmetic intensity)
     # per layer (its operands + y must cross HBM at least once), summed as times.
@@ -504,6 +587,7 @@ def main():
             ach_s += t_meas
             rows.append({"c": spec.c, "h": spec.h, "ops_per_byte": round(ops / byt, 1),
                          "bound": "tensor" if ops / (i8 * 1e12) > byt / (hbm * 1e9) else "hbm",
+                         "tensor_frac": round(ops / t_meas / 1e12 / i8, 3) if t_meas > 0 else None,
                          "frac_of_attainable": round(t_floor / t_meas, 3) if t_meas > 0 else None})
         roofline["gemm_stage_int8"]["frac_of_attainable"] = att_s / ach_s if ach_s > 0 else None
         roofline["gemm_stage_int8"]["per_layer_attainable"] = rows
@@ -513,11 +597,11 @@ def main():
     e2e = None
     if not args.no_e2e:
         pinned = []
-        for spec, conv, x, w, y, host in state:
+        for spec, conv, x, w, y, xs, ws_host in state:
             hx = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
-            hx.copy_(torch.from_numpy(host[: x.numel()]).view(x.shape))
+            hx.copy_(torch.from_numpy(xs).view(x.shape))
             hw = torch.empty(w.shape, dtype=torch.float32, pin_memory=True)
-            hw.copy_(torch.from_numpy(host[x.numel():]).view(w.shape))
+            hw.copy_(torch.from_numpy(ws_host).view(w.shape))
             hy = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
             pinned.append((spec, hx.numpy(), hw.numpy(), hy.numpy()))
         h2d = sum(a.nbytes + b.nbytes for _, a, b, _ in pinned)
@@ -535,27 +619,64 @@ def main():
             e2e_step()
         te = time.perf_counter() - t0
         if pg:
-            t = torch.tensor([te], device=dev, dtype=torch.float64)
+            t = torch.tensor([te], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
             pg.all_reduce(t, op=pg.ReduceOp.MAX)
             te = float(t.item())
-        e2e = {"value": N * args.e2e_steps * ws / te, "unit": "images/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+        e2e = {"value": (G if args.scaling == "strong" else G * ws) * args.e2e_steps / te,
+               "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "steps": args.e2e_steps,
                "api": "lance_gemm(x, w, spec, cfg) host drop-in (K2 + K0 + K1 + K3/K4 per call, pinned host buffers)"}
+        lance.api._lib.lib().lance_host_cache_clear()
+
+    # ---- parity of the timed step against the CPU reference (outside the timed region) ----
+    parity = None
+    if not args.no_verify:
+        parity = verify_with_cpu_reference(state, cfg, TM, rank)
+        if pg:
+            t = torch.tensor([parity["mismatches"]], dtype=torch.float64,
+                             device=dev if backend == "nccl" else "cpu")
+            pg.all_reduce(t, op=pg.ReduceOp.SUM)
+            parity["mismatches"] = int(t.item())
+            parity["bitexact"] = parity["mismatches"] == 0
+            parity["ranks"] = ws
+
+    # ---- multi-GPU: NCCL verification of the global-fit mode (outside the timed region) ----
+    sharded = None
+    if ws > 1:
+        vi = next((i for i, l in enumerate(layers) if tuple(l) == (512, 512, 7)), len(layers) - 1)
+        vspec, *_ = state[vi]
+        c, k, h = layers[vi]
+        full = lance.uniform_floats(G * h * h * c + k * 9 * c, 42 + vi)
+        xf = full[:G * h * h * c].reshape(G, h, h, c)
+        wf = full[G * h * h * c:].reshape(k, 3, 3, c)
+        t0 = time.perf_counter()
+        yg = shard.verify_sharded(xf if rank == 0 else None, wf, lance.ConvSpec(G, c, h, h, k, 1),
+                                  cfg, tile_m=TM)
+        tv = time.perf_counter() - t0
+        sharded = {"layer": [c, k, h], "global_batch": G, "ranks": ws, "backend": backend,
+                   "wall_s": round(tv, 3)}
+        if rank == 0:
+            one = lance.LanceConv(lance.ConvSpec(G, c, h, h, k, 1), cfg, device=local, tile_m=TM)
+            one.set_filters(torch.from_numpy(np.ascontiguousarray(wf)).to(dev))
+            y1 = one.forward(torch.from_numpy(np.ascontiguousarray(xf)).to(dev))
+            one.sync()
+            yy = y1.cpu().numpy()
+            one.close()
+            sharded["bitexact_vs_one_full_batch_forward"] = bool(np.array_equal(
+                yy.view(np.uint32), yg.view(np.uint32)))
 
     cpu = None
+    gpu_layer_us = {}
+    for (spec, *_), pl in zip(state, per_layer):
+        gpu_layer_us.setdefault((spec.c, spec.k, spec.h), sum(pl["us_per_forward"]))
     if rank == 0 and ws == 1 and not args.no_cpu and TM == 4:
         v, tot = cpu_port_f4_images_per_s(1, layers)
-        cpu = {"value": v, "unit": "images/s", "cores": 1, "kind": "port",
+        cpu = {"value": v, "unit": "images/s", "cores": 1, "kind": "port", "cpu_model": cpu_model(),
                "sample": f"13 ResNet-18 3x3 layers at batch 1, oracle lo_lance_gemm_tiled(tile_m=4) "
                          f"single thread ({tot:.2f} s/pass); the reference has no F(4x4)"}
     elif rank == 0 and ws == 1 and not args.no_cpu:
         try:
-            threads = os.cpu_count() or 1
-            v, tot = cpu_reference_images_per_s(args.cpu_batch, 3, threads, layers)
-            cpu = {"value": v, "unit": "images/s", "cores": threads, "kind": "reference",
-                   "sample": f"{len(layers)} {wl_name} layers at batch {args.cpu_batch} (of {N}), reference "
-                             f"lance_gemm median of 3 steady_clock repeats per layer ({tot:.2f} s/pass)"}
+            cpu = cpu_baseline_reference(layers, wl_name, N, args, gpu_layer_us)
         except Exception as e:  # reference shim absent
             cpu = {"value": None, "unit": "images/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -564,22 +685,32 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (lance::UniformSource seed 42+layer, x then w; bench.hpp:129-133)",
-            "config": {"workload": wl_name + ("_f4x4" if TM == 4 else ""), "batch_per_gpu": N,
-                       "global_batch": N * ws,
+            "config": {"workload": wl_name + ("_f4x4" if TM == 4 else ""), "global_batch": G,
+                       "batch_per_gpu": N if args.scaling == "strong" else G,
                        "layers": [list(l) for l in layers], "winograd": f"F({TM}x{TM},3x3)",
                        "bits_w": 8, "bits_i": 8, "granularity": "PerPosition", "pad": 1,
-                       "parallelism": f"batch-shard x{ws}, no collective",
+                       "parallelism": (f"batch-shard x{ws}: contiguous slices of the global batch, "
+                                       + ("per-shard fit, no collective" if not use_global else
+                                          "global fit (one 2P+1-float NCCL MAX all-reduce per layer)"))
+                       if ws > 1 else "single GPU",
                        "filters": "prepared once per layer (K2) outside the step",
                        "l2": "no flush: per-step working set (13 layers x, codes, y) ~4 GB >> 126 MB L2"},
             "tops_equivalent": tops_eq,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 3 * len(layers) * args.steps,
+            "parity": parity,
+            "gpu_launches": (3 + (1 if use_global else 0)) * len(layers) * args.steps,
             "clocks": clk,
         }
+        if ws > 1:
+            line["multi_gpu"] = {"backend": backend, "ranks": ws, "devices_visible": ndev,
+                                 "verify_sharded": sharded}
+            if shared_device:
+                line["multi_gpu"]["note"] = ("more ranks than GPUs: ranks share a device over gloo; "
+                                             "a logic check, not a scaling measurement")
         print(json.dumps(line), flush=True)
     if pg:
         pg.barrier()

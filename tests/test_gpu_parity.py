@@ -264,3 +264,45 @@ def test_static_params_out_of_range_bitexact(lo, spec):
     for k in ("codes_a", "rowsum", "acc", "y"):
         assert np.array_equal(np.asarray(got[k]).view(np.uint8), np.asarray(ref[k]).view(np.uint8)), \
             f"{k}: {mismatch_report(got[k], ref[k])}"
+
+
+@pytest.mark.parametrize("tile_m", [2, 4])
+def test_device_ranges_across_shards(lo, tile_m):
+    # Global-fit mode through the device API (lance_plan_ranges ->
+    # element-wise MAX of the [-t_min, t_max, nan] buffers, what the NCCL
+    # all-reduce does across GPUs -> lance_plan_forward_ranges): the shards'
+    # outputs concatenate to one full-batch reference call bitwise.
+    spec = Spec(5, 64, 14, 14, 48, 1)
+    x, w = make_inputs(lo.uniform, spec, "relu", 43)
+    wd = torch.from_numpy(w).cuda()
+    from paper_2003_08646_b200 import shard
+    convs, bufs = [], []
+    for r in range(2):
+        a, b = shard.shard_range(spec.n, 2, r)
+        c = lance.LanceConv(lance.ConvSpec(b - a, spec.c, spec.h, spec.w, spec.k, 1), gemm_cfg(),
+                            tile_m=tile_m)
+        c.set_filters(wd)
+        xs = torch.from_numpy(np.ascontiguousarray(x[a:b])).cuda()
+        bufs.append(c.ranges(xs))
+        convs.append((c, xs))
+    g = torch.maximum(bufs[0], bufs[1])
+    ys = []
+    for c, xs in convs:
+        ys.append(c.forward(xs, ranges=g))
+        c.sync()
+    got = torch.cat(ys).cpu().numpy()
+    ref = lo.lance_gemm(spec, x, w, tile_m=tile_m)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), mismatch_report(got, ref)
+    # a NaN on one shard is reported by every shard's forward (the reference
+    # throws from fit_params over the whole batch, quant.hpp:62)
+    xb = x[:2].copy()
+    xb[1, 3, 3, 5] = np.nan
+    c0, xs0 = convs[0]
+    bad = c0.ranges(torch.from_numpy(xb).cuda())
+    g2 = torch.maximum(bad, bufs[1])
+    c1, xs1 = convs[1]
+    c1.forward(xs1, ranges=g2)
+    with pytest.raises(lance.LanceNaNError):
+        c1.sync()
+    for c, _ in convs:
+        c.close()

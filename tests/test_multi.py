@@ -136,3 +136,43 @@ def test_gloo_world3_scatter_gather_and_36_position_allreduce():
     assert np.array_equal(results["back"], np.arange(7 * 60, dtype=np.float32).reshape(7, 3, 4, 5))
     assert np.array_equal(results["glo"], np.linspace(-1, 0, 36).astype(np.float32) - 2)
     assert np.array_equal(results["ghi"], np.linspace(0, 1, 36).astype(np.float32) + 2)
+
+
+def _ranges_worker(rank, world, port, results):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # a LanceConv.ranges buffer: [-t_min[16], t_max[16], nan]; rank 1 saw a NaN
+        o = Oracle()
+        v = o.uniform(11 + rank, 16 * 50).reshape(16, 50) * np.float32(2.5 + rank)
+        buf = torch.from_numpy(np.concatenate([-v.min(axis=1), v.max(axis=1),
+                                               [1.0 if rank == 1 else 0.0]]).astype(np.float32))
+        shard.allreduce_ranges(buf)
+        results[rank] = buf.numpy()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_device_ranges_buffer_reduce():
+    # The 2P+1-float buffer of the global-fit mode: one element-wise MAX gives
+    # the global (min, max) per position (-(-x) exact) and propagates the NaN
+    # flag (fmax would drop a NaN value itself, so it travels as 1.0).
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_ranges_worker, args=(2, _free_port(), results), nprocs=2, join=True)
+    o = Oracle()
+    vs = [o.uniform(11 + r, 16 * 50).reshape(16, 50) * np.float32(2.5 + r) for r in range(2)]
+    allv = np.concatenate(vs, axis=1)
+    for r in range(2):
+        got = results[r]
+        assert np.array_equal(-got[:16], allv.min(axis=1))
+        assert np.array_equal(got[16:32], allv.max(axis=1))
+        assert got[32] == 1.0
+        ps = shard.params_from_minmax(-got[:16], got[16:32], 8)
+        for p, row in zip(ps, allv):
+            ref = o.fit_params(row, 8)
+            assert (p.t_min, p.t_max, p.scale) == (ref.t_min, ref.t_max, ref.scale)
