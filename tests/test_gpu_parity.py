@@ -295,7 +295,7 @@ def test_device_ranges_across_shards(lo, tile_m):
     assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), mismatch_report(got, ref)
     # a NaN on one shard is reported by every shard's forward (the reference
     # throws from fit_params over the whole batch, quant.hpp:62)
-    xb = x[:2].copy()
+    xb = x[:3].copy()  # shard 0 holds images 0..2
     xb[1, 3, 3, 5] = np.nan
     c0, xs0 = convs[0]
     bad = c0.ranges(torch.from_numpy(xb).cuda())
