@@ -494,18 +494,24 @@ __global__ void static_params_kernel(LanceDevState* st, StaticParams prm, int C)
 }
 
 // --------------------------------------------------------------------------
-// K0 (C % 64 == 0): the two new input columns of the next D
-// tiles are staged per lane with cp.async (8-byte copies, zero-fill outside
-// the image) in a shared-memory ring instead of registers, so the lookahead
-// is not limited by the register budget.  A lane only ever reads back the
-// slots it copied itself, so per-thread cp.async groups are the only ordering
-// needed.  Arithmetic as input_range_kernel.
-template <int D>
-__global__ void __launch_bounds__(256, 2) input_range_async_kernel(const float* __restrict__ x,
-                                                                   float* __restrict__ partials,
-                                                                   LanceDevState* __restrict__ st,
-                                                                   InGeom g) {
-  extern __shared__ float2 s_ring[];  // [8 warps][D slots][2 columns][4 rows][32 lanes]
+// K0 (C % 64 == 0), lean ring version.  A warp walks a strip (img, tile row
+// ti, tiles tj0..tj1, 64 channels = 2 per lane).  Pair q = input columns
+// xx0 + 2q, xx0 + 2q + 1 (tile t of the strip uses pairs t and t + 1); every
+// pair is staged per lane with eight 8-byte cp.async (zero fill for rows /
+// columns outside the image = extract_tiles' zero padding, tensor.hpp:141-147)
+// into a ring of D + 1 slots, D pairs ahead of the tile being transformed.
+// Addressing is four 64-bit row pointers bumped by 2C per pair, with the
+// pair's second column at an immediate offset when C is a template constant
+// (CC > 0): no per-copy multiplies.  A lane only reads back the slots it
+// copied itself, so per-thread cp.async groups are the only ordering needed.
+// Transform and range arithmetic as input_range_kernel.
+template <int D, int CC>
+__global__ void __launch_bounds__(256, 2) input_range_ring_kernel(const float* __restrict__ x,
+                                                                  float* __restrict__ partials,
+                                                                  LanceDevState* __restrict__ st,
+                                                                  InGeom g) {
+  constexpr int R = D + 1;
+  extern __shared__ float2 s_ring[];  // [8 warps][R slots][2 columns x 4 rows][32 lanes]
   __shared__ float s_red[256];
   float lo[16], hi[16];
 #pragma unroll
@@ -514,49 +520,81 @@ __global__ void __launch_bounds__(256, 2) input_range_async_kernel(const float* 
     hi[p] = __int_as_float(0xff800000);
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float2* ring = s_ring + static_cast<size_t>(warp) * D * 8 * 32;
+  const int C = CC > 0 ? CC : g.C;
+  const int W = g.W;
+  float2* const ring = s_ring + static_cast<size_t>(warp) * R * 8 * 32 + lane;
   const long long stride = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
   for (long long item = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + warp;
        item < g.num_items; item += stride) {
     const StripItem it = strip_item(g, item, lane);
-    const Strip<true> sp(x, g, it);
-    // Zero-fill copies read nothing when their size is 0, so the (possibly
-    // out-of-image) address is passed unconditionally and only the size is
-    // predicated: per-row sizes once per strip, one AND per copy.
+    const int xx0 = 2 * it.tj0 - g.pad;
+    const float* img = x + static_cast<long long>(it.img) * g.H * W * C + it.ch;
+    const float* cp[4];
     uint32_t rsz[4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) rsz[a] = (sp.rok[a] && sp.c0ok) ? 8u : 0u;
-    auto issue = [&](int tj) {  // the 2 new columns of tile tj into slot tj % D
-      float2* slot = ring + (tj % D) * 8 * 32;
-      if (tj < it.tj1) {
+    for (int a = 0; a < 4; ++a) {
+      const int yy = 2 * it.ti - g.pad + a;
+      const bool ok = (yy >= 0) && (yy < g.H);
+      cp[a] = img + (static_cast<long long>(ok ? yy : 0) * W + xx0) * C;
+      rsz[a] = ok ? 8u : 0u;
+    }
+    const int n = it.tj1 - it.tj0;  // tiles; pairs 0..n
+    int c0 = xx0;                   // first column of the next pair to issue
+    int q_issue = 0;
+    float2* wslot = ring;
+    auto issue = [&]() {
+      if (q_issue <= n) {
+        if (c0 >= 0 && c0 + 1 < W) {  // interior pair (warp-uniform)
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          const int xx = 2 * tj - g.pad + 2 + cc;
-          const uint32_t cz = (static_cast<unsigned>(xx) < static_cast<unsigned>(g.W)) ? 0xFFFFFFFFu : 0u;
-          const long long co = static_cast<long long>(xx) * g.C;
+          for (int a = 0; a < 4; ++a) {
+            cp_async8_sz(wslot + a * 32, cp[a], rsz[a]);
+            cp_async8_sz(wslot + (4 + a) * 32, cp[a] + C, rsz[a]);
+          }
+        } else {
+          const uint32_t m0 = (static_cast<unsigned>(c0) < static_cast<unsigned>(W)) ? ~0u : 0u;
+          const uint32_t m1 = (static_cast<unsigned>(c0 + 1) < static_cast<unsigned>(W)) ? ~0u : 0u;
 #pragma unroll
-          for (int a = 0; a < 4; ++a)
-            cp_async8_sz(slot + (cc * 4 + a) * 32 + lane, sp.row[a] + co, rsz[a] & cz);
+          for (int a = 0; a < 4; ++a) {
+            cp_async8_sz(wslot + a * 32, cp[a], rsz[a] & m0);
+            cp_async8_sz(wslot + (4 + a) * 32, cp[a] + C, rsz[a] & m1);
+          }
         }
-      }
-      cp_async_commit();  // one group per tile, empty past the strip end
-    };
-    float2 ta[4], tb[4], tc[4], td[4];
-    const int xx0 = 2 * it.tj0 - g.pad;
-    sp.column(xx0, ta);
-    sp.column(xx0 + 1, tb);
 #pragma unroll
-    for (int q = 0; q < D; ++q) issue(it.tj0 + q);
-    for (int tj = it.tj0; tj < it.tj1; ++tj) {
-      cp_async_wait<D - 1>();  // this tile's group has landed
-      const float2* slot = ring + (tj % D) * 8 * 32;
-      float2 pc[4], pd[4];
+        for (int a = 0; a < 4; ++a) cp[a] += 2 * C;
+        c0 += 2;
+      }
+      cp_async_commit();  // one group per pair, empty past the strip end
+      ++q_issue;
+      wslot += 8 * 32;
+      if (wslot == ring + R * 8 * 32) wslot = ring;
+    };
+#pragma unroll
+    for (int q = 0; q < R; ++q) issue();  // pairs 0..D
+    float2 ta[4], tb[4];
+    const float2* rslot = ring;
+    {
+      cp_async_wait<D>();  // pair 0
+      float2 d0[4], d1[4];
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        pc[a] = slot[a * 32 + lane];
-        pd[a] = slot[(4 + a) * 32 + lane];
+        d0[a] = rslot[a * 32];
+        d1[a] = rslot[(4 + a) * 32];
       }
-      issue(tj + D);  // refill the slot just read (program order: reads first)
+      colpass(d0, ta);
+      colpass(d1, tb);
+      rslot += 8 * 32;
+    }
+    for (int t = 0; t < n; ++t) {
+      cp_async_wait<D - 1>();  // pair t + 1
+      float2 pc[4], pd[4], tc[4], td[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        pc[a] = rslot[a * 32];
+        pd[a] = rslot[(4 + a) * 32];
+      }
+      rslot += 8 * 32;
+      if (rslot == ring + R * 8 * 32) rslot = ring;
+      issue();  // pair t + 1 + D into the slot of pair t (consumed last iteration)
       colpass(pc, tc);
       colpass(pd, td);
       float2 v[16];
@@ -572,8 +610,8 @@ __global__ void __launch_bounds__(256, 2) input_range_async_kernel(const float* 
         tb[a] = td[a];
       }
     }
-    cp_async_wait<0>();
   }
+  cp_async_wait<0>();
   if (block_minmax_and_ticket(lo, hi, partials, &st->ticket_in, s_red)) {
     fit_from_ranges(s_red, g.granularity, st->bits_i, st->a_tmin, st->a_tmax, st->a_scale,
                     st->a_rcp, &st->nan_in);
@@ -708,11 +746,21 @@ cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceD
   if (g.C < 32) {
     input_range_smallc_kernel<<<grid, 256, 0, s>>>(x, partials, st, g);
   } else if (g.C % 64 == 0) {
-    const size_t smem = static_cast<size_t>(8) * kDepth * 8 * 32 * sizeof(float2);
-    const cudaError_t attr =
-        ensure_smem_attr(reinterpret_cast<const void*>(input_range_async_kernel<kDepth>), smem);
-    if (attr != cudaSuccess) return attr;
-    input_range_async_kernel<kDepth><<<grid, 256, smem, s>>>(x, partials, st, g);
+    const size_t smem = static_cast<size_t>(8) * (kDepth + 1) * 8 * 32 * sizeof(float2);
+#define LANCE_K0_RING(CCV)                                                                        \
+    if (CCV == 0 || g.C == CCV) {                                                                \
+      const cudaError_t attr =                                                                   \
+          ensure_smem_attr(reinterpret_cast<const void*>(input_range_ring_kernel<kDepth, CCV>), smem); \
+      if (attr != cudaSuccess) return attr;                                                      \
+      input_range_ring_kernel<kDepth, CCV><<<grid, 256, smem, s>>>(x, partials, st, g);          \
+      return cudaGetLastError();                                                                 \
+    }
+    LANCE_K0_RING(64)
+    LANCE_K0_RING(128)
+    LANCE_K0_RING(256)
+    LANCE_K0_RING(512)
+    LANCE_K0_RING(0)
+#undef LANCE_K0_RING
   } else if (vec2) {
     input_range_kernel<true><<<grid, 256, 0, s>>>(x, partials, st, g);
   } else {
