@@ -340,7 +340,7 @@ def verify_with_cpu_reference(state, cfg, TM, rank):
         pa, _ = conv.params()
         arr = lance.params_array(pa)
         yh = y.cpu().numpy()
-        xh = x.cpu().numpy()
+        xh = np.asarray(host).reshape(spec.n, spec.h, spec.w, spec.c)  # NHWC whatever the device layout
         wh = w.cpu().numpy()
         for img in sorted({0, spec.n - 1}):
             s1 = oracle.Spec(1, spec.c, spec.h, spec.w, spec.k, spec.pad)
@@ -411,6 +411,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--layers", type=str, default="", help="comma list of layer indices (debug)")
+    ap.add_argument("--layout", default="nhwc", choices=["nhwc", "nchw"],
+                    help="input layout of x (nchw: the north-star NCHW option, F(2x2) only)")
     ap.add_argument("--tile-m", type=int, default=2, choices=[2, 4],
                     help="Winograd output tile: 2 = F(2x2,3x3) (reference), 4 = F(4x4,3x3) (BASELINE config 4)")
     args = ap.parse_args()
@@ -471,8 +473,10 @@ def main():
         per = h * h * c
         xs = host[a0 * per:b0 * per]
         x = torch.from_numpy(xs).to(dev).view(N, h, h, c)
+        if args.layout == "nchw":  # same images, PyTorch's [N, C, H, W] layout
+            x = x.permute(0, 3, 1, 2).contiguous()
         w = torch.from_numpy(host[gx:gx + nw]).to(dev).view(k, 3, 3, c)
-        conv = lance.LanceConv(spec, cfg, device=local, tile_m=TM)
+        conv = lance.LanceConv(spec, cfg, device=local, tile_m=TM, layout=args.layout)
         conv.set_filters(w)
         y = torch.empty((N, spec.out_h(), spec.out_w(), k), dtype=torch.float32, device=dev)
         state.append((spec, conv, x, w, y, xs, host[gx:gx + nw]))
@@ -494,8 +498,6 @@ def main():
         step()
     for _, conv, *_ in state:
         conv.sync(stream)
-    for _, conv, *_ in state:
-        conv.stage_timing(True)
     if pg:
         pg.barrier()
     torch.cuda.synchronize(dev)
@@ -514,6 +516,15 @@ def main():
     elapsed = e0.elapsed_time(e1) * 1e-3
     for _, conv, *_ in state:
         conv.sync(stream)  # surfaces a NaN error from any range pass
+
+    # Per-stage device times: a separate pass with CUDA events between the
+    # kernels (events serialise the programmatic-dependent launches, so the
+    # headline step above runs without them).
+    for _, conv, *_ in state:
+        conv.stage_timing(True)
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize(dev)
 
     # per-stage device times over the timed region
     stage_ms = np.zeros(3)
@@ -598,8 +609,9 @@ def main():
     if not args.no_e2e:
         pinned = []
         for spec, conv, x, w, y, xs, ws_host in state:
-            hx = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
-            hx.copy_(torch.from_numpy(xs).view(x.shape))
+            xshape = (spec.n, spec.h, spec.w, spec.c)  # the host drop-in is the reference's NHWC
+            hx = torch.empty(xshape, dtype=torch.float32, pin_memory=True)
+            hx.copy_(torch.from_numpy(xs).view(xshape))
             hw = torch.empty(w.shape, dtype=torch.float32, pin_memory=True)
             hw.copy_(torch.from_numpy(ws_host).view(w.shape))
             hy = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
@@ -689,7 +701,7 @@ def main():
             "data": "synthetic (lance::UniformSource seed 42+layer, x then w; bench.hpp:129-133)",
             "config": {"workload": wl_name + ("_f4x4" if TM == 4 else ""), "global_batch": G,
                        "batch_per_gpu": N if args.scaling == "strong" else G,
-                       "layers": [list(l) for l in layers], "winograd": f"F({TM}x{TM},3x3)",
+                       "layers": [list(l) for l in layers], "winograd": f"F({TM}x{TM},3x3)", "input_layout": args.layout.upper(),
                        "bits_w": 8, "bits_i": 8, "granularity": "PerPosition", "pad": 1,
                        "parallelism": (f"batch-shard x{ws}: contiguous slices of the global batch, "
                                        + ("per-shard fit, no collective" if not use_global else

@@ -140,6 +140,18 @@ LANCE_API int lance_plan_ranges(lance_plan_t plan, const float* x_dev, float* mi
 LANCE_API int lance_plan_forward_ranges(lance_plan_t plan, const float* minmax_dev,
                                         const float* x_dev, float* y_dev, void* stream);
 
+/* Input layout of subsequent forwards / range passes (north-star option; the
+ * reference is NHWC-only, tensor.hpp:24-55).  LANCE_LAYOUT_NCHW reads x as
+ * [N][C][H][W] fp32 (PyTorch's default): a shared-memory tiled transpose with
+ * coalesced 128-bit channel-row loads stages it as NHWC in plan memory (one
+ * extra launch, N*H*W*C*4 bytes), then the NHWC kernels run, so codes,
+ * parameters and y (NHWC) are bit-identical to the NHWC path.  Needs
+ * N * H < 65536. */
+#define LANCE_LAYOUT_NHWC 0
+#define LANCE_LAYOUT_NCHW 1
+LANCE_API int lance_plan_set_input_layout(lance_plan_t plan, int layout);
+LANCE_API int lance_plan_input_layout(lance_plan_t plan);
+
 /* Optional fused bias + ReLU epilogue for subsequent forwards (north-star
  * extension; no reference oracle: equals relu(lance_gemm(x, w) + bias)).
  * bias_dev may be NULL (no bias).  relu is 0 or 1. */

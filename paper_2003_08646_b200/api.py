@@ -194,17 +194,28 @@ class LanceConv:
     streams); every kernel is the in-tree sm_100a library.
     """
 
-    def __init__(self, spec: ConvSpec, cfg: LanceConfig, device: int = 0, tile_m: int = 2):
+    def __init__(self, spec: ConvSpec, cfg: LanceConfig, device: int = 0, tile_m: int = 2,
+                 layout: str = "nhwc"):
         """tile_m=2: the reference F(2x2,3x3) path; tile_m=4: the F(4x4,3x3)
-        extension (36 positions in params / dumps)."""
+        extension (36 positions in params / dumps).  layout="nchw" reads x as
+        [N, C, H, W] (north-star option: a staging transpose on the device,
+        then the NHWC kernels; y stays NHWC, the reference layout)."""
         self.spec = spec
         self.cfg = cfg
         self.device = device
         self.tile_m = int(tile_m)
+        if layout not in ("nhwc", "nchw"):
+            raise LanceError("layout must be 'nhwc' or 'nchw'")
+        self.layout = layout
         self._plan = ct.c_void_p()
         L = _lib.lib()
         _check(L.lance_plan_create_tiled(ct.byref(spec._c()), ct.byref(cfg._c()), self.tile_m,
                                          device, ct.byref(self._plan)))
+        if layout == "nchw":
+            rc = L.lance_plan_set_input_layout(self._plan, 1)
+            if rc:
+                self.close()
+                _check(rc)
         self.positions = int(L.lance_plan_positions(self._plan))
         self._acc = None
         self._bias = None
@@ -229,6 +240,11 @@ class LanceConv:
     @property
     def device_bytes(self) -> int:
         return int(_lib.lib().lance_plan_device_bytes(self._plan))
+
+    @property
+    def input_shape(self):
+        s = self.spec
+        return (s.n, s.c, s.h, s.w) if self.layout == "nchw" else (s.n, s.h, s.w, s.c)
 
     def _check_tensor(self, t, shape, name):
         import torch
@@ -272,7 +288,7 @@ class LanceConv:
         engines.hpp:157-165)."""
         import torch
         s = self.spec
-        self._check_tensor(x, (s.n, s.h, s.w, s.c), "input tensor")
+        self._check_tensor(x, self.input_shape, "input tensor")
         n = 2 * self.positions + 1
         if out is None:
             out = torch.empty(n, dtype=torch.float32, device=x.device)
@@ -290,7 +306,7 @@ class LanceConv:
         from global ranges instead of this batch's (no host round trip)."""
         import torch
         s = self.spec
-        self._check_tensor(x, (s.n, s.h, s.w, s.c), "input tensor")
+        self._check_tensor(x, self.input_shape, "input tensor")
         if y is None:
             y = torch.empty((s.n, s.out_h(), s.out_w(), s.k), dtype=torch.float32,
                             device=x.device)

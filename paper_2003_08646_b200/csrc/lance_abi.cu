@@ -71,6 +71,11 @@ cudaError_t ensure_smem_attr(const void* fn, size_t bytes) {
   return e;
 }
 
+bool pdl_enabled() {
+  static const bool on = lance_knob("LANCE_PDL", 0) != 0;
+  return on;
+}
+
 int current_sm_count() {
   static std::mutex mu;
   static std::map<int, int> cache;
@@ -175,6 +180,8 @@ struct lance_plan_s {
   int sm_count = 148;
   int range_grid = 1, filter_grid = 1;
   InGeom in_geom{};
+  int layout = LANCE_LAYOUT_NHWC;
+  float* x_nhwc = nullptr;  // NCHW input: staging buffer of the transposed batch
   FilterGeom f_geom{};
   GemmGeom gemm_geom{};
   bool vec2 = false;
@@ -232,6 +239,7 @@ void free_plan(lance_plan_s* p) {
   cudaFree(p->gemm_geom.trace);
   for (cudaEvent_t e : p->events) cudaEventDestroy(e);
   p->events.clear();
+  cudaFree(p->x_nhwc);
   cudaFree(p->codes_a);
   cudaFree(p->rowsum);
   cudaFree(p->codes_w);
@@ -643,6 +651,11 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
     ++p->recorded;
     LANCE_CUDA(cudaEventRecord(ev[0], s));
   }
+  if (p->layout == LANCE_LAYOUT_NCHW) {  // staging transpose, then the NHWC kernels
+    LANCE_CUDA(launch_nchw_to_nhwc(x_dev, p->x_nhwc, p->spec.n, p->spec.c, p->spec.h, p->spec.w, s));
+    x_dev = p->x_nhwc;
+    ++launches;
+  }
   if (p->tm == 4) {
     if (static_params) {
       StaticParams prm{};
@@ -667,7 +680,7 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
     LANCE_CUDA(launch_f4_gemm(p->codes_a, p->codes_w, p->rowsum, p->colsum, p->small_acc, p->state, y_dev,
                               p->acc_dump, p->bias, p->relu, p->f4, s));
     if (ev) LANCE_CUDA(cudaEventRecord(ev[3], s));
-    p->last_launches = 3;
+    p->last_launches = launches + 3;
     return LANCE_OK;
   }
   if (static_params) {
@@ -719,8 +732,13 @@ int lance_plan_ranges(lance_plan_t p, const float* x_dev, float* minmax_dev, voi
   auto s = static_cast<cudaStream_t>(stream);
   if (p->tm == 4)
     LANCE_CUDA(launch_f4_range(x_dev, p->partials, p->range_grid, p->state, p->f4, s));
-  else
+  else {
+    if (p->layout == LANCE_LAYOUT_NCHW) {
+      LANCE_CUDA(launch_nchw_to_nhwc(x_dev, p->x_nhwc, p->spec.n, p->spec.c, p->spec.h, p->spec.w, s));
+      x_dev = p->x_nhwc;
+    }
     LANCE_CUDA(launch_input_range(x_dev, p->partials, p->range_grid, p->state, p->in_geom, p->vec2, s));
+  }
   LANCE_CUDA(launch_export_minmax(p->state, minmax_dev, p->np, s));
   return LANCE_OK;
 }
@@ -730,6 +748,23 @@ int lance_plan_forward_ranges(lance_plan_t p, const float* minmax_dev, const flo
   if (!minmax_dev) return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_forward_ranges: null ranges");
   return run_forward(p, x_dev, y_dev, static_cast<cudaStream_t>(stream), nullptr, minmax_dev);
 }
+
+int lance_plan_set_input_layout(lance_plan_t p, int layout) {
+  if (!p) return fail(LANCE_ERR_INVALID_ARGUMENT, "null plan");
+  if (layout != LANCE_LAYOUT_NHWC && layout != LANCE_LAYOUT_NCHW)
+    return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_set_input_layout: layout must be NHWC or NCHW");
+  if (layout == LANCE_LAYOUT_NCHW && static_cast<long long>(p->spec.n) * p->spec.h >= 65536)
+    return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_set_input_layout: NCHW input needs N * H < 65536");
+  if (layout == LANCE_LAYOUT_NCHW && !p->x_nhwc) {
+    DeviceGuard guard(p->device);
+    int rc = dev_alloc(p, &p->x_nhwc, sizeof(float) * size_t(p->spec.n) * p->spec.h * p->spec.w * p->spec.c);
+    if (rc) return rc;
+  }
+  p->layout = layout;
+  return LANCE_OK;
+}
+
+int lance_plan_input_layout(lance_plan_t p) { return p ? p->layout : -1; }
 
 int lance_plan_set_epilogue(lance_plan_t p, const float* bias_dev, int relu) {
   if (!p) return fail(LANCE_ERR_INVALID_ARGUMENT, "null plan");

@@ -15,6 +15,18 @@
 
 namespace lance_dev {
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: every forward-path kernel is launched with
+// programmatic stream serialisation (launch_k), so it may become resident
+// while its predecessor drains.  pdl_entry() first lets this grid's own
+// dependent launch early, then blocks until the predecessor grid has completed
+// and its memory is visible (griddepcontrol.wait): nothing before it may touch
+// global memory.  Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
 // ---------------------------------------------------------------- packed f32x2
 // sm_100a FADD2 / FMUL2 / FFMA2: two IEEE-RN operations per instruction.
 #define LANCE_F2_BINOP(name, op)                                                             \

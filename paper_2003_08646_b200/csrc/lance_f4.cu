@@ -341,6 +341,7 @@ __global__ void __launch_bounds__(256, 2) f4_range_kernel(const float* __restric
                                                           float* __restrict__ partials,
                                                           LanceDevState* __restrict__ st,
                                                           F4Geom g) {
+  pdl_entry();
   __shared__ float s_red[8 * 72];
   __shared__ float s_fin[72];
   float lo[kNP4], hi[kNP4];
@@ -418,6 +419,7 @@ __global__ void __launch_bounds__(256, 2) f4_quant_kernel(const float* __restric
                                                           int32_t* __restrict__ rowsum,
                                                           const LanceDevState* __restrict__ st,
                                                           F4Geom g) {
+  pdl_entry();
   __shared__ float2 s_tmin2[18], s_rcp2[18], s_scale2[18];
   if (threadIdx.x < 18) {
     const int p = threadIdx.x;
@@ -538,6 +540,7 @@ __global__ void __launch_bounds__(256, 2) f4_filter_transform_kernel(const float
                                                                      float* __restrict__ partials,
                                                                      LanceDevState* __restrict__ st,
                                                                      F4Geom g) {
+  pdl_entry();
   __shared__ float s_red[8 * 72];
   __shared__ float s_fin[72];
   float lo[kNP4], hi[kNP4];
@@ -587,6 +590,7 @@ __global__ void __launch_bounds__(128) f4_filter_quant_kernel(const float* __res
                                                               int32_t* __restrict__ colsum,
                                                               const LanceDevState* __restrict__ st,
                                                               F4Geom g) {
+  pdl_entry();
   __shared__ int s_sum[4];
   const int k = blockIdx.x;
   const float top = static_cast<float>((1 << st->bits_w) - 1);
@@ -677,6 +681,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
     mbar_init(b_full, 1);
     fence_barrier_init();
   }
+  pdl_entry();  // barriers above are shared-memory only
   if (threadIdx.x < kNP4) {
     s_k1[threadIdx.x] = st->k1[threadIdx.x];
     s_k2[threadIdx.x] = st->k2[threadIdx.x];
@@ -762,7 +767,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
                                           : sa + a_bytes + uu * Cfg::kBBytes;
 #pragma unroll
                 for (int kk = 0; kk < BK / 32; ++kk) {
-                  if (g.exp & 2) break;
+                  if (kExpSwitches && (g.exp & 2)) break;
                   const uint64_t adesc = umma_smem_desc(ua + kk * 32, 8 * BK, Cfg::kLayout);
                   const uint64_t bdesc = umma_smem_desc(ub + kk * 32, 8 * BK, Cfg::kLayout);
                   umma_i8(d_base + static_cast<uint32_t>(a * kF4BN), adesc, bdesc, kIdesc,
@@ -868,7 +873,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
                   acc_dump[(static_cast<long long>(6 * a + j) * g.M + m) * g.K + kf0 + 2 * fh + f] =
                       static_cast<int32_t>(ac[a][f]);
           }
-          if (g.exp & 1) continue;
+          if (kExpSwitches && (g.exp & 1)) continue;
           float2 mm[6];
 #pragma unroll
           for (int a = 0; a < 6; ++a) {
@@ -925,7 +930,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
       // c ^ (tile & 7): conflict-free both ways), then its 4 warps write whole
       // 64-byte pixel segments (4 lanes per pixel) instead of one scattered
       // 16-byte piece per lane.
-      if (g.exp & 4) continue;
+      if (kExpSwitches && (g.exp & 4)) continue;
       int pix0 = 0, vmask = 0;  // first output pixel of this lane's tile; bit 4i + b valid
       if (row_ok) {
         const int img = m / g.P, tt = m - (m / g.P) * g.P;
@@ -1020,11 +1025,11 @@ cudaError_t launch_f4_range(const float* x, float* partials, int grid, LanceDevS
                                  : ensure_smem_attr(reinterpret_cast<const void*>(f4_range_kernel<4>), smem);
     if (e != cudaSuccess) return e;
     if (d == 2)
-      f4_range_kernel<2><<<grid, 256, smem, s>>>(x, partials, st, g);
+      LANCE_LAUNCH_CHECK(launch_k(f4_range_kernel<2>, grid, 256, smem, s, x, partials, st, g));
     else
-      f4_range_kernel<4><<<grid, 256, smem, s>>>(x, partials, st, g);
+      LANCE_LAUNCH_CHECK(launch_k(f4_range_kernel<4>, grid, 256, smem, s, x, partials, st, g));
   } else {
-    f4_range_kernel<0><<<grid, 256, 0, s>>>(x, partials, st, g);
+    LANCE_LAUNCH_CHECK(launch_k(f4_range_kernel<0>, grid, 256, 0, s, x, partials, st, g));
   }
   return cudaGetLastError();
 }
@@ -1046,13 +1051,13 @@ cudaError_t launch_f4_quant(const float* x, uint8_t* codes, int32_t* rowsum,
           : ensure_smem_attr(reinterpret_cast<const void*>(f4_quant_kernel<false, BKV, NKV, 2>), qsmem); \
       if (ea != cudaSuccess) return ea;                                                       \
       if (static_mode)                                                                        \
-        f4_quant_kernel<true, BKV, NKV, 2><<<grid, 256, qsmem, s>>>(x, codes, rowsum, st, g); \
+        LANCE_LAUNCH_CHECK(launch_k(f4_quant_kernel<true, BKV, NKV, 2>, grid, 256, qsmem, s, x, codes, rowsum, st, g)); \
       else                                                                                    \
-        f4_quant_kernel<false, BKV, NKV, 2><<<grid, 256, qsmem, s>>>(x, codes, rowsum, st, g); \
+        LANCE_LAUNCH_CHECK(launch_k(f4_quant_kernel<false, BKV, NKV, 2>, grid, 256, qsmem, s, x, codes, rowsum, st, g)); \
     } else if (static_mode) {                                                                 \
-      f4_quant_kernel<true, BKV, NKV><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);          \
+      LANCE_LAUNCH_CHECK(launch_k(f4_quant_kernel<true, BKV, NKV>, grid, 256, 0, s, x, codes, rowsum, st, g));          \
     } else {                                                                                  \
-      f4_quant_kernel<false, BKV, NKV><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);         \
+      LANCE_LAUNCH_CHECK(launch_k(f4_quant_kernel<false, BKV, NKV>, grid, 256, 0, s, x, codes, rowsum, st, g));         \
     }                                                                                         \
     return cudaGetLastError();                                                                \
   }
@@ -1069,10 +1074,10 @@ cudaError_t launch_f4_quant(const float* x, uint8_t* codes, int32_t* rowsum,
 cudaError_t launch_f4_filter_prepare(const float* w, float* u_tmp, float* partials, int grid,
                                      uint8_t* codes_w, int32_t* colsum, LanceDevState* st,
                                      const F4Geom& g, cudaStream_t s) {
-  f4_filter_transform_kernel<<<grid, 256, 0, s>>>(w, u_tmp, partials, st, g);
+  LANCE_LAUNCH_CHECK(launch_k(f4_filter_transform_kernel, grid, 256, 0, s, w, u_tmp, partials, st, g));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  f4_filter_quant_kernel<<<g.K, 128, 0, s>>>(u_tmp, codes_w, colsum, st, g);
+  LANCE_LAUNCH_CHECK(launch_k(f4_filter_quant_kernel, g.K, 128, 0, s, u_tmp, codes_w, colsum, st, g));
   return cudaGetLastError();
 }
 
@@ -1117,8 +1122,8 @@ static cudaError_t launch_f4_gemm_t(const uint8_t* codes_a, const uint8_t* codes
   }
   const int cap = g.b_resident ? res_grid : sms;
   const int grid = static_cast<int>(tiles < cap ? tiles : cap);
-  f4_gemm_kernel<BK, SMALL, DUMP><<<grid, kF4Threads, smem, s>>>(codes_a, codes_w, rowsum, colsum,
-                                                                  st, y, acc_dump, bias, relu, g);
+  LANCE_LAUNCH_CHECK(launch_k(f4_gemm_kernel<BK, SMALL, DUMP>, grid, kF4Threads, smem, s, codes_a, codes_w, rowsum, colsum,
+                                                                  st, y, acc_dump, bias, relu, g));
   return cudaGetLastError();
 }
 

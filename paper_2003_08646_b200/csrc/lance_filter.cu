@@ -16,6 +16,7 @@ __global__ void __launch_bounds__(256) filter_transform_kernel(const float* __re
                                                                float* __restrict__ partials,
                                                                LanceDevState* __restrict__ st,
                                                                FilterGeom g) {
+  pdl_entry();
   __shared__ float s_red[256];
   float lo[16], hi[16];
 #pragma unroll
@@ -53,6 +54,7 @@ __global__ void __launch_bounds__(128) filter_quant_kernel(const float* __restri
                                                            int32_t* __restrict__ colsum,
                                                            const LanceDevState* __restrict__ st,
                                                            FilterGeom g) {
+  pdl_entry();
   __shared__ int s_sum[4];
   const int k = blockIdx.x;
   const float top = static_cast<float>((1 << st->bits_w) - 1);
@@ -78,10 +80,10 @@ __global__ void __launch_bounds__(128) filter_quant_kernel(const float* __restri
 cudaError_t launch_filter_prepare(const float* w, float* u_tmp, float* partials, int grid,
                                   uint8_t* codes_w, int32_t* colsum, LanceDevState* st,
                                   const FilterGeom& g, cudaStream_t s) {
-  filter_transform_kernel<<<grid, 256, 0, s>>>(w, u_tmp, partials, st, g);
+  LANCE_LAUNCH_CHECK(launch_k(filter_transform_kernel, grid, 256, 0, s, w, u_tmp, partials, st, g));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  filter_quant_kernel<<<g.K, 128, 0, s>>>(u_tmp, codes_w, colsum, st, g);
+  LANCE_LAUNCH_CHECK(launch_k(filter_quant_kernel, g.K, 128, 0, s, u_tmp, codes_w, colsum, st, g));
   return cudaGetLastError();
 }
 

@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     mbar_init(b_full, 1);
     fence_barrier_init();
   }
+  pdl_entry();  // barriers above are shared-memory only; st / codes / y below
   if (warp < kEpiWarps) {
     const int e = threadIdx.x;
     if (e < 32) {
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
                     b_res ? b_res_base + (u0 + kc) * Cfg::kBBytes : sa + Cfg::kABytes;
 #pragma unroll
                 for (int kk = 0; kk < BK / 32; ++kk) {
-                  if (g.exp & 2) break;
+                  if (kExpSwitches && (g.exp & 2)) break;
                   const uint64_t adesc = umma_smem_desc(sa + kk * 32, 8 * BK, Cfg::kLayout);
                   const uint64_t bdesc = umma_smem_desc(sb + kk * 32, 8 * BK, Cfg::kLayout);
                   umma_i8(d_base + static_cast<uint32_t>(a * BN), adesc, bdesc, kIdesc,
@@ -527,7 +528,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
                   acc_dump[(static_cast<long long>(4 * a + j) * g.M + m) * g.K + kf0 + 4 * c + i] =
                       static_cast<int32_t>(ac[a][i]);
           }
-          if (g.exp & 1) continue;
+          if (kExpSwitches && (g.exp & 1)) continue;
           float2 T0[2], T1[2];
           affine_group4<BN>(ac, fast, k1s, k4, rterm, ct_tile + j * BN + f0 + 4 * c, T0, T1);
 #pragma unroll
@@ -555,7 +556,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
             }
           }
         }
-        if (g.exp & 1) continue;
+        if (kExpSwitches && (g.exp & 1)) continue;
         if (j == 2)
           store_col(0, S[0], S[2]);  // S00 and S10 are final after T_2
         else if (j == 3)
@@ -591,9 +592,8 @@ static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
   const int sms = current_sm_count();
   const long long tiles = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * g.num_n_tiles;
   const int grid = static_cast<int>(tiles < sms ? tiles : sms);
-  gemm_epilogue_kernel<BK, BN, SMALL, DUMP><<<grid, kGemmThreadsP, smem, s>>>(
-      codes_a, codes_w, *tmR, rowsum_out, colsum, st, y, acc_dump, bias, relu, g);
-  return cudaGetLastError();
+  return launch_k(gemm_epilogue_kernel<BK, BN, SMALL, DUMP>, grid, kGemmThreadsP, smem, s, codes_a,
+                  codes_w, *tmR, rowsum_out, colsum, st, y, acc_dump, bias, relu, g);
 }
 
 template <int BK, int BN>

@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(256, 2) input_range_kernel(const float* __rest
                                                              float* __restrict__ partials,
                                                              LanceDevState* __restrict__ st,
                                                              InGeom g) {
+  pdl_entry();
   __shared__ float s_red[256];
   float lo[16], hi[16];
 #pragma unroll
@@ -192,6 +193,80 @@ __global__ void __launch_bounds__(256, 2) input_range_kernel(const float* __rest
   }
 }
 
+// Quantise one tile's v (this lane's channel pair) and store the codes into
+// the A operand's UMMA images at dst (position planes pstride apart); returns
+// this lane's row sum (lane p < 16: position p) of the warp's 64 channels.
+// Generic over C (lane_on / two: the lane's channels exist).
+template <bool STATIC>
+__device__ __forceinline__ uint32_t quant_store_generic(const float2 (&v)[16], bool lane_on, bool two,
+                                                        uint8_t* dst, long long pstride,
+                                                        const float* s_tmin, const float* s_scale,
+                                                        const float* s_rcp, float top, int lane) {
+  uint32_t mine = 0u;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    uint32_t pk[2] = {0u, 0u};
+    if (lane_on) {
+      float2 dd[2], gq[2], r[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int p = 2 * k + h;
+        dd[h] = sub2(v[p], bcast2(s_tmin[p]));
+        if (STATIC) {
+          float2 q = mul2_rn(dd[h], bcast2(s_rcp[p]));
+          q.x = fminf(fmaxf(q.x, 0.0f), top);  // NaN -> 0 like quant.hpp:81
+          q.y = fminf(fmaxf(q.y, 0.0f), top);
+          gq[h] = add2(q, bcast2(kMagic));
+          r[h] = sub2(q, sub2(gq[h], bcast2(kMagic)));
+        } else {
+          gq[h] = fma2(dd[h], bcast2(s_rcp[p]), bcast2(kMagic));
+          r[h] = fma2(dd[h], bcast2(s_rcp[p]),
+                      make_float2(-__fsub_rn(gq[h].x, kMagic), -__fsub_rn(gq[h].y, kMagic)));
+        }
+        pk[h] = __byte_perm(__float_as_uint(gq[h].x), __float_as_uint(gq[h].y), 0x0040) & 0xFFFFu;
+      }
+      const float rmax = fmax3_nan(fmax3_nan(fabsf(r[0].x), fabsf(r[0].y), fabsf(r[1].x)),
+                                   fabsf(r[1].y), 0.0f);
+      if (!(rmax < kTieGuard)) {
+        // Rare (~1e-4 per value): re-derive the flagged codes exactly.
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int p = 2 * k + h;
+          uint32_t c0, c1;
+          if (STATIC) {
+            c0 = quantize_code(v[p].x, s_tmin[p], s_scale[p], top);
+            c1 = quantize_code(v[p].y, s_tmin[p], s_scale[p], top);
+          } else {
+            c0 = (fabsf(r[h].x) < kTieGuard)
+                     ? (pk[h] & 0xFFu)
+                     : exact_code_near_boundary(dd[h].x, s_scale[p], gq[h].x, r[h].x, top);
+            c1 = (fabsf(r[h].y) < kTieGuard)
+                     ? (pk[h] >> 8)
+                     : exact_code_near_boundary(dd[h].y, s_scale[p], gq[h].y, r[h].y, top);
+          }
+          pk[h] = c0 | (c1 << 8);
+        }
+      }
+      if (!two) {  // odd C: padding channel code 0
+        pk[0] &= 0x00FFu;
+        pk[1] &= 0x00FFu;
+      }
+      // Codes: 64 contiguous bytes per warp per position (the A operand row).
+      // position planes in j-major image order (umma_image_offset)
+      const int p0 = 2 * k, p1 = 2 * k + 1;
+      *reinterpret_cast<uint16_t*>(dst + image_plane(p0) * pstride) = static_cast<uint16_t>(pk[0]);
+      *reinterpret_cast<uint16_t*>(dst + image_plane(p1) * pstride) = static_cast<uint16_t>(pk[1]);
+    }
+    // Row sums (lowpgemm.hpp:121-123): the lane's two codes of positions
+    // (2k, 2k+1) as 16-bit halves, one warp reduction (REDUX) per pair.
+    const uint32_t a = pk[0] | (pk[1] << 16);                          // [p.c0, p.c1, q.c0, q.c1]
+    const uint32_t w = (a & 0x00FF00FFu) + ((a >> 8) & 0x00FF00FFu);  // [p sum | q sum]
+    const uint32_t tot = __reduce_add_sync(0xffffffffu, w);
+    if ((lane >> 1) == k) mine = (lane & 1) ? (tot >> 16) : (tot & 0xFFFFu);
+  }
+  return mine;
+}
+
 // --------------------------------------------------------------------------
 // K1: codes + row sums, one strip per warp.
 //
@@ -210,6 +285,7 @@ __global__ void __launch_bounds__(256, 2) input_quant_kernel(const float* __rest
                                                              int32_t* __restrict__ rowsum,
                                                              const LanceDevState* __restrict__ st,
                                                              InGeom g) {
+  pdl_entry();
   __shared__ float s_tmin[16], s_scale[16], s_rcp[16];
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid < 16) {
@@ -258,68 +334,8 @@ __global__ void __launch_bounds__(256, 2) input_quant_kernel(const float* __rest
       }
     }
     uint8_t* dst = codes + umma_image_offset(m, it.ch, 0, kBM, g.a_bk, g.a_nk);
-    uint32_t mine = 0u;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      uint32_t pk[2] = {0u, 0u};
-      if (lane_on) {
-        float2 dd[2], gq[2], r[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int p = 2 * k + h;
-          dd[h] = sub2(v[p], bcast2(s_tmin[p]));
-          if (STATIC) {
-            float2 q = mul2_rn(dd[h], bcast2(s_rcp[p]));
-            q.x = fminf(fmaxf(q.x, 0.0f), top);  // NaN -> 0 like quant.hpp:81
-            q.y = fminf(fmaxf(q.y, 0.0f), top);
-            gq[h] = add2(q, bcast2(kMagic));
-            r[h] = sub2(q, sub2(gq[h], bcast2(kMagic)));
-          } else {
-            gq[h] = fma2(dd[h], bcast2(s_rcp[p]), bcast2(kMagic));
-            r[h] = fma2(dd[h], bcast2(s_rcp[p]),
-                        make_float2(-__fsub_rn(gq[h].x, kMagic), -__fsub_rn(gq[h].y, kMagic)));
-          }
-          pk[h] = __byte_perm(__float_as_uint(gq[h].x), __float_as_uint(gq[h].y), 0x0040) & 0xFFFFu;
-        }
-        const float rmax = fmax3_nan(fmax3_nan(fabsf(r[0].x), fabsf(r[0].y), fabsf(r[1].x)),
-                                     fabsf(r[1].y), 0.0f);
-        if (!(rmax < kTieGuard)) {
-          // Rare (~1e-4 per value): re-derive the flagged codes exactly.
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int p = 2 * k + h;
-            uint32_t c0, c1;
-            if (STATIC) {
-              c0 = quantize_code(v[p].x, s_tmin[p], s_scale[p], top);
-              c1 = quantize_code(v[p].y, s_tmin[p], s_scale[p], top);
-            } else {
-              c0 = (fabsf(r[h].x) < kTieGuard)
-                       ? (pk[h] & 0xFFu)
-                       : exact_code_near_boundary(dd[h].x, s_scale[p], gq[h].x, r[h].x, top);
-              c1 = (fabsf(r[h].y) < kTieGuard)
-                       ? (pk[h] >> 8)
-                       : exact_code_near_boundary(dd[h].y, s_scale[p], gq[h].y, r[h].y, top);
-            }
-            pk[h] = c0 | (c1 << 8);
-          }
-        }
-        if (!two) {  // odd C: padding channel code 0
-          pk[0] &= 0x00FFu;
-          pk[1] &= 0x00FFu;
-        }
-        // Codes: 64 contiguous bytes per warp per position (the A operand row).
-        // position planes in j-major image order (umma_image_offset)
-        const int p0 = 2 * k, p1 = 2 * k + 1;
-        *reinterpret_cast<uint16_t*>(dst + image_plane(p0) * pstride) = static_cast<uint16_t>(pk[0]);
-        *reinterpret_cast<uint16_t*>(dst + image_plane(p1) * pstride) = static_cast<uint16_t>(pk[1]);
-      }
-      // Row sums (lowpgemm.hpp:121-123): the lane's two codes of positions
-      // (2k, 2k+1) as 16-bit halves, one warp reduction (REDUX) per pair.
-      const uint32_t a = pk[0] | (pk[1] << 16);                          // [p.c0, p.c1, q.c0, q.c1]
-      const uint32_t w = (a & 0x00FF00FFu) + ((a >> 8) & 0x00FF00FFu);  // [p sum | q sum]
-      const uint32_t tot = __reduce_add_sync(0xffffffffu, w);
-      if ((lane >> 1) == k) mine = (lane & 1) ? (tot >> 16) : (tot & 0xFFFFu);
-    }
+    const uint32_t mine = quant_store_generic<STATIC>(v, lane_on, two, dst, pstride, s_tmin, s_scale,
+                                                      s_rcp, top, lane);
     if (g.rowsums && lane < 16) {
       int32_t* rs = rowsum + static_cast<long long>(lane) * g.rs_pitch + m;
       if (g.nchunks == 1)
@@ -359,6 +375,7 @@ __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* _
                                                                   int32_t* __restrict__ rowsum,
                                                                   const LanceDevState* __restrict__ st,
                                                                   InGeom g) {
+  pdl_entry();
   __shared__ float s_tmin[16], s_scale[16], s_rcp[16];
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid < 16) {
@@ -480,6 +497,7 @@ __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* _
 
 // Static-params mode: caller-supplied input QuantParams[16].
 __global__ void static_params_kernel(LanceDevState* st, StaticParams prm, int C) {
+  pdl_entry();
   if (threadIdx.x < prm.np) {
     const int p = threadIdx.x;
     const float s = prm.scale[p];
@@ -510,6 +528,7 @@ __global__ void __launch_bounds__(256, 2) input_range_ring_kernel(const float* _
                                                                   float* __restrict__ partials,
                                                                   LanceDevState* __restrict__ st,
                                                                   InGeom g) {
+  pdl_entry();
   constexpr int R = D + 1;
   extern __shared__ float2 s_ring[];  // [8 warps][R slots][2 columns x 4 rows][32 lanes]
   __shared__ float s_red[256];
@@ -621,6 +640,77 @@ __global__ void __launch_bounds__(256, 2) input_range_ring_kernel(const float* _
 }
 
 // --------------------------------------------------------------------------
+// NCHW input (north-star layout option; the reference itself is NHWC-only,
+// tensor.hpp:24-55): a shared-memory tiled transpose NCHW -> NHWC into the
+// plan's staging buffer, then the NHWC K0 / K1 unchanged, so codes,
+// parameters and y are bit-identical to the NHWC path by construction.
+// (Measured: K0 / K1 variants that stage 64-channel input windows per CTA and
+// transpose them in shared memory ran 4-7x slower than the NHWC kernels --
+// one 59 KB window per CTA leaves too few CTAs in flight to cover the load
+// latency -- while this transpose is a pure HBM stream.)
+//
+// CTA = one (image, input row y, 32-pixel run x0.., 64-channel chunk c0..):
+// load 64 channel rows x 32 pixels (one 128-byte run per channel row: a
+// thread loads one 16-byte float4, 8 threads per row) into s[c][x] (row
+// stride 33: conflict-free), then write 32 pixels x 64 channels (16 lanes x
+// float4 = 256 contiguous bytes per pixel).  Ragged W / C (W % 4 or C % 4 !=
+// 0, unaligned pointers) take predicated scalar accesses.
+__global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restrict__ x,
+                                                           float* __restrict__ xt, int N, int C,
+                                                           int H, int W) {
+  pdl_entry();
+  __shared__ float s[64][33];
+  const int tid = threadIdx.x;
+  const int xb = blockIdx.x;             // 32-pixel run
+  const int y = blockIdx.y % H, img = blockIdx.y / H;
+  const int c0 = blockIdx.z * 64;
+  const int x0 = xb * 32;
+  const long long HW = static_cast<long long>(H) * W;
+  const bool vec_in = ((W & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  {
+    const int q = tid & 7;  // float4 quad within the 32-pixel run
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int cl = (tid >> 3) + 32 * k, c = c0 + cl;
+      const int xx = x0 + 4 * q;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      if (c < C) {
+        const float* src = x + (static_cast<long long>(img) * C + c) * HW + static_cast<long long>(y) * W;
+        if (vec_in && xx + 3 < W) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(src + xx));
+          v[0] = f.x, v[1] = f.y, v[2] = f.z, v[3] = f.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (xx + j < W) v[j] = __ldg(src + xx + j);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s[cl][4 * q + j] = v[j];
+    }
+  }
+  __syncthreads();
+  const bool vec_out = ((C & 3) == 0) && ((reinterpret_cast<uintptr_t>(xt) & 15) == 0);
+  const int cq = tid & 15;  // channel quad
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int xl = (tid >> 4) + 16 * k, xx = x0 + xl;
+    const int c = c0 + 4 * cq;
+    if (xx >= W || c >= C) continue;
+    float* dst = xt + ((static_cast<long long>(img) * H + y) * W + xx) * C + c;
+    const float4 f = make_float4(s[4 * cq][xl], s[4 * cq + 1][xl], s[4 * cq + 2][xl], s[4 * cq + 3][xl]);
+    if (vec_out && c + 3 < C) {
+      *reinterpret_cast<float4*>(dst) = f;
+    } else {
+      const float e[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (c + j < C) dst[j] = e[j];
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
 // Small-C path (C < 32, e.g. the RGB first layer of VGG, C = 3): the strip
 // kernels put channels on lanes, which would leave most lanes idle; here one
 // thread owns one (tile, channel) and walks a grid-stride loop.  Same
@@ -664,6 +754,7 @@ __global__ void __launch_bounds__(256) input_range_smallc_kernel(const float* __
                                                                  float* __restrict__ partials,
                                                                  LanceDevState* __restrict__ st,
                                                                  InGeom g) {
+  pdl_entry();
   __shared__ float s_red[256];
   float lo[16], hi[16];
 #pragma unroll
@@ -698,6 +789,7 @@ __global__ void __launch_bounds__(256) input_quant_smallc_kernel(const float* __
                                                                  int32_t* __restrict__ rowsum,
                                                                  const LanceDevState* __restrict__ st,
                                                                  InGeom g) {
+  pdl_entry();
   __shared__ float s_tmin[16], s_scale[16], s_rcp[16];
   if (threadIdx.x < 16) {
     s_tmin[threadIdx.x] = st->a_tmin[threadIdx.x];
@@ -744,7 +836,7 @@ cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceD
   // than register lookahead on the 56x56 / 28x28 layers; 8 halves residency).
   constexpr int kDepth = 4;
   if (g.C < 32) {
-    input_range_smallc_kernel<<<grid, 256, 0, s>>>(x, partials, st, g);
+    LANCE_LAUNCH_CHECK(launch_k(input_range_smallc_kernel, grid, 256, 0, s, x, partials, st, g));
   } else if (g.C % 64 == 0) {
     const size_t smem = static_cast<size_t>(8) * (kDepth + 1) * 8 * 32 * sizeof(float2);
 #define LANCE_K0_RING(CCV)                                                                        \
@@ -752,7 +844,7 @@ cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceD
       const cudaError_t attr =                                                                   \
           ensure_smem_attr(reinterpret_cast<const void*>(input_range_ring_kernel<kDepth, CCV>), smem); \
       if (attr != cudaSuccess) return attr;                                                      \
-      input_range_ring_kernel<kDepth, CCV><<<grid, 256, smem, s>>>(x, partials, st, g);          \
+      LANCE_LAUNCH_CHECK(launch_k(input_range_ring_kernel<kDepth, CCV>, grid, 256, smem, s, x, partials, st, g));          \
       return cudaGetLastError();                                                                 \
     }
     LANCE_K0_RING(64)
@@ -762,9 +854,9 @@ cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceD
     LANCE_K0_RING(0)
 #undef LANCE_K0_RING
   } else if (vec2) {
-    input_range_kernel<true><<<grid, 256, 0, s>>>(x, partials, st, g);
+    LANCE_LAUNCH_CHECK(launch_k(input_range_kernel<true>, grid, 256, 0, s, x, partials, st, g));
   } else {
-    input_range_kernel<false><<<grid, 256, 0, s>>>(x, partials, st, g);
+    LANCE_LAUNCH_CHECK(launch_k(input_range_kernel<false>, grid, 256, 0, s, x, partials, st, g));
   }
   return cudaGetLastError();
 }
@@ -781,22 +873,22 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
       if (e != cudaSuccess) return e;
     }
     if (static_mode)
-      input_quant_smallc_kernel<true><<<sgrid, 256, 0, s>>>(x, codes, rowsum, st, g);
+      LANCE_LAUNCH_CHECK(launch_k(input_quant_smallc_kernel<true>, sgrid, 256, 0, s, x, codes, rowsum, st, g));
     else
-      input_quant_smallc_kernel<false><<<sgrid, 256, 0, s>>>(x, codes, rowsum, st, g);
+      LANCE_LAUNCH_CHECK(launch_k(input_quant_smallc_kernel<false>, sgrid, 256, 0, s, x, codes, rowsum, st, g));
     return cudaGetLastError();
   }
   if (g.C % 64 == 0) {  // fast path: every lane owns two real channels
 #define LANCE_K1_FAST(BKV, NKV)                                                          \
   if (g.a_bk == BKV && g.a_nk == NKV) {                                                  \
     if (static_mode && g.rowsums)                                                        \
-      input_quant_fast_kernel<BKV, NKV, true, true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g); \
+      LANCE_LAUNCH_CHECK(launch_k(input_quant_fast_kernel<BKV, NKV, true, true>, grid, 256, 0, s, x, codes, rowsum, st, g)); \
     else if (static_mode)                                                                \
-      input_quant_fast_kernel<BKV, NKV, false, true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g); \
+      LANCE_LAUNCH_CHECK(launch_k(input_quant_fast_kernel<BKV, NKV, false, true>, grid, 256, 0, s, x, codes, rowsum, st, g)); \
     else if (g.rowsums)                                                                  \
-      input_quant_fast_kernel<BKV, NKV, true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g); \
+      LANCE_LAUNCH_CHECK(launch_k(input_quant_fast_kernel<BKV, NKV, true>, grid, 256, 0, s, x, codes, rowsum, st, g)); \
     else                                                                                 \
-      input_quant_fast_kernel<BKV, NKV, false><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g); \
+      LANCE_LAUNCH_CHECK(launch_k(input_quant_fast_kernel<BKV, NKV, false>, grid, 256, 0, s, x, codes, rowsum, st, g)); \
     return cudaGetLastError();                                                           \
   }
     LANCE_K1_FAST(64, 1)
@@ -810,16 +902,23 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
   }
   if (vec2) {
     if (static_mode)
-      input_quant_kernel<true, true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
+      LANCE_LAUNCH_CHECK(launch_k(input_quant_kernel<true, true>, grid, 256, 0, s, x, codes, rowsum, st, g));
     else
-      input_quant_kernel<true, false><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
+      LANCE_LAUNCH_CHECK(launch_k(input_quant_kernel<true, false>, grid, 256, 0, s, x, codes, rowsum, st, g));
   } else {
     if (static_mode)
-      input_quant_kernel<false, true><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
+      LANCE_LAUNCH_CHECK(launch_k(input_quant_kernel<false, true>, grid, 256, 0, s, x, codes, rowsum, st, g));
     else
-      input_quant_kernel<false, false><<<grid, 256, 0, s>>>(x, codes, rowsum, st, g);
+      LANCE_LAUNCH_CHECK(launch_k(input_quant_kernel<false, false>, grid, 256, 0, s, x, codes, rowsum, st, g));
   }
   return cudaGetLastError();
+}
+
+// NCHW -> NHWC staging transpose (x [N][C][H][W] -> xt [N][H][W][C]).
+cudaError_t launch_nchw_to_nhwc(const float* x, float* xt, int N, int C, int H, int W, cudaStream_t s) {
+  const dim3 grid((W + 31) / 32, static_cast<unsigned>(N) * H, (C + 63) / 64);
+  LANCE_LAUNCH_CHECK(launch_k(nchw_to_nhwc_kernel, grid, 256, 0, s, x, xt, N, C, H, W));
+  return cudaSuccess;
 }
 
 // Global-fit mode (SURVEY 8(e) mode 2) on the device.  Export: the fitted
@@ -827,6 +926,7 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
 // nan] -- the layout one element-wise MAX all-reduce combines across ranks
 // (-(-x) is exact; a NaN flag rides along as 1.0 because fmax drops NaNs).
 __global__ void export_minmax_kernel(const LanceDevState* st, float* minmax, int np) {
+  pdl_entry();
   const int p = threadIdx.x;
   if (p < np) {
     minmax[p] = -st->a_tmin[p];
@@ -839,6 +939,7 @@ __global__ void export_minmax_kernel(const LanceDevState* st, float* minmax, int
 // QuantParams and affine constants of the plan (PerTensor folds, engines.hpp:151-156).
 __global__ void fit_minmax_kernel(LanceDevState* st, const float* __restrict__ minmax, int np,
                                   int gran, int C) {
+  pdl_entry();
   const int p = threadIdx.x;
   bool bad = false;
   if (p < np) {
@@ -867,19 +968,19 @@ __global__ void fit_minmax_kernel(LanceDevState* st, const float* __restrict__ m
 }
 
 cudaError_t launch_export_minmax(const LanceDevState* st, float* minmax, int np, cudaStream_t s) {
-  export_minmax_kernel<<<1, 64, 0, s>>>(st, minmax, np);
+  LANCE_LAUNCH_CHECK(launch_k(export_minmax_kernel, 1, 64, 0, s, st, minmax, np));
   return cudaGetLastError();
 }
 
 cudaError_t launch_fit_minmax(LanceDevState* st, const float* minmax, int np, int gran, int C,
                               cudaStream_t s) {
-  fit_minmax_kernel<<<1, 64, 0, s>>>(st, minmax, np, gran, C);
+  LANCE_LAUNCH_CHECK(launch_k(fit_minmax_kernel, 1, 64, 0, s, st, minmax, np, gran, C));
   return cudaGetLastError();
 }
 
 cudaError_t launch_static_params(LanceDevState* st, const StaticParams& prm, int C,
                                  cudaStream_t s) {
-  static_params_kernel<<<1, 64, 0, s>>>(st, prm, C);
+  LANCE_LAUNCH_CHECK(launch_k(static_params_kernel, 1, 64, 0, s, st, prm, C));
   return cudaGetLastError();
 }
 

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <utility>
 
 #ifndef LANCE_JMAJOR
 #define LANCE_JMAJOR 0
@@ -141,6 +142,14 @@ __host__ __device__ __forceinline__ long long umma_image_offset_np(long long row
          umma_swizzle(static_cast<uint32_t>(r * bk + cb), bk);
 }
 
+// Profiling-only kernel experiment switches (GemmGeom::exp / F4Geom::exp):
+// compiled out of release builds, so their per-chunk tests cost nothing.
+#ifdef LANCE_PROFILING
+constexpr bool kExpSwitches = true;
+#else
+constexpr bool kExpSwitches = false;
+#endif
+
 // Experiment switches: the environment value in LANCE_PROFILING builds, else def.
 int lance_knob(const char* name, int def);
 
@@ -152,6 +161,32 @@ cudaError_t ensure_smem_attr(const void* fn, size_t bytes);
 // Multiprocessor count of the current device (cached, thread-safe).
 int current_sm_count();
 
+// Programmatic dependent launch (kernels call pdl_entry() first).  Off by
+// default: measured 1.2 % SLOWER on the ResNet-18 step (2.444 vs 2.416 ms,
+// gpurun_out/pdl); LANCE_PDL=1 in profiling builds turns it on.
+bool pdl_enabled();
+#define LANCE_LAUNCH_CHECK(call)                  \
+  do {                                            \
+    const cudaError_t lance_e_ = (call);          \
+    if (lance_e_ != cudaSuccess) return lance_e_; \
+  } while (0)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args&&... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 // Host-side launchers.  All stream-ordered.
 int input_range_grid(const InGeom& g, int sm_count);
 cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceDevState* st,
@@ -159,6 +194,9 @@ cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceD
 cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
                                const LanceDevState* st, const InGeom& g, int vec2,
                                int static_mode, cudaStream_t s);
+// NCHW input: staging transpose x [N][C][H][W] -> xt [N][H][W][C] (then the
+// NHWC K0 / K1).  grid.y = N * H must stay below 65536 (checked by the plan).
+cudaError_t launch_nchw_to_nhwc(const float* x, float* xt, int N, int C, int H, int W, cudaStream_t s);
 cudaError_t launch_static_params(LanceDevState* st, const StaticParams& prm, int C,
                                  cudaStream_t s);
 // Global-fit mode: [-t_min[np], t_max[np], nan] export / re-fit on the device.

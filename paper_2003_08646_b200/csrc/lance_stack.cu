@@ -6,7 +6,7 @@
 
 #include <cstdint>
 
-#include "lance_kernels.cuh"
+#include "lance_common.cuh"
 
 namespace lance_dev {
 
@@ -15,6 +15,7 @@ namespace lance_dev {
 __global__ void __launch_bounds__(256) maxpool2x2_kernel(const float* __restrict__ x,
                                                          float* __restrict__ y, int N, int H,
                                                          int W, int C) {
+  pdl_entry();
   const int OH = H / 2, OW = W / 2;
   const bool v4 = (C & 3) == 0;
   const int cw = v4 ? C / 4 : C;
@@ -48,7 +49,7 @@ cudaError_t launch_maxpool2x2(const float* x, float* y, int N, int H, int W, int
   if (total == 0) return cudaSuccess;
   const long long blocks = (total + 255) / 256;
   const int grid = static_cast<int>(blocks < 8LL * sm_count ? blocks : 8LL * sm_count);
-  maxpool2x2_kernel<<<grid, 256, 0, s>>>(x, y, N, H, W, C);
+  LANCE_LAUNCH_CHECK(launch_k(maxpool2x2_kernel, grid, 256, 0, s, x, y, N, H, W, C));
   return cudaGetLastError();
 }
 
