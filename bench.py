@@ -316,7 +316,9 @@ def run_stack(args, ws, rank, local, N):
             "data": "synthetic (UniformSource); He-scaled random weights, zero bias",
             "config": {"workload": "vgg16_cifar_stack_chained" + ("_f4x4" if args.tile_m == 4 else ""),
                        "batch_per_gpu": N, "convs": convs, "pools": 4,
-                       "epilogue": "bias + ReLU fused", "launch": "one CUDA graph per step",
+                       "epilogue": "bias + ReLU fused" + (", 2x2 max-pools fused into the preceding conv's GEMM epilogue"
+                                                          if stack.fuse_pool else ", separate max-pool kernels"),
+                       "launch": "one CUDA graph per step",
                        "winograd": f"F({args.tile_m}x{args.tile_m},3x3)"},
             "tops_equivalent": 2 * sum(direct_macs(c, k, h, N) for c, k, h in convs) * args.steps * ws / elapsed / 1e12,
             "gpu_launches": stack.launches_per_forward() * args.steps,

@@ -157,6 +157,12 @@ LANCE_API int lance_plan_input_layout(lance_plan_t plan);
  * bias_dev may be NULL (no bias).  relu is 0 or 1. */
 LANCE_API int lance_plan_set_epilogue(lance_plan_t plan, const float* bias_dev, int relu);
 
+/* Optional fused 2x2 / stride-2 max-pool after the (bias + ReLU) epilogue
+ * (layer-stack option; no reference oracle:
+ * equals lance_maxpool2x2_nhwc(relu(lance_gemm(x, w) + bias)), floor pooling).
+ * With pool = 1, y is [N][OH/2][OW/2][K].  F(2x2) plans only. */
+LANCE_API int lance_plan_set_epilogue_pool(lance_plan_t plan, int pool);
+
 /* Synchronise `stream` and report a NaN seen by the range pass of the last
  * forward (LANCE_ERR_NAN) or any pending CUDA error. */
 LANCE_API int lance_plan_sync(lance_plan_t plan, void* stream);

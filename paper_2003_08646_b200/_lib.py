@@ -75,6 +75,7 @@ def lib():
         L.lance_plan_ranges.argtypes = [P, P, P, P]
         L.lance_plan_set_input_layout.argtypes = [P, ct.c_int]
         L.lance_plan_input_layout.argtypes = [P]
+        L.lance_plan_set_epilogue_pool.argtypes = [P, ct.c_int]
         L.lance_plan_forward_ranges.argtypes = [P, P, P, P, P]
         L.lance_plan_sync.argtypes = [P, P]
         L.lance_plan_get_params.argtypes = [P, ct.POINTER(CQParams), ct.POINTER(CQParams)]
@@ -106,7 +107,7 @@ EXPORTED = [
     "lance_host_cache_clear",
     "lance_plan_create", "lance_plan_destroy", "lance_plan_device_bytes",
     "lance_plan_set_filters", "lance_plan_forward", "lance_plan_forward_static",
-    "lance_plan_set_epilogue", "lance_plan_ranges", "lance_plan_set_input_layout", "lance_plan_input_layout", "lance_plan_forward_ranges", "lance_plan_sync", "lance_plan_get_params",
+    "lance_plan_set_epilogue", "lance_plan_ranges", "lance_plan_set_input_layout", "lance_plan_input_layout", "lance_plan_set_epilogue_pool", "lance_plan_forward_ranges", "lance_plan_sync", "lance_plan_get_params",
     "lance_plan_debug_read", "lance_plan_set_acc_dump", "lance_plan_last_launch_count",
     "lance_plan_stage_timing", "lance_plan_read_stage_times",
     "lance_plan_create_tiled", "lance_plan_positions", "lance_gemm_host_tiled",

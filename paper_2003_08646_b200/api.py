@@ -262,13 +262,25 @@ class LanceConv:
         _check(_lib.lib().lance_plan_set_filters(self._plan, ct.c_void_p(w.data_ptr()),
                                                  _stream_ptr(stream)))
 
-    def set_epilogue(self, bias=None, relu: bool = False):
-        """Optional fused bias + ReLU (north-star extension)."""
+    def set_epilogue(self, bias=None, relu: bool = False, pool: bool = False):
+        """Optional fused bias + ReLU (north-star extension) and fused 2x2 /
+        stride-2 max-pool (layer-stack option, F(2x2) only): with pool=True
+        the forward writes [N, OH/2, OW/2, K]."""
         if bias is not None:
             self._check_tensor(bias, (self.spec.k,), "bias")
         self._bias = bias
-        _check(_lib.lib().lance_plan_set_epilogue(
+        L = _lib.lib()
+        _check(L.lance_plan_set_epilogue(
             self._plan, ct.c_void_p(bias.data_ptr()) if bias is not None else None, int(relu)))
+        _check(L.lance_plan_set_epilogue_pool(self._plan, int(bool(pool))))
+        self.pool = bool(pool)
+
+    @property
+    def out_shape(self):
+        s = self.spec
+        if getattr(self, "pool", False):
+            return (s.n, s.out_h() // 2, s.out_w() // 2, s.k)
+        return (s.n, s.out_h(), s.out_w(), s.k)
 
     def set_acc_dump(self, acc):
         """Also write the raw int32 accumulators [positions][M][K] on later forwards."""
@@ -308,9 +320,8 @@ class LanceConv:
         s = self.spec
         self._check_tensor(x, self.input_shape, "input tensor")
         if y is None:
-            y = torch.empty((s.n, s.out_h(), s.out_w(), s.k), dtype=torch.float32,
-                            device=x.device)
-        self._check_tensor(y, (s.n, s.out_h(), s.out_w(), s.k), "output")
+            y = torch.empty(self.out_shape, dtype=torch.float32, device=x.device)
+        self._check_tensor(y, self.out_shape, "output")
         L = _lib.lib()
         if ranges is not None:
             if not (ranges.is_cuda and ranges.dtype == torch.float32 and ranges.is_contiguous()

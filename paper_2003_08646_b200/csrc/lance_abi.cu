@@ -766,6 +766,17 @@ int lance_plan_set_input_layout(lance_plan_t p, int layout) {
 
 int lance_plan_input_layout(lance_plan_t p) { return p ? p->layout : -1; }
 
+int lance_plan_set_epilogue_pool(lance_plan_t p, int pool) {
+  if (!p) return fail(LANCE_ERR_INVALID_ARGUMENT, "null plan");
+  if (pool != 0 && pool != 1) return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_set_epilogue_pool: pool must be 0 or 1");
+  if (pool && p->tm != 2)
+    return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_set_epilogue_pool: the fused pool needs tile_m = 2");
+  if (pool && (p->OH < 2 || p->OW < 2))
+    return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_set_epilogue_pool: output smaller than 2x2");
+  p->gemm_geom.pool = pool;
+  return LANCE_OK;
+}
+
 int lance_plan_set_epilogue(lance_plan_t p, const float* bias_dev, int relu) {
   if (!p) return fail(LANCE_ERR_INVALID_ARGUMENT, "null plan");
   p->bias = bias_dev;

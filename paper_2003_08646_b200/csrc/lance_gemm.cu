@@ -409,13 +409,14 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       const int kf0 = n0 + f0;
       // Output pixels of this lane's tile (2ti + a, 2tj + b) and their
       // validity (merge_tiles discards the ceil-overhang, tensor.hpp:172-175).
-      int pix0, pmask;
+      int pix0, pmask, ppix;
       {
         const int mm = row_ok ? m : 0;
         const int img = mm / g.P;
         const int tt = mm - img * g.P;
         const int ti = tt / g.TW, tj = tt - ti * g.TW;
         pix0 = (img * g.OH + 2 * ti) * g.OW + 2 * tj;
+        ppix = (img * (g.OH >> 1) + ti) * (g.OW >> 1) + tj;  // fused 2x2 max-pool output pixel
         const bool r1 = 2 * ti + 1 < g.OH, c1 = 2 * tj + 1 < g.OW;
         pmask = row_ok ? (1 | (c1 ? 2 : 0) | (r1 ? 4 : 0) | (r1 && c1 ? 8 : 0)) : 0;
       }
@@ -477,6 +478,46 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
           }
         }
         named_bar_sync(2 + q, 128);  // staging buffer free again
+      };
+      // Fused 2x2 / stride-2 max-pool (layer-stack option; floor pooling like
+      // lance_maxpool2x2_nhwc): a tile's 4 output pixels are exactly one pool
+      // window, so each thread folds its own S00, S01, S10, S11 -- after the
+      // same bias / ReLU / +0 as the unpooled store -- in that kernel's order
+      // max(max(y00, y01), max(y10, y11)) and writes one pooled pixel; tiles
+      // that overhang the map (pmask != 15) have no pooled pixel.
+      auto store_pool = [&](float2 (&s00)[FPT / 2], float2 (&s01)[FPT / 2], float2 (&s10)[FPT / 2],
+                            float2 (&s11)[FPT / 2]) {
+        if (pmask != 15) return;
+        float* d = y + static_cast<long long>(ppix) * g.K + kf0;
+        auto fin = [&](float2 v, int i) {
+          if (bias != nullptr)
+            v = add2(v, make_float2(kf0 + 2 * i < g.K ? __ldg(bias + kf0 + 2 * i) : 0.0f,
+                                    kf0 + 2 * i + 1 < g.K ? __ldg(bias + kf0 + 2 * i + 1) : 0.0f));
+          if (relu) {
+            v.x = fmaxf(v.x, 0.0f);
+            v.y = fmaxf(v.y, 0.0f);
+          }
+          return add2(v, bcast2(0.0f));
+        };
+#pragma unroll
+        for (int i = 0; i < FPT / 2; i += 2) {
+          float2 r[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float2 a = fin(s00[i + h], i + h), b = fin(s01[i + h], i + h);
+            const float2 c = fin(s10[i + h], i + h), e = fin(s11[i + h], i + h);
+            r[h] = make_float2(fmaxf(fmaxf(a.x, b.x), fmaxf(c.x, e.x)), fmaxf(fmaxf(a.y, b.y), fmaxf(c.y, e.y)));
+          }
+          const int kf = kf0 + 2 * i;
+          if (k4ok && kf + 4 <= g.K) {
+            *reinterpret_cast<float4*>(d + 2 * i) = make_float4(r[0].x, r[0].y, r[1].x, r[1].y);
+          } else {
+            const float e4[4] = {r[0].x, r[0].y, r[1].x, r[1].y};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (kf + e < g.K) d[2 * i + e] = e4[e];
+          }
+        }
       };
       const uint32_t rb = lt & 1u;
       const int32_t* rs_tile = s_rs + rb * 16 * kBM + row;
@@ -557,10 +598,13 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
           }
         }
         if (kExpSwitches && (g.exp & 1)) continue;
-        if (j == 2)
+        if (g.pool) {
+          if (j == 3) store_pool(S[0], S[1], S[2], S[3]);
+        } else if (j == 2) {
           store_col(0, S[0], S[2]);  // S00 and S10 are final after T_2
-        else if (j == 3)
+        } else if (j == 3) {
           store_col(1, S[1], S[3]);
+        }
       }
     }
   }

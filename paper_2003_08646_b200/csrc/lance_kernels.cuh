@@ -69,6 +69,7 @@ struct GemmGeom {
   int rs_warps;     // 1: the GEMM sums the A rows itself; 0: K1's row sums via TMA
   int ld_lanes;     // producer lanes issuing each stage's bulk copies (1, 2, 4 or 8)
   int exp;          // experiment switches (LANCE_GEMM_EXP, profiling only; 0 = normal)
+  int pool;         // 1: fused 2x2 / stride-2 max-pool, y is [N][OH/2][OW/2][K]
   unsigned long long* trace;  // CTA-0 event timestamps (LANCE_GEMM_TRACE, profiling only)
 };
 

@@ -1,7 +1,8 @@
 """Layer-stack driver.
 
 Runs a chain of 3x3 / stride-1 / pad-1 LANCE conv layers with the fused bias +
-ReLU epilogue and 2x2 max-pools between stages, device-resident end to end:
+ReLU epilogue and 2x2 max-pools between stages (F(2x2): fused into the
+preceding conv's GEMM epilogue), device-resident end to end:
 every layer's output buffer is the next layer's input, filters are prepared
 once (K2), and the whole forward can be captured once into a CUDA graph and
 replayed (one graph launch per batch instead of 3-4 kernel launches per layer).
@@ -40,6 +41,7 @@ class _Stage:
     k: int = 0
     conv: LanceConv | None = None
     out: object = None  # torch tensor
+    fused: bool = False  # pool folded into the previous conv's epilogue
 
 
 class LanceStack:
@@ -50,7 +52,7 @@ class LanceStack:
     """
 
     def __init__(self, layers, n: int, h: int, w: int, cfg: LanceConfig, device: int = 0,
-                 tile_m: int = 2, relu: bool = True):
+                 tile_m: int = 2, relu: bool = True, fuse_pool: bool = True):
         import torch
         self.device = device
         self.relu = relu
@@ -80,6 +82,15 @@ class LanceStack:
             self.stages.append(st)
         if not self.stages or self.stages[0].kind != "conv":
             raise LanceError("stack: the first layer must be a conv")
+        # A pool right after a conv is fused into that conv's GEMM epilogue
+        # (F(2x2): a Winograd tile's 2x2 outputs are one pool window), which
+        # then writes the pooled map directly; the pool stage becomes a no-op.
+        self.fuse_pool = fuse_pool and tile_m == 2
+        if self.fuse_pool:
+            for prev, st in zip(self.stages, self.stages[1:]):
+                if st.kind == "pool" and prev.kind == "conv":
+                    st.fused = True
+                    prev.out = st.out
         self.in_shape = (n, self.stages[0].h, self.stages[0].w, self.stages[0].c)
         self.out_shape = tuple(self.stages[-1].out.shape)
         self._graph = None
@@ -97,9 +108,10 @@ class LanceStack:
             raise LanceError(f"stack: {len(convs)} convs but {len(weights)} weight tensors")
         biases = biases if biases is not None else [None] * len(convs)
         self._bias = list(biases)  # keep alive: the plans hold raw pointers
+        pooled = {id(prev) for prev, st in zip(self.stages, self.stages[1:]) if st.fused}
         for st, wt, b in zip(convs, weights, biases):
             st.conv.set_filters(wt, stream)
-            st.conv.set_epilogue(b, self.relu)
+            st.conv.set_epilogue(b, self.relu, pool=id(st) in pooled)
 
     def forward(self, x, stream=None):
         """All layers on `stream` (default: torch's current stream); returns the
@@ -108,6 +120,8 @@ class LanceStack:
         for st in self.stages:
             if st.kind == "conv":
                 st.conv.forward(cur, st.out, stream=stream)
+            elif st.fused:
+                pass  # written by the previous conv's epilogue
             else:
                 _check(_lib.lib().lance_maxpool2x2_nhwc(ct.c_void_p(cur.data_ptr()),
                                                         ct.c_void_p(st.out.data_ptr()), st.n, st.h,
@@ -116,7 +130,7 @@ class LanceStack:
         return cur
 
     def launches_per_forward(self) -> int:
-        return sum(3 if s.kind == "conv" else 1 for s in self.stages)
+        return sum(3 if s.kind == "conv" else (0 if s.fused else 1) for s in self.stages)
 
     def capture(self, x_example):
         """Record one forward into a CUDA graph (after an eager warm-up that also
