@@ -443,18 +443,24 @@ int lance_plan_create_tiled(const lance_conv_spec* spec, const lance_config* cfg
   gg.trace = nullptr;
   gg.b_resident = 0;
   gg.rs_pitch = static_cast<int>(p->rs_pitch);
+  // Output staging + stage shape.  C >= 512 (BK = 128, 4 k chunks per
+  // position): no y staging buffer, and stages of 2 k chunks (one 32 KB A
+  // and one 16 KB B copy, 8 MMAs per producer / MMA handshake) -- measured
+  // R512 GEMM 61 -> 49.5 us (gpurun_out/gsweep: only this combination helps;
+  // more producer lanes, 4-chunk stages or unstaged y at C <= 256 do not).
+  // LANCE_GEMM_STAGE / LANCE_GEMM_UNITS override.
+  gg.stage_out = lance_knob("LANCE_GEMM_STAGE", p->C_pad >= 512 && p->BK == 128 ? 0 : 1) ? 1 : 0;
   // Row sums: in the GEMM's spare warps when its stages are 64-byte K chunks
   // (their shared-memory reads then cost the SS-UMMA little), else in K1.
   // LANCE_RS_GEMM overrides.
   gg.rs_warps = lance_knob("LANCE_RS_GEMM", p->BK <= 64 ? 1 : 0) ? 1 : 0;
   p->in_geom.rowsums = gg.rs_warps ? 0 : 1;
-  // One thread sustains ~1 bulk copy per ~460 SM cycles from L2 whatever its
-  // size (scratch/l2_ingress_bench.cu), so each stage's copies are split over
-  // several producer lanes (LANCE_GEMM_LANES).  Measured in the GEMM, more
-  // lanes are slower (SS-UMMA already saturates shared-memory bandwidth), so 1.
+  // Producer lanes (LANCE_GEMM_LANES): 2 would issue a stage's A and B copies
+  // from different threads; measured neutral (gpurun_out/gsweep), so 1.
   {
     const int v = lance_knob("LANCE_GEMM_LANES", 1);
-    gg.ld_lanes = (v == 1 || v == 2 || v == 4 || v == 8) ? v : 1;
+    gg.ld_lanes = (v == 1 || v == 2) ? v : 1;
+    gg.units = lance_knob("LANCE_GEMM_UNITS", p->C_pad >= 512 && p->BK == 128 ? 2 : 1);
   }
   p->in_geom.rev_items = lance_knob("LANCE_K1_REVERSE", 1) ? 1 : 0;
 

@@ -73,12 +73,24 @@ struct GemmCfg {
       1024 /*align*/ + 2 * kRsBytes + kOutBytes + kCtBytes + 32 * 8 /*barriers, holder*/;
 };
 
+// STAGE = false: no output staging buffer (y written straight from registers,
+// 64 contiguous bytes per thread and pixel); its 4 * 32 * 2 * BN * 4 bytes go
+// to deeper operand stages instead.  Measured on the load-latency-bound deep
+// layers (C >= 256) where bytes in flight per SM set the GEMM rate.
+template <int BK, int BN>
+__host__ __device__ constexpr size_t gemm_fixed_bytes(bool stage_out) {
+  return GemmCfg<BK, BN>::kFixed - (stage_out ? 0 : GemmCfg<BK, BN>::kOutBytes);
+}
+
 // b_res: the whole B operand of the (single) filter tile stays resident in
 // shared memory and stages carry only A.
+// A stage holds `units` consecutive k chunks of one position (one bulk copy
+// for A and one for B per stage: the images of a position are contiguous).
 template <int BK, int BN>
-__host__ __device__ constexpr size_t gemm_smem_bytes(int stages, int nk, int b_res) {
-  return GemmCfg<BK, BN>::kFixed +
-         static_cast<size_t>(stages) *
+__host__ __device__ constexpr size_t gemm_smem_bytes(int stages, int nk, int b_res, bool stage_out,
+                                                     int units) {
+  return gemm_fixed_bytes<BK, BN>(stage_out) +
+         static_cast<size_t>(stages) * units *
              (b_res ? GemmCfg<BK, BN>::kABytes : GemmCfg<BK, BN>::kStageBytes) +
          (b_res ? static_cast<size_t>(16) * nk * GemmCfg<BK, BN>::kBBytes : 0) +
          static_cast<size_t>(stages) * 16;
@@ -140,7 +152,7 @@ __device__ __forceinline__ void tmem_ld_group4(uint32_t addr, int bn, uint32_t (
 
 // SMALL: see the file comment.  DUMP: also write the raw int32 accumulators
 // (parity tests).  bias / relu: fused epilogue (north-star extension).
-template <int BK, int BN, bool SMALL, bool DUMP>
+template <int BK, int BN, bool SMALL, bool DUMP, bool STAGE>
 __global__ void __launch_bounds__(kGemmThreadsP, 1)
     gemm_epilogue_kernel(const uint8_t* __restrict__ codes_a,
                          const uint8_t* __restrict__ codes_w,
@@ -167,12 +179,13 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   const int stages = g.stages;
   const int nk = g.num_kchunks;
   const bool b_res = g.b_resident != 0;
-  const uint32_t stage_bytes = b_res ? Cfg::kABytes : Cfg::kStageBytes;
+  const int U = g.units;  // k chunks per stage (divides nk)
+  const uint32_t stage_bytes = U * (b_res ? Cfg::kABytes : Cfg::kStageBytes);
   uint8_t* stage_base = smem;
   uint8_t* b_base = smem + static_cast<size_t>(stages) * stage_bytes;  // resident B images
   int32_t* s_rs = reinterpret_cast<int32_t*>(b_base + (b_res ? 16 * nk * Cfg::kBBytes : 0));
   float* s_out = reinterpret_cast<float*>(s_rs + 2 * 16 * kBM);  // [4 quadrants][64 segs][BN]
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(s_out + Cfg::kOutBytes / 4);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(s_out + (STAGE ? Cfg::kOutBytes / 4 : 0));
   uint64_t* empty_bar = full_bar + stages;
   uint64_t* acc_full = empty_bar + stages;  // [4]
   uint64_t* acc_empty = acc_full + 4;       // [4]
@@ -225,11 +238,12 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
     setmaxnreg_dec<kCtrlRegs>();
     if (warp == kProducerWarp && lane < g.ld_lanes) {
       // ---------------- TMA producer ----------------
-      // Lanes 0..ld_lanes-1 each copy a 1/ld_lanes slice of every stage (the
-      // images are contiguous bytes); lane 0 alone posts the expected bytes,
-      // before the slices in program order, so the phase cannot complete early.
-      const int nl = g.ld_lanes;
-      const uint32_t a_part = Cfg::kABytes / nl, b_part = Cfg::kBBytes / nl;
+      // One bulk copy per operand per stage (U k chunks of one position).
+      // ld_lanes = 2: lane 0 copies A and lane 1 copies B, so the two copies
+      // of a stage are issued by different threads (a single thread sustains
+      // roughly one bulk copy per ~460 SM cycles, scratch/l2_ingress_bench.cu);
+      // lane 0 posts the stage's expected bytes before either copy.
+      const bool do_a = lane == 0, do_b = !b_res && lane == g.ld_lanes - 1;
       if (b_res && lane == 0) {  // the single filter tile's B images, once
         mbar_arrive_expect_tx(b_full, 16 * nk * Cfg::kBBytes);
         bulk_load(b_base, codes_w, 16 * nk * Cfg::kBBytes, b_full);
@@ -241,8 +255,8 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         const int mt = t / nt, ntile = t % nt;
         const int m0 = mt * kBM;
         // Operand images of this tile (lance_kernels.cuh umma_image_offset).
-        const uint8_t* a_tile = codes_a + static_cast<long long>(mt) * 16 * nk * Cfg::kABytes + lane * a_part;
-        const uint8_t* b_tile = codes_w + static_cast<long long>(ntile) * 16 * nk * Cfg::kBBytes + lane * b_part;
+        const uint8_t* a_tile = codes_a + static_cast<long long>(mt) * 16 * nk * Cfg::kABytes;
+        const uint8_t* b_tile = codes_w + static_cast<long long>(ntile) * 16 * nk * Cfg::kBBytes;
         if (!g.rs_warps && lane == 0) {  // row sums of the tile's 128 rows, all 16 positions (OOB rows read 0)
           const uint32_t rb = lt & 1u;
           mbar_wait(&rs_empty[rb], ((lt >> 1) & 1u) ^ 1u);
@@ -252,14 +266,14 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         for (int j = 0; j < 4; ++j)
           for (int a = 0; a < 4; ++a) {
             const int u0 = image_plane(4 * a + j) * nk;
-            for (int kc = 0; kc < nk; ++kc) {
+            for (int kc = 0; kc < nk; kc += U) {
               mbar_wait(&empty_bar[s], ph ^ 1u);
               uint8_t* sa = stage_base + static_cast<size_t>(s) * stage_bytes;
               if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
-              __syncwarp((1u << nl) - 1u);
-              bulk_load(sa + lane * a_part, a_tile + (u0 + kc) * Cfg::kABytes, a_part, &full_bar[s]);
-              if (!b_res)
-                bulk_load(sa + Cfg::kABytes + lane * b_part, b_tile + (u0 + kc) * Cfg::kBBytes, b_part,
+              __syncwarp((1u << g.ld_lanes) - 1u);
+              if (do_a) bulk_load(sa, a_tile + (u0 + kc) * Cfg::kABytes, U * Cfg::kABytes, &full_bar[s]);
+              if (do_b)
+                bulk_load(sa + U * Cfg::kABytes, b_tile + (u0 + kc) * Cfg::kBBytes, U * Cfg::kBBytes,
                           &full_bar[s]);
               if (++s == stages) {
                 s = 0;
@@ -290,19 +304,22 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
             const uint32_t d_base = tmem_base + buf * Cfg::kGroupCols;
             for (int a = 0; a < 4; ++a) {
               const int u0 = image_plane(4 * a + j) * nk;
-              for (int kc = 0; kc < nk; ++kc) {
+              for (int kc = 0; kc < nk; kc += U) {
                 mbar_wait(&full_bar[s], ph);
                 tc_fence_after();
-                const uint32_t sa = smem_u32(stage_base + static_cast<size_t>(s) * stage_bytes);
-                const uint32_t sb =
-                    b_res ? b_res_base + (u0 + kc) * Cfg::kBBytes : sa + Cfg::kABytes;
+                const uint32_t sa0 = smem_u32(stage_base + static_cast<size_t>(s) * stage_bytes);
+                for (int u = 0; u < U; ++u) {
+                  const uint32_t sa = sa0 + u * Cfg::kABytes;
+                  const uint32_t sb = b_res ? b_res_base + (u0 + kc + u) * Cfg::kBBytes
+                                            : sa0 + U * Cfg::kABytes + u * Cfg::kBBytes;
 #pragma unroll
-                for (int kk = 0; kk < BK / 32; ++kk) {
-                  if (kExpSwitches && (g.exp & 2)) break;
-                  const uint64_t adesc = umma_smem_desc(sa + kk * 32, 8 * BK, Cfg::kLayout);
-                  const uint64_t bdesc = umma_smem_desc(sb + kk * 32, 8 * BK, Cfg::kLayout);
-                  umma_i8(d_base + static_cast<uint32_t>(a * BN), adesc, bdesc, kIdesc,
-                          (kc > 0 || kk > 0) ? 1u : 0u);
+                  for (int kk = 0; kk < BK / 32; ++kk) {
+                    if (kExpSwitches && (g.exp & 2)) break;
+                    const uint64_t adesc = umma_smem_desc(sa + kk * 32, 8 * BK, Cfg::kLayout);
+                    const uint64_t bdesc = umma_smem_desc(sb + kk * 32, 8 * BK, Cfg::kLayout);
+                    umma_i8(d_base + static_cast<uint32_t>(a * BN), adesc, bdesc, kIdesc,
+                            (kc + u > 0 || kk > 0) ? 1u : 0u);
+                  }
                 }
                 umma_commit(&empty_bar[s]);
                 if (++s == stages) {
@@ -445,6 +462,23 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
           }
 #pragma unroll
           for (int i = 0; i < FPT / 2; ++i) v[i] = add2(v[i], bcast2(0.0f));  // the reference never yields -0
+          if (!STAGE) {  // straight from registers: this thread's FPT filters of pixel (a, b)
+            if (!((pmask >> (2 * a + b)) & 1)) continue;
+            float* d = y + static_cast<long long>(pix0 + a * g.OW + b) * g.K + kf0;
+#pragma unroll
+            for (int i = 0; i < FPT / 4; ++i) {
+              const int kf = kf0 + 4 * i;
+              if (k4ok && kf + 4 <= g.K) {
+                *reinterpret_cast<float4*>(d + 4 * i) = make_float4(v[2 * i].x, v[2 * i].y, v[2 * i + 1].x, v[2 * i + 1].y);
+              } else {
+                const float e4[4] = {v[2 * i].x, v[2 * i].y, v[2 * i + 1].x, v[2 * i + 1].y};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  if (kf + e < g.K) d[4 * i + e] = e4[e];
+              }
+            }
+            continue;
+          }
           const int seg = 2 * lane + a;
 #pragma unroll
           for (int i = 0; i < FPT / 4; ++i) {
@@ -453,6 +487,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
                 make_float4(v[2 * i].x, v[2 * i].y, v[2 * i + 1].x, v[2 * i + 1].y);
           }
         }
+        if (!STAGE) return;
         named_bar_sync(2 + q, 128);
         const int wq = ew >> 2;  // warp within the quadrant
         // Chunk id = wq * 32 + lane + 128 k: segment id / CPR, chunk id % CPR.
@@ -615,7 +650,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   }
 }
 
-template <int BK, int BN, bool SMALL, bool DUMP>
+template <int BK, int BN, bool SMALL, bool DUMP, bool STAGE>
 static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
                                  const CUtensorMap* tmR, int32_t* rowsum_out, const int32_t* colsum,
                                  const LanceDevState* st, float* y, int32_t* acc_dump,
@@ -624,20 +659,40 @@ static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
   const int nk = g.num_kchunks;
   // Resident B: one filter tile whose 16 positions x C_pad images fit in 64 KB.
   const int b_res = (g.num_n_tiles == 1 && 16 * nk * GemmCfg<BK, BN>::kBBytes <= 64 * 1024) ? 1 : 0;
+  // Units per stage: g.units (0 = auto: 1) if it divides nk and leaves >= 3
+  // stages; the row-sum warps read one image per stage, so U = 1 with them.
+  int units = g.units > 0 ? g.units : 1;
+  if (g.rs_warps || nk % units != 0 || gemm_smem_bytes<BK, BN>(3, nk, b_res, STAGE, units) > kSmemLimit)
+    units = 1;
   int stages = 16;
-  while (stages > 2 && gemm_smem_bytes<BK, BN>(stages, nk, b_res) > kSmemLimit) --stages;
-  const size_t smem = gemm_smem_bytes<BK, BN>(stages, nk, b_res);
+  while (stages > 2 && gemm_smem_bytes<BK, BN>(stages, nk, b_res, STAGE, units) > kSmemLimit) --stages;
+  const size_t smem = gemm_smem_bytes<BK, BN>(stages, nk, b_res, STAGE, units);
   if (smem > kSmemLimit) return cudaErrorInvalidValue;
   g.b_resident = b_res;
   g.stages = stages;
+  g.units = units;
   const cudaError_t e =
-      ensure_smem_attr(reinterpret_cast<const void*>(gemm_epilogue_kernel<BK, BN, SMALL, DUMP>), smem);
+      ensure_smem_attr(reinterpret_cast<const void*>(gemm_epilogue_kernel<BK, BN, SMALL, DUMP, STAGE>), smem);
   if (e != cudaSuccess) return e;
   const int sms = current_sm_count();
   const long long tiles = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * g.num_n_tiles;
   const int grid = static_cast<int>(tiles < sms ? tiles : sms);
-  return launch_k(gemm_epilogue_kernel<BK, BN, SMALL, DUMP>, grid, kGemmThreadsP, smem, s, codes_a,
+  return launch_k(gemm_epilogue_kernel<BK, BN, SMALL, DUMP, STAGE>, grid, kGemmThreadsP, smem, s, codes_a,
                   codes_w, *tmR, rowsum_out, colsum, st, y, acc_dump, bias, relu, g);
+}
+
+template <int BK, int BN, bool SMALL, bool DUMP>
+static cudaError_t launch_gemm_s(const uint8_t* codes_a, const uint8_t* codes_w,
+                                 const CUtensorMap* tmR, int32_t* rowsum_out, const int32_t* colsum,
+                                 const LanceDevState* st, float* y, int32_t* acc_dump,
+                                 const float* bias, int relu, const GemmGeom& g, cudaStream_t s) {
+  if constexpr (BN == 64) {
+    if (!g.stage_out)
+      return launch_gemm_t<BK, BN, SMALL, DUMP, false>(codes_a, codes_w, tmR, rowsum_out, colsum, st, y,
+                                                       acc_dump, bias, relu, g, s);
+  }
+  return launch_gemm_t<BK, BN, SMALL, DUMP, true>(codes_a, codes_w, tmR, rowsum_out, colsum, st, y,
+                                                  acc_dump, bias, relu, g, s);
 }
 
 template <int BK, int BN>
@@ -647,13 +702,13 @@ static cudaError_t launch_gemm_bk(const uint8_t* codes_a, const uint8_t* codes_w
                                   const float* bias, int relu, const GemmGeom& g, cudaStream_t s) {
   const bool dump = acc_dump != nullptr;
   if (small_acc)
-    return dump ? launch_gemm_t<BK, BN, true, true>(codes_a, codes_w, tmR, rowsum_out, colsum, st, y, acc_dump,
+    return dump ? launch_gemm_s<BK, BN, true, true>(codes_a, codes_w, tmR, rowsum_out, colsum, st, y, acc_dump,
                                                     bias, relu, g, s)
-                : launch_gemm_t<BK, BN, true, false>(codes_a, codes_w, tmR, rowsum_out, colsum, st, y, acc_dump,
+                : launch_gemm_s<BK, BN, true, false>(codes_a, codes_w, tmR, rowsum_out, colsum, st, y, acc_dump,
                                                      bias, relu, g, s);
-  return dump ? launch_gemm_t<BK, BN, false, true>(codes_a, codes_w, tmR, rowsum_out, colsum, st, y, acc_dump,
+  return dump ? launch_gemm_s<BK, BN, false, true>(codes_a, codes_w, tmR, rowsum_out, colsum, st, y, acc_dump,
                                                    bias, relu, g, s)
-              : launch_gemm_t<BK, BN, false, false>(codes_a, codes_w, tmR, rowsum_out, colsum, st, y, acc_dump,
+              : launch_gemm_s<BK, BN, false, false>(codes_a, codes_w, tmR, rowsum_out, colsum, st, y, acc_dump,
                                                     bias, relu, g, s);
 }
 
