@@ -224,7 +224,7 @@ void free_plan(lance_plan_s* p) {
 #ifdef LANCE_PROFILING
   if (p->gemm_geom.trace != nullptr) {
     if (const char* path = std::getenv("LANCE_GEMM_TRACE")) {
-      std::vector<unsigned long long> h(500000);
+      std::vector<unsigned long long> h(800000);
       if (cudaMemcpy(h.data(), p->gemm_geom.trace, h.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess) {
         const std::string f = std::string(path) + "_c" + std::to_string(p->spec.c) + "_h" +
                               std::to_string(p->spec.h) + ".bin";
@@ -493,8 +493,13 @@ int lance_plan_create_tiled(const lance_conv_spec* spec, const lance_config* cfg
     delete p;
     return cuda_fail(e, "plan init");
   }
-  if (lance_knob("LANCE_GEMM_TRACE", 0) != 0 &&
-      (rc = dev_alloc(p, &p->gemm_geom.trace, sizeof(unsigned long long) * 500000))) {
+#ifdef LANCE_PROFILING
+  const bool want_trace = std::getenv("LANCE_GEMM_TRACE") != nullptr;  // value = dump path prefix
+#else
+  const bool want_trace = false;
+#endif
+  if (want_trace &&
+      (rc = dev_alloc(p, &p->gemm_geom.trace, sizeof(unsigned long long) * 800000))) {
     free_plan(p);
     delete p;
     return rc;

@@ -134,7 +134,8 @@ __device__ __forceinline__ void affine_group4(const uint32_t (&acc)[4][4], bool 
   }
 }
 
-// Profiling trace (LANCE_GEMM_TRACE): CTA 0 records globaltimer-free SM clocks.
+// Profiling trace (LANCE_GEMM_TRACE): CTA 0 records SM clocks, 8 slots x 100000
+// events (buffer allocated by lance_abi.cu in LANCE_PROFILING builds).
 __device__ __forceinline__ void trace_event(unsigned long long* tr, int slot, int i) {
 #ifdef LANCE_GEMM_TRACE
   if (tr != nullptr && blockIdx.x == 0 && i < 100000) tr[slot * 100000 + i] = clock64();
@@ -251,6 +252,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       int s = 0;
       uint32_t ph = 0;
       uint32_t lt = 0;
+      int tr_p = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
         const int mt = t / nt, ntile = t % nt;
         const int m0 = mt * kBM;
@@ -268,6 +270,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
             const int u0 = image_plane(4 * a + j) * nk;
             for (int kc = 0; kc < nk; kc += U) {
               mbar_wait(&empty_bar[s], ph ^ 1u);
+              if (lane == 0) trace_event(g.trace, 0, tr_p++);
               uint8_t* sa = stage_base + static_cast<size_t>(s) * stage_bytes;
               if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
               __syncwarp((1u << g.ld_lanes) - 1u);
@@ -296,16 +299,19 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         int s = 0;
         uint32_t ph = 0;
         uint32_t grp = 0;
+        int tr_m = 0;
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
           for (int j = 0; j < 4; ++j, ++grp) {
             const uint32_t buf = grp % NB;
             mbar_wait(&acc_empty[buf], (grp / NB) & 1u);  // epilogue drained it
+            trace_event(g.trace, 7, grp);
             tc_fence_after();
             const uint32_t d_base = tmem_base + buf * Cfg::kGroupCols;
             for (int a = 0; a < 4; ++a) {
               const int u0 = image_plane(4 * a + j) * nk;
               for (int kc = 0; kc < nk; kc += U) {
                 mbar_wait(&full_bar[s], ph);
+                trace_event(g.trace, 1, tr_m);
                 tc_fence_after();
                 const uint32_t sa0 = smem_u32(stage_base + static_cast<size_t>(s) * stage_bytes);
                 for (int u = 0; u < U; ++u) {
@@ -322,6 +328,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
                   }
                 }
                 umma_commit(&empty_bar[s]);
+                trace_event(g.trace, 2, tr_m++);
                 if (++s == stages) {
                   s = 0;
                   ph ^= 1u;
@@ -566,6 +573,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         const uint32_t buf = static_cast<uint32_t>(j % NB);
         float rterm[4], k1s[4], k4[4];  // per position 4a + j of this j-group
         if (g.rs_warps || j == 0) mbar_wait(&rs_ready[rb * 4 + (g.rs_warps ? j : 0)], (lt >> 1) & 1u);
+        if (ew == 0 && lane == 0) trace_event(g.trace, 6, grp);
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
           // k2[p] * float(sum_a): second term of affine_term
@@ -632,6 +640,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
             }
           }
         }
+        if (ew == 0 && lane == 0) trace_event(g.trace, 5, grp);
         if (kExpSwitches && (g.exp & 1)) continue;
         if (g.pool) {
           if (j == 3) store_pool(S[0], S[1], S[2], S[3]);
