@@ -413,6 +413,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--layers", type=str, default="", help="comma list of layer indices (debug)")
+    ap.add_argument("--graph", type=int, default=1,
+                    help="1: replay each step from one CUDA graph (default); 0: eager launches")
     ap.add_argument("--layout", default="nhwc", choices=["nhwc", "nchw"],
                     help="input layout of x (nchw: the north-star NCHW option, F(2x2) only)")
     ap.add_argument("--tile-m", type=int, default=2, choices=[2, 4],
@@ -487,12 +489,13 @@ def main():
     stream = torch.cuda.current_stream(dev)
     use_global = args.mode == "global" and ws > 1
 
-    def step():
+    def step(st=None):
+        st = stream if st is None else st
         for spec, conv, x, w, y, *_ in state:
             if use_global:
-                shard.global_forward(conv, x, y, stream=stream)
+                shard.global_forward(conv, x, y, stream=st)
             else:
-                conv.forward(x, y, stream=stream)
+                conv.forward(x, y, stream=st)
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -500,6 +503,21 @@ def main():
         step()
     for _, conv, *_ in state:
         conv.sync(stream)
+    # One CUDA graph per step (the 3 x 13 stream-ordered launches of the plans;
+    # the launch-bound small per-GPU batches of the strong-scaling split need
+    # it).  The global-fit mode keeps its NCCL call eager.
+    graph = None
+    if args.graph and not use_global:
+        cap = torch.cuda.Stream(device=dev)
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            step(cap)  # warm the capture stream (kernel attributes already set)
+        stream.wait_stream(cap)
+        torch.cuda.synchronize(dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cap):
+            step(cap)
+        torch.cuda.synchronize(dev)
     if pg:
         pg.barrier()
     torch.cuda.synchronize(dev)
@@ -508,7 +526,10 @@ def main():
     clocks.mark()
     e0.record(stream)
     for _ in range(args.steps):
-        step()
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
     e1.record(stream)
     torch.cuda.synchronize(dev)
     clocks.mark()
@@ -710,7 +731,8 @@ def main():
                                           "global fit (one 2P+1-float NCCL MAX all-reduce per layer)"))
                        if ws > 1 else "single GPU",
                        "filters": "prepared once per layer (K2) outside the step",
-                       "l2": "no flush: per-step working set (13 layers x, codes, y) ~4 GB >> 126 MB L2"},
+                       "l2": "no flush: per-step working set (13 layers x, codes, y) ~4 GB at batch 256 (0.5 GB at 32) >> 126 MB L2",
+                       "launch": "one CUDA graph per step (3 x 13 kernels)" if (args.graph and not use_global) else "eager"},
             "tops_equivalent": tops_eq,
             "roofline": roofline,
             "cpu_baseline": cpu,
