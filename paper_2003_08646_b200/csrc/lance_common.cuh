@@ -167,11 +167,9 @@ __device__ __forceinline__ uint32_t exact_code_near_boundary(float d, float s, f
 }
 
 // ---------------------------------------------------------------- ranges
-// Block-wide (min, max) partials -> the last block to finish folds all
-// partials; returns true in that block with the 32 results in s_red[0..31].
-__device__ __forceinline__ bool block_minmax_and_ticket(float (&lo)[16], float (&hi)[16],
-                                                        float* partials, unsigned int* ticket,
-                                                        float* s_red /*[blockDim.x]*/) {
+// Block-wide (min, max) of lo[16] / hi[16] -> this block's 32 partials.
+__device__ __forceinline__ void block_minmax_to_partials(float (&lo)[16], float (&hi)[16],
+                                                         float* partials, float* s_red /*[blockDim.x]*/) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
 #pragma unroll
@@ -197,18 +195,16 @@ __device__ __forceinline__ bool block_minmax_and_ticket(float (&lo)[16], float (
       r = (i < 16) ? fmin_nan(r, s_red[w * 32 + i]) : fmax_nan(r, s_red[w * 32 + i]);
     partials[static_cast<long long>(blockIdx.x) * 32 + i] = r;
   }
-  __threadfence();
-  __syncthreads();
-  __shared__ unsigned int s_last;
-  if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
-  __syncthreads();
-  if (!s_last) return false;
-  __threadfence();
+}
+
+// Fold the 32-float partials of nb blocks -> s_red[0..31] (whole block).
+__device__ __forceinline__ void fold_partials(const float* partials, int nb, float* s_red) {
+  const int warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
   const int col = threadIdx.x & 31;
   float r = (col < 16) ? __int_as_float(0x7f800000) : __int_as_float(0xff800000);
   // Eight independent partial loads in flight per thread (a serial chain of
   // dependent L2 round trips here cost tens of microseconds on small layers).
-  const int nb = static_cast<int>(gridDim.x);
   for (int b0 = warp; b0 < nb; b0 += 8 * nw) {
     float v[8];
 #pragma unroll
@@ -230,6 +226,22 @@ __device__ __forceinline__ bool block_minmax_and_ticket(float (&lo)[16], float (
     s_red[threadIdx.x] = q;
   }
   __syncthreads();
+}
+
+// Block-wide (min, max) partials -> the last block to finish folds all
+// partials; returns true in that block with the 32 results in s_red[0..31].
+__device__ __forceinline__ bool block_minmax_and_ticket(float (&lo)[16], float (&hi)[16],
+                                                        float* partials, unsigned int* ticket,
+                                                        float* s_red /*[blockDim.x]*/) {
+  block_minmax_to_partials(lo, hi, partials, s_red);
+  __threadfence();
+  __syncthreads();
+  __shared__ unsigned int s_last;
+  if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  fold_partials(partials, static_cast<int>(gridDim.x), s_red);
   if (threadIdx.x == 0) *ticket = 0u;
   return true;
 }

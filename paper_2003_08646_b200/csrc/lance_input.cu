@@ -369,28 +369,13 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // and the code to [0, top]; far-out values then round to 0 / top exactly as the
 // reference's clamps do, and near-ties (|residual| >= 0.5 - 2^-14, which
 // includes the 0.5 and top + 0.5 boundaries) take the IEEE-division quantiser.
-template <int BK, int NK, bool RS, bool STATIC = false>
-__global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* __restrict__ x,
-                                                                  uint8_t* __restrict__ codes,
-                                                                  int32_t* __restrict__ rowsum,
-                                                                  const LanceDevState* __restrict__ st,
-                                                                  InGeom g) {
-  pdl_entry();
-  __shared__ float s_tmin[16], s_scale[16], s_rcp[16];
-  const int tid = threadIdx.x, lane = tid & 31;
-  if (tid < 16) {
-    s_tmin[tid] = st->a_tmin[tid];
-    s_scale[tid] = st->a_scale[tid];
-    s_rcp[tid] = st->a_rcp[tid];
-  }
-  const float top = static_cast<float>((1 << st->bits_i) - 1);
-  __syncthreads();
-  // Reverse order: the range pass (K0) just streamed x front to back, so the
-  // tail of x is still in L2 when this kernel starts; and the GEMM, which
-  // reads the codes front to back, then finds the last-written rows in L2.
-  const long long wi = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
-  if (wi >= g.num_items) return;
-  const long long item = g.rev_items ? g.num_items - 1 - wi : wi;
+// One K1 strip (item) of the fast path: v recomputed, quantised, codes +
+// row sums written.
+template <int BK, int NK, bool RS, bool STATIC>
+__device__ __forceinline__ void quant_fast_item(const float* __restrict__ x, uint8_t* __restrict__ codes,
+                                                int32_t* __restrict__ rowsum, const InGeom& g,
+                                                long long item, int lane, const float* s_tmin,
+                                                const float* s_scale, const float* s_rcp, float top) {
   const StripItem it = strip_item(g, item, lane);
   const Strip<true> sp(x, g, it);
   const bool rows_in = sp.rows_ok();
@@ -495,6 +480,32 @@ __global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* _
   }
 }
 
+
+template <int BK, int NK, bool RS, bool STATIC = false>
+__global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* __restrict__ x,
+                                                                  uint8_t* __restrict__ codes,
+                                                                  int32_t* __restrict__ rowsum,
+                                                                  const LanceDevState* __restrict__ st,
+                                                                  InGeom g) {
+  pdl_entry();
+  __shared__ float s_tmin[16], s_scale[16], s_rcp[16];
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < 16) {
+    s_tmin[tid] = st->a_tmin[tid];
+    s_scale[tid] = st->a_scale[tid];
+    s_rcp[tid] = st->a_rcp[tid];
+  }
+  const float top = static_cast<float>((1 << st->bits_i) - 1);
+  __syncthreads();
+  // Reverse order: the range pass (K0) just streamed x front to back, so the
+  // tail of x is still in L2 when this kernel starts; and the GEMM, which
+  // reads the codes front to back, then finds the last-written rows in L2.
+  const long long wi = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
+  if (wi >= g.num_items) return;
+  const long long item = g.rev_items ? g.num_items - 1 - wi : wi;
+  quant_fast_item<BK, NK, RS, STATIC>(x, codes, rowsum, g, item, lane, s_tmin, s_scale, s_rcp, top);
+}
+
 // Static-params mode: caller-supplied input QuantParams[16].
 __global__ void static_params_kernel(LanceDevState* st, StaticParams prm, int C) {
   pdl_entry();
@@ -523,21 +534,12 @@ __global__ void static_params_kernel(LanceDevState* st, StaticParams prm, int C)
 // (CC > 0): no per-copy multiplies.  A lane only reads back the slots it
 // copied itself, so per-thread cp.async groups are the only ordering needed.
 // Transform and range arithmetic as input_range_kernel.
+// The K0 strip loop (ring below) over this block's grid-stride items, folding
+// every v into lo / hi.  s_ring: [8 warps][D + 1 slots][8][32] float2.
 template <int D, int CC>
-__global__ void __launch_bounds__(256, 2) input_range_ring_kernel(const float* __restrict__ x,
-                                                                  float* __restrict__ partials,
-                                                                  LanceDevState* __restrict__ st,
-                                                                  InGeom g) {
-  pdl_entry();
+__device__ __forceinline__ void range_ring_phase(const float* __restrict__ x, const InGeom& g,
+                                                 float (&lo)[16], float (&hi)[16], float2* s_ring) {
   constexpr int R = D + 1;
-  extern __shared__ float2 s_ring[];  // [8 warps][R slots][2 columns x 4 rows][32 lanes]
-  __shared__ float s_red[256];
-  float lo[16], hi[16];
-#pragma unroll
-  for (int p = 0; p < 16; ++p) {
-    lo[p] = __int_as_float(0x7f800000);
-    hi[p] = __int_as_float(0xff800000);
-  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int C = CC > 0 ? CC : g.C;
   const int W = g.W;
@@ -631,6 +633,23 @@ __global__ void __launch_bounds__(256, 2) input_range_ring_kernel(const float* _
     }
   }
   cp_async_wait<0>();
+}
+
+template <int D, int CC>
+__global__ void __launch_bounds__(256, 2) input_range_ring_kernel(const float* __restrict__ x,
+                                                                  float* __restrict__ partials,
+                                                                  LanceDevState* __restrict__ st,
+                                                                  InGeom g) {
+  pdl_entry();
+  extern __shared__ float2 s_ring[];  // [8 warps][R slots][2 columns x 4 rows][32 lanes]
+  __shared__ float s_red[256];
+  float lo[16], hi[16];
+#pragma unroll
+  for (int p = 0; p < 16; ++p) {
+    lo[p] = __int_as_float(0x7f800000);
+    hi[p] = __int_as_float(0xff800000);
+  }
+  range_ring_phase<D, CC>(x, g, lo, hi, s_ring);
   if (block_minmax_and_ticket(lo, hi, partials, &st->ticket_in, s_red)) {
     fit_from_ranges(s_red, g.granularity, st->bits_i, st->a_tmin, st->a_tmax, st->a_scale,
                     st->a_rcp, &st->nan_in);
