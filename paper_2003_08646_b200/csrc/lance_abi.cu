@@ -364,12 +364,15 @@ int lance_plan_create_tiled(const lance_conv_spec* spec, const lance_config* cfg
   // columns, 16 filters' S partials per epilogue thread) unless the layer has
   // fewer.  LANCE_GEMM_BN overrides.
   p->BN = spec->k > 32 ? 64 : (spec->k > 16 ? 32 : 16);
-  // Small-M layers (fewer 64-filter tiles than SMs, e.g. VGG's 4x4 / 2x2 maps)
-  // get twice the tiles at BN = 32 (measured: -10..-17 % GEMM time there).
+  // Small-M layers (64-filter tiles for at most half the SMs, e.g. VGG's
+  // 4x4 / 2x2 maps, ResNet's 7x7 / 14x14 maps at per-GPU batches <= 32) get
+  // twice the tiles at BN = 32.  Between half and all of the SMs, BN = 64 is
+  // faster (R128 at batch 32: 19.7 vs 24.8 us; R256 at batch 64: 24.7 vs
+  // 36.6 us, gpurun_out/gsmall).
   {
     const long long row_blocks = (static_cast<long long>(spec->n) * ((out_h(*spec) + 1) / 2) *
                                       ((out_w(*spec) + 1) / 2) + kBM - 1) / kBM;
-    if (p->BN == 64 && row_blocks * ((spec->k + 63) / 64) < p->sm_count) p->BN = 32;
+    if (p->BN == 64 && 2 * row_blocks * ((spec->k + 63) / 64) <= p->sm_count) p->BN = 32;
   }
   {
     const int v = lance_knob("LANCE_GEMM_BN", 0);
@@ -460,7 +463,11 @@ int lance_plan_create_tiled(const lance_conv_spec* spec, const lance_config* cfg
   {
     const int v = lance_knob("LANCE_GEMM_LANES", 1);
     gg.ld_lanes = (v == 1 || v == 2) ? v : 1;
-    gg.units = lance_knob("LANCE_GEMM_UNITS", p->C_pad >= 512 && p->BK == 128 ? 2 : 1);
+    // 2 k chunks per stage also for 32-filter tiles with an even chunk count
+    // (small-M layers: R256 at batch 32 22.7 -> 20.0 us, gpurun_out/gsmall).
+    const int nk = p->C_pad / p->BK;
+    const bool u2 = (p->C_pad >= 512 && p->BK == 128) || (p->BN == 32 && nk % 2 == 0);
+    gg.units = lance_knob("LANCE_GEMM_UNITS", u2 ? 2 : 1);
   }
   p->in_geom.rev_items = lance_knob("LANCE_K1_REVERSE", 1) ? 1 : 0;
 
