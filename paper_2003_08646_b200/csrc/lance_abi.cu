@@ -181,6 +181,9 @@ struct lance_plan_s {
   int range_grid = 1, filter_grid = 1;
   InGeom in_geom{};
   int layout = LANCE_LAYOUT_NHWC;
+  bool jsplit = false;      // GEMM j-split over 4 CTAs per tile (small M)
+  float* tscratch = nullptr;
+  int* tticket = nullptr;
   float* x_nhwc = nullptr;  // NCHW input: staging buffer of the transposed batch
   FilterGeom f_geom{};
   GemmGeom gemm_geom{};
@@ -240,6 +243,8 @@ void free_plan(lance_plan_s* p) {
   for (cudaEvent_t e : p->events) cudaEventDestroy(e);
   p->events.clear();
   cudaFree(p->x_nhwc);
+  cudaFree(p->tscratch);
+  cudaFree(p->tticket);
   cudaFree(p->codes_a);
   cudaFree(p->rowsum);
   cudaFree(p->codes_w);
@@ -372,7 +377,11 @@ int lance_plan_create_tiled(const lance_conv_spec* spec, const lance_config* cfg
   {
     const long long row_blocks = (static_cast<long long>(spec->n) * ((out_h(*spec) + 1) / 2) *
                                       ((out_w(*spec) + 1) / 2) + kBM - 1) / kBM;
-    if (p->BN == 64 && 2 * row_blocks * ((spec->k + 63) / 64) <= p->sm_count) p->BN = 32;
+    // j-split (JS): when even 4 CTAs per 64-filter tile fit in one wave, keep
+    // BN = 64 and run each tile's 4 j-groups on 4 CTAs instead.
+    p->jsplit = lance_knob("LANCE_GEMM_JSPLIT", 1) != 0 && p->BN == 64 &&
+                4 * row_blocks * ((spec->k + 63) / 64) <= p->sm_count;
+    if (p->BN == 64 && !p->jsplit && 2 * row_blocks * ((spec->k + 63) / 64) <= p->sm_count) p->BN = 32;
   }
   {
     const int v = lance_knob("LANCE_GEMM_BN", 0);
@@ -457,6 +466,8 @@ int lance_plan_create_tiled(const lance_conv_spec* spec, const lance_config* cfg
   // (their shared-memory reads then cost the SS-UMMA little), else in K1.
   // LANCE_RS_GEMM overrides.
   gg.rs_warps = lance_knob("LANCE_RS_GEMM", p->BK <= 64 ? 1 : 0) ? 1 : 0;
+  if (p->jsplit && gg.rs_warps) p->jsplit = false;  // JS reads K1's row sums (BK = 128 layers)
+  gg.jsplit = p->jsplit ? 1 : 0;
   p->in_geom.rowsums = gg.rs_warps ? 0 : 1;
   // Producer lanes (LANCE_GEMM_LANES): 2 would issue a stage's A and B copies
   // from different threads; measured neutral (gpurun_out/gsweep), so 1.
@@ -510,6 +521,22 @@ int lance_plan_create_tiled(const lance_conv_spec* spec, const lance_config* cfg
     free_plan(p);
     delete p;
     return rc;
+  }
+  if (p->jsplit) {
+    const long long tiles = (p->M + kBM - 1) / kBM * (p->K_pad / p->BN);
+    if ((rc = dev_alloc(p, &p->tscratch, sizeof(float) * tiles * 4 * 2 * kBM * p->BN)) ||
+        (rc = dev_alloc(p, &p->tticket, sizeof(int) * tiles))) {
+      free_plan(p);
+      delete p;
+      return rc;
+    }
+    if (cudaMemset(p->tticket, 0, sizeof(int) * tiles) != cudaSuccess) {
+      free_plan(p);
+      delete p;
+      return cuda_fail(cudaGetLastError(), "plan init (j-split tickets)");
+    }
+    p->gemm_geom.tscratch = p->tscratch;
+    p->gemm_geom.tticket = p->tticket;
   }
   if ((rc = make_rowsum_map(&p->tmR, p->rowsum, p->M, p->rs_pitch))) {
     free_plan(p);
@@ -792,6 +819,7 @@ int lance_plan_set_epilogue_pool(lance_plan_t p, int pool) {
   if (pool && (p->OH < 2 || p->OW < 2))
     return fail(LANCE_ERR_INVALID_ARGUMENT, "lance_plan_set_epilogue_pool: output smaller than 2x2");
   p->gemm_geom.pool = pool;
+  p->gemm_geom.jsplit = (p->jsplit && !pool) ? 1 : 0;  // the fused pool needs the single-CTA fold
   return LANCE_OK;
 }
 

@@ -134,11 +134,15 @@ __device__ __forceinline__ void affine_group4(const uint32_t (&acc)[4][4], bool 
   }
 }
 
-// Profiling trace (LANCE_GEMM_TRACE): CTA 0 records SM clocks, 8 slots x 100000
+#ifndef LANCE_GEMM_TRACE_CTA
+#define LANCE_GEMM_TRACE_CTA 0
+#endif
+// Profiling trace (LANCE_GEMM_TRACE): CTA LANCE_GEMM_TRACE_CTA records SM clocks, 8 slots x 100000
 // events (buffer allocated by lance_abi.cu in LANCE_PROFILING builds).
 __device__ __forceinline__ void trace_event(unsigned long long* tr, int slot, int i) {
 #ifdef LANCE_GEMM_TRACE
-  if (tr != nullptr && blockIdx.x == 0 && i < 100000) tr[slot * 100000 + i] = clock64();
+  if (tr != nullptr && blockIdx.x == static_cast<unsigned>(LANCE_GEMM_TRACE_CTA) && i < 100000)
+    tr[slot * 100000 + i] = clock64();
 #else
   (void)tr;
   (void)slot;
@@ -153,7 +157,13 @@ __device__ __forceinline__ void tmem_ld_group4(uint32_t addr, int bn, uint32_t (
 
 // SMALL: see the file comment.  DUMP: also write the raw int32 accumulators
 // (parity tests).  bias / relu: fused epilogue (north-star extension).
-template <int BK, int BN, bool SMALL, bool DUMP, bool STAGE>
+// JS (j-split, small-M layers): a tile's 4 j-groups run on 4 CTAs as separate
+// work units (tile, j).  Each unit writes its T0j / T1j (the column folds of
+// A^T m, exact fp32, matrix.hpp:75-84) to g.tscratch; the unit that finishes
+// last (per-tile ticket) reads all four and completes the left fold
+// S00 = (T00 + T01) + T02, S01 = (T01 - T02) - T03 (S1b likewise) in the
+// reference order, so y is bit-identical to the single-CTA fold.
+template <int BK, int BN, bool SMALL, bool DUMP, bool STAGE, bool JS>
 __global__ void __launch_bounds__(kGemmThreadsP, 1)
     gemm_epilogue_kernel(const uint8_t* __restrict__ codes_a,
                          const uint8_t* __restrict__ codes_w,
@@ -200,6 +210,8 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   const int nt = g.num_n_tiles;
   const int K_pad = nt * BN;
   const int num_tiles = ((g.M + kBM - 1) / kBM) * nt;
+  // Work units: tiles, or (tile, j-group) pairs under JS (j fastest).
+  const int num_work = JS ? 4 * num_tiles : num_tiles;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -253,7 +265,9 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       uint32_t ph = 0;
       uint32_t lt = 0;
       int tr_p = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+      for (int w = blockIdx.x; w < num_work; w += gridDim.x, ++lt) {
+        const int t = JS ? w >> 2 : w;
+        const int j_lo = JS ? (w & 3) : 0, j_hi = JS ? j_lo + 1 : 4;
         const int mt = t / nt, ntile = t % nt;
         const int m0 = mt * kBM;
         // Operand images of this tile (lance_kernels.cuh umma_image_offset).
@@ -265,7 +279,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
           mbar_arrive_expect_tx(&rs_ready[rb * 4], Cfg::kRsBytes);
           tma_load_2d(s_rs + rb * 16 * kBM, &tmR, m0, 0, &rs_ready[rb * 4]);
         }
-        for (int j = 0; j < 4; ++j)
+        for (int j = j_lo; j < j_hi; ++j)
           for (int a = 0; a < 4; ++a) {
             const int u0 = image_plane(4 * a + j) * nk;
             for (int kc = 0; kc < nk; kc += U) {
@@ -300,8 +314,9 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         uint32_t ph = 0;
         uint32_t grp = 0;
         int tr_m = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-          for (int j = 0; j < 4; ++j, ++grp) {
+        for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
+          const int j_lo = JS ? (w & 3) : 0, j_hi = JS ? j_lo + 1 : 4;
+          for (int j = j_lo; j < j_hi; ++j, ++grp) {
             const uint32_t buf = grp % NB;
             mbar_wait(&acc_empty[buf], (grp / NB) & 1u);  // epilogue drained it
             trace_event(g.trace, 7, grp);
@@ -418,14 +433,17 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         s_cterm[b * 16 * BN + i] = __fmul_rn(s_k3[p], csum);
       }
     };
-    if (static_cast<int>(blockIdx.x) < num_tiles) cterm_slice(blockIdx.x, 0);
+    if (static_cast<int>(blockIdx.x) < num_work) cterm_slice(JS ? blockIdx.x >> 2 : blockIdx.x, 0);
     uint32_t grp = 0;
     uint32_t lt = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+    __shared__ int s_last;  // JS: this unit is its tile's last
+    for (int w = blockIdx.x; w < num_work; w += gridDim.x, ++lt) {
+      const int t = JS ? w >> 2 : w;
       // Slice lt is visible to every epilogue warp after this barrier, and
       // every warp is done with tile lt - 1, so its buffer takes tile lt + 1.
       named_bar_sync(6, 32 * kEpiWarps);
-      if (t + static_cast<int>(gridDim.x) < num_tiles) cterm_slice(t + gridDim.x, (lt + 1) & 1u);
+      if (w + static_cast<int>(gridDim.x) < num_work)
+        cterm_slice(JS ? (w + gridDim.x) >> 2 : w + gridDim.x, (lt + 1) & 1u);
       const float* ct_tile = s_cterm + (lt & 1u) * 16 * BN;
       const int m0 = (t / nt) * kBM, n0 = (t % nt) * BN;
       const int m = m0 + row;
@@ -563,6 +581,132 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       };
       const uint32_t rb = lt & 1u;
       const int32_t* rs_tile = s_rs + rb * 16 * kBM + row;
+      if constexpr (JS) {
+        // ---- one j-group of the tile: T0j / T1j to the scratch, then the
+        // tile's last unit folds all four and writes y.
+        const int j = w & 3;
+        const uint32_t buf = grp % NB;
+        float rterm[4], k1s[4], k4[4];
+        mbar_wait(&rs_ready[rb * 4], (lt >> 1) & 1u);
+        if (ew == 0 && lane == 0) trace_event(g.trace, 6, grp);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          rterm[a] = __fmul_rn(s_k2[4 * a + j], static_cast<float>(rs_tile[(4 * a + j) * kBM]));
+          k1s[a] = s_k1[4 * a + j];
+          k4[a] = s_k4[4 * a + j];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rs_empty[rb]);
+        mbar_wait(&acc_full[buf], (grp / NB) & 1u);
+        if (ew == 0 && lane == 0) trace_event(g.trace, 3, grp);
+        tc_fence_after();
+        const uint32_t acc_addr = lane_base + buf * Cfg::kGroupCols + f0;
+        // T scratch of this tile: [j][T0 / T1][BN / 4 filter quads][128 rows][4]
+        // (a warp's 32 rows of one quad are 512 contiguous bytes).
+        float* tsc = g.tscratch + static_cast<long long>(t) * 4 * 2 * kBM * BN;
+        auto tptr = [&](int jj, int which, int quad) {
+          return tsc + ((static_cast<long long>(jj * 2 + which) * (BN / 4) + quad) * kBM + row) * 4;
+        };
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          uint32_t ac[4][4];
+          tmem_ld_group4(acc_addr + 4 * c, BN, ac);
+          tmem_ld_wait();
+#pragma unroll
+          for (int a = 0; a < 4; ++a) reg_fence(ac[a]);
+          if (c == NCH - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[buf]);
+          }
+          if (DUMP && row_ok) {
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if (kf0 + 4 * c + i < g.K)
+                  acc_dump[(static_cast<long long>(4 * a + j) * g.M + m) * g.K + kf0 + 4 * c + i] =
+                      static_cast<int32_t>(ac[a][i]);
+          }
+          float2 T0[2], T1[2];
+          affine_group4<BN>(ac, fast, k1s, k4, rterm, ct_tile + j * BN + f0 + 4 * c, T0, T1);
+          __stcg(reinterpret_cast<float4*>(tptr(j, 0, f0 / 4 + c)), make_float4(T0[0].x, T0[0].y, T0[1].x, T0[1].y));
+          __stcg(reinterpret_cast<float4*>(tptr(j, 1, f0 / 4 + c)), make_float4(T1[0].x, T1[0].y, T1[1].x, T1[1].y));
+        }
+        if (ew == 0 && lane == 0) trace_event(g.trace, 4, grp);
+        ++grp;
+        // Publish; the tile's fourth unit to arrive folds.
+        __threadfence();
+        named_bar_sync(7, 32 * kEpiWarps);
+        if (threadIdx.x == 0) {
+          const int old = atomicAdd(g.tticket + t, 1);
+          s_last = old == 3;
+          if (old == 3) g.tticket[t] = 0;  // reusable by the next launch
+        }
+        named_bar_sync(7, 32 * kEpiWarps);
+        if (ew == 0 && lane == 0) trace_event(g.trace, 5, grp - 1);
+#ifdef LANCE_GEMM_TRACE
+        if (g.trace != nullptr && ew == 0 && lane == 0) g.trace[700000 + 4 * blockIdx.x + 2] = clock64();  // ticket done
+#endif
+        if (!s_last) continue;
+#ifdef LANCE_GEMM_TRACE
+        if (g.trace != nullptr && ew == 0 && lane == 0) g.trace[700000 + 4 * blockIdx.x] = clock64();  // fold start
+#endif
+        __threadfence();
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          float4 tv[4][2];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            tv[jj][0] = __ldcg(reinterpret_cast<const float4*>(tptr(jj, 0, f0 / 4 + c)));
+            tv[jj][1] = __ldcg(reinterpret_cast<const float4*>(tptr(jj, 1, f0 / 4 + c)));
+          }
+          // pixel (a, b): S00, S10 (b = 0) and S01, S11 (b = 1), the fold of
+          // the streaming path in the same order
+          float2 px[4][2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            auto lo2 = [&](const float4& v) { return h ? make_float2(v.z, v.w) : make_float2(v.x, v.y); };
+            const float2 t00 = lo2(tv[0][0]), t01 = lo2(tv[1][0]), t02 = lo2(tv[2][0]), t03 = lo2(tv[3][0]);
+            const float2 t10 = lo2(tv[0][1]), t11 = lo2(tv[1][1]), t12 = lo2(tv[2][1]), t13 = lo2(tv[3][1]);
+            px[0][h] = add2(add2(t00, t01), t02);  // S00: (a, b) = (0, 0)
+            px[1][h] = add2(add2(t10, t11), t12);  // S10: (1, 0)
+            px[2][h] = sub2(sub2(t01, t02), t03);  // S01: (0, 1)
+            px[3][h] = sub2(sub2(t11, t12), t13);  // S11: (1, 1)
+          }
+#pragma unroll
+          for (int pp = 0; pp < 4; ++pp) {
+            const int a = pp & 1, b = pp >> 1;
+            if (!((pmask >> (2 * a + b)) & 1)) continue;
+            const int kf = kf0 + 4 * c;
+            float2 v[2] = {px[pp][0], px[pp][1]};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (bias != nullptr)
+                v[h] = add2(v[h], make_float2(kf + 2 * h < g.K ? __ldg(bias + kf + 2 * h) : 0.0f,
+                                              kf + 2 * h + 1 < g.K ? __ldg(bias + kf + 2 * h + 1) : 0.0f));
+              if (relu) {
+                v[h].x = fmaxf(v[h].x, 0.0f);
+                v[h].y = fmaxf(v[h].y, 0.0f);
+              }
+              v[h] = add2(v[h], bcast2(0.0f));  // the reference never yields -0
+            }
+            float* d = y + static_cast<long long>(pix0 + a * g.OW + b) * g.K + kf;
+            if (k4ok && kf + 4 <= g.K) {
+              *reinterpret_cast<float4*>(d) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
+            } else {
+              const float e4[4] = {v[0].x, v[0].y, v[1].x, v[1].y};
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (kf + e < g.K) d[e] = e4[e];
+            }
+          }
+        }
+#ifdef LANCE_GEMM_TRACE
+        if (g.trace != nullptr && ew == 0 && lane == 0) g.trace[700000 + 4 * blockIdx.x + 1] = clock64();  // fold end
+#endif
+        continue;
+      }
       float2 S[4][FPT / 2];  // running S_ab partials, filter pairs
 #pragma unroll
       for (int j = 0; j < 4; ++j, ++grp) {
@@ -659,7 +803,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
   }
 }
 
-template <int BK, int BN, bool SMALL, bool DUMP, bool STAGE>
+template <int BK, int BN, bool SMALL, bool DUMP, bool STAGE, bool JS>
 static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
                                  const CUtensorMap* tmR, int32_t* rowsum_out, const int32_t* colsum,
                                  const LanceDevState* st, float* y, int32_t* acc_dump,
@@ -681,12 +825,12 @@ static cudaError_t launch_gemm_t(const uint8_t* codes_a, const uint8_t* codes_w,
   g.stages = stages;
   g.units = units;
   const cudaError_t e =
-      ensure_smem_attr(reinterpret_cast<const void*>(gemm_epilogue_kernel<BK, BN, SMALL, DUMP, STAGE>), smem);
+      ensure_smem_attr(reinterpret_cast<const void*>(gemm_epilogue_kernel<BK, BN, SMALL, DUMP, STAGE, JS>), smem);
   if (e != cudaSuccess) return e;
   const int sms = current_sm_count();
-  const long long tiles = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * g.num_n_tiles;
+  const long long tiles = ((static_cast<long long>(g.M) + kBM - 1) / kBM) * g.num_n_tiles * (JS ? 4 : 1);
   const int grid = static_cast<int>(tiles < sms ? tiles : sms);
-  return launch_k(gemm_epilogue_kernel<BK, BN, SMALL, DUMP, STAGE>, grid, kGemmThreadsP, smem, s, codes_a,
+  return launch_k(gemm_epilogue_kernel<BK, BN, SMALL, DUMP, STAGE, JS>, grid, kGemmThreadsP, smem, s, codes_a,
                   codes_w, *tmR, rowsum_out, colsum, st, y, acc_dump, bias, relu, g);
 }
 
@@ -696,12 +840,15 @@ static cudaError_t launch_gemm_s(const uint8_t* codes_a, const uint8_t* codes_w,
                                  const LanceDevState* st, float* y, int32_t* acc_dump,
                                  const float* bias, int relu, const GemmGeom& g, cudaStream_t s) {
   if constexpr (BN == 64) {
+    if (g.jsplit)  // y leaves from registers: no staging buffer, deeper operand stages
+      return launch_gemm_t<BK, BN, SMALL, DUMP, false, true>(codes_a, codes_w, tmR, rowsum_out, colsum, st,
+                                                             y, acc_dump, bias, relu, g, s);
     if (!g.stage_out)
-      return launch_gemm_t<BK, BN, SMALL, DUMP, false>(codes_a, codes_w, tmR, rowsum_out, colsum, st, y,
-                                                       acc_dump, bias, relu, g, s);
+      return launch_gemm_t<BK, BN, SMALL, DUMP, false, false>(codes_a, codes_w, tmR, rowsum_out, colsum, st,
+                                                              y, acc_dump, bias, relu, g, s);
   }
-  return launch_gemm_t<BK, BN, SMALL, DUMP, true>(codes_a, codes_w, tmR, rowsum_out, colsum, st, y,
-                                                  acc_dump, bias, relu, g, s);
+  return launch_gemm_t<BK, BN, SMALL, DUMP, true, false>(codes_a, codes_w, tmR, rowsum_out, colsum, st, y,
+                                                         acc_dump, bias, relu, g, s);
 }
 
 template <int BK, int BN>

@@ -71,6 +71,9 @@ struct GemmGeom {
   int units;        // k chunks per stage (0 = auto); the launcher settles it
   int exp;          // experiment switches (LANCE_GEMM_EXP, profiling only; 0 = normal)
   int pool;         // 1: fused 2x2 / stride-2 max-pool, y is [N][OH/2][OW/2][K]
+  int jsplit;       // 1: a tile's 4 j-groups on 4 CTAs (small-M layers, BN = 64)
+  float* tscratch;  // jsplit: [tiles][4 j][T0, T1][128 rows][BN] fp32
+  int* tticket;     // jsplit: per-tile arrival counters (self-resetting)
   int stage_out;    // 1: y through the shared-memory staging buffer (128-byte lines); 0: from registers (BN = 64)
   unsigned long long* trace;  // CTA-0 event timestamps (LANCE_GEMM_TRACE, profiling only)
 };
