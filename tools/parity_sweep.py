@@ -22,7 +22,7 @@ bad = 0
 n_cases = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 for i in range(n_cases):
     c = int(rng.choice([64, 128, 192, 256, 96, 40, 7]))
-    k = int(rng.choice([16, 24, 64, 80, 128]))
+    k = int(rng.choice([16, 24, 64, 80, 128, 192]))
     h, w = int(rng.integers(5, 23)), int(rng.integers(5, 23))
     n = int(rng.integers(1, 4))
     pad = int(rng.integers(0, 2))
