@@ -301,60 +301,70 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
       }
     } else if (warp == kMmaWarp) {
       // ---------------- TMEM + UMMA issuer ----------------
+      // The whole warp runs the (warp-uniform) loop, so stage addresses and
+      // descriptors live in uniform registers; one elected lane issues each
+      // tcgen05.mma / commit.  This thread's per-stage instruction latency
+      // bounds the shallow layers (16 one-position stages per tile on C = 64).
       tmem_alloc(tmem_holder, 512);
       tmem_relinquish();
       tc_fence_before();
       named_bar_sync(1, 32 + 32 * kEpiWarps);
       tc_fence_after();
       const uint32_t tmem_base = *tmem_holder;
-      if (lane == 0) {
-        if (b_res) mbar_wait(b_full, 0);
-        const uint32_t b_res_base = smem_u32(b_base);
-        int s = 0;
-        uint32_t ph = 0;
-        uint32_t grp = 0;
-        int tr_m = 0;
-        for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
-          const int j_lo = JS ? (w & 3) : 0, j_hi = JS ? j_lo + 1 : 4;
-          for (int j = j_lo; j < j_hi; ++j, ++grp) {
-            const uint32_t buf = grp % NB;
-            mbar_wait(&acc_empty[buf], (grp / NB) & 1u);  // epilogue drained it
-            trace_event(g.trace, 7, grp);
-            tc_fence_after();
-            const uint32_t d_base = tmem_base + buf * Cfg::kGroupCols;
-            for (int a = 0; a < 4; ++a) {
-              const int u0 = image_plane(4 * a + j) * nk;
-              for (int kc = 0; kc < nk; kc += U) {
-                mbar_wait(&full_bar[s], ph);
-                trace_event(g.trace, 1, tr_m);
-                tc_fence_after();
-                const uint32_t sa0 = smem_u32(stage_base + static_cast<size_t>(s) * stage_bytes);
-                for (int u = 0; u < U; ++u) {
-                  const uint32_t sa = sa0 + u * Cfg::kABytes;
-                  const uint32_t sb = b_res ? b_res_base + (u0 + kc + u) * Cfg::kBBytes
-                                            : sa0 + U * Cfg::kABytes + u * Cfg::kBBytes;
+      if (b_res) mbar_wait(b_full, 0);
+      const uint32_t b_res_base = smem_u32(b_base);
+      const uint32_t stage0 = smem_u32(stage_base);
+      uint32_t sa0 = stage0;  // shared address of stage s
+      int s = 0;
+      uint32_t ph = 0;
+      uint32_t grp = 0;
+      int tr_m = 0;
+      for (int w = blockIdx.x; w < num_work; w += gridDim.x) {
+        const int j_lo = JS ? (w & 3) : 0, j_hi = JS ? j_lo + 1 : 4;
+        for (int j = j_lo; j < j_hi; ++j, ++grp) {
+          const uint32_t buf = grp % NB;
+          mbar_wait(&acc_empty[buf], (grp / NB) & 1u);  // epilogue drained it
+          if (lane == 0) trace_event(g.trace, 7, grp);
+          tc_fence_after();
+          const uint32_t d_base = tmem_base + buf * Cfg::kGroupCols;
+          for (int a = 0; a < 4; ++a) {
+            const int u0 = image_plane(4 * a + j) * nk;
+            const uint32_t d_a = d_base + static_cast<uint32_t>(a * BN);
+            for (int kc = 0; kc < nk; kc += U) {
+              mbar_wait(&full_bar[s], ph);
+              if (lane == 0) trace_event(g.trace, 1, tr_m);
+              tc_fence_after();
+              for (int u = 0; u < U; ++u) {
+                const uint32_t sa = sa0 + u * Cfg::kABytes;
+                const uint32_t sb = b_res ? b_res_base + (u0 + kc + u) * Cfg::kBBytes
+                                          : sa0 + U * Cfg::kABytes + u * Cfg::kBBytes;
+                const uint64_t adesc0 = umma_smem_desc(sa, 8 * BK, Cfg::kLayout);
+                const uint64_t bdesc0 = umma_smem_desc(sb, 8 * BK, Cfg::kLayout);
 #pragma unroll
-                  for (int kk = 0; kk < BK / 32; ++kk) {
-                    if (kExpSwitches && (g.exp & 2)) break;
-                    const uint64_t adesc = umma_smem_desc(sa + kk * 32, 8 * BK, Cfg::kLayout);
-                    const uint64_t bdesc = umma_smem_desc(sb + kk * 32, 8 * BK, Cfg::kLayout);
-                    umma_i8(d_base + static_cast<uint32_t>(a * BN), adesc, bdesc, kIdesc,
-                            (kc + u > 0 || kk > 0) ? 1u : 0u);
-                  }
-                }
-                umma_commit(&empty_bar[s]);
-                trace_event(g.trace, 2, tr_m++);
-                if (++s == stages) {
-                  s = 0;
-                  ph ^= 1u;
+                for (int kk = 0; kk < BK / 32; ++kk) {
+                  if (kExpSwitches && (g.exp & 2)) break;
+                  // +32 bytes along K = +2 in the descriptor's start-address field
+                  if (elect_one())
+                    umma_i8(d_a, adesc0 + 2 * kk, bdesc0 + 2 * kk, kIdesc, (kc + u > 0 || kk > 0) ? 1u : 0u);
+                  __syncwarp();
                 }
               }
+              if (elect_one()) umma_commit(&empty_bar[s]);
+              __syncwarp();
+              if (lane == 0) trace_event(g.trace, 2, tr_m);
+              ++tr_m;
+              sa0 += stage_bytes;
+              if (++s == stages) {
+                s = 0;
+                ph ^= 1u;
+                sa0 = stage0;
+              }
             }
-            umma_commit(&acc_full[buf]);
           }
+          if (elect_one()) umma_commit(&acc_full[buf]);
+          __syncwarp();
         }
       }
-      __syncwarp();
     } else if (warp >= kRowSumWarp0 && g.rs_warps) {
       // ---------------- row sums (lowpgemm.hpp:121-123) ----------------
       // sum_c A[p][m][c] straight from every A stage: thread t owns rows t and

@@ -275,6 +275,17 @@ __device__ __forceinline__ uint64_t umma_smem_desc(uint32_t saddr, uint32_t sbo_
   return d;
 }
 
+// One elected lane of a converged warp (elect.sync): lets a warp-uniform loop
+// keep its addresses in uniform registers while a single thread issues the
+// tcgen05 / bulk-copy instruction.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // Instruction descriptor for kind::i8: D = s32, A = B = u8, both K-major.
 __host__ __device__ constexpr uint32_t umma_idesc_u8(int m, int n) {
   return (2u << 4)                                   // c_format = S32
