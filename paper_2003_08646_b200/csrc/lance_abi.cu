@@ -469,11 +469,7 @@ int lance_plan_create_tiled(const lance_conv_spec* spec, const lance_config* cfg
   if (p->jsplit && gg.rs_warps) p->jsplit = false;  // JS reads K1's row sums (BK = 128 layers)
   gg.jsplit = p->jsplit ? 1 : 0;
   p->in_geom.rowsums = gg.rs_warps ? 0 : 1;
-  // Producer lanes (LANCE_GEMM_LANES): 2 would issue a stage's A and B copies
-  // from different threads; measured neutral (gpurun_out/gsweep), so 1.
   {
-    const int v = lance_knob("LANCE_GEMM_LANES", 1);
-    gg.ld_lanes = (v == 1 || v == 2) ? v : 1;
     // 2 k chunks per stage also for 32-filter tiles with an even chunk count
     // (small-M layers: R256 at batch 32 22.7 -> 20.0 us, gpurun_out/gsmall).
     const int nk = p->C_pad / p->BK;

@@ -737,54 +737,62 @@ __global__ void __launch_bounds__(kF4Threads, 1)
       }
     } else if (warp == kF4EpiWarps + 1) {
       // ---------------- TMEM + UMMA issuer ----------------
+      // Warp-uniform loop (addresses / descriptors in uniform registers), one
+      // elected lane issues each tcgen05.mma / commit; the (position, k chunk)
+      // of a unit is tracked incrementally (no division on the issue path).
       tmem_alloc(&s_tmem, 512);
       tmem_relinquish();
       tc_fence_before();
       named_bar_sync(1, 32 + 32 * kF4EpiWarps);
       tc_fence_after();
       const uint32_t tmem_base = s_tmem;
-      if (lane == 0) {
-        if (b_res) mbar_wait(b_full, 0);
-        const uint32_t b_res_base = smem_u32(b_base);
-        int s = 0;
-        uint32_t ph = 0;
-        uint32_t grp = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-          for (int j = 0; j < 6; ++j, ++grp) {
-            const uint32_t buf = grp % kF4AccBufs;
-            mbar_wait(&acc_empty[buf], (grp / kF4AccBufs) & 1u);
+      if (b_res) mbar_wait(b_full, 0);
+      const uint32_t b_res_base = smem_u32(b_base);
+      int s = 0;
+      uint32_t ph = 0;
+      uint32_t grp = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        for (int j = 0; j < 6; ++j, ++grp) {
+          const uint32_t buf = grp % kF4AccBufs;
+          mbar_wait(&acc_empty[buf], (grp / kF4AccBufs) & 1u);
+          tc_fence_after();
+          const uint32_t d_base = tmem_base + buf * kF4GroupCols;
+          int a = 0, kc = 0;  // unit lu = a * nk + kc of the j-group
+          for (int lu0 = 0; lu0 < grp_units; lu0 += U) {
+            mbar_wait(&full_bar[s], ph);
             tc_fence_after();
-            const uint32_t d_base = tmem_base + buf * kF4GroupCols;
-            for (int lu0 = 0; lu0 < grp_units; lu0 += U) {
-              mbar_wait(&full_bar[s], ph);
-              tc_fence_after();
-              const uint32_t sa = smem_u32(smem + static_cast<size_t>(s) * stage_bytes);
-              for (int uu = 0; uu < U; ++uu) {
-                const int lu = lu0 + uu;          // unit within the j-group
-                const int a = lu / nk, kc = lu - (lu / nk) * nk;
-                const uint32_t ua = sa + uu * Cfg::kABytes;
-                const uint32_t ub = b_res ? b_res_base + (j * grp_units + lu) * Cfg::kBBytes
-                                          : sa + a_bytes + uu * Cfg::kBBytes;
+            const uint32_t sa = smem_u32(smem + static_cast<size_t>(s) * stage_bytes);
+            for (int uu = 0; uu < U; ++uu) {
+              const int lu = lu0 + uu;
+              const uint32_t ua = sa + uu * Cfg::kABytes;
+              const uint32_t ub = b_res ? b_res_base + (j * grp_units + lu) * Cfg::kBBytes
+                                        : sa + a_bytes + uu * Cfg::kBBytes;
+              const uint64_t adesc0 = umma_smem_desc(ua, 8 * BK, Cfg::kLayout);
+              const uint64_t bdesc0 = umma_smem_desc(ub, 8 * BK, Cfg::kLayout);
+              const uint32_t d_a = d_base + static_cast<uint32_t>(a * kF4BN);
 #pragma unroll
-                for (int kk = 0; kk < BK / 32; ++kk) {
-                  if (kExpSwitches && (g.exp & 2)) break;
-                  const uint64_t adesc = umma_smem_desc(ua + kk * 32, 8 * BK, Cfg::kLayout);
-                  const uint64_t bdesc = umma_smem_desc(ub + kk * 32, 8 * BK, Cfg::kLayout);
-                  umma_i8(d_base + static_cast<uint32_t>(a * kF4BN), adesc, bdesc, kIdesc,
-                          (kc > 0 || kk > 0) ? 1u : 0u);
-                }
+              for (int kk = 0; kk < BK / 32; ++kk) {
+                if (kExpSwitches && (g.exp & 2)) break;
+                if (elect_one())
+                  umma_i8(d_a, adesc0 + 2 * kk, bdesc0 + 2 * kk, kIdesc, (kc > 0 || kk > 0) ? 1u : 0u);
+                __syncwarp();
               }
-              umma_commit(&empty_bar[s]);
-              if (++s == stages) {
-                s = 0;
-                ph ^= 1u;
+              if (++kc == nk) {
+                kc = 0;
+                ++a;
               }
             }
-            umma_commit(&acc_full[buf]);
+            if (elect_one()) umma_commit(&empty_bar[s]);
+            __syncwarp();
+            if (++s == stages) {
+              s = 0;
+              ph ^= 1u;
+            }
           }
+          if (elect_one()) umma_commit(&acc_full[buf]);
+          __syncwarp();
         }
       }
-      __syncwarp();
     }
   } else {
     // ---------------- epilogue ----------------

@@ -249,18 +249,16 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
 
   if (warp >= kEpiWarps) {
     setmaxnreg_dec<kCtrlRegs>();
-    if (warp == kProducerWarp && lane < g.ld_lanes) {
+    if (warp == kProducerWarp) {
       // ---------------- TMA producer ----------------
-      // One bulk copy per operand per stage (U k chunks of one position).
-      // ld_lanes = 2: lane 0 copies A and lane 1 copies B, so the two copies
-      // of a stage are issued by different threads (a single thread sustains
-      // roughly one bulk copy per ~460 SM cycles, scratch/l2_ingress_bench.cu);
-      // lane 0 posts the stage's expected bytes before either copy.
-      const bool do_a = lane == 0, do_b = !b_res && lane == g.ld_lanes - 1;
-      if (b_res && lane == 0) {  // the single filter tile's B images, once
+      // One bulk copy per operand per stage (U k chunks of one position).  As
+      // for the MMA issuer, the whole warp runs the uniform loop and one
+      // elected lane posts the expected bytes and issues the copies.
+      if (b_res && elect_one()) {  // the single filter tile's B images, once
         mbar_arrive_expect_tx(b_full, 16 * nk * Cfg::kBBytes);
         bulk_load(b_base, codes_w, 16 * nk * Cfg::kBBytes, b_full);
       }
+      __syncwarp();
       int s = 0;
       uint32_t ph = 0;
       uint32_t lt = 0;
@@ -273,25 +271,31 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
         // Operand images of this tile (lance_kernels.cuh umma_image_offset).
         const uint8_t* a_tile = codes_a + static_cast<long long>(mt) * 16 * nk * Cfg::kABytes;
         const uint8_t* b_tile = codes_w + static_cast<long long>(ntile) * 16 * nk * Cfg::kBBytes;
-        if (!g.rs_warps && lane == 0) {  // row sums of the tile's 128 rows, all 16 positions (OOB rows read 0)
+        if (!g.rs_warps) {  // row sums of the tile's 128 rows, all 16 positions (OOB rows read 0)
           const uint32_t rb = lt & 1u;
           mbar_wait(&rs_empty[rb], ((lt >> 1) & 1u) ^ 1u);
-          mbar_arrive_expect_tx(&rs_ready[rb * 4], Cfg::kRsBytes);
-          tma_load_2d(s_rs + rb * 16 * kBM, &tmR, m0, 0, &rs_ready[rb * 4]);
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&rs_ready[rb * 4], Cfg::kRsBytes);
+            tma_load_2d(s_rs + rb * 16 * kBM, &tmR, m0, 0, &rs_ready[rb * 4]);
+          }
+          __syncwarp();
         }
         for (int j = j_lo; j < j_hi; ++j)
           for (int a = 0; a < 4; ++a) {
             const int u0 = image_plane(4 * a + j) * nk;
             for (int kc = 0; kc < nk; kc += U) {
               mbar_wait(&empty_bar[s], ph ^ 1u);
-              if (lane == 0) trace_event(g.trace, 0, tr_p++);
+              if (lane == 0) trace_event(g.trace, 0, tr_p);
+              ++tr_p;
               uint8_t* sa = stage_base + static_cast<size_t>(s) * stage_bytes;
-              if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
-              __syncwarp((1u << g.ld_lanes) - 1u);
-              if (do_a) bulk_load(sa, a_tile + (u0 + kc) * Cfg::kABytes, U * Cfg::kABytes, &full_bar[s]);
-              if (do_b)
-                bulk_load(sa + U * Cfg::kABytes, b_tile + (u0 + kc) * Cfg::kBBytes, U * Cfg::kBBytes,
-                          &full_bar[s]);
+              if (elect_one()) {
+                mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
+                bulk_load(sa, a_tile + (u0 + kc) * Cfg::kABytes, U * Cfg::kABytes, &full_bar[s]);
+                if (!b_res)
+                  bulk_load(sa + U * Cfg::kABytes, b_tile + (u0 + kc) * Cfg::kBBytes, U * Cfg::kBBytes,
+                            &full_bar[s]);
+              }
+              __syncwarp();
               if (++s == stages) {
                 s = 0;
                 ph ^= 1u;

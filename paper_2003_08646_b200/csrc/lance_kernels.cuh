@@ -67,7 +67,6 @@ struct GemmGeom {
   int b_resident;   // B operand resident in shared memory (set by the launcher)
   int rs_pitch;     // row-sum plane pitch (acc-dump builds write the GEMM's row sums)
   int rs_warps;     // 1: the GEMM sums the A rows itself; 0: K1's row sums via TMA
-  int ld_lanes;     // producer lanes: 1 (lane 0 copies A and B) or 2 (lane 0 A, lane 1 B)
   int units;        // k chunks per stage (0 = auto); the launcher settles it
   int exp;          // experiment switches (LANCE_GEMM_EXP, profiling only; 0 = normal)
   int pool;         // 1: fused 2x2 / stride-2 max-pool, y is [N][OH/2][OW/2][K]
