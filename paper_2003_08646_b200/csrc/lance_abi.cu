@@ -587,10 +587,6 @@ static int create_f4(lance_plan_s* p, const lance_conv_spec* spec, const lance_c
   g.units = 0;
   g.b_resident = 0;
   g.exp = lance_knob("LANCE_F4_EXP", 0);
-  {
-    const int v = lance_knob("LANCE_F4_LANES", 2);
-    g.ld_lanes = (v == 1 || v == 2 || v == 4) ? v : 2;
-  }
   // Warp strips along tile rows: whole rows unless that leaves too few warps
   // to fill the SMs; then shorter strips.
   g.seg_len = p->TW;

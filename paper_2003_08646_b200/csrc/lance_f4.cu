@@ -702,33 +702,34 @@ __global__ void __launch_bounds__(kF4Threads, 1)
 
   if (warp >= kF4EpiWarps) {
     setmaxnreg_dec<32>();
-    if (warp == kF4EpiWarps && lane < g.ld_lanes) {
+    if (warp == kF4EpiWarps) {
       // ---------------- bulk-copy producer ----------------
       // A stage is U consecutive (plane, k chunk) units of the tile's j-major
-      // operand images: one contiguous run, copied as ld_lanes slices (a single
-      // thread issues ~1 bulk copy per ~460 cycles from L2, whatever its size).
-      const int nl = g.ld_lanes;
-      const uint32_t a_part = a_bytes / nl, b_part = b_bytes / nl;
-      if (b_res && lane == 0) {  // the CTA's fixed filter tile (grid % nt == 0)
+      // operand images: one contiguous run per operand.  The whole warp runs
+      // the uniform loop; one elected lane posts the bytes and issues the
+      // copies.
+      if (b_res && elect_one()) {  // the CTA's fixed filter tile (grid % nt == 0)
         const uint32_t bb = kNP4 * nk * Cfg::kBBytes;
         mbar_arrive_expect_tx(b_full, bb);
         bulk_load(b_base, codes_w + static_cast<long long>(blockIdx.x % nt) * bb, bb, b_full);
       }
+      __syncwarp();
       int s = 0;
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         const int mt = t / nt, ntile = t - (t / nt) * nt;
-        const uint8_t* a_tile = codes_a + static_cast<long long>(mt) * kNP4 * nk * Cfg::kABytes + lane * a_part;
-        const uint8_t* b_tile = codes_w + static_cast<long long>(ntile) * kNP4 * nk * Cfg::kBBytes + lane * b_part;
+        const uint8_t* a_tile = codes_a + static_cast<long long>(mt) * kNP4 * nk * Cfg::kABytes;
+        const uint8_t* b_tile = codes_w + static_cast<long long>(ntile) * kNP4 * nk * Cfg::kBBytes;
         for (int u = 0; u < kNP4 * nk; u += U) {
           mbar_wait(&empty_bar[s], ph ^ 1u);
           uint8_t* sa = smem + static_cast<size_t>(s) * stage_bytes;
-          if (lane == 0) mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
-          __syncwarp((1u << nl) - 1u);
-          bulk_load(sa + lane * a_part, a_tile + static_cast<long long>(u) * Cfg::kABytes, a_part, &full_bar[s]);
-          if (!b_res)
-            bulk_load(sa + a_bytes + lane * b_part, b_tile + static_cast<long long>(u) * Cfg::kBBytes, b_part,
-                      &full_bar[s]);
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
+            bulk_load(sa, a_tile + static_cast<long long>(u) * Cfg::kABytes, a_bytes, &full_bar[s]);
+            if (!b_res)
+              bulk_load(sa + a_bytes, b_tile + static_cast<long long>(u) * Cfg::kBBytes, b_bytes, &full_bar[s]);
+          }
+          __syncwarp();
           if (++s == stages) {
             s = 0;
             ph ^= 1u;

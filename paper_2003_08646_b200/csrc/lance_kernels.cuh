@@ -124,7 +124,6 @@ struct F4Geom {
   int stages;        // GEMM ring depth (set by the launcher)
   int units;         // (position, k chunk) units per GEMM stage (divides 6 * nk; launcher)
   int b_resident;    // the CTA's filter tile stays in shared memory (launcher)
-  int ld_lanes;      // producer lanes splitting each stage's copies
   int exp;           // experiment switches (LANCE_F4_EXP, profiling only; 0 = normal)
   int seg_len, nseg; // F0 / F1 strips: tiles per warp strip, strips per tile row
   long long num_items;  // N * TH * nseg * ceil(C / 32) warp strips
