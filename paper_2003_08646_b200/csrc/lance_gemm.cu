@@ -18,14 +18,22 @@
 //
 // Persistent kernel, one CTA per SM, tiles = 128 Winograd tiles (UMMA M) x
 // BN filters, n-tile fastest so concurrent CTAs share the A rows in L2.
-//   warp 0       TMA producer (one lane): per stage the A box
-//                [128 rows x BK ch] and the B box [BN filters x BK ch] of one
-//                (position, channel chunk)
-//   warp 1       TMEM allocator + UMMA issuer (one lane)
-//   warps 2..17  epilogue: warp w drains TMEM lane quadrant w % 4 and
-//                filters BN/4 * ((w-2)/4) .. +BN/4 of the tile; each thread
+//   warps 0..15  epilogue: warp w drains TMEM lane quadrant w % 4 and
+//                filters BN/4 * (w / 4) .. +BN/4 of the tile; each thread
 //                owns one Winograd tile (row) and keeps the S partials of its
-//                filters in registers; y is written with 16-byte stores.
+//                filters in registers; y leaves through a swizzled shared
+//                staging buffer as whole 128-byte lines (or straight from
+//                registers when the layer runs without staging).
+//   warp 16      producer: per stage one bulk copy of U consecutive A images
+//                [128 rows x BK ch] (and B images [BN filters x BK ch] unless
+//                B is resident) of one position
+//   warp 17      TMEM allocator + UMMA issuer
+//   warps 18-19  row sums of the A stages (BK = 64 layers; else K1 writes them)
+// The producer and the UMMA issuer run warp-uniform loops (addresses and
+// descriptors in uniform registers) with one elect.sync lane issuing each
+// copy / tcgen05.mma / commit: these two threads' per-stage latency is serial
+// work, and the lane-0-only form cost up to 2x on the deep layers.
+// JS (small M): a tile's 4 j-groups run on 4 CTAs (see the kernel comment).
 // Exact int -> float epilogue without a conversion instruction (SMALL: every
 // accumulator dot < 2^24, i.e. C * top_a * top_b < 2^24).  The int32 bits of
 // dot read as an fp32 are the subnormal / first-binade float D = dot * 2^-149
