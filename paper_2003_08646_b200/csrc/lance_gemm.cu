@@ -727,8 +727,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
 #ifdef LANCE_GEMM_TRACE
         if (g.trace != nullptr && ew == 0 && lane == 0) g.trace[700000 + 4 * blockIdx.x + 1] = clock64();  // fold end
 #endif
-        continue;
-      }
+      } else {
       float2 S[4][FPT / 2];  // running S_ab partials, filter pairs
 #pragma unroll
       for (int j = 0; j < 4; ++j, ++grp) {
@@ -816,6 +815,7 @@ __global__ void __launch_bounds__(kGemmThreadsP, 1)
           store_col(1, S[1], S[3]);
         }
       }
+      }  // !JS
     }
   }
   __syncthreads();
