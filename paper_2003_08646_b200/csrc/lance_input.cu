@@ -31,6 +31,13 @@ namespace lance_dev {
 #define LANCE_K1_INTERIOR 1
 #endif
 constexpr bool K1_INTERIOR = LANCE_K1_INTERIOR != 0;
+// K1 fast path: position pairs per tie vote.  2 (four positions, eight values
+// per lane per __any_sync) measured 2.256 -> 2.190 ms on the step (K1 R64 121
+// -> 113 us, R128 85 -> 77 us); 4 is no better and 1 was the round-1 form.
+#ifndef LANCE_K1_KG
+#define LANCE_K1_KG 2
+#endif
+constexpr int K1_KG = LANCE_K1_KG;
 
 // Warp work item: (img, ti, tile segment, channel chunk).
 struct StripItem {
@@ -414,61 +421,75 @@ __device__ __forceinline__ void quant_fast_item(const float* __restrict__ x, uin
     const uint32_t lin = static_cast<uint32_t>((m & (kBM - 1)) * BK + cb);
     uint8_t* dst = cbase + (m >> 7) * blkstride + (lin ^ (((lin >> 7) & kMask) << 4));
     uint32_t mine = 0u;
+    // KG position pairs share one tie vote (KG = 2: 8 values per lane per vote).
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      float2 dd[2], gq[2], r[2];
+    for (int kg = 0; kg < 8; kg += K1_KG) {
+      float2 dd[2 * K1_KG], gq[2 * K1_KG], r[2 * K1_KG];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int p = 2 * k + h;
+      for (int h = 0; h < 2 * K1_KG; ++h) {
+        const int p = 2 * kg + h;
         const float rcp = s_rcp[p];
         dd[h] = sub2(v[p], bcast2(s_tmin[p]));
         gq[h] = fma2(dd[h], bcast2(rcp), bcast2(kMagic));
         r[h] = fma2(dd[h], bcast2(rcp), sub2(bcast2(kMagic), gq[h]));
       }
-      uint32_t pk0 = __byte_perm(__float_as_uint(gq[0].x), __float_as_uint(gq[0].y), 0x0040);
-      uint32_t pk1 = __byte_perm(__float_as_uint(gq[1].x), __float_as_uint(gq[1].y), 0x0040);
-      float rmax = fmax3_nan(fmax3_nan(fabsf(r[0].x), fabsf(r[0].y), fabsf(r[1].x)),
-                             fabsf(r[1].y), 0.0f);
+      uint32_t pk[2 * K1_KG];
+#pragma unroll
+      for (int h = 0; h < 2 * K1_KG; ++h)
+        pk[h] = __byte_perm(__float_as_uint(gq[h].x), __float_as_uint(gq[h].y), 0x0040);
+      float rmax = 0.0f;
+#pragma unroll
+      for (int h = 0; h < 2 * K1_KG; h += 2)
+        rmax = fmax3_nan(fmax3_nan(fabsf(r[h].x), fabsf(r[h].y), fabsf(r[h + 1].x)), fabsf(r[h + 1].y), rmax);
       if (STATIC) {
         // Caller params: a value whose rounded code falls outside [0, top]
         // (or whose product is too large for the magic-number rounding) joins
         // the exact path, which applies the reference's clamps.
-        const float glo = fmin3_nan(fmin3_nan(gq[0].x, gq[0].y, gq[1].x), gq[1].y, kMagic);
-        const float ghi = fmax3_nan(fmax3_nan(gq[0].x, gq[0].y, gq[1].x), gq[1].y, kMagic);
+        float glo = kMagic, ghi = kMagic;
+#pragma unroll
+        for (int h = 0; h < 2 * K1_KG; ++h) {
+          glo = fmin3_nan(glo, gq[h].x, gq[h].y);
+          ghi = fmax3_nan(ghi, gq[h].x, gq[h].y);
+        }
         if (!(glo >= kMagic) || !(ghi <= __fadd_rn(kMagic, top))) rmax = 1.0f;
       }
       if (__builtin_expect(__any_sync(0xffffffffu, !(rmax < kTieGuard)), 0)) {
         // Rare (~1e-4 per value): re-derive flagged codes exactly.
         if (!(rmax < kTieGuard)) {
-          uint32_t c[4];
-          const float dv[4] = {dd[0].x, dd[0].y, dd[1].x, dd[1].y};
-          const float gv[4] = {gq[0].x, gq[0].y, gq[1].x, gq[1].y};
-          const float rv[4] = {r[0].x, r[0].y, r[1].x, r[1].y};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float sc = s_scale[2 * k + (e >> 1)];
-            const float2 vv = v[2 * k + (e >> 1)];
-            if (STATIC)
-              c[e] = (fabsf(rv[e]) < kTieGuard && gv[e] >= kMagic && gv[e] <= __fadd_rn(kMagic, top))
-                         ? (__float_as_uint(gv[e]) & 0xFFu)
-                         : quantize_code((e & 1) ? vv.y : vv.x, s_tmin[2 * k + (e >> 1)], sc, top);
-            else
-              c[e] = (fabsf(rv[e]) < kTieGuard) ? (__float_as_uint(gv[e]) & 0xFFu)
-                                                : exact_code_near_boundary(dv[e], sc, gv[e], rv[e], top);
+          for (int h = 0; h < 2 * K1_KG; ++h) {
+            const int p = 2 * kg + h;
+            const float sc = s_scale[p];
+            uint32_t c[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const float dv = e ? dd[h].y : dd[h].x, gv = e ? gq[h].y : gq[h].x, rv = e ? r[h].y : r[h].x;
+              if (STATIC)
+                c[e] = (fabsf(rv) < kTieGuard && gv >= kMagic && gv <= __fadd_rn(kMagic, top))
+                           ? (__float_as_uint(gv) & 0xFFu)
+                           : quantize_code(e ? v[p].y : v[p].x, s_tmin[p], sc, top);
+              else
+                c[e] = (fabsf(rv) < kTieGuard) ? (__float_as_uint(gv) & 0xFFu)
+                                               : exact_code_near_boundary(dv, sc, gv, rv, top);
+            }
+            pk[h] = c[0] | (c[1] << 8);
           }
-          pk0 = c[0] | (c[1] << 8);
-          pk1 = c[2] | (c[3] << 8);
         }
       }
-      *reinterpret_cast<uint16_t*>(dst + image_plane(2 * k) * pstride) = static_cast<uint16_t>(pk0);
-      *reinterpret_cast<uint16_t*>(dst + image_plane(2 * k + 1) * pstride) = static_cast<uint16_t>(pk1);
+#pragma unroll
+      for (int h = 0; h < 2 * K1_KG; ++h)
+        *reinterpret_cast<uint16_t*>(dst + image_plane(2 * kg + h) * pstride) = static_cast<uint16_t>(pk[h]);
       // Row sums (lowpgemm.hpp:121-123): positions (2k, 2k+1) as 16-bit halves
       // (RS = false: the GEMM sums the A rows from its stages instead).
       if (!RS) continue;
-      const uint32_t a = (pk0 & 0xFFFFu) | (pk1 << 16);                  // [p.c0, p.c1, q.c0, q.c1]
-      const uint32_t w = (a & 0x00FF00FFu) + ((a >> 8) & 0x00FF00FFu);  // [p sum | q sum]
-      const uint32_t tot = __reduce_add_sync(0xffffffffu, w);
-      if ((lane >> 1) == k) mine = (lane & 1) ? (tot >> 16) : (tot & 0xFFFFu);
+#pragma unroll
+      for (int kk = 0; kk < K1_KG; ++kk) {
+        const int k = kg + kk;
+        const uint32_t a = (pk[2 * kk] & 0xFFFFu) | (pk[2 * kk + 1] << 16);  // [p.c0, p.c1, q.c0, q.c1]
+        const uint32_t w = (a & 0x00FF00FFu) + ((a >> 8) & 0x00FF00FFu);   // [p sum | q sum]
+        const uint32_t tot = __reduce_add_sync(0xffffffffu, w);
+        if ((lane >> 1) == k) mine = (lane & 1) ? (tot >> 16) : (tot & 0xFFFFu);
+      }
     }
     if (RS && lane < 16) {
       int32_t* rs = rowsum + static_cast<long long>(lane) * g.rs_pitch + m;
