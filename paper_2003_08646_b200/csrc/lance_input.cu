@@ -38,6 +38,25 @@ constexpr bool K1_INTERIOR = LANCE_K1_INTERIOR != 0;
 #define LANCE_K1_KG 2
 #endif
 constexpr int K1_KG = LANCE_K1_KG;
+// K1 fast path CTA shape: 4-warp CTAs, 5 per SM (registers capped at 96,
+// 20 warps per SM instead of 16).  Measured 2.180 -> 2.103 ms on the step,
+// K1 R64 113 -> 103 us; 6 per SM (80 registers) spills and is slower.
+#ifndef LANCE_K1_THREADS
+#define LANCE_K1_THREADS 128
+#endif
+#ifndef LANCE_K1_MINB
+#define LANCE_K1_MINB 5
+#endif
+constexpr int K1_THREADS = LANCE_K1_THREADS;
+// K0 ring kernel CTA shape (the ring is per warp: 10 KB of shared memory
+// each).  4-warp CTAs at 5 per SM (96 registers) measured slower than 8-warp
+// CTAs at 2 per SM: R64 79 vs 70 us, R512 32 vs 25 us.
+#ifndef LANCE_K0_THREADS
+#define LANCE_K0_THREADS 256
+#endif
+#ifndef LANCE_K0_MINB
+#define LANCE_K0_MINB 2
+#endif
 
 // Warp work item: (img, ti, tile segment, channel chunk).
 struct StripItem {
@@ -376,6 +395,112 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // and the code to [0, top]; far-out values then round to 0 / top exactly as the
 // reference's clamps do, and near-ties (|residual| >= 0.5 - 2^-14, which
 // includes the 0.5 and top + 0.5 boundaries) take the IEEE-division quantiser.
+// v (row pass, winograd.hpp:40-84 order) is formed per position from the four
+// column-pass results right where it is quantised, so at most one row of v is
+// live at a time (the fast path then fits 96 registers).
+__device__ __forceinline__ float2 row_pass_at(int p, const float2 (&t0)[4], const float2 (&t1)[4],
+                                              const float2 (&t2)[4], const float2 (&t3)[4]) {
+  const int a = p >> 2, b = p & 3;
+  return b == 0 ? sub2(t0[a], t2[a]) : b == 1 ? add2(t1[a], t2[a]) : b == 2 ? sub2(t2[a], t1[a]) : sub2(t1[a], t3[a]);
+}
+
+// Quantise one tile's 16 positions (this lane's channel pair), store the
+// codes into the UMMA images and (RS) the row sums of tile m.
+template <int BK, int NK, bool RS, bool STATIC>
+__device__ __forceinline__ void quant_fast_tile(const float2 (&t0)[4], const float2 (&t1)[4],
+                                                const float2 (&t2)[4], const float2 (&t3)[4],
+                                                int m, uint8_t* const cbase, int cb,
+                                                int32_t* __restrict__ rowsum, const InGeom& g, int lane,
+                                                const float* s_tmin, const float* s_scale,
+                                                const float* s_rcp, float top) {
+  constexpr int kImg = kBM * BK;                       // bytes of one image
+  constexpr uint32_t kMask = BK == 128 ? 7u : (BK == 64 ? 3u : 1u);
+  constexpr int pstride = NK * kImg;           // one position plane (compile-time: immediate offsets)
+  constexpr long long blkstride = 16LL * pstride;  // one 128-row block
+  const uint32_t lin = static_cast<uint32_t>((m & (kBM - 1)) * BK + cb);
+  uint8_t* dst = cbase + (m >> 7) * blkstride + (lin ^ (((lin >> 7) & kMask) << 4));
+  uint32_t mine = 0u;
+  // KG position pairs share one tie vote (KG = 2: 8 values per lane per vote).
+#pragma unroll
+  for (int kg = 0; kg < 8; kg += K1_KG) {
+    float2 v[2 * K1_KG], dd[2 * K1_KG], gq[2 * K1_KG], r[2 * K1_KG];
+#pragma unroll
+    for (int h = 0; h < 2 * K1_KG; ++h) {
+      const int p = 2 * kg + h;
+      const float rcp = s_rcp[p];
+      v[h] = row_pass_at(p, t0, t1, t2, t3);
+      dd[h] = sub2(v[h], bcast2(s_tmin[p]));
+      gq[h] = fma2(dd[h], bcast2(rcp), bcast2(kMagic));
+      r[h] = fma2(dd[h], bcast2(rcp), sub2(bcast2(kMagic), gq[h]));
+    }
+    uint32_t pk[2 * K1_KG];
+#pragma unroll
+    for (int h = 0; h < 2 * K1_KG; ++h)
+      pk[h] = __byte_perm(__float_as_uint(gq[h].x), __float_as_uint(gq[h].y), 0x0040);
+    float rmax = 0.0f;
+#pragma unroll
+    for (int h = 0; h < 2 * K1_KG; h += 2)
+      rmax = fmax3_nan(fmax3_nan(fabsf(r[h].x), fabsf(r[h].y), fabsf(r[h + 1].x)), fabsf(r[h + 1].y), rmax);
+    if (STATIC) {
+      // Caller params: a value whose rounded code falls outside [0, top]
+      // (or whose product is too large for the magic-number rounding) joins
+      // the exact path, which applies the reference's clamps.
+      float glo = kMagic, ghi = kMagic;
+#pragma unroll
+      for (int h = 0; h < 2 * K1_KG; ++h) {
+        glo = fmin3_nan(glo, gq[h].x, gq[h].y);
+        ghi = fmax3_nan(ghi, gq[h].x, gq[h].y);
+      }
+      if (!(glo >= kMagic) || !(ghi <= __fadd_rn(kMagic, top))) rmax = 1.0f;
+    }
+    if (__builtin_expect(__any_sync(0xffffffffu, !(rmax < kTieGuard)), 0)) {
+      // Rare (~1e-4 per value): re-derive flagged codes exactly.
+      if (!(rmax < kTieGuard)) {
+#pragma unroll
+        for (int h = 0; h < 2 * K1_KG; ++h) {
+          const int p = 2 * kg + h;
+          const float sc = s_scale[p];
+          uint32_t c[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const float dv = e ? dd[h].y : dd[h].x, gv = e ? gq[h].y : gq[h].x, rv = e ? r[h].y : r[h].x;
+            if (STATIC)
+              c[e] = (fabsf(rv) < kTieGuard && gv >= kMagic && gv <= __fadd_rn(kMagic, top))
+                         ? (__float_as_uint(gv) & 0xFFu)
+                         : quantize_code(e ? v[h].y : v[h].x, s_tmin[p], sc, top);
+            else
+              c[e] = (fabsf(rv) < kTieGuard) ? (__float_as_uint(gv) & 0xFFu)
+                                             : exact_code_near_boundary(dv, sc, gv, rv, top);
+          }
+          pk[h] = c[0] | (c[1] << 8);
+        }
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2 * K1_KG; ++h)
+      *reinterpret_cast<uint16_t*>(dst + image_plane(2 * kg + h) * pstride) = static_cast<uint16_t>(pk[h]);
+    // Row sums (lowpgemm.hpp:121-123): positions (2k, 2k+1) as 16-bit halves
+    // (RS = false: the GEMM sums the A rows from its stages instead).
+    if constexpr (RS) {
+#pragma unroll
+      for (int kk = 0; kk < K1_KG; ++kk) {
+        const int k = kg + kk;
+        const uint32_t a = (pk[2 * kk] & 0xFFFFu) | (pk[2 * kk + 1] << 16);  // [p.c0, p.c1, q.c0, q.c1]
+        const uint32_t w = (a & 0x00FF00FFu) + ((a >> 8) & 0x00FF00FFu);   // [p sum | q sum]
+        const uint32_t tot = __reduce_add_sync(0xffffffffu, w);
+        if ((lane >> 1) == k) mine = (lane & 1) ? (tot >> 16) : (tot & 0xFFFFu);
+      }
+    }
+  }
+  if (RS && lane < 16) {
+    int32_t* rs = rowsum + static_cast<long long>(lane) * g.rs_pitch + m;
+    if (g.nchunks == 1)
+      *rs = static_cast<int32_t>(mine);
+    else  // channel chunks of one tile run in different warps (rowsum pre-zeroed)
+      atomicAdd(rs, static_cast<int32_t>(mine));
+  }
+}
+
 // One K1 strip (item) of the fast path: v recomputed, quantised, codes +
 // row sums written.
 template <int BK, int NK, bool RS, bool STATIC>
@@ -386,11 +511,8 @@ __device__ __forceinline__ void quant_fast_item(const float* __restrict__ x, uin
   const StripItem it = strip_item(g, item, lane);
   const Strip<true> sp(x, g, it);
   const bool rows_in = sp.rows_ok();
-  constexpr int kImg = kBM * BK;                       // bytes of one image
-  constexpr uint32_t kMask = BK == 128 ? 7u : (BK == 64 ? 3u : 1u);
+  constexpr int kImg = kBM * BK;
   const int kc = it.ch / BK, cb = it.ch % BK;
-  constexpr int pstride = NK * kImg;           // one position plane (compile-time: immediate offsets)
-  constexpr long long blkstride = 16LL * pstride;  // one 128-row block
   uint8_t* const cbase = codes + static_cast<long long>(kc) * kImg;
   float2 ta[4], tb[4], tc[4], td[4], pc[4], pd[4];
   int xx = 2 * it.tj0 - g.pad;
@@ -400,7 +522,6 @@ __device__ __forceinline__ void quant_fast_item(const float* __restrict__ x, uin
   sp.load(xx + 3, pd);
   int m = (it.img * g.TH + it.ti) * g.TW + it.tj0;
   for (int tj = it.tj0; tj < it.tj1; ++tj, xx += 2, ++m) {
-    float2 v[16];
     colpass(pc, tc);
     colpass(pd, td);
     if (tj + 1 < it.tj1) {  // software prefetch of the next tile's two new columns
@@ -412,98 +533,18 @@ __device__ __forceinline__ void quant_fast_item(const float* __restrict__ x, uin
         sp.load(xx + 5, pd);
       }
     }
-    row_pass(ta, tb, tc, td, v);
+    quant_fast_tile<BK, NK, RS, STATIC>(ta, tb, tc, td, m, cbase, cb, rowsum, g, lane, s_tmin, s_scale, s_rcp, top);
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       ta[a] = tc[a];
       tb[a] = td[a];
-    }
-    const uint32_t lin = static_cast<uint32_t>((m & (kBM - 1)) * BK + cb);
-    uint8_t* dst = cbase + (m >> 7) * blkstride + (lin ^ (((lin >> 7) & kMask) << 4));
-    uint32_t mine = 0u;
-    // KG position pairs share one tie vote (KG = 2: 8 values per lane per vote).
-#pragma unroll
-    for (int kg = 0; kg < 8; kg += K1_KG) {
-      float2 dd[2 * K1_KG], gq[2 * K1_KG], r[2 * K1_KG];
-#pragma unroll
-      for (int h = 0; h < 2 * K1_KG; ++h) {
-        const int p = 2 * kg + h;
-        const float rcp = s_rcp[p];
-        dd[h] = sub2(v[p], bcast2(s_tmin[p]));
-        gq[h] = fma2(dd[h], bcast2(rcp), bcast2(kMagic));
-        r[h] = fma2(dd[h], bcast2(rcp), sub2(bcast2(kMagic), gq[h]));
-      }
-      uint32_t pk[2 * K1_KG];
-#pragma unroll
-      for (int h = 0; h < 2 * K1_KG; ++h)
-        pk[h] = __byte_perm(__float_as_uint(gq[h].x), __float_as_uint(gq[h].y), 0x0040);
-      float rmax = 0.0f;
-#pragma unroll
-      for (int h = 0; h < 2 * K1_KG; h += 2)
-        rmax = fmax3_nan(fmax3_nan(fabsf(r[h].x), fabsf(r[h].y), fabsf(r[h + 1].x)), fabsf(r[h + 1].y), rmax);
-      if (STATIC) {
-        // Caller params: a value whose rounded code falls outside [0, top]
-        // (or whose product is too large for the magic-number rounding) joins
-        // the exact path, which applies the reference's clamps.
-        float glo = kMagic, ghi = kMagic;
-#pragma unroll
-        for (int h = 0; h < 2 * K1_KG; ++h) {
-          glo = fmin3_nan(glo, gq[h].x, gq[h].y);
-          ghi = fmax3_nan(ghi, gq[h].x, gq[h].y);
-        }
-        if (!(glo >= kMagic) || !(ghi <= __fadd_rn(kMagic, top))) rmax = 1.0f;
-      }
-      if (__builtin_expect(__any_sync(0xffffffffu, !(rmax < kTieGuard)), 0)) {
-        // Rare (~1e-4 per value): re-derive flagged codes exactly.
-        if (!(rmax < kTieGuard)) {
-#pragma unroll
-          for (int h = 0; h < 2 * K1_KG; ++h) {
-            const int p = 2 * kg + h;
-            const float sc = s_scale[p];
-            uint32_t c[2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const float dv = e ? dd[h].y : dd[h].x, gv = e ? gq[h].y : gq[h].x, rv = e ? r[h].y : r[h].x;
-              if (STATIC)
-                c[e] = (fabsf(rv) < kTieGuard && gv >= kMagic && gv <= __fadd_rn(kMagic, top))
-                           ? (__float_as_uint(gv) & 0xFFu)
-                           : quantize_code(e ? v[p].y : v[p].x, s_tmin[p], sc, top);
-              else
-                c[e] = (fabsf(rv) < kTieGuard) ? (__float_as_uint(gv) & 0xFFu)
-                                               : exact_code_near_boundary(dv, sc, gv, rv, top);
-            }
-            pk[h] = c[0] | (c[1] << 8);
-          }
-        }
-      }
-#pragma unroll
-      for (int h = 0; h < 2 * K1_KG; ++h)
-        *reinterpret_cast<uint16_t*>(dst + image_plane(2 * kg + h) * pstride) = static_cast<uint16_t>(pk[h]);
-      // Row sums (lowpgemm.hpp:121-123): positions (2k, 2k+1) as 16-bit halves
-      // (RS = false: the GEMM sums the A rows from its stages instead).
-      if (!RS) continue;
-#pragma unroll
-      for (int kk = 0; kk < K1_KG; ++kk) {
-        const int k = kg + kk;
-        const uint32_t a = (pk[2 * kk] & 0xFFFFu) | (pk[2 * kk + 1] << 16);  // [p.c0, p.c1, q.c0, q.c1]
-        const uint32_t w = (a & 0x00FF00FFu) + ((a >> 8) & 0x00FF00FFu);   // [p sum | q sum]
-        const uint32_t tot = __reduce_add_sync(0xffffffffu, w);
-        if ((lane >> 1) == k) mine = (lane & 1) ? (tot >> 16) : (tot & 0xFFFFu);
-      }
-    }
-    if (RS && lane < 16) {
-      int32_t* rs = rowsum + static_cast<long long>(lane) * g.rs_pitch + m;
-      if (g.nchunks == 1)
-        *rs = static_cast<int32_t>(mine);
-      else  // channel chunks of one tile run in different warps (rowsum pre-zeroed)
-        atomicAdd(rs, static_cast<int32_t>(mine));
     }
   }
 }
 
 
 template <int BK, int NK, bool RS, bool STATIC = false>
-__global__ void __launch_bounds__(256, 2) input_quant_fast_kernel(const float* __restrict__ x,
+__global__ void __launch_bounds__(LANCE_K1_THREADS, LANCE_K1_MINB) input_quant_fast_kernel(const float* __restrict__ x,
                                                                   uint8_t* __restrict__ codes,
                                                                   int32_t* __restrict__ rowsum,
                                                                   const LanceDevState* __restrict__ st,
@@ -556,7 +597,7 @@ __global__ void static_params_kernel(LanceDevState* st, StaticParams prm, int C)
 // copied itself, so per-thread cp.async groups are the only ordering needed.
 // Transform and range arithmetic as input_range_kernel.
 // The K0 strip loop (ring below) over this block's grid-stride items, folding
-// every v into lo / hi.  s_ring: [8 warps][D + 1 slots][8][32] float2.
+// every v into lo / hi.  s_ring: [warps][D + 1 slots][8][32] float2.
 template <int D, int CC>
 __device__ __forceinline__ void range_ring_phase(const float* __restrict__ x, const InGeom& g,
                                                  float (&lo)[16], float (&hi)[16], float2* s_ring) {
@@ -657,13 +698,13 @@ __device__ __forceinline__ void range_ring_phase(const float* __restrict__ x, co
 }
 
 template <int D, int CC>
-__global__ void __launch_bounds__(256, 2) input_range_ring_kernel(const float* __restrict__ x,
+__global__ void __launch_bounds__(LANCE_K0_THREADS, LANCE_K0_MINB) input_range_ring_kernel(const float* __restrict__ x,
                                                                   float* __restrict__ partials,
                                                                   LanceDevState* __restrict__ st,
                                                                   InGeom g) {
   pdl_entry();
-  extern __shared__ float2 s_ring[];  // [8 warps][R slots][2 columns x 4 rows][32 lanes]
-  __shared__ float s_red[256];
+  extern __shared__ float2 s_ring[];  // [warps][R slots][2 columns x 4 rows][32 lanes]
+  __shared__ float s_red[LANCE_K0_THREADS];
   float lo[16], hi[16];
 #pragma unroll
   for (int p = 0; p < 16; ++p) {
@@ -865,6 +906,12 @@ __global__ void __launch_bounds__(256) input_quant_smallc_kernel(const float* __
 
 // --------------------------------------------------------------------------
 int input_range_grid(const InGeom& g, int sm_count) {
+  if (g.C >= 32 && g.C % 64 == 0) {  // ring kernel: K0_MINB resident K0_THREADS-thread blocks per SM
+    constexpr int wpb = LANCE_K0_THREADS / 32;
+    const long long blocks = (g.num_items + wpb - 1) / wpb;
+    const long long cap = static_cast<long long>(LANCE_K0_MINB) * sm_count;
+    return static_cast<int>(blocks < cap ? blocks : cap);
+  }
   const long long blocks = (g.num_items + 7) / 8;
   const long long cap = 2LL * sm_count;  // 2 resident 256-thread blocks per SM
   return static_cast<int>(blocks < cap ? blocks : cap);
@@ -878,13 +925,13 @@ cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceD
   if (g.C < 32) {
     LANCE_LAUNCH_CHECK(launch_k(input_range_smallc_kernel, grid, 256, 0, s, x, partials, st, g));
   } else if (g.C % 64 == 0) {
-    const size_t smem = static_cast<size_t>(8) * (kDepth + 1) * 8 * 32 * sizeof(float2);
+    const size_t smem = static_cast<size_t>(LANCE_K0_THREADS / 32) * (kDepth + 1) * 8 * 32 * sizeof(float2);
 #define LANCE_K0_RING(CCV)                                                                        \
     if (CCV == 0 || g.C == CCV) {                                                                \
       const cudaError_t attr =                                                                   \
           ensure_smem_attr(reinterpret_cast<const void*>(input_range_ring_kernel<kDepth, CCV>), smem); \
       if (attr != cudaSuccess) return attr;                                                      \
-      LANCE_LAUNCH_CHECK(launch_k(input_range_ring_kernel<kDepth, CCV>, grid, 256, smem, s, x, partials, st, g));          \
+      LANCE_LAUNCH_CHECK(launch_k(input_range_ring_kernel<kDepth, CCV>, grid, LANCE_K0_THREADS, smem, s, x, partials, st, g));          \
       return cudaGetLastError();                                                                 \
     }
     LANCE_K0_RING(64)
@@ -919,16 +966,17 @@ cudaError_t launch_input_quant(const float* x, uint8_t* codes, int32_t* rowsum,
     return cudaGetLastError();
   }
   if (g.C % 64 == 0) {  // fast path: every lane owns two real channels
-#define LANCE_K1_FAST(BKV, NKV)                                                          \
+    const unsigned grid = static_cast<unsigned>((g.num_items + K1_THREADS / 32 - 1) / (K1_THREADS / 32));
+#define LANCE_K1_FAST(BKV, NKV)                                                             \
   if (g.a_bk == BKV && g.a_nk == NKV) {                                                  \
     if (static_mode && g.rowsums)                                                        \
-      LANCE_LAUNCH_CHECK(launch_k(input_quant_fast_kernel<BKV, NKV, true, true>, grid, 256, 0, s, x, codes, rowsum, st, g)); \
+      LANCE_LAUNCH_CHECK(launch_k(input_quant_fast_kernel<BKV, NKV, true, true>, grid, K1_THREADS, 0, s, x, codes, rowsum, st, g)); \
     else if (static_mode)                                                                \
-      LANCE_LAUNCH_CHECK(launch_k(input_quant_fast_kernel<BKV, NKV, false, true>, grid, 256, 0, s, x, codes, rowsum, st, g)); \
+      LANCE_LAUNCH_CHECK(launch_k(input_quant_fast_kernel<BKV, NKV, false, true>, grid, K1_THREADS, 0, s, x, codes, rowsum, st, g)); \
     else if (g.rowsums)                                                                  \
-      LANCE_LAUNCH_CHECK(launch_k(input_quant_fast_kernel<BKV, NKV, true>, grid, 256, 0, s, x, codes, rowsum, st, g)); \
+      LANCE_LAUNCH_CHECK(launch_k(input_quant_fast_kernel<BKV, NKV, true>, grid, K1_THREADS, 0, s, x, codes, rowsum, st, g)); \
     else                                                                                 \
-      LANCE_LAUNCH_CHECK(launch_k(input_quant_fast_kernel<BKV, NKV, false>, grid, 256, 0, s, x, codes, rowsum, st, g)); \
+      LANCE_LAUNCH_CHECK(launch_k(input_quant_fast_kernel<BKV, NKV, false>, grid, K1_THREADS, 0, s, x, codes, rowsum, st, g)); \
     return cudaGetLastError();                                                           \
   }
     LANCE_K1_FAST(64, 1)
