@@ -412,14 +412,14 @@ __device__ __forceinline__ void quant_fast_tile(const float2 (&t0)[4], const flo
                                                 int m, uint8_t* const cbase, int cb,
                                                 int32_t* __restrict__ rowsum, const InGeom& g, int lane,
                                                 const float* s_tmin, const float* s_scale,
-                                                const float* s_rcp, float top) {
+                                                const float* s_rcp, float top, uint32_t* s_rsw) {
   constexpr int kImg = kBM * BK;                       // bytes of one image
   constexpr uint32_t kMask = BK == 128 ? 7u : (BK == 64 ? 3u : 1u);
   constexpr int pstride = NK * kImg;           // one position plane (compile-time: immediate offsets)
   constexpr long long blkstride = 16LL * pstride;  // one 128-row block
   const uint32_t lin = static_cast<uint32_t>((m & (kBM - 1)) * BK + cb);
   uint8_t* dst = cbase + (m >> 7) * blkstride + (lin ^ (((lin >> 7) & kMask) << 4));
-  uint32_t mine = 0u;
+  uint32_t tot[8];  // RS: warp sums of positions (2k, 2k + 1) as 16-bit halves (warp-uniform)
   // KG position pairs share one tie vote (KG = 2: 8 values per lane per vote).
 #pragma unroll
   for (int kg = 0; kg < 8; kg += K1_KG) {
@@ -484,20 +484,27 @@ __device__ __forceinline__ void quant_fast_tile(const float2 (&t0)[4], const flo
     if constexpr (RS) {
 #pragma unroll
       for (int kk = 0; kk < K1_KG; ++kk) {
-        const int k = kg + kk;
-        const uint32_t a = (pk[2 * kk] & 0xFFFFu) | (pk[2 * kk + 1] << 16);  // [p.c0, p.c1, q.c0, q.c1]
-        const uint32_t w = (a & 0x00FF00FFu) + ((a >> 8) & 0x00FF00FFu);   // [p sum | q sum]
-        const uint32_t tot = __reduce_add_sync(0xffffffffu, w);
-        if ((lane >> 1) == k) mine = (lane & 1) ? (tot >> 16) : (tot & 0xFFFFu);
+        const uint32_t a = __byte_perm(pk[2 * kk], pk[2 * kk + 1], 0x5410);  // [p.c0, p.c1, q.c0, q.c1]
+        const uint32_t hi = __byte_perm(a, 0u, 0x4341);                      // [p.c1, 0, q.c1, 0]
+        tot[kg + kk] = __reduce_add_sync(0xffffffffu, a - 255u * hi);       // [p sum | q sum]
       }
     }
   }
-  if (RS && lane < 16) {
-    int32_t* rs = rowsum + static_cast<long long>(lane) * g.rs_pitch + m;
-    if (g.nchunks == 1)
-      *rs = static_cast<int32_t>(mine);
-    else  // channel chunks of one tile run in different warps (rowsum pre-zeroed)
-      atomicAdd(rs, static_cast<int32_t>(mine));
+  if constexpr (RS) {
+    // Lane l < 16 takes position l's sum: the 16-bit half l of the eight
+    // warp-uniform totals, through 32 bytes of per-warp shared scratch.
+    reinterpret_cast<uint4*>(s_rsw)[0] = make_uint4(tot[0], tot[1], tot[2], tot[3]);
+    reinterpret_cast<uint4*>(s_rsw)[1] = make_uint4(tot[4], tot[5], tot[6], tot[7]);
+    __syncwarp();
+    if (lane < 16) {
+      const uint32_t mine = reinterpret_cast<const uint16_t*>(s_rsw)[lane];
+      int32_t* rs = rowsum + static_cast<long long>(lane) * g.rs_pitch + m;
+      if (g.nchunks == 1)
+        *rs = static_cast<int32_t>(mine);
+      else  // channel chunks of one tile run in different warps (rowsum pre-zeroed)
+        atomicAdd(rs, static_cast<int32_t>(mine));
+    }
+    __syncwarp();
   }
 }
 
@@ -507,7 +514,8 @@ template <int BK, int NK, bool RS, bool STATIC>
 __device__ __forceinline__ void quant_fast_item(const float* __restrict__ x, uint8_t* __restrict__ codes,
                                                 int32_t* __restrict__ rowsum, const InGeom& g,
                                                 long long item, int lane, const float* s_tmin,
-                                                const float* s_scale, const float* s_rcp, float top) {
+                                                const float* s_scale, const float* s_rcp, float top,
+                                                uint32_t* s_rsw) {
   const StripItem it = strip_item(g, item, lane);
   const Strip<true> sp(x, g, it);
   const bool rows_in = sp.rows_ok();
@@ -533,7 +541,8 @@ __device__ __forceinline__ void quant_fast_item(const float* __restrict__ x, uin
         sp.load(xx + 5, pd);
       }
     }
-    quant_fast_tile<BK, NK, RS, STATIC>(ta, tb, tc, td, m, cbase, cb, rowsum, g, lane, s_tmin, s_scale, s_rcp, top);
+    quant_fast_tile<BK, NK, RS, STATIC>(ta, tb, tc, td, m, cbase, cb, rowsum, g, lane, s_tmin, s_scale, s_rcp, top,
+                                        s_rsw);
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       ta[a] = tc[a];
@@ -551,6 +560,7 @@ __global__ void __launch_bounds__(LANCE_K1_THREADS, LANCE_K1_MINB) input_quant_f
                                                                   InGeom g) {
   pdl_entry();
   __shared__ float s_tmin[16], s_scale[16], s_rcp[16];
+  __shared__ __align__(16) uint32_t s_rsw[K1_THREADS / 32][8];  // RS: per-warp row-sum scratch
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid < 16) {
     s_tmin[tid] = st->a_tmin[tid];
@@ -565,7 +575,8 @@ __global__ void __launch_bounds__(LANCE_K1_THREADS, LANCE_K1_MINB) input_quant_f
   const long long wi = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + (tid >> 5);
   if (wi >= g.num_items) return;
   const long long item = g.rev_items ? g.num_items - 1 - wi : wi;
-  quant_fast_item<BK, NK, RS, STATIC>(x, codes, rowsum, g, item, lane, s_tmin, s_scale, s_rcp, top);
+  quant_fast_item<BK, NK, RS, STATIC>(x, codes, rowsum, g, item, lane, s_tmin, s_scale, s_rcp, top,
+                                      s_rsw[tid >> 5]);
 }
 
 // Static-params mode: caller-supplied input QuantParams[16].
