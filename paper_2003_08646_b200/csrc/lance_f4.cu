@@ -413,8 +413,16 @@ __global__ void __launch_bounds__(256, 2) f4_range_kernel(const float* __restric
 // offsets are immediates; NK = 0: runtime geometry (any shape).  The tie
 // check is one branch per row pair (12 codes), the rare fix-up recomputes
 // that row's flagged codes exactly before they are stored.
+// F1 CTA shape.  4-warp CTAs at 5 per SM (registers capped at 96, as the
+// F(2x2) K1 runs) measured slower here: the F(4x4) tile state spills.
+#ifndef LANCE_F4Q_THREADS
+#define LANCE_F4Q_THREADS 256
+#endif
+#ifndef LANCE_F4Q_MINB
+#define LANCE_F4Q_MINB 2
+#endif
 template <bool STATIC, int BK, int NK, int D = 0>
-__global__ void __launch_bounds__(256, 2) f4_quant_kernel(const float* __restrict__ x,
+__global__ void __launch_bounds__(LANCE_F4Q_THREADS, LANCE_F4Q_MINB) f4_quant_kernel(const float* __restrict__ x,
                                                           uint8_t* __restrict__ codes,
                                                           int32_t* __restrict__ rowsum,
                                                           const LanceDevState* __restrict__ st,
@@ -434,10 +442,11 @@ __global__ void __launch_bounds__(256, 2) f4_quant_kernel(const float* __restric
   const int bk = NK > 0 ? BK : g.bk;
   const int img_bytes = kBM * bk;                              // one UMMA image
   const int pstride = (NK > 0 ? NK : g.nk) * img_bytes;        // one position plane
-  extern __shared__ float f4qring_all[];  // D > 0: [8 warps][D][24][32]
+  extern __shared__ float f4qring_all[];  // D > 0: [warps][D][24][32]
   float* f4ring = f4qring_all + static_cast<size_t>(warp) * (D > 0 ? D : 1) * 24 * 32;
-  for (long long item = static_cast<long long>(blockIdx.x) * 8 + warp; item < g.num_items;
-       item += static_cast<long long>(gridDim.x) * 8) {
+  constexpr int kWarps = LANCE_F4Q_THREADS / 32;
+  for (long long item = static_cast<long long>(blockIdx.x) * kWarps + warp; item < g.num_items;
+       item += static_cast<long long>(gridDim.x) * kWarps) {
     const F4Strip sp = f4_strip(g, item, lane);
     const float* rowbase = x + (static_cast<long long>(sp.img) * g.H + (4 * sp.ti - g.pad)) * rowstride + sp.c;
     const int kc = sp.c / bk, cb = sp.c - kc * bk;
@@ -1046,12 +1055,14 @@ cudaError_t launch_f4_range(const float* x, float* partials, int grid, LanceDevS
 cudaError_t launch_f4_quant(const float* x, uint8_t* codes, int32_t* rowsum,
                             const LanceDevState* st, const F4Geom& g, int static_mode,
                             int sm_count, cudaStream_t s) {
-  const long long blocks = (g.num_items + 7) / 8;
-  const int grid = static_cast<int>(blocks < 4LL * sm_count ? blocks : 4LL * sm_count);
+  constexpr int kWarps = LANCE_F4Q_THREADS / 32;
+  const long long blocks = (g.num_items + kWarps - 1) / kWarps;
+  const long long cap = (32LL / kWarps) * sm_count;  // grid-stride over 32 warps' worth per SM
+  const int grid = static_cast<int>(blocks < cap ? blocks : cap);
   cudaError_t e = cudaMemsetAsync(rowsum, 0, sizeof(int32_t) * kNP4 * static_cast<size_t>(g.rs_pitch), s);
   if (e != cudaSuccess) return e;
   const int qd = f4_quant_depth();
-  const size_t qsmem = static_cast<size_t>(8) * 2 * 24 * 32 * sizeof(float);
+  const size_t qsmem = static_cast<size_t>(kWarps) * 2 * 24 * 32 * sizeof(float);
 #define LANCE_F4Q(BKV, NKV)                                                                   \
   if ((NKV == 0) || (g.bk == BKV && g.nk == NKV)) {                                           \
     if (qd == 2) {                                                                            \
@@ -1060,13 +1071,13 @@ cudaError_t launch_f4_quant(const float* x, uint8_t* codes, int32_t* rowsum,
           : ensure_smem_attr(reinterpret_cast<const void*>(f4_quant_kernel<false, BKV, NKV, 2>), qsmem); \
       if (ea != cudaSuccess) return ea;                                                       \
       if (static_mode)                                                                        \
-        LANCE_LAUNCH_CHECK(launch_k(f4_quant_kernel<true, BKV, NKV, 2>, grid, 256, qsmem, s, x, codes, rowsum, st, g)); \
+        LANCE_LAUNCH_CHECK(launch_k(f4_quant_kernel<true, BKV, NKV, 2>, grid, LANCE_F4Q_THREADS, qsmem, s, x, codes, rowsum, st, g)); \
       else                                                                                    \
-        LANCE_LAUNCH_CHECK(launch_k(f4_quant_kernel<false, BKV, NKV, 2>, grid, 256, qsmem, s, x, codes, rowsum, st, g)); \
+        LANCE_LAUNCH_CHECK(launch_k(f4_quant_kernel<false, BKV, NKV, 2>, grid, LANCE_F4Q_THREADS, qsmem, s, x, codes, rowsum, st, g)); \
     } else if (static_mode) {                                                                 \
-      LANCE_LAUNCH_CHECK(launch_k(f4_quant_kernel<true, BKV, NKV>, grid, 256, 0, s, x, codes, rowsum, st, g));          \
+      LANCE_LAUNCH_CHECK(launch_k(f4_quant_kernel<true, BKV, NKV>, grid, LANCE_F4Q_THREADS, 0, s, x, codes, rowsum, st, g));          \
     } else {                                                                                  \
-      LANCE_LAUNCH_CHECK(launch_k(f4_quant_kernel<false, BKV, NKV>, grid, 256, 0, s, x, codes, rowsum, st, g));         \
+      LANCE_LAUNCH_CHECK(launch_k(f4_quant_kernel<false, BKV, NKV>, grid, LANCE_F4Q_THREADS, 0, s, x, codes, rowsum, st, g));         \
     }                                                                                         \
     return cudaGetLastError();                                                                \
   }
