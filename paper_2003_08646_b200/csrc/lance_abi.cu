@@ -493,6 +493,12 @@ int lance_plan_create_tiled(const lance_conv_spec* spec, const lance_config* cfg
     delete p;
     return rc;
   }
+  // K1's atomically accumulated row sums (several channel chunks per tile)
+  // are cleared by K0 of the same forward.
+  if (p->in_geom.nchunks > 1 && p->in_geom.rowsums) {
+    p->in_geom.rs_zero = p->rowsum;
+    p->in_geom.rs_zero_words = 16LL * p->rs_pitch;
+  }
   // Channel / filter padding stays zero forever: both GEMM operands are padded
   // with code 0, which adds nothing to the accumulators.
   cudaError_t e = cudaMemset(p->codes_a, 0, codes_a_bytes);
@@ -739,7 +745,9 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
   }
   ++launches;
   if (ev) LANCE_CUDA(cudaEventRecord(ev[1], s));
-  if (p->in_geom.nchunks > 1 && p->in_geom.rowsums)
+  // K1 accumulates the row sums of multi-chunk layers atomically: K0 cleared
+  // them above; the static / device-range modes run no K0, so clear here.
+  if (p->in_geom.nchunks > 1 && p->in_geom.rowsums && (static_params || minmax_dev))
     LANCE_CUDA(cudaMemsetAsync(p->rowsum, 0, sizeof(int32_t) * 16 * p->rs_pitch, s));
   LANCE_CUDA(launch_input_quant(x_dev, p->codes_a, p->rowsum, p->state, p->in_geom, p->vec2,
                                 static_params != nullptr, s));

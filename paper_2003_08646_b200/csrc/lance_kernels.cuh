@@ -49,6 +49,8 @@ struct InGeom {
   int nseg;
   long long num_items;  // N * TH * nseg * nchunks warp items
   int granularity;  // 1 = PerPosition, 2 = PerTensor
+  int32_t* rs_zero;       // K0 zeroes these words for K1's atomic row sums (nullptr: nothing)
+  long long rs_zero_words;
 };
 
 struct FilterGeom {
