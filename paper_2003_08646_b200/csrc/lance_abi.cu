@@ -617,6 +617,8 @@ static int create_f4(lance_plan_s* p, const lance_conv_spec* spec, const lance_c
       (rc = dev_alloc(p, &p->partials, sizeof(float) * 72 * part_rows)) ||
       (rc = dev_alloc(p, &p->state, sizeof(LanceDevState))))
     return rc;
+  p->f4.rs_zero = p->rowsum;  // cleared by F0 of each forward that runs it
+  p->f4.rs_zero_words = 36LL * p->rs_pitch;
   cudaError_t e = cudaMemset(p->codes_a, 0, codes_a_bytes);
   if (e == cudaSuccess) e = cudaMemset(p->codes_w, 0, codes_w_bytes);
   if (e == cudaSuccess) e = cudaMemset(p->colsum, 0, sizeof(int32_t) * 36 * p->K_pad);
@@ -718,7 +720,7 @@ static int run_forward(lance_plan_t p, const float* x_dev, float* y_dev, cudaStr
     }
     if (ev) LANCE_CUDA(cudaEventRecord(ev[1], s));
     LANCE_CUDA(launch_f4_quant(x_dev, p->codes_a, p->rowsum, p->state, p->f4, static_params != nullptr,
-                               p->sm_count, s));
+                               /*clear_rowsum=*/(static_params || minmax_dev) ? 1 : 0, p->sm_count, s));
     if (ev) LANCE_CUDA(cudaEventRecord(ev[2], s));
     LANCE_CUDA(launch_f4_gemm(p->codes_a, p->codes_w, p->rowsum, p->colsum, p->small_acc, p->state, y_dev,
                               p->acc_dump, p->bias, p->relu, p->f4, s));

@@ -197,6 +197,18 @@ __device__ __forceinline__ void block_minmax_to_partials(float (&lo)[16], float 
   }
 }
 
+// Zero `words` int32 from every thread of the grid (16-byte stores, scalar
+// tail); nullptr: nothing.  The range kernels clear the row-sum planes that
+// the quantisers then accumulate atomically.
+__device__ __forceinline__ void grid_zero_i32(int32_t* z, long long words) {
+  if (z == nullptr) return;
+  const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long nth = static_cast<long long>(gridDim.x) * blockDim.x;
+  const long long n4 = words >> 2;
+  for (long long i = tid; i < n4; i += nth) reinterpret_cast<int4*>(z)[i] = make_int4(0, 0, 0, 0);
+  for (long long i = 4 * n4 + tid; i < words; i += nth) z[i] = 0;
+}
+
 // Fold the 32-float partials of nb blocks -> s_red[0..31] (whole block).
 __device__ __forceinline__ void fold_partials(const float* partials, int nb, float* s_red) {
   const int warp = threadIdx.x >> 5;

@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(256, 2) f4_range_kernel(const float* __restric
                                                           LanceDevState* __restrict__ st,
                                                           F4Geom g) {
   pdl_entry();
+  grid_zero_i32(g.rs_zero, g.rs_zero_words);  // F1's atomic row sums
   __shared__ float s_red[8 * 72];
   __shared__ float s_fin[72];
   float lo[kNP4], hi[kNP4];
@@ -1054,13 +1055,15 @@ cudaError_t launch_f4_range(const float* x, float* partials, int grid, LanceDevS
 
 cudaError_t launch_f4_quant(const float* x, uint8_t* codes, int32_t* rowsum,
                             const LanceDevState* st, const F4Geom& g, int static_mode,
-                            int sm_count, cudaStream_t s) {
+                            int clear_rowsum, int sm_count, cudaStream_t s) {
   constexpr int kWarps = LANCE_F4Q_THREADS / 32;
   const long long blocks = (g.num_items + kWarps - 1) / kWarps;
   const long long cap = (32LL / kWarps) * sm_count;  // grid-stride over 32 warps' worth per SM
   const int grid = static_cast<int>(blocks < cap ? blocks : cap);
-  cudaError_t e = cudaMemsetAsync(rowsum, 0, sizeof(int32_t) * kNP4 * static_cast<size_t>(g.rs_pitch), s);
-  if (e != cudaSuccess) return e;
+  if (clear_rowsum) {  // else F0 of this forward cleared them
+    const cudaError_t e = cudaMemsetAsync(rowsum, 0, sizeof(int32_t) * kNP4 * static_cast<size_t>(g.rs_pitch), s);
+    if (e != cudaSuccess) return e;
+  }
   const int qd = f4_quant_depth();
   const size_t qsmem = static_cast<size_t>(kWarps) * 2 * 24 * 32 * sizeof(float);
 #define LANCE_F4Q(BKV, NKV)                                                                   \

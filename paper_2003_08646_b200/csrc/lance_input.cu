@@ -155,24 +155,13 @@ __device__ __forceinline__ void row_pass(const float2 (&t0)[4], const float2 (&t
 
 // --------------------------------------------------------------------------
 // K0: per-position range of v over the whole batch (grid-stride over strips).
-// K0 clears the row-sum planes that K1 accumulates atomically (channel chunks
-// of one tile in different warps), instead of a separate memset in the stream.
-__device__ __forceinline__ void k0_zero_rowsums(const InGeom& g) {
-  if (g.rs_zero == nullptr) return;
-  int4* z = reinterpret_cast<int4*>(g.rs_zero);
-  const long long n4 = g.rs_zero_words >> 2;
-  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
-       i += static_cast<long long>(gridDim.x) * blockDim.x)
-    z[i] = make_int4(0, 0, 0, 0);
-}
-
 template <bool VEC2>
 __global__ void __launch_bounds__(256, 2) input_range_kernel(const float* __restrict__ x,
                                                              float* __restrict__ partials,
                                                              LanceDevState* __restrict__ st,
                                                              InGeom g) {
   pdl_entry();
-  k0_zero_rowsums(g);
+  grid_zero_i32(g.rs_zero, g.rs_zero_words);  // K1's atomic row sums (multi-chunk layers)
   __shared__ float s_red[256];
   float lo[16], hi[16];
 #pragma unroll
@@ -726,7 +715,7 @@ __global__ void __launch_bounds__(LANCE_K0_THREADS, LANCE_K0_MINB) input_range_r
                                                                   LanceDevState* __restrict__ st,
                                                                   InGeom g) {
   pdl_entry();
-  k0_zero_rowsums(g);
+  grid_zero_i32(g.rs_zero, g.rs_zero_words);  // K1's atomic row sums (multi-chunk layers)
   extern __shared__ float2 s_ring[];  // [warps][R slots][2 columns x 4 rows][32 lanes]
   __shared__ float s_red[LANCE_K0_THREADS];
   float lo[16], hi[16];
@@ -860,7 +849,7 @@ __global__ void __launch_bounds__(256) input_range_smallc_kernel(const float* __
                                                                  LanceDevState* __restrict__ st,
                                                                  InGeom g) {
   pdl_entry();
-  k0_zero_rowsums(g);
+  grid_zero_i32(g.rs_zero, g.rs_zero_words);  // K1's atomic row sums (multi-chunk layers)
   __shared__ float s_red[256];
   float lo[16], hi[16];
 #pragma unroll

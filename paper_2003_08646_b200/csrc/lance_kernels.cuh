@@ -129,6 +129,8 @@ struct F4Geom {
   int exp;           // experiment switches (LANCE_F4_EXP, profiling only; 0 = normal)
   int seg_len, nseg; // F0 / F1 strips: tiles per warp strip, strips per tile row
   long long num_items;  // N * TH * nseg * ceil(C / 32) warp strips
+  int32_t* rs_zero;     // F0 zeroes the row sums F1 accumulates (nullptr: F1's launcher does)
+  long long rs_zero_words;
 };
 
 // F(4x4) operand planes are j-major: position p = 6a + j is plane 6j + a, so
@@ -229,7 +231,7 @@ cudaError_t launch_f4_range(const float* x, float* partials, int grid, LanceDevS
                             const F4Geom& g, cudaStream_t s);
 cudaError_t launch_f4_quant(const float* x, uint8_t* codes, int32_t* rowsum,
                             const LanceDevState* st, const F4Geom& g, int static_mode,
-                            int sm_count, cudaStream_t s);
+                            int clear_rowsum, int sm_count, cudaStream_t s);
 cudaError_t launch_f4_filter_prepare(const float* w, float* u_tmp, float* partials, int grid,
                                      uint8_t* codes_w, int32_t* colsum, LanceDevState* st,
                                      const F4Geom& g, cudaStream_t s);
