@@ -415,12 +415,17 @@ int lance_plan_create_tiled(const lance_conv_spec* spec, const lance_config* cfg
   g.a_bk = p->BK;
   g.a_nk = p->C_pad / p->BK;
   // Warp strips: whole tile rows unless that leaves too few warps to fill
-  // 148 SMs x 32 warps; then halve the strip length.
+  // 148 SMs x 32 warps; then halve the strip length.  Long strips are also
+  // halved down to 64 items per SM as long as they stay >= 7 tiles: K1 runs
+  // one strip per warp in ~2.4 waves at 32 items per SM and ~4.8 at 64, so
+  // its last partial wave shrinks (R64 K1 102.6 -> 99 us); shorter strips
+  // than that cost more per-strip setup than they save (R256 / R512).
   g.seg_len = p->TW;
   for (;;) {
     g.nseg = (p->TW + g.seg_len - 1) / g.seg_len;
     g.num_items = static_cast<long long>(spec->n) * p->TH * g.nseg * g.nchunks;
-    if (g.num_items >= 32LL * p->sm_count || g.seg_len <= 2) break;
+    if (g.seg_len <= 2 || g.num_items >= 64LL * p->sm_count) break;
+    if (g.num_items >= 32LL * p->sm_count && (g.seg_len + 1) / 2 < 7) break;
     g.seg_len = (g.seg_len + 1) / 2;
   }
   g.granularity = cfg->granularity;
