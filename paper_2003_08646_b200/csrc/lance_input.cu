@@ -57,6 +57,9 @@ constexpr int K1_THREADS = LANCE_K1_THREADS;
 #ifndef LANCE_K0_MINB
 #define LANCE_K0_MINB 2
 #endif
+#ifndef LANCE_K0_DEPTH
+#define LANCE_K0_DEPTH 4  // K0 ring: column pairs in flight per warp (2: +0.5 %, 6: +5 % step time)
+#endif
 
 // Warp work item: (img, ti, tile segment, channel chunk).
 struct StripItem {
@@ -935,7 +938,7 @@ cudaError_t launch_input_range(const float* x, float* partials, int grid, LanceD
                                const InGeom& g, int vec2, cudaStream_t s) {
   // K0 input staging: cp.async ring of 4 tiles per warp (measured: 7-8 % faster
   // than register lookahead on the 56x56 / 28x28 layers; 8 halves residency).
-  constexpr int kDepth = 4;
+  constexpr int kDepth = LANCE_K0_DEPTH;
   if (g.C < 32) {
     LANCE_LAUNCH_CHECK(launch_k(input_range_smallc_kernel, grid, 256, 0, s, x, partials, st, g));
   } else if (g.C % 64 == 0) {
